@@ -1,0 +1,128 @@
+/*
+ * bplb.h -- C ABI of the B200 lower-bound-collection engine
+ * (paper_2402_14821_b200/libbplb.so).
+ *
+ * This is the drop-in boundary for the reference's bound-engine plug-in
+ *   BoundEngine = Callable[[ReducedInstance, int], BoundResult]
+ *   (/root/reference/pkg/src/binpack/propagator.py:40, called at
+ *    propagator.py:274-276 and search.py:352)
+ * and for the functions behind it (bounds.py:463-527, parallel.py:122-174).
+ * Plain pointers and sizes only; no CUDA or torch types cross the boundary
+ * (streams are passed as void*).  INTEGRATION.md shows the ctypes binding a
+ * reference maintainer would add.
+ *
+ * Conventions
+ *  - Kinds: 0=MT 1=RAD2 2=FS1 3=CCM1 4=VB2 5=BJ1 (bounds.py:48-67 order).
+ *  - Weights are int32 in [1, c]; 1 <= c <= BPLB_MAX_C.  Per-node r may be 0.
+ *  - Every call returns 0 on success or a negative BPLB_E* code; the message
+ *    of the last failure on the calling thread is bplb_last_error().
+ *  - Calls on one engine are serialised by an internal mutex and are
+ *    synchronous (they return after results are back in host memory), the
+ *    "internally concurrent, externally synchronous" model of SPEC.md:223.
+ *  - Caller owns every host array; outputs are caller-allocated.
+ */
+#ifndef BPLB_H
+#define BPLB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BPLB_API __attribute__((visibility("default")))
+#else
+#define BPLB_API
+#endif
+
+#define BPLB_OK 0
+#define BPLB_EINVAL (-1)    /* bad argument (maps to ValueError)              */
+#define BPLB_ERANGE (-2)    /* input outside the GPU integer envelope         */
+#define BPLB_ECUDA (-3)     /* CUDA runtime / launch failure (RuntimeError)   */
+#define BPLB_ENOMEM (-4)    /* device or pinned allocation failed             */
+#define BPLB_ENODEV (-5)    /* no CUDA device / unsupported architecture      */
+
+#define BPLB_NKINDS 6
+#define BPLB_MAX_C ((int64_t)1 << 30)   /* capacity envelope */
+#define BPLB_MAX_R ((int64_t)1 << 24)   /* items per reduced instance         */
+
+/* flags */
+#define BPLB_F_PHASED 0x1   /* kinds in order; stop after the first kind whose
+                               best exceeds k (Alg. 2 early exit, bounds.py:523-525) */
+#define BPLB_F_CANCEL 0x2   /* Alg. 4 guard "if lb <= k" per work unit
+                               (parallel.py:76-77): units observing lb > k skip */
+#define BPLB_F_TIMING 0x4   /* record device time of the last call (bplb_last_device_ms) */
+
+typedef struct bplb_engine bplb_engine;
+
+/* Result of one feasibility check (BoundResult, bounds.py:101-108). */
+typedef struct {
+    int64_t best[BPLB_NKINDS];      /* per-kind best bound, indexed by kind id        */
+    int64_t arg_lambda[BPLB_NKINDS];/* lowest lambda attaining best                   */
+    int64_t n_lambda[BPLB_NKINDS];  /* |Lambda_k| (VB2 capped per instance)            */
+    int64_t evals[BPLB_NKINDS];     /* lambda points actually evaluated per kind       */
+    int32_t evaluated[BPLB_NKINDS]; /* 1 if any lambda of the kind was evaluated       */
+    int32_t n_done;                 /* PHASED: number of kinds (in order) processed    */
+    int32_t exceeded;               /* lb > k                                          */
+    int64_t lb;                     /* max over evaluated kinds                        */
+    int64_t evals_total;            /* sum of evals                                    */
+} bplb_result;
+
+/* Engine lifetime.  One engine owns a CUDA stream, grow-only device buffers
+ * and pinned staging buffers on `device`. */
+BPLB_API int bplb_engine_create(int device, bplb_engine **out);
+BPLB_API int bplb_engine_destroy(bplb_engine *eng);
+
+/* One feasibility check of one reduced instance (w[0..r)).
+ * kinds[0..nkinds) gives the evaluation order (PHASED) / the subset.
+ * Replaces: lower_bound_seq (bounds.py:504-527) when flags = PHASED,
+ *           lower_bound_par (parallel.py:122-137) when flags = CANCEL or 0,
+ *           ParallelBoundEngine.__call__ (parallel.py:160-163). */
+BPLB_API int bplb_check(bplb_engine *eng, const int32_t *w, int64_t r, int64_t c, int64_t k,
+               const int32_t *kinds, int32_t nkinds, int32_t flags, bplb_result *out);
+
+/* Per-lambda bounds of one kind over [lo, hi] (inclusive), out[hi-lo+1].
+ * Replaces: dff_bound_batch (bounds.py:463-501) and, with lo == hi,
+ *           dff_bound (bounds.py:276-290).
+ * [lo, hi] must lie inside the kind's (uncapped) parameter domain. */
+BPLB_API int bplb_dff_bound_batch(bplb_engine *eng, int32_t kind, const int32_t *w, int64_t r,
+                         int64_t c, int64_t lo, int64_t hi, int64_t *out);
+
+/* Batched feasibility check over n_nodes reduced instances in CSR layout
+ * (w_concat[offsets[i] .. offsets[i+1])), all with capacity c and budget k.
+ * Outputs (host, caller-allocated; best/arg may be NULL):
+ *   lb_out[n], exceeded_out[n], best_out[n*6], arg_out[n*6] (by kind id;
+ *   kinds not evaluated report 0).  No reference counterpart: the reference
+ *   evaluates one node per engine call (propagator.py:274-276). */
+BPLB_API int bplb_check_batch(bplb_engine *eng, const int32_t *w_concat, const int64_t *offsets,
+                     int64_t n_nodes, int64_t c, int64_t k, const int32_t *kinds,
+                     int32_t nkinds, int32_t flags, int64_t *lb_out, uint8_t *exceeded_out,
+                     int64_t *best_out, int64_t *arg_out);
+
+/* Same as bplb_check_batch with every array already resident in device
+ * memory (`stream` is a cudaStream_t, or NULL for the engine's stream).
+ * Asynchronous: returns after enqueueing; the caller synchronises.
+ * d_best/d_arg may be NULL.  Work buffers are owned by the engine, so
+ * concurrent device calls on one engine must be ordered on one stream. */
+BPLB_API int bplb_check_batch_device(bplb_engine *eng, const int32_t *d_w_concat,
+                            const int64_t *d_offsets, int64_t n_nodes, int64_t max_r,
+                            int64_t c, int64_t k, const int32_t *kinds, int32_t nkinds,
+                            int32_t flags, int64_t *d_lb, uint8_t *d_exceeded,
+                            int64_t *d_best, int64_t *d_arg, void *stream);
+
+/* Number of kernel launches issued by the engine since creation (for the
+ * bench's gpu_launches claim), and device time of the last TIMING call. */
+BPLB_API int64_t bplb_launch_count(bplb_engine *eng);
+BPLB_API double bplb_last_device_ms(bplb_engine *eng);
+
+/* Thread-local message describing the last error on this thread. */
+BPLB_API const char *bplb_last_error(void);
+
+/* Library / device description ("bplb <ver> sm_100a ..."). */
+BPLB_API const char *bplb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BPLB_H */

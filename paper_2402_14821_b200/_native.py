@@ -1,0 +1,230 @@
+"""ctypes binding of libbplb.so (include/bplb.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+sm_100 device is visible, every bound call raises.  Build the library with
+``python -c "import __graft_entry__ as g; g.build()"`` (or
+``python paper_2402_14821_b200/build_native.py``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbplb.so")
+
+NKINDS = 6
+F_PHASED = 0x1
+F_CANCEL = 0x2
+F_TIMING = 0x4
+
+E_INVAL, E_RANGE, E_CUDA, E_NOMEM, E_NODEV = -1, -2, -3, -4, -5
+
+INT64_MAX = (1 << 63) - 1
+INT64_MIN = -(1 << 63)
+
+
+class BplbResult(ctypes.Structure):
+    _fields_ = [
+        ("best", ctypes.c_int64 * NKINDS),
+        ("arg_lambda", ctypes.c_int64 * NKINDS),
+        ("n_lambda", ctypes.c_int64 * NKINDS),
+        ("evals", ctypes.c_int64 * NKINDS),
+        ("evaluated", ctypes.c_int32 * NKINDS),
+        ("n_done", ctypes.c_int32),
+        ("exceeded", ctypes.c_int32),
+        ("lb", ctypes.c_int64),
+        ("evals_total", ctypes.c_int64),
+    ]
+
+
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_vp = ctypes.c_void_p
+
+# symbol -> (restype, argtypes); also the list the CPU test checks is exported
+SIGNATURES = {
+    "bplb_engine_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    "bplb_engine_destroy": (ctypes.c_int, [_vp]),
+    "bplb_check": (ctypes.c_int, [_vp, _i32p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                  _i32p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BplbResult)]),
+    "bplb_dff_bound_batch": (ctypes.c_int, [_vp, ctypes.c_int32, _i32p, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_int64, ctypes.c_int64, _i64p]),
+    "bplb_check_batch": (ctypes.c_int, [_vp, _i32p, _i64p, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int64, _i32p, ctypes.c_int32, ctypes.c_int32,
+                                        _i64p, _u8p, _i64p, _i64p]),
+    "bplb_check_batch_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.c_int64, _i32p, ctypes.c_int32,
+                                               ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "bplb_launch_count": (ctypes.c_int64, [_vp]),
+    "bplb_last_device_ms": (ctypes.c_double, [_vp]),
+    "bplb_last_error": (ctypes.c_char_p, []),
+    "bplb_version": (ctypes.c_char_p, []),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libbplb.so and declare every exported signature."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"libbplb.so not found at {path}: the CUDA engine is required (no CPU fallback). "
+                "Build it with `python paper_2402_14821_b200/build_native.py`.")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _raise(rc: int, what: str):
+    msg = load_library().bplb_last_error().decode(errors="replace")
+    text = f"{what}: {msg}"
+    if rc == E_INVAL:
+        raise ValueError(text)
+    if rc == E_RANGE:
+        raise ValueError(text + " (outside the GPU integer envelope, see DESIGN.md)")
+    if rc == E_NOMEM:
+        raise MemoryError(text)
+    raise RuntimeError(text)
+
+
+def _clamp_k(k: int) -> int:
+    k = int(k)
+    return INT64_MAX if k > INT64_MAX else (INT64_MIN if k < INT64_MIN else k)
+
+
+def as_i32(weights) -> np.ndarray:
+    """Weights as a contiguous int32 array (values outside int32 are rejected)."""
+    if isinstance(weights, np.ndarray) and weights.dtype == np.int32 and weights.flags.c_contiguous:
+        return weights
+    a = np.asarray(weights)
+    if a.dtype.kind not in "iu" and a.size:
+        a = a.astype(np.int64)
+    if a.size and (a.max() > 2**31 - 1 or a.min() < -(2**31)):
+        raise ValueError("weight outside the GPU integer envelope (int32)")
+    return np.ascontiguousarray(a, dtype=np.int32).reshape(-1)
+
+
+class Engine:
+    """One libbplb engine: a CUDA stream plus grow-only device/pinned buffers
+    on one device.  Calls are synchronous and serialised inside the library."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_library()
+        h = _vp()
+        rc = self._lib.bplb_engine_create(int(device), ctypes.byref(h))
+        if rc != 0:
+            _raise(rc, "bplb_engine_create")
+        self._h = h
+        self.device = int(device)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.bplb_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("engine is closed")
+        return self._h
+
+    def launch_count(self) -> int:
+        return int(self._lib.bplb_launch_count(self.handle))
+
+    def last_device_ms(self) -> float:
+        return float(self._lib.bplb_last_device_ms(self.handle))
+
+    def check(self, w: np.ndarray, c: int, k: int, kinds, flags: int) -> BplbResult:
+        w = as_i32(w)
+        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        res = BplbResult()
+        rc = self._lib.bplb_check(self.handle, w.ctypes.data_as(_i32p), len(w), int(c), _clamp_k(k),
+                                  ks.ctypes.data_as(_i32p), len(ks), int(flags), ctypes.byref(res))
+        if rc != 0:
+            _raise(rc, "bplb_check")
+        return res
+
+    def dff_bound_batch(self, kind: int, w: np.ndarray, c: int, lo: int, hi: int) -> np.ndarray:
+        w = as_i32(w)
+        n = max(0, int(hi) - int(lo) + 1)
+        out = np.zeros(n, dtype=np.int64)
+        if n == 0:
+            return out
+        rc = self._lib.bplb_dff_bound_batch(self.handle, int(kind), w.ctypes.data_as(_i32p), len(w), int(c),
+                                            int(lo), int(hi), out.ctypes.data_as(_i64p))
+        if rc != 0:
+            _raise(rc, "bplb_dff_bound_batch")
+        return out
+
+    def check_batch(self, w: np.ndarray, offsets: np.ndarray, c: int, k: int, kinds, flags: int,
+                    want_best: bool = False, out=None):
+        w = as_i32(w)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        n = len(off) - 1
+        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        if out is None:
+            lb = np.empty(n, dtype=np.int64)
+            ex = np.empty(n, dtype=np.uint8)
+        else:
+            lb, ex = out
+        best = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        arg = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        rc = self._lib.bplb_check_batch(
+            self.handle, w.ctypes.data_as(_i32p), off.ctypes.data_as(_i64p), n, int(c), _clamp_k(k),
+            ks.ctypes.data_as(_i32p), len(ks), int(flags), lb.ctypes.data_as(_i64p),
+            ex.ctypes.data_as(_u8p),
+            best.ctypes.data_as(_i64p) if best is not None else None,
+            arg.ctypes.data_as(_i64p) if arg is not None else None)
+        if rc != 0:
+            _raise(rc, "bplb_check_batch")
+        if want_best:
+            return lb, ex.view(bool), best, arg
+        return lb, ex.view(bool)
+
+    def check_batch_device(self, w_ptr: int, off_ptr: int, n_nodes: int, max_r: int, c: int, k: int,
+                           kinds, flags: int, lb_ptr: int, ex_ptr: int, best_ptr: int = 0,
+                           arg_ptr: int = 0, stream_ptr: int = 0) -> None:
+        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        rc = self._lib.bplb_check_batch_device(
+            self.handle, _vp(w_ptr), _vp(off_ptr), int(n_nodes), int(max_r), int(c), _clamp_k(k),
+            ks.ctypes.data_as(_i32p), len(ks), int(flags), _vp(lb_ptr), _vp(ex_ptr),
+            _vp(best_ptr or None), _vp(arg_ptr or None), _vp(stream_ptr or None))
+        if rc != 0:
+            _raise(rc, "bplb_check_batch_device")
+
+
+_engines: dict[int, Engine] = {}
+_engines_lock = threading.Lock()
+
+
+def default_engine(device: int | None = None) -> Engine:
+    """Process-wide engine per device (created on first use)."""
+    if device is None:
+        device = int(os.environ.get("BPLB_DEVICE", "0"))
+    with _engines_lock:
+        eng = _engines.get(device)
+        if eng is None:
+            eng = Engine(device)
+            _engines[device] = eng
+        return eng

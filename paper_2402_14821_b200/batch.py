@@ -1,0 +1,46 @@
+"""Array-native batched feasibility checks over many search-node states.
+
+No reference counterpart: the reference evaluates one node per engine call
+(propagator.py:274-276).  A batch is a CSR of reduced weights
+(``weights[offsets[i]:offsets[i+1]]`` = node i) sharing capacity ``c`` and
+bin budget ``k``.  One call = one upload + one kernel launch (the paper's
+"batch all copies and launches into a single API call").
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .bounds import DEFAULT_DFF_ORDER, kind_ids
+
+__all__ = ["lower_bound_batch", "csr_from_lists"]
+
+
+def csr_from_lists(nodes: Sequence[Sequence[int]]) -> tuple[np.ndarray, np.ndarray]:
+    lens = np.fromiter((len(n) for n in nodes), dtype=np.int64, count=len(nodes))
+    off = np.zeros(len(nodes) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    w = np.fromiter((x for n in nodes for x in n), dtype=np.int32, count=int(off[-1]))
+    return w, off
+
+
+def lower_bound_batch(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
+                      kinds: Sequence = DEFAULT_DFF_ORDER, *, mode: str = "full",
+                      want_best: bool = False, engine: _native.Engine | None = None):
+    """Evaluate the LB collection for every node of a CSR batch on the GPU.
+
+    mode: ``"full"`` (every kind completes; lb = max over kinds),
+          ``"seq"`` (kinds in order, early exit once lb > k -- per node
+          identical to lower_bound_seq's lb/exceeded_k),
+          ``"cancel"`` (units skip once the node's lb > k; decision bit
+          identical, lb any computed value > k).
+    Returns ``(lb int64[n], exceeded bool[n])`` and, with ``want_best``,
+    also ``best int64[n, 6]`` and ``arg_lambda int64[n, 6]`` indexed by kind
+    id (MT, RAD2, FS1, CCM1, VB2, BJ1).
+    """
+    flags = {"full": 0, "seq": _native.F_PHASED, "cancel": _native.F_CANCEL}[mode]
+    eng = engine or _native.default_engine()
+    return eng.check_batch(weights, offsets, c, k, kind_ids(kinds), flags, want_best=want_best)

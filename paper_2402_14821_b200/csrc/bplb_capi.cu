@@ -1,0 +1,439 @@
+// bplb_capi.cu -- the C ABI of libbplb.so (include/bplb.h): engine lifetime,
+// host<->device staging, kernel selection and launch.  No torch types; the
+// Python host side binds these symbols with ctypes
+// (paper_2402_14821_b200/_native.py).
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <algorithm>
+
+#include "../../include/bplb.h"
+#include "bplb_core.h"
+#include "bplb_node.cuh"
+#include "bplb_wide.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(BPLB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int64_t NODE_R_MAX_SORT = 8192;
+constexpr int64_t NODE_R_MAX_TABLE = 16384;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int grow(size_t bytes) {
+        if (bytes <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t n = std::max<size_t>(bytes, 256);
+        if (cudaMalloc(&p, n) != cudaSuccess) return fail(BPLB_ENOMEM, "cudaMalloc failed");
+        cap = n;
+        return 0;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    int grow(size_t bytes) {
+        if (bytes <= cap) return 0;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t n = std::max<size_t>(bytes, 4096);
+        if (cudaMallocHost(&p, n) != cudaSuccess) return fail(BPLB_ENOMEM, "cudaMallocHost failed");
+        cap = n;
+        return 0;
+    }
+    void release() { if (p) cudaFreeHost(p); p = nullptr; cap = 0; }
+};
+
+bool is_pinned(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+struct bplb_engine {
+    int device = 0;
+    int num_sms = 0;
+    size_t smem_optin = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::mutex mu;
+    DevBuf d_w, d_off, d_res, d_lb, d_ex, d_best, d_arg, d_err, d_lam, d_wide;
+    HostBuf h_stage, h_res;
+    int64_t launches = 0;
+    double last_ms = 0.0;
+};
+
+namespace {
+
+// Copy host -> device (direct DMA when the source is pinned, through the
+// engine's pinned staging buffer otherwise).
+int h2d(bplb_engine* e, void* dst, const void* src, size_t bytes, size_t stage_off = 0) {
+    if (bytes == 0) return 0;
+    if (bytes <= 65536 || is_pinned(src)) {
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, e->stream));
+        return 0;
+    }
+    if (int rc = e->h_stage.grow(stage_off + bytes)) return rc;
+    char* st = (char*)e->h_stage.p + stage_off;
+    std::memcpy(st, src, bytes);
+    CUDA_TRY(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyHostToDevice, e->stream));
+    return 0;
+}
+
+int check_kinds(const int32_t* kinds, int32_t nkinds, int* out) {
+    if (nkinds < 0 || nkinds > K_COUNT) return fail(BPLB_EINVAL, "nkinds must be in [0, 6]");
+    bool seen[K_COUNT] = {false, false, false, false, false, false};
+    for (int i = 0; i < nkinds; ++i) {
+        int k = kinds[i];
+        if (k < 0 || k >= K_COUNT) return fail(BPLB_EINVAL, "kind id out of range");
+        if (seen[k]) return fail(BPLB_EINVAL, "duplicate kind in kinds");
+        seen[k] = true;
+        out[i] = k;
+    }
+    return 0;
+}
+
+int check_c(int64_t c) {
+    if (c < 1) return fail(BPLB_EINVAL, "capacity must be >= 1");
+    if (c > BPLB_MAX_C) return fail(BPLB_ERANGE, "capacity exceeds the GPU envelope (2^30)");
+    return 0;
+}
+
+void fill_params(bplb::KParams& p, int64_t c, int64_t k, const int* kinds, int nk, int flags) {
+    std::memset(&p, 0, sizeof(p));
+    p.c = c;
+    p.k = k;
+    for (int i = 0; i < nk; ++i) p.kinds[i] = kinds[i];
+    p.nk = nk;
+    p.flags = flags;
+    p.one = 1;
+}
+
+// Launch the node-resident kernel over n nodes.  max_r bounds every node.
+int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r, int grid_cap) {
+    const bool table = p.c <= bplb::TABLE_MAX_C;
+    if (max_r > (table ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT))
+        return fail(BPLB_ERANGE, "node larger than the node-resident envelope");
+    int rcap = 1;
+    if (table) rcap = (int)std::max<int64_t>(max_r, 1);
+    else while (rcap < max_r) rcap <<= 1;
+    size_t smem = bplb::node_smem_bytes(table, rcap, p.c);
+    if (smem > e->smem_optin) return fail(BPLB_ERANGE, "node needs more shared memory than available");
+    auto kern = table ? bplb::node_kernel<true> : bplb::node_kernel<false>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::NT, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
+    if (grid_cap > 0) grid = std::min<int64_t>(grid, grid_cap);
+    if (grid < 1) return 0;
+    p.n_nodes = n_nodes;
+    kern<<<(unsigned)grid, bplb::NT, smem, e->stream>>>(p, rcap);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bplb_last_error(void) { return g_err.c_str(); }
+
+const char* bplb_version(void) { return "bplb 0.1 sm_100a (node-resident + grid-wide LB-collection engine)"; }
+
+int bplb_engine_create(int device, bplb_engine** out) {
+    if (!out) return fail(BPLB_EINVAL, "out is null");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(BPLB_ENODEV, "no CUDA device visible");
+    }
+    if (device < 0 || device >= n) return fail(BPLB_EINVAL, "device index out of range");
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(BPLB_ENODEV, std::string("libbplb is built for sm_100a; device is ") + prop.name);
+    CUDA_TRY(cudaSetDevice(device));
+    bplb_engine* e = new bplb_engine();
+    e->device = device;
+    e->num_sms = prop.multiProcessorCount;
+    e->smem_optin = prop.sharedMemPerBlockOptin;
+    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess) {
+        delete e;
+        return fail(BPLB_ECUDA, "stream/event creation failed");
+    }
+    *out = e;
+    return 0;
+}
+
+int bplb_engine_destroy(bplb_engine* e) {
+    if (!e) return 0;
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
+                      &e->d_err, &e->d_lam, &e->d_wide})
+        b->release();
+    e->h_stage.release();
+    e->h_res.release();
+    cudaEventDestroy(e->ev0);
+    cudaEventDestroy(e->ev1);
+    cudaStreamDestroy(e->stream);
+    delete e;
+    return 0;
+}
+
+int64_t bplb_launch_count(bplb_engine* e) { return e ? e->launches : 0; }
+double bplb_last_device_ms(bplb_engine* e) { return e ? e->last_ms : 0.0; }
+
+int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k,
+               const int32_t* kinds, int32_t nkinds, int32_t flags, bplb_result* out) {
+    if (!e || !out) return fail(BPLB_EINVAL, "null engine or output");
+    if (r < 0 || (r > 0 && !w)) return fail(BPLB_EINVAL, "bad weight array");
+    if (r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items for the GPU envelope");
+    if (int rc = check_c(c)) return rc;
+    int ks[K_COUNT];
+    if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    const bool timing = flags & BPLB_F_TIMING;
+    if (int rc = e->d_w.grow((size_t)std::max<int64_t>(r, 1) * 4 + 64)) return rc;
+    if (int rc = e->d_res.grow(sizeof(bplb_result) + 16)) return rc;
+    if (int rc = e->d_err.grow(16)) return rc;
+    if (int rc = e->h_res.grow(sizeof(bplb_result) + 16)) return rc;
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+    if (int rc = h2d(e, e->d_w.p, w, (size_t)r * 4)) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    bplb::KParams p;
+    fill_params(p, c, k, ks, nkinds, flags);
+    p.w = (const int*)e->d_w.p;
+    p.res_out = (bplb_result*)e->d_res.p;
+    p.err_out = (int*)e->d_err.p;
+    int rc;
+    if (bplb::wide_preferred(r, c)) {
+        rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
+                              p, r, nullptr);
+        if (rc) return fail(rc, bplb::wide_error());
+    } else {
+        // single node: offsets live in the tail of the result buffer
+        int64_t off_h[2] = {0, r};
+        if ((rc = e->d_off.grow(16))) return rc;
+        CUDA_TRY(cudaMemcpyAsync(e->d_off.p, off_h, 16, cudaMemcpyHostToDevice, e->stream));
+        p.off = (const int64_t*)e->d_off.p;
+        if ((rc = launch_node(e, p, 1, r, 1))) return rc;
+    }
+    CUDA_TRY(cudaMemcpyAsync(e->h_res.p, e->d_res.p, sizeof(bplb_result), cudaMemcpyDeviceToHost,
+                             e->stream));
+    CUDA_TRY(cudaMemcpyAsync((char*)e->h_res.p + sizeof(bplb_result), e->d_err.p, 4,
+                             cudaMemcpyDeviceToHost, e->stream));
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (timing) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+        e->last_ms = ms;
+    }
+    int err = *(int*)((char*)e->h_res.p + sizeof(bplb_result));
+    if (err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+    std::memcpy(out, e->h_res.p, sizeof(bplb_result));
+    return 0;
+}
+
+int bplb_dff_bound_batch(bplb_engine* e, int32_t kind, const int32_t* w, int64_t r, int64_t c,
+                         int64_t lo, int64_t hi, int64_t* out) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (kind < 0 || kind >= K_COUNT) return fail(BPLB_EINVAL, "kind id out of range");
+    if (r < 0 || (r > 0 && !w)) return fail(BPLB_EINVAL, "bad weight array");
+    if (r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items for the GPU envelope");
+    if (int rc = check_c(c)) return rc;
+    if (hi < lo) return 0;
+    if (!out) return fail(BPLB_EINVAL, "null output");
+    int64_t dlo, dhi;
+    bplb_domain(kind, c, &dlo, &dhi);
+    if (lo < dlo || hi > dhi)
+        return fail(BPLB_EINVAL, "lambda range outside the parameter domain of the kind");
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    const int64_t L = hi - lo + 1;
+    int rc;
+    if ((rc = e->d_w.grow((size_t)std::max<int64_t>(r, 1) * 4 + 64))) return rc;
+    if ((rc = e->d_res.grow(sizeof(bplb_result) + 16))) return rc;
+    if ((rc = e->d_err.grow(16))) return rc;
+    if ((rc = e->d_lam.grow((size_t)L * 8))) return rc;
+    if ((rc = h2d(e, e->d_w.p, w, (size_t)r * 4))) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    bplb::KParams p;
+    int ks[1] = {kind};
+    fill_params(p, c, 0, ks, 1, 0);
+    p.w = (const int*)e->d_w.p;
+    p.res_out = (bplb_result*)e->d_res.p;
+    p.err_out = (int*)e->d_err.p;
+    p.lam_out = (int64_t*)e->d_lam.p;
+    p.out_lo = lo;
+    p.out_hi = hi;
+    p.use_range = 1;
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        p.rng_lo[kd] = lo;
+        p.rng_hi[kd] = kd == kind ? hi : lo - 1;
+    }
+    if (r == 0) {  // bounds.py:478-479
+        CUDA_TRY(cudaMemsetAsync(e->d_lam.p, 0, (size_t)L * 8, e->stream));
+    } else if (bplb::wide_preferred(r, c)) {
+        rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
+                              p, r, nullptr);
+        if (rc) return fail(rc, bplb::wide_error());
+    } else {
+        int64_t off_h[2] = {0, r};
+        if ((rc = e->d_off.grow(16))) return rc;
+        CUDA_TRY(cudaMemcpyAsync(e->d_off.p, off_h, 16, cudaMemcpyHostToDevice, e->stream));
+        p.off = (const int64_t*)e->d_off.p;
+        if ((rc = launch_node(e, p, 1, r, 1))) return rc;
+    }
+    int err = 0;
+    CUDA_TRY(cudaMemcpyAsync(out, e->d_lam.p, (size_t)L * 8, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(&err, e->d_err.p, 4, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+    return 0;
+}
+
+int bplb_check_batch_device(bplb_engine* e, const int32_t* d_w, const int64_t* d_off,
+                            int64_t n_nodes, int64_t max_r, int64_t c, int64_t k,
+                            const int32_t* kinds, int32_t nkinds, int32_t flags, int64_t* d_lb,
+                            uint8_t* d_ex, int64_t* d_best, int64_t* d_arg, void* stream) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (n_nodes < 0 || max_r < 0) return fail(BPLB_EINVAL, "bad batch shape");
+    if (int rc = check_c(c)) return rc;
+    int ks[K_COUNT];
+    if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
+    if (n_nodes == 0) return 0;
+    cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    bplb::KParams p;
+    fill_params(p, c, k, ks, nkinds, flags);
+    p.w = d_w;
+    p.off = d_off;
+    p.lb_out = d_lb;
+    p.ex_out = d_ex;
+    p.best_out = d_best;
+    p.arg_out = d_arg;
+    if (int rc = e->d_err.grow(16)) return rc;
+    p.err_out = (int*)e->d_err.p;
+    cudaStream_t saved = e->stream;
+    e->stream = s;
+    int rc = launch_node(e, p, n_nodes, max_r, 0);
+    e->stream = saved;
+    return rc;
+}
+
+int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64_t n_nodes,
+                     int64_t c, int64_t k, const int32_t* kinds, int32_t nkinds, int32_t flags,
+                     int64_t* lb_out, uint8_t* ex_out, int64_t* best_out, int64_t* arg_out) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (n_nodes < 0 || (n_nodes > 0 && (!off || !lb_out || !ex_out)))
+        return fail(BPLB_EINVAL, "bad batch arguments");
+    if (int rc = check_c(c)) return rc;
+    int ks[K_COUNT];
+    if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
+    if (n_nodes == 0) return 0;
+    if (off[0] != 0) return fail(BPLB_EINVAL, "offsets[0] must be 0");
+    int64_t max_r = 0;
+    for (int64_t i = 0; i < n_nodes; ++i) {
+        int64_t d = off[i + 1] - off[i];
+        if (d < 0) return fail(BPLB_EINVAL, "offsets must be non-decreasing");
+        max_r = std::max(max_r, d);
+    }
+    if (max_r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items in a node for the GPU envelope");
+    const int64_t total = off[n_nodes];
+    if (total > 0 && !w) return fail(BPLB_EINVAL, "null weights");
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    int rc;
+    const bool timing = flags & BPLB_F_TIMING;
+    if ((rc = e->d_w.grow((size_t)std::max<int64_t>(total, 1) * 4 + 64))) return rc;
+    if ((rc = e->d_off.grow((size_t)(n_nodes + 1) * 8))) return rc;
+    if ((rc = e->d_lb.grow((size_t)n_nodes * 8))) return rc;
+    if ((rc = e->d_ex.grow((size_t)n_nodes))) return rc;
+    if (best_out && (rc = e->d_best.grow((size_t)n_nodes * 48))) return rc;
+    if (arg_out && (rc = e->d_arg.grow((size_t)n_nodes * 48))) return rc;
+    if ((rc = e->d_err.grow(16))) return rc;
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+    if ((rc = h2d(e, e->d_w.p, w, (size_t)total * 4))) return rc;
+    if ((rc = h2d(e, e->d_off.p, off, (size_t)(n_nodes + 1) * 8, (size_t)total * 4 + 64))) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    bplb::KParams p;
+    fill_params(p, c, k, ks, nkinds, flags);
+    p.w = (const int*)e->d_w.p;
+    p.off = (const int64_t*)e->d_off.p;
+    p.lb_out = (int64_t*)e->d_lb.p;
+    p.ex_out = (uint8_t*)e->d_ex.p;
+    p.best_out = best_out ? (int64_t*)e->d_best.p : nullptr;
+    p.arg_out = arg_out ? (int64_t*)e->d_arg.p : nullptr;
+    p.err_out = (int*)e->d_err.p;
+    if (max_r <= ((c <= bplb::TABLE_MAX_C) ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT)) {
+        if ((rc = launch_node(e, p, n_nodes, max_r, 0))) return rc;
+    } else {
+        // nodes beyond the node-resident envelope go one by one through the
+        // grid-wide path (rare: r > 8192)
+        for (int64_t i = 0; i < n_nodes; ++i) {
+            bplb::KParams q = p;
+            q.w = (const int*)e->d_w.p + off[i];
+            q.lb_out = p.lb_out + i;
+            q.ex_out = p.ex_out + i;
+            q.best_out = p.best_out ? p.best_out + i * K_COUNT : nullptr;
+            q.arg_out = p.arg_out ? p.arg_out + i * K_COUNT : nullptr;
+            rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap,
+                                  &e->launches, q, off[i + 1] - off[i], nullptr);
+            if (rc) return fail(rc, bplb::wide_error());
+        }
+    }
+    int err = 0;
+    CUDA_TRY(cudaMemcpyAsync(lb_out, e->d_lb.p, (size_t)n_nodes * 8, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(ex_out, e->d_ex.p, (size_t)n_nodes, cudaMemcpyDeviceToHost, e->stream));
+    if (best_out)
+        CUDA_TRY(cudaMemcpyAsync(best_out, e->d_best.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
+    if (arg_out)
+        CUDA_TRY(cudaMemcpyAsync(arg_out, e->d_arg.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(&err, e->d_err.p, 4, cudaMemcpyDeviceToHost, e->stream));
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (timing) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+        e->last_ms = ms;
+    }
+    if (err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+    return 0;
+}
+
+}  // extern "C"

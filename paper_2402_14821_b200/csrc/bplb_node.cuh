@@ -1,0 +1,494 @@
+// bplb_node.cuh -- node-resident kernel: one CTA evaluates the full LB
+// collection of one reduced instance at a time (persistent over a batch of
+// search nodes).  The instance lives in shared memory for the whole sweep,
+// as in the paper's calcDffLowerBound, but one launch covers
+// all six families, every lambda and every node of the batch.
+//
+// Work inside a CTA is cut into "units" taken from a shared-memory counter:
+//   T_LOOKUP  32 lambdas, one per lane, analytic sweep with histogram/sorted
+//             lookups (MT, RAD2, CCM1/BJ1 at large lambda)
+//   T_MOD     LMOD lambdas x all VB2 (or FS1) items, modular walk
+//   T_DIV     LDIV lambdas, warp-cooperative item pass (CCM1/BJ1 small lambda)
+#pragma once
+#include <climits>
+#include "bplb_device.cuh"
+#include "../../include/bplb.h"
+
+namespace bplb {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int TABLE_MAX_C = 4094;  // node kernel uses cumulative tables when c <= this
+constexpr int MAX_SEGS = 2 * K_COUNT;
+
+struct Seg {
+    int kind, type;
+    int64_t lo, hi;   // inclusive lambda range of the segment
+    int chunk;        // lambdas per unit
+    int first, count; // unit index range
+};
+
+struct KParams {
+    const int* w;          // CSR weights
+    const int64_t* off;    // CSR offsets [n_nodes + 1]
+    int64_t n_nodes;
+    int64_t c;
+    int64_t k;
+    int kinds[K_COUNT];
+    int nk;
+    int flags;
+    uint32_t one;          // == 1 (kept opaque to ptxas so adds land on the IMAD pipe)
+    int64_t* lb_out;       // [n] or null
+    uint8_t* ex_out;       // [n] or null
+    int64_t* best_out;     // [n*6] or null
+    int64_t* arg_out;      // [n*6] or null
+    bplb_result* res_out;  // [n] or null
+    int* err_out;          // set to 1 if a weight is outside [1, c]
+    // single-node per-lambda output (dff_bound_batch): kinds = {kind}
+    int64_t* lam_out;
+    int64_t out_lo, out_hi;
+    int use_range;
+    int64_t rng_lo[K_COUNT], rng_hi[K_COUNT];
+};
+
+struct NodeCtl {
+    NodeStats st;
+    int64_t lo[K_COUNT], hi[K_COUNT];
+    Seg segs[MAX_SEGS];
+    int nseg, nunits;
+    int kind_seg_first[K_COUNT], kind_seg_count[K_COUNT];
+    u64 key[K_COUNT];
+    unsigned long long evals[K_COUNT];
+    int evaluated[K_COUNT];
+    int unit_next;
+    int unit_end;
+    int lb;
+    int n_vb2;
+    int n_done;
+    int bad;
+};
+
+__device__ __forceinline__ bool kind_in(const KParams& p, int kind) {
+    for (int i = 0; i < p.nk; ++i)
+        if (p.kinds[i] == kind) return true;
+    return false;
+}
+
+// Threshold below which CCM1/BJ1 lambdas are summed densely instead of via
+// harmonic lookups (cost model in DESIGN.md).
+__device__ __forceinline__ int64_t div_split(int kind, const NodeStats& st, int64_t c) {
+    int lg = 1;
+    while ((1 << lg) <= st.r) ++lg;
+    int64_t n = st.r > 0 ? st.r : 1;
+    if (kind == K_CCM1) {
+        int64_t hs = (c - 1) / 2;
+        return (8 * hs * (lg + 1)) / (3 * n) + 1;
+    }
+    int64_t mw = st.maxw;
+    return (12 * mw * (lg + 1)) / (5 * n) + 1;
+}
+
+// Build the unit segments of one kind (thread 0).
+__device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c) {
+    int64_t lo = ctl.lo[kind], hi = ctl.hi[kind];
+    ctl.kind_seg_first[kind] = ctl.nseg;
+    ctl.kind_seg_count[kind] = 0;
+    if (hi < lo) return;
+    auto push = [&](int type, int64_t a, int64_t b, int chunk) {
+        if (b < a) return;
+        Seg& s = ctl.segs[ctl.nseg++];
+        s.kind = kind;
+        s.type = type;
+        s.lo = a;
+        s.hi = b;
+        s.chunk = chunk;
+        s.first = ctl.nunits;
+        s.count = (int)((b - a + chunk) / chunk);
+        ctl.nunits += s.count;
+        ctl.kind_seg_count[kind]++;
+    };
+    switch (kind) {
+    case K_MT: case K_RAD2: push(T_LOOKUP, lo, hi, LLOOK); break;
+    case K_FS1: case K_VB2: push(T_MOD, lo, hi, LMOD); break;
+    default: {  // CCM1, BJ1
+        if (table) {
+            push(T_LOOKUP, lo, hi, LLOOK);
+        } else {
+            int64_t sp = div_split(kind, ctl.st, c);
+            if (sp < lo) sp = lo;
+            if (sp > hi + 1) sp = hi + 1;
+            push(T_DIV, lo, sp - 1, LDIV);
+            push(T_LOOKUP, sp, hi, LLOOK);
+        }
+    }
+    }
+}
+
+template <class LK>
+__device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const int* sw,
+                         const int* vb2, u64* tot, u64* ztot, int u, bool single) {
+    const int lane = threadIdx.x & 31;
+    int si = 0;
+    while (si + 1 < ctl.nseg && ctl.segs[si + 1].first <= u) ++si;
+    const Seg sg = ctl.segs[si];
+    const int kind = sg.kind;
+    const int64_t c = p.c;
+    const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
+    const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+    int64_t* lam_out = single ? p.lam_out : nullptr;
+    const NodeStats& st = ctl.st;
+    int64_t wmax;
+    if (sg.type == T_LOOKUP) {
+        const int64_t lam = lam_a + lane;
+        const bool valid = lam <= lam_b;
+        int64_t S = 0;
+        if (valid) {
+            switch (kind) {
+            case K_MT: S = bplb_mt_sum(lk, c, st.r, lam); break;
+            case K_RAD2: S = bplb_rad2_sum(lk, c, st.r, lam); break;
+            case K_CCM1: S = bplb_ccm1_sum(lk, st, c, lam); break;
+            default: S = bplb_bj1_sum(lk, st, c, lam); break;
+            }
+        }
+        int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+        wmax = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
+    } else if (sg.type == T_DIV) {
+        int64_t mine = 0;
+        for (int64_t lam = lam_a; lam <= lam_b; ++lam) {
+            int64_t S = (kind == K_CCM1) ? ccm1_dense(sw, st, c, lam) : bj1_dense(sw, st.r, c, lam);
+            if (lam - lam_a == lane) mine = S;
+        }
+        const int64_t lam = lam_a + lane;
+        const bool valid = lam <= lam_b;
+        int64_t b = valid ? bplb_bound(mine, bplb_fc(kind, c, lam)) : 0;
+        wmax = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
+    } else {
+        const int warp = threadIdx.x >> 5;
+        u64* t = tot + warp * LMOD;
+        u64* z = ztot + warp * LMOD;
+        const int L = (int)(lam_b - lam_a + 1);
+        for (int j = lane; j < LMOD; j += kWarp) { t[j] = 0; z[j] = 0; }
+        __syncwarp();
+        const uint32_t c32 = (uint32_t)c;
+        const u64 cinv = bplb_cinv(c32);
+        const bool wide = c >= (1 << 23);
+        if (kind == K_VB2) {
+            if (wide) mod_walk<false, true>(vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
+            else mod_walk<false, false>(vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
+        } else {
+            if (wide) mod_walk<true, true>(sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
+            else mod_walk<true, false>(sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
+        }
+        __syncwarp();
+        wmax = -1;
+        for (int j0 = 0; j0 < L; j0 += kWarp) {
+            const int j = j0 + lane;
+            const bool valid = j < L;
+            const int64_t lam = lam_a + j;
+            int64_t S = 0;
+            if (valid)
+                S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j]) : bplb_fs1_sum(st, lam, t[j], z[j]);
+            int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+            int64_t m = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
+            wmax = m > wmax ? m : wmax;
+        }
+    }
+    if (lane == 0) {
+        atomicAdd(&ctl.evals[kind], (unsigned long long)(lam_b - lam_a + 1));
+        ctl.evaluated[kind] = 1;
+        if (wmax >= 0) atomicMax(&ctl.lb, (int)wmax);
+    }
+}
+
+// Process units [ctl.unit_next, ctl.unit_end) with all warps.
+template <class LK>
+__device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const int* sw,
+                          const int* vb2, u64* tot, u64* ztot, bool single, bool cancel) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&ctl.unit_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= ctl.unit_end) break;
+        if (cancel) {
+            int cur = *(volatile int*)&ctl.lb;
+            if ((int64_t)cur > p.k) continue;  // Alg. 4 guard
+        }
+        run_unit(p, ctl, lk, sw, vb2, tot, ztot, u, single);
+    }
+}
+
+__device__ __forceinline__ void block_sort(int* a, int n) {  // bitonic, n power of two
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += NT) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    int x = a[i], y = a[ixj];
+                    bool up = (i & k) == 0;
+                    if ((x > y) == up) { a[i] = y; a[ixj] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Exclusive-style inclusive scan helpers over shared arrays (one CTA).
+// out_n[i] = sum_{j < i} cnt_in[j]-style prefix is built by the callers.
+__device__ __forceinline__ void block_prefix_i64(const int* v, long long* pre, int n,
+                                                 long long* scratch /*NT*/) {
+    // pre[0] = 0, pre[i+1] = pre[i] + v[i]
+    const int per = (n + NT - 1) / NT;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    long long s = 0;
+    for (int i = b; i < e; ++i) s += v[i];
+    scratch[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long run = 0;
+        for (int t = 0; t < NT; ++t) { long long x = scratch[t]; scratch[t] = run; run += x; }
+    }
+    __syncthreads();
+    long long run = scratch[threadIdx.x];
+    if (threadIdx.x == 0) pre[0] = 0;
+    for (int i = b; i < e; ++i) { run += v[i]; pre[i + 1] = run; }
+    __syncthreads();
+}
+
+// cnt[i] holds the histogram count of value i-1 (i in [0, c+1]); converts in
+// place to cnt[i] = #{w <= i-1} and fills wle[i] = sum{w <= i-1}.
+__device__ __forceinline__ void block_table_scan(int* cnt, long long* wle, int n,
+                                                 long long* scratch /*2*NT*/) {
+    const int per = (n + NT - 1) / NT;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    long long sc = 0, sw = 0;
+    for (int i = b; i < e; ++i) { sc += cnt[i]; sw += (long long)cnt[i] * (i - 1); }
+    scratch[threadIdx.x] = sc;
+    scratch[NT + threadIdx.x] = sw;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long rc = 0, rw = 0;
+        for (int t = 0; t < NT; ++t) {
+            long long x = scratch[t], y = scratch[NT + t];
+            scratch[t] = rc; scratch[NT + t] = rw;
+            rc += x; rw += y;
+        }
+    }
+    __syncthreads();
+    long long rc = scratch[threadIdx.x], rw = scratch[NT + threadIdx.x];
+    for (int i = b; i < e; ++i) {
+        int x = cnt[i];
+        rc += x;
+        rw += (long long)x * (i - 1);
+        cnt[i] = (int)rc;
+        wle[i] = rw;
+    }
+    __syncthreads();
+}
+
+// Dynamic shared memory size of the node kernel.
+__host__ __device__ inline size_t node_smem_bytes(bool table, int rcap, int64_t c) {
+    size_t s = 0;
+    s += (size_t)rcap * 4;                 // sw
+    s += (size_t)rcap * 4;                 // vb2
+    s += (size_t)NW * LMOD * 8 * 2;        // tot, ztot
+    s += (size_t)2 * NT * 8;               // scratch
+    if (table) s += (size_t)(c + 2) * 8 + (size_t)(c + 2) * 4 + 8;
+    else s += (size_t)(rcap + 1) * 8;
+    return s;
+}
+
+template <bool TABLE>
+__global__ void __launch_bounds__(NT) node_kernel(KParams p, int rcap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ NodeCtl ctl;
+    int* sw = (int*)smem;
+    int* vb2 = sw + rcap;
+    u64* tot = (u64*)(vb2 + rcap);
+    u64* ztot = tot + NW * LMOD;
+    long long* scratch = (long long*)(ztot + NW * LMOD);
+    long long* pre = scratch + 2 * NT;               // SORT: [rcap+1]; TABLE: wle [c+2]
+    int* cnt = (int*)(pre + (TABLE ? p.c + 2 : 0));  // TABLE only: [c+2]
+    const int64_t c = p.c;
+    const bool single = p.lam_out != nullptr;
+    const bool phased = p.flags & BPLB_F_PHASED;
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
+
+    for (int64_t node = blockIdx.x; node < p.n_nodes; node += gridDim.x) {
+        const int64_t base = p.off[node];
+        const int r = (int)(p.off[node + 1] - base);
+        if (threadIdx.x == 0) {
+            NodeStats& st = ctl.st;
+            st.r = r; st.maxw = 0; st.n_small = st.n_eq = st.n_big = st.n_full = 0;
+            st.W = st.Vs = st.Vm = 0;
+            for (int i = 0; i < K_COUNT; ++i) {
+                ctl.key[i] = 0; ctl.evals[i] = 0; ctl.evaluated[i] = 0;
+            }
+            ctl.lb = 0; ctl.n_vb2 = 0; ctl.nseg = 0; ctl.nunits = 0; ctl.n_done = 0;
+            ctl.bad = 0;
+        }
+        // ---- stage weights -------------------------------------------------
+        int pw = 1;
+        while (pw < r) pw <<= 1;
+        if (TABLE) {
+            for (int i = threadIdx.x; i < c + 2; i += NT) cnt[i] = 0;
+        }
+        for (int i = threadIdx.x; i < (TABLE ? r : pw); i += NT)
+            sw[i] = i < r ? p.w[base + i] : INT_MAX;
+        __syncthreads();
+        // ---- statistics ------------------------------------------------------
+        {
+            int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
+            long long l_W = 0, l_Vs = 0, l_Vm = 0;
+            for (int i = threadIdx.x; i < r; i += NT) {
+                int x = sw[i];
+                l_max = max(l_max, x);
+                if (x < 1 || (int64_t)x > c) l_bad = 1;
+                l_W += x;
+                if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
+                else if (2 * (int64_t)x == c) l_e++;
+                else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
+                if (TABLE && x >= 1 && x <= c) atomicAdd(&cnt[x + 1], 1);
+            }
+            l_max = __reduce_max_sync(0xffffffffu, (unsigned)l_max);
+            l_bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)l_bad);
+            l_s = __reduce_add_sync(0xffffffffu, l_s);
+            l_e = __reduce_add_sync(0xffffffffu, l_e);
+            l_b = __reduce_add_sync(0xffffffffu, l_b);
+            l_f = __reduce_add_sync(0xffffffffu, l_f);
+            l_W = (long long)warp_sum_u64((u64)l_W);
+            l_Vs = (long long)warp_sum_u64((u64)l_Vs);
+            l_Vm = (long long)warp_sum_u64((u64)l_Vm);
+            if ((threadIdx.x & 31) == 0) {
+                atomicMax(&ctl.st.maxw, l_max);
+                if (l_bad) ctl.bad = 1;
+                atomicAdd(&ctl.st.n_small, l_s);
+                atomicAdd(&ctl.st.n_eq, l_e);
+                atomicAdd(&ctl.st.n_big, l_b);
+                atomicAdd(&ctl.st.n_full, l_f);
+                atomicAdd((unsigned long long*)&ctl.st.W, (unsigned long long)l_W);
+                atomicAdd((unsigned long long*)&ctl.st.Vs, (unsigned long long)l_Vs);
+                atomicAdd((unsigned long long*)&ctl.st.Vm, (unsigned long long)l_Vm);
+            }
+        }
+        __syncthreads();
+        // ---- lookup structure -----------------------------------------------
+        if (TABLE) {
+            block_table_scan(cnt, pre, (int)(c + 2), scratch);
+            // VB2 items: 2w != c and w < c (order irrelevant, G11)
+            for (int i = threadIdx.x; i < r; i += NT) {
+                int x = sw[i];
+                if (2 * (int64_t)x != c && x < c) vb2[atomicAdd(&ctl.n_vb2, 1)] = x;
+            }
+        } else {
+            block_sort(sw, pw);
+            block_prefix_i64(sw, pre, r, scratch);
+            const NodeStats& st = ctl.st;
+            const int nm = st.n_big - st.n_full;
+            for (int i = threadIdx.x; i < st.n_small + nm; i += NT)
+                vb2[i] = i < st.n_small ? sw[i] : sw[i + st.n_eq];
+            if (threadIdx.x == 0) ctl.n_vb2 = st.n_small + nm;
+        }
+        if (threadIdx.x == 0) {
+            bplb_stats_finish(&ctl.st, c);
+            for (int kd = 0; kd < K_COUNT; ++kd) {
+                int64_t lo, hi;
+                if (p.use_range) { lo = p.rng_lo[kd]; hi = p.rng_hi[kd]; }
+                else {
+                    bplb_domain(kd, c, &lo, &hi);
+                    if (kd == K_VB2) hi = bplb_vb2_hi(c, r, ctl.st.maxw);
+                }
+                if (!kind_in(p, kd)) hi = lo - 1;
+                ctl.lo[kd] = lo; ctl.hi[kd] = hi;
+            }
+            // segment order: kinds in p.kinds order
+            for (int i = 0; i < p.nk; ++i) add_kind_segs(ctl, p.kinds[i], TABLE, c);
+            if (ctl.bad) {
+                ctl.nunits = 0; ctl.nseg = 0;
+                for (int kd = 0; kd < K_COUNT; ++kd) ctl.kind_seg_count[kd] = 0;
+            }
+        }
+        __syncthreads();
+        // ---- sweep -------------------------------------------------------------
+        if (TABLE) {
+            LkTable lk{cnt, pre, c};
+            if (phased) {
+                for (int i = 0; i < p.nk; ++i) {
+                    const int kd = p.kinds[i];
+                    if (threadIdx.x == 0) {
+                        const int f = ctl.kind_seg_first[kd], n = ctl.kind_seg_count[kd];
+                        ctl.unit_next = n ? ctl.segs[f].first : 0;
+                        ctl.unit_end = n ? ctl.segs[f + n - 1].first + ctl.segs[f + n - 1].count : 0;
+                        ctl.n_done = i + 1;
+                    }
+                    __syncthreads();
+                    run_units(p, ctl, lk, sw, vb2, tot, ztot, single, false);
+                    __syncthreads();
+                    if ((int64_t)ctl.lb > p.k) break;
+                }
+            } else {
+                if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
+                __syncthreads();
+                run_units(p, ctl, lk, sw, vb2, tot, ztot, single, cancel);
+            }
+        } else {
+            int top = 0;
+            if (r > 0) { top = 1; while (top * 2 <= r) top *= 2; }
+            LkSorted lk{sw, pre, r, top};
+            if (phased) {
+                for (int i = 0; i < p.nk; ++i) {
+                    const int kd = p.kinds[i];
+                    if (threadIdx.x == 0) {
+                        const int f = ctl.kind_seg_first[kd], n = ctl.kind_seg_count[kd];
+                        ctl.unit_next = n ? ctl.segs[f].first : 0;
+                        ctl.unit_end = n ? ctl.segs[f + n - 1].first + ctl.segs[f + n - 1].count : 0;
+                        ctl.n_done = i + 1;
+                    }
+                    __syncthreads();
+                    run_units(p, ctl, lk, sw, vb2, tot, ztot, single, false);
+                    __syncthreads();
+                    if ((int64_t)ctl.lb > p.k) break;
+                }
+            } else {
+                if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
+                __syncthreads();
+                run_units(p, ctl, lk, sw, vb2, tot, ztot, single, cancel);
+            }
+        }
+        __syncthreads();
+        // ---- outputs ----------------------------------------------------------
+        if (threadIdx.x == 0) {
+            if (ctl.bad && p.err_out) atomicExch(p.err_out, 1);
+            int64_t lb = 0;
+            bplb_result res;
+            for (int kd = 0; kd < K_COUNT; ++kd) {
+                const u64 key = ctl.key[kd];
+                const bool ev = ctl.evaluated[kd];
+                res.best[kd] = ev ? (int64_t)(key >> 32) : 0;
+                res.arg_lambda[kd] = ev ? ctl.lo[kd] + (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu))
+                                        : ctl.lo[kd];
+                res.n_lambda[kd] = ctl.hi[kd] >= ctl.lo[kd] ? ctl.hi[kd] - ctl.lo[kd] + 1 : 0;
+                res.evals[kd] = (int64_t)ctl.evals[kd];
+                res.evaluated[kd] = ev;
+                if (ev && res.best[kd] > lb) lb = res.best[kd];
+            }
+            res.lb = lb;
+            res.exceeded = lb > p.k;
+            res.n_done = ctl.n_done;
+            int64_t et = 0;
+            for (int kd = 0; kd < K_COUNT; ++kd) et += res.evals[kd];
+            res.evals_total = et;
+            if (p.res_out) p.res_out[node] = res;
+            if (p.lb_out) p.lb_out[node] = lb;
+            if (p.ex_out) p.ex_out[node] = (uint8_t)(lb > p.k);
+            if (p.best_out)
+                for (int kd = 0; kd < K_COUNT; ++kd) p.best_out[node * K_COUNT + kd] = res.best[kd];
+            if (p.arg_out)
+                for (int kd = 0; kd < K_COUNT; ++kd) p.arg_out[node * K_COUNT + kd] = res.arg_lambda[kd];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace bplb

@@ -1,0 +1,614 @@
+// bplb_wide.cuh -- grid-wide path for one large reduced instance (cfg3-style
+// c = 1e5 single checks, cfg4-style r = 1e5 / c = 1e6 checks, and
+// dff_bound_batch).  The instance is described by global cumulative tables
+// over the weight values (L2-resident: 12 bytes per value), every SM pulls
+// warp units from one global counter, and the VB2/FS1 modular walk is cut
+// into (lambda chunk x item slice) tiles whose partial sums meet in a global
+// per-lambda accumulator.
+//
+// Launch sequence (one stream, no host round trip):
+//   wide_init     zero state, tables and accumulators (one kernel)
+//   wide_stats    per-item statistics, histogram, VB2 item compaction
+//   wide_scan_*   3-phase scan of the histogram into N<=(x), W<=(x) tables,
+//                 last block computes lambda ranges and the unit plan
+//   wide_units    all warp units (one launch per kind in PHASED mode:
+//                 the Alg. 3/4 "one launch per DFF, guard lb <= k" shape)
+//   wide_final    per-lambda bounds of item-sliced VB2/FS1 accumulators
+//   wide_finish   one warp writes the bplb_result / batch outputs
+#pragma once
+#include <algorithm>
+#include <string>
+#include "bplb_node.cuh"
+
+namespace bplb {
+
+constexpr int WT = 256;              // threads per CTA (wide kernels)
+constexpr int ISLICE = 32 * GMOD * 8; // items per modular tile (4096)
+constexpr int LLW = 128;             // lambdas per lane-lookup unit (4 x 32)
+constexpr int WIDE_MAX_SEGS = 3 * K_COUNT;
+constexpr int64_t WIDE_MAX_C = (int64_t)1 << 27;
+constexpr int SCAN_TILE = 4096;      // entries per scan block
+
+enum { T_WLOOK = 3 };  // warp-cooperative harmonic lookup: one lambda per unit
+
+struct WSeg {
+    int kind, type;
+    int64_t lo, hi;
+    int chunk;
+    int nslice;       // T_MOD: item slices per lambda chunk
+    long long first, count;
+};
+
+struct WideState {
+    NodeStats st;
+    int bad;
+    int n_vb2;
+    int64_t lo[K_COUNT], hi[K_COUNT];
+    WSeg segs[WIDE_MAX_SEGS];
+    int nseg;
+    long long nunits;
+    int kind_seg_first[K_COUNT], kind_seg_count[K_COUNT];
+    u64 key[K_COUNT];
+    unsigned long long evals[K_COUNT];
+    int evaluated[K_COUNT];
+    int lb;
+    int stop;              // PHASED: set when a completed kind exceeded k
+    int n_done;
+    long long unit_next;
+    long long unit_end;
+    int need_final;        // VB2/FS1 were item-sliced
+    int scan_blocks_done;
+};
+
+struct WideBufs {
+    WideState* state;
+    unsigned int* cnt;          // [c+2] histogram -> N<=(x) at index x+1
+    unsigned long long* wle;    // [c+2] W<=(x)
+    unsigned long long* bsum;   // [2 * nblocks] block sums for the scan
+    int* vb2;                   // [r]
+    unsigned long long* acc;    // [c+1] VB2 per-lambda D (indexed by lambda)
+    unsigned long long* pz;     // [2*101] FS1 P and Z (indexed by lambda)
+};
+
+inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
+    int64_t n = c + 2;
+    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    *nblocks_out = nb;
+    size_t b = 0;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    b += al(sizeof(WideState));
+    b += al((size_t)n * 4);
+    b += al((size_t)n * 8);
+    b += al((size_t)nb * 16);
+    b += al((size_t)std::max<int64_t>(r, 1) * 4);
+    b += al((size_t)(c + 1) * 8);
+    b += al((size_t)2 * 101 * 8);
+    return b;
+}
+
+inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
+    int64_t n = c + 2, nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    char* p = (char*)base;
+    WideBufs w;
+    w.state = (WideState*)p; p += al(sizeof(WideState));
+    w.cnt = (unsigned int*)p; p += al((size_t)n * 4);
+    w.wle = (unsigned long long*)p; p += al((size_t)n * 8);
+    w.bsum = (unsigned long long*)p; p += al((size_t)nb * 16);
+    w.vb2 = (int*)p; p += al((size_t)std::max<int64_t>(r, 1) * 4);
+    w.acc = (unsigned long long*)p; p += al((size_t)(c + 1) * 8);
+    w.pz = (unsigned long long*)p;
+    return w;
+}
+
+// -------------------------------------------------------------------------
+__global__ void wide_init(WideBufs b, int64_t c) {
+    const int64_t n = c + 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t i = i0; i < n; i += stride) { b.cnt[i] = 0; }
+    for (int64_t i = i0; i < c + 1; i += stride) b.acc[i] = 0;
+    for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
+    if (i0 == 0) {
+        WideState* s = b.state;
+        memset(s, 0, sizeof(WideState));
+    }
+}
+
+__global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restrict__ w, int64_t r,
+                                                 int64_t c) {
+    int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
+    long long l_W = 0, l_Vs = 0, l_Vm = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r; i += stride) {
+        const int x = w[i];
+        if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
+        l_max = max(l_max, x);
+        l_W += x;
+        if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
+        else if (2 * (int64_t)x == c) l_e++;
+        else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
+        atomicAdd(&b.cnt[x + 1], 1u);
+        if (2 * (int64_t)x != c && x < c) b.vb2[atomicAdd(&b.state->n_vb2, 1)] = x;
+    }
+    l_max = __reduce_max_sync(0xffffffffu, (unsigned)l_max);
+    l_bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)l_bad);
+    l_s = __reduce_add_sync(0xffffffffu, l_s);
+    l_e = __reduce_add_sync(0xffffffffu, l_e);
+    l_b = __reduce_add_sync(0xffffffffu, l_b);
+    l_f = __reduce_add_sync(0xffffffffu, l_f);
+    l_W = (long long)warp_sum_u64((u64)l_W);
+    l_Vs = (long long)warp_sum_u64((u64)l_Vs);
+    l_Vm = (long long)warp_sum_u64((u64)l_Vm);
+    if ((threadIdx.x & 31) == 0) {
+        NodeStats* st = &b.state->st;
+        atomicMax(&st->maxw, l_max);
+        if (l_bad) atomicExch(&b.state->bad, 1);
+        if (l_s) atomicAdd(&st->n_small, l_s);
+        if (l_e) atomicAdd(&st->n_eq, l_e);
+        if (l_b) atomicAdd(&st->n_big, l_b);
+        if (l_f) atomicAdd(&st->n_full, l_f);
+        atomicAdd((unsigned long long*)&st->W, (unsigned long long)l_W);
+        atomicAdd((unsigned long long*)&st->Vs, (unsigned long long)l_Vs);
+        atomicAdd((unsigned long long*)&st->Vm, (unsigned long long)l_Vm);
+    }
+}
+
+// Block-level inclusive scan of (count, count*(i-1)) over one SCAN_TILE tile.
+__device__ __forceinline__ void tile_sums(const unsigned int* cnt, int64_t n, int64_t t0,
+                                          unsigned long long* sc, unsigned long long* sw) {
+    unsigned long long a = 0, bw = 0;
+    for (int64_t i = t0 + threadIdx.x; i < min(n, t0 + SCAN_TILE); i += WT) {
+        unsigned long long x = cnt[i];
+        a += x;
+        bw += x * (unsigned long long)(i - 1);
+    }
+    *sc = a;
+    *sw = bw;
+}
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* red) {
+    v = warp_sum_u64(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (WT / 32) ? red[threadIdx.x] : 0;
+        t = warp_sum_u64(t);
+    }
+    __syncthreads();
+    return t;  // valid in warp 0
+}
+
+__global__ void __launch_bounds__(WT) wide_scan_reduce(WideBufs b, int64_t c) {
+    __shared__ unsigned long long red[WT / 32];
+    const int64_t n = c + 2;
+    unsigned long long sc, sw;
+    tile_sums(b.cnt, n, (int64_t)blockIdx.x * SCAN_TILE, &sc, &sw);
+    unsigned long long tc = block_sum_u64(sc, red);
+    unsigned long long tw = block_sum_u64(sw, red);
+    if (threadIdx.x == 0) {
+        b.bsum[2 * blockIdx.x] = tc;
+        b.bsum[2 * blockIdx.x + 1] = tw;
+    }
+}
+
+// Thread 0 of every block serially prefix-sums the block totals before it
+// (nblocks <= 65K at c = 2^27; cheap relative to the tile), then the block
+// writes its tile with a warp-level scan.
+__global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
+    __shared__ unsigned long long carry_c[WT / 32 + 1], carry_w[WT / 32 + 1];
+    __shared__ unsigned long long base_c, base_w;
+    const int64_t n = c + 2;
+    if (threadIdx.x == 0) {
+        unsigned long long a = 0, bw = 0;
+        for (int j = 0; j < (int)blockIdx.x; ++j) { a += b.bsum[2 * j]; bw += b.bsum[2 * j + 1]; }
+        base_c = a;
+        base_w = bw;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long rc = base_c, rw = base_w;
+    const int64_t t0 = (int64_t)blockIdx.x * SCAN_TILE;
+    const int64_t t1 = min(n, t0 + SCAN_TILE);
+    for (int64_t s = t0; s < t1; s += WT) {
+        const int64_t i = s + threadIdx.x;
+        unsigned long long x = i < t1 ? b.cnt[i] : 0;
+        unsigned long long y = x * (unsigned long long)(i - 1);
+        // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long xo = __shfl_up_sync(0xffffffffu, x, o);
+            unsigned long long yo = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) { x += xo; y += yo; }
+        }
+        if (lane == 31) { carry_c[warp + 1] = x; carry_w[warp + 1] = y; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry_c[0] = 0; carry_w[0] = 0;
+            for (int j = 1; j <= WT / 32; ++j) { carry_c[j] += carry_c[j - 1]; carry_w[j] += carry_w[j - 1]; }
+        }
+        __syncthreads();
+        if (i < t1) {
+            b.cnt[i] = (unsigned int)(rc + carry_c[warp] + x);
+            b.wle[i] = rw + carry_w[warp] + y;
+        }
+        rc += carry_c[WT / 32];
+        rw += carry_w[WT / 32];
+        __syncthreads();
+    }
+}
+
+// Lambda ranges and the unit plan (one thread).
+__global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int use_range,
+                          int64_t lo0, int64_t hi0, int kinds0, int kinds1, int kinds2, int kinds3,
+                          int kinds4, int kinds5, int phased) {
+    WideState* s = b.state;
+    const int kinds[K_COUNT] = {kinds0, kinds1, kinds2, kinds3, kinds4, kinds5};
+    bplb_stats_finish(&s->st, c);
+    s->st.r = s->st.n_small + s->st.n_eq + s->st.n_big;
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        int64_t lo, hi;
+        bplb_domain(kd, c, &lo, &hi);
+        if (kd == K_VB2) hi = bplb_vb2_hi(c, s->st.r, s->st.maxw);
+        bool in = false;
+        for (int i = 0; i < nk; ++i) in |= kinds[i] == kd;
+        if (use_range) { lo = lo0; hi = hi0; }
+        if (!in) hi = lo - 1;
+        s->lo[kd] = lo;
+        s->hi[kd] = hi;
+        s->kind_seg_count[kd] = 0;
+        s->kind_seg_first[kd] = 0;
+    }
+    s->nseg = 0;
+    s->nunits = 0;
+    s->need_final = 0;
+    if (s->bad) return;
+    const NodeStats& st = s->st;
+    auto push = [&](int kind, int type, int64_t a, int64_t z, int chunk, int nslice) {
+        if (z < a) return;
+        WSeg& g = s->segs[s->nseg++];
+        g.kind = kind; g.type = type; g.lo = a; g.hi = z; g.chunk = chunk; g.nslice = nslice;
+        g.first = s->nunits;
+        g.count = ((z - a + chunk) / chunk) * nslice;
+        s->nunits += g.count;
+        s->kind_seg_count[kind]++;
+    };
+    // Heavy modular units first in concurrent mode (longest-processing-time
+    // order); kind order in PHASED mode.
+    int order[K_COUNT];
+    int no = 0;
+    if (!phased) {
+        for (int i = 0; i < nk; ++i) if (kinds[i] == K_VB2 || kinds[i] == K_FS1) order[no++] = kinds[i];
+        for (int i = 0; i < nk; ++i) if (!(kinds[i] == K_VB2 || kinds[i] == K_FS1)) order[no++] = kinds[i];
+    } else {
+        for (int i = 0; i < nk; ++i) order[no++] = kinds[i];
+    }
+    for (int i = 0; i < no; ++i) {
+        const int kd = order[i];
+        const int64_t lo = s->lo[kd], hi = s->hi[kd];
+        s->kind_seg_first[kd] = s->nseg;
+        if (hi < lo) continue;
+        switch (kd) {
+        case K_MT: case K_RAD2: push(kd, T_LOOKUP, lo, hi, LLW, 1); break;
+        case K_FS1: case K_VB2: {
+            const int64_t items = kd == K_VB2 ? s->n_vb2 : st.r;
+            int nsl = (int)((items + ISLICE - 1) / ISLICE);
+            if (nsl < 1) nsl = 1;
+            if (nsl > 1) s->need_final = 1;
+            push(kd, T_MOD, lo, hi, LMOD, nsl);
+            break;
+        }
+        default: {
+            // CCM1 / BJ1: one warp per lambda while the harmonic loop is long
+            const int64_t span = kd == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
+            int64_t sp = span / 64 + 1;
+            if (sp < lo) sp = lo;
+            if (sp > hi + 1) sp = hi + 1;
+            push(kd, T_WLOOK, lo, sp - 1, 1, 1);
+            push(kd, T_LOOKUP, sp, hi, LLW, 1);
+        }
+        }
+    }
+}
+
+__device__ __forceinline__ int find_wseg(const WideState* s, long long u) {
+    int si = 0;
+    while (si + 1 < s->nseg && s->segs[si + 1].first <= u) ++si;
+    return si;
+}
+
+// One warp unit of the wide path.
+__device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkTableG& lk,
+                          long long u, u64* tot, u64* ztot) {
+    const int lane = threadIdx.x & 31;
+    const WSeg sg = s->segs[find_wseg(s, u)];
+    const int kind = sg.kind;
+    const int64_t c = p.c;
+    const NodeStats& st = s->st;
+    const long long rel = u - sg.first;
+    int64_t* lam_out = p.lam_out;
+    int64_t wmax = -1;
+    int64_t n_eval = 0;
+    if (sg.type == T_LOOKUP) {
+        const int64_t lam_a = sg.lo + rel * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        n_eval = lam_b - lam_a + 1;
+        for (int64_t l0 = lam_a; l0 <= lam_b; l0 += 32) {
+            const int64_t lam = l0 + lane;
+            const bool valid = lam <= lam_b;
+            int64_t S = 0;
+            if (valid) {
+                switch (kind) {
+                case K_MT: S = bplb_mt_sum(lk, c, st.r, lam); break;
+                case K_RAD2: S = bplb_rad2_sum(lk, c, st.r, lam); break;
+                case K_CCM1: S = bplb_ccm1_sum(lk, st, c, lam); break;
+                default: S = bplb_bj1_sum(lk, st, c, lam); break;
+                }
+            }
+            int64_t bd = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+            int64_t m = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
+            wmax = m > wmax ? m : wmax;
+        }
+    } else if (sg.type == T_WLOOK) {
+        const int64_t lam = sg.lo + rel;
+        n_eval = 1;
+        int64_t S;
+        if (kind == K_CCM1) {
+            int64_t part = bplb_ccm1_part(lk, st, c, lam, 1 + lane, 32);
+            part = (int64_t)warp_sum_u64((u64)part);
+            S = bplb_ccm1_from_part(st, c, lam, part);
+        } else {
+            int64_t fl, rem;
+            bplb_bj1_part(lk, st, c, lam, lane, 32, &fl, &rem);
+            fl = (int64_t)warp_sum_u64((u64)fl);
+            rem = (int64_t)warp_sum_u64((u64)rem);
+            S = bplb_bj1_from_parts(c, lam, fl, rem);
+        }
+        int64_t bd = bplb_bound(S, bplb_fc(kind, c, lam));
+        wmax = emit_warp(lane == 0, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
+    } else {  // T_MOD
+        const long long chunk = rel / sg.nslice;
+        const int slice = (int)(rel % sg.nslice);
+        const int64_t lam_a = sg.lo + chunk * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        const int L = (int)(lam_b - lam_a + 1);
+        const int n_items = kind == K_VB2 ? s->n_vb2 : st.r;
+        const int* items = kind == K_VB2 ? b.vb2 : p.w;
+        const int i0 = slice * ISLICE, i1 = min(n_items, i0 + ISLICE);
+        const int warp = threadIdx.x >> 5;
+        u64* t = tot + warp * LMOD;
+        u64* z = ztot + warp * LMOD;
+        for (int j = lane; j < LMOD; j += kWarp) { t[j] = 0; z[j] = 0; }
+        __syncwarp();
+        const uint32_t c32 = (uint32_t)c;
+        const u64 cinv = bplb_cinv(c32);
+        const bool wide = c >= (1 << 23);
+        if (kind == K_VB2) {
+            if (wide) mod_walk<false, true>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
+            else mod_walk<false, false>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
+        } else {
+            if (wide) mod_walk<true, true>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
+            else mod_walk<true, false>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
+        }
+        __syncwarp();
+        if (sg.nslice > 1) {
+            for (int j = lane; j < L; j += kWarp) {
+                if (kind == K_VB2) atomicAdd(&b.acc[lam_a + j], t[j]);
+                else { atomicAdd(&b.pz[lam_a + j], t[j]); atomicAdd(&b.pz[101 + lam_a + j], z[j]); }
+            }
+            n_eval = slice == 0 ? L : 0;  // count each lambda once
+        } else {
+            n_eval = L;
+            for (int j0 = 0; j0 < L; j0 += kWarp) {
+                const int j = j0 + lane;
+                const bool valid = j < L;
+                const int64_t lam = lam_a + j;
+                int64_t S = 0;
+                if (valid)
+                    S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j]) : bplb_fs1_sum(st, lam, t[j], z[j]);
+                int64_t bd = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+                int64_t m = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
+                wmax = m > wmax ? m : wmax;
+            }
+        }
+    }
+    if (lane == 0) {
+        if (n_eval) atomicAdd(&s->evals[kind], (unsigned long long)n_eval);
+        s->evaluated[kind] = 1;
+        if (wmax >= 0) atomicMax(&s->lb, (int)wmax);
+    }
+}
+
+// Persistent warp-unit kernel.  phase_kind >= 0 restricts to that kind's
+// segments (PHASED mode) and applies the Alg. 4 entry guard lb <= k.
+__global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phase_kind) {
+    __shared__ u64 tot[(WT / 32) * LMOD];
+    __shared__ u64 ztot[(WT / 32) * LMOD];
+    __shared__ long long u_begin, u_end;
+    __shared__ int skip;
+    WideState* s = b.state;
+    if (threadIdx.x == 0) {
+        skip = 0;
+        if (s->bad) skip = 1;
+        if (phase_kind >= 0) {
+            if (s->stop) skip = 1;
+            const int f = s->kind_seg_first[phase_kind], n = s->kind_seg_count[phase_kind];
+            u_begin = n ? s->segs[f].first : 0;
+            u_end = n ? s->segs[f + n - 1].first + s->segs[f + n - 1].count : 0;
+        } else {
+            u_begin = 0;
+            u_end = s->nunits;
+        }
+    }
+    __syncthreads();
+    if (skip) return;
+    const LkTableG lk{b.cnt, b.wle, p.c};
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && phase_kind < 0;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        long long u = 0;
+        if (lane == 0) u = u_begin + atomicAdd((unsigned long long*)&s->unit_next, 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= u_end) break;
+        if (cancel && (int64_t)(*(volatile int*)&s->lb) > p.k) continue;
+        wide_unit(p, b, s, lk, u, tot, ztot);
+    }
+}
+
+// Reset the unit counter between phased launches and record the kind.
+__global__ void wide_phase_begin(WideBufs b, int idx) {
+    WideState* s = b.state;
+    s->unit_next = 0;
+    if (!s->stop) s->n_done = idx + 1;
+}
+
+// Per-lambda bounds of item-sliced modular kinds.
+__global__ void __launch_bounds__(WT) wide_final(KParams p, WideBufs b, int only_kind) {
+    WideState* s = b.state;
+    if (s->bad || !s->need_final) return;
+    const int mod_kinds[2] = {K_FS1, K_VB2};
+    for (int mi = 0; mi < 2; ++mi) {
+        const int kd = mod_kinds[mi];
+        if (only_kind >= 0 && only_kind != kd) continue;
+        if (only_kind >= 0 && s->stop) return;
+        const int64_t lo = s->lo[kd], hi = s->hi[kd];
+        if (hi < lo) continue;
+        const int64_t items = kd == K_VB2 ? s->n_vb2 : s->st.r;
+        if (items <= ISLICE) continue;  // finished inside the units
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        int64_t wmax = -1;
+        for (int64_t l0 = lo + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); l0 <= hi;
+             l0 += stride) {
+            const int64_t lam = l0 + (threadIdx.x & 31);
+            const bool valid = lam <= hi;
+            int64_t S = 0;
+            if (valid)
+                S = kd == K_VB2 ? bplb_vb2_sum(s->st, p.c, lam, b.acc[lam])
+                                : bplb_fs1_sum(s->st, lam, b.pz[lam], b.pz[101 + lam]);
+            int64_t bd = valid ? bplb_bound(S, bplb_fc(kd, p.c, lam)) : 0;
+            int64_t m = emit_warp(valid, lam, bd, lo, &s->key[kd], p.lam_out, p.out_lo, p.out_hi);
+            wmax = m > wmax ? m : wmax;
+        }
+        if ((threadIdx.x & 31) == 0 && wmax >= 0) atomicMax(&s->lb, (int)wmax);
+    }
+}
+
+// After each phased kind: stop further kinds once lb > k (bounds.py:523-525).
+__global__ void wide_phase_end(WideBufs b, int64_t k) {
+    WideState* s = b.state;
+    if ((int64_t)s->lb > k) s->stop = 1;
+}
+
+__global__ void wide_finish(KParams p, WideBufs b, int phased) {
+    if (threadIdx.x != 0) return;
+    WideState* s = b.state;
+    if (s->bad && p.err_out) atomicExch(p.err_out, 1);
+    bplb_result res;
+    int64_t lb = 0;
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        const u64 key = s->key[kd];
+        const bool ev = s->evaluated[kd];
+        res.best[kd] = ev ? (int64_t)(key >> 32) : 0;
+        res.arg_lambda[kd] = ev ? s->lo[kd] + (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu)) : s->lo[kd];
+        res.n_lambda[kd] = s->hi[kd] >= s->lo[kd] ? s->hi[kd] - s->lo[kd] + 1 : 0;
+        res.evals[kd] = (int64_t)s->evals[kd];
+        res.evaluated[kd] = ev;
+        if (ev && res.best[kd] > lb) lb = res.best[kd];
+    }
+    res.lb = lb;
+    res.exceeded = lb > p.k;
+    res.n_done = phased ? s->n_done : p.nk;
+    int64_t et = 0;
+    for (int kd = 0; kd < K_COUNT; ++kd) et += res.evals[kd];
+    res.evals_total = et;
+    if (p.res_out) p.res_out[0] = res;
+    if (p.lb_out) p.lb_out[0] = lb;
+    if (p.ex_out) p.ex_out[0] = (uint8_t)(lb > p.k);
+    if (p.best_out) for (int kd = 0; kd < K_COUNT; ++kd) p.best_out[kd] = res.best[kd];
+    if (p.arg_out) for (int kd = 0; kd < K_COUNT; ++kd) p.arg_out[kd] = res.arg_lambda[kd];
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+inline std::string& wide_err_ref() {
+    static thread_local std::string e;
+    return e;
+}
+inline const std::string& wide_error() { return wide_err_ref(); }
+
+// Work heuristic: the grid-wide path pays ~8 launches; use it when the node
+// does not fit the node-resident kernel or when one CTA would take longer
+// than a few tens of microseconds (canonical cells > ~2e6).
+inline bool wide_preferred(int64_t r, int64_t c) {
+    const bool table = c <= TABLE_MAX_C;
+    if (r > (table ? 16384 : 8192)) return true;
+    const int64_t cells = r * (3 * c);  // ~ sum of lambda ranges x items
+    return cells > 2000000 && c <= WIDE_MAX_C;
+}
+
+inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int64_t* launches,
+                      const KParams& p0, int64_t r, void*) {
+    KParams p = p0;
+    const int64_t c = p.c;
+    if (c > WIDE_MAX_C) {
+        wide_err_ref() = "capacity above the grid-wide envelope (2^27) for this instance size";
+        return BPLB_ERANGE;
+    }
+    int64_t nb;
+    const size_t need = wide_bytes(r, c, &nb);
+    if (need > *cap) {
+        if (*buf) cudaFree(*buf);
+        *buf = nullptr;
+        *cap = 0;
+        if (cudaMalloc(buf, need) != cudaSuccess) {
+            wide_err_ref() = "cudaMalloc failed (wide path)";
+            return BPLB_ENOMEM;
+        }
+        *cap = need;
+    }
+    WideBufs b = wide_carve(*buf, r, c);
+    const bool phased = p.flags & BPLB_F_PHASED;
+    int ks[K_COUNT] = {0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < p.nk; ++i) ks[i] = p.kinds[i];
+    int64_t lo0 = p.use_range ? p.rng_lo[p.kinds[0]] : 0;
+    int64_t hi0 = p.use_range ? p.rng_hi[p.kinds[0]] : 0;
+    const int g_init = (int)std::min<int64_t>((c + 2 + WT - 1) / WT, (int64_t)num_sms * 8);
+    wide_init<<<std::max(g_init, 1), WT, 0, st>>>(b, c);
+    const int g_stats = (int)std::max<int64_t>(1, std::min<int64_t>((r + WT - 1) / WT, (int64_t)num_sms * 4));
+    wide_stats<<<g_stats, WT, 0, st>>>(b, p.w, r, c);
+    wide_scan_reduce<<<(unsigned)nb, WT, 0, st>>>(b, c);
+    wide_scan_apply<<<(unsigned)nb, WT, 0, st>>>(b, c);
+    wide_plan<<<1, 1, 0, st>>>(b, c, p.nk, nullptr, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3],
+                               ks[4], ks[5], phased ? 1 : 0);
+    *launches += 5;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_units, WT, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = per_sm * num_sms;
+    const int g_fin = num_sms * 2;
+    if (phased) {
+        for (int i = 0; i < p.nk; ++i) {
+            wide_phase_begin<<<1, 1, 0, st>>>(b, i);
+            wide_units<<<grid, WT, 0, st>>>(p, b, p.kinds[i]);
+            wide_final<<<g_fin, WT, 0, st>>>(p, b, p.kinds[i]);
+            wide_phase_end<<<1, 1, 0, st>>>(b, p.k);
+            *launches += 4;
+        }
+    } else {
+        wide_units<<<grid, WT, 0, st>>>(p, b, -1);
+        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
+        *launches += 2;
+    }
+    wide_finish<<<1, 32, 0, st>>>(p, b, phased ? 1 : 0);
+    *launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        wide_err_ref() = std::string("wide path launch: ") + cudaGetErrorString(e);
+        return BPLB_ECUDA;
+    }
+    return 0;
+}
+
+}  // namespace bplb

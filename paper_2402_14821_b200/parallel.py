@@ -1,0 +1,148 @@
+"""Drop-in mirror of the reference's parallel engine, GPU-backed.
+
+Reference: /root/reference/pkg/src/binpack/parallel.py.  ``lower_bound_par``
+and ``ParallelBoundEngine`` keep their signatures and contracts
+(parallel.py:122-174): the decision bit equals the
+sequential engine's, the value equals the completed sweep whenever the bound
+stays within budget, ``cancellation=False`` evaluates every grid point, and
+with cancellation work units that observe ``lb > k`` are skipped (the
+in-kernel form of Alg. 4's guard ``if lb <= k``).  ``workers``
+is accepted and validated for compatibility; the parallelism is the GPU's.
+
+``GpuBoundEngine`` is the ``BoundEngine`` callable (propagator.py:40) a
+search plugs in; ``ParallelBoundEngine`` is an alias-compatible subclass.
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+from typing import Sequence
+
+from . import _native
+from .bounds import DEFAULT_DFF_ORDER, BoundResult, DffKind, _kind, _result_seq
+from .instances import as_reduced
+
+__all__ = ["SharedMax", "lower_bound_par", "GpuBoundEngine", "ParallelBoundEngine",
+           "default_workers", "CHUNK"]
+
+#: Reference cancellation granularity (parallel.py:33); the GPU checks its
+#: guard once per work unit (32-128 lambdas).
+CHUNK = 64
+
+
+def default_workers() -> int:
+    return os.cpu_count() or 1
+
+
+class SharedMax:
+    """Thread-safe non-decreasing maximum (parallel.py:40-55).  The GPU
+    engine's equivalent is the in-kernel atomicMax on the node's bound."""
+
+    def __init__(self, value: int = 0):
+        self._value = value
+        self._lock = threading.Lock()
+
+    def offer(self, value: int) -> int:
+        with self._lock:
+            if value > self._value:
+                self._value = value
+            return self._value
+
+    def get(self) -> int:
+        with self._lock:
+            return self._value
+
+
+def _result_par(res: _native.BplbResult, kinds: Sequence[DffKind], k: int) -> BoundResult:
+    # parallel.py:105-119: kinds with at least one evaluated unit, in kinds
+    # order; empty ranges never appear.
+    out = BoundResult(lb=0, evals=int(res.evals_total))
+    for kind in kinds:
+        kid = kind.id
+        if res.evaluated[kid]:
+            best = int(res.best[kid])
+            out.per_dff[kind] = best
+            out.arg[kind] = int(res.arg_lambda[kid])
+            if best > out.lb:
+                out.lb = best
+    out.exceeded_k = out.lb > k
+    return out
+
+
+def _run_par(engine: _native.Engine, red, k: int, kinds, cancellation: bool) -> BoundResult:
+    kinds = [_kind(x) for x in kinds]
+    c, w = as_reduced(red)
+    if not kinds:
+        return BoundResult(lb=0, exceeded_k=0 > k)
+    res = engine.check(w, c, k, [x.id for x in kinds], _native.F_CANCEL if cancellation else 0)
+    return _result_par(res, kinds, k)
+
+
+def lower_bound_par(red, k: int, kinds: Sequence = DEFAULT_DFF_ORDER, workers: int = 1,
+                    cancellation: bool = True) -> BoundResult:
+    """Parallel counterpart of the sequential sweep (parallel.py:122-137)."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    return _run_par(_native.default_engine(), red, k, kinds, cancellation)
+
+
+class GpuBoundEngine:
+    """Reusable B200 bound engine: ``engine(red, k) -> BoundResult``.
+
+    ``mode="par"`` (default) has lower_bound_par semantics (concurrent
+    kinds, cancellation guard); ``mode="seq"`` has lower_bound_seq
+    semantics (kinds in order, early exit).  Owns one libbplb engine (CUDA
+    stream + resident buffers) on ``device``; ``close()`` releases it.
+    """
+
+    def __init__(self, kinds: Sequence = DEFAULT_DFF_ORDER, device: int | None = None,
+                 cancellation: bool = True, mode: str = "par"):
+        self.kinds = tuple(_kind(x) for x in kinds)
+        self.cancellation = cancellation
+        if mode not in ("par", "seq"):
+            raise ValueError("mode must be 'par' or 'seq'")
+        self.mode = mode
+        self.device = int(os.environ.get("BPLB_DEVICE", "0")) if device is None else int(device)
+        self._engine: _native.Engine | None = None
+        self._lock = threading.Lock()
+
+    def _eng(self) -> _native.Engine:
+        with self._lock:
+            if self._engine is None:
+                self._engine = _native.Engine(self.device)
+            return self._engine
+
+    def __call__(self, red, k: int) -> BoundResult:
+        eng = self._eng()
+        if self.mode == "seq":
+            kinds = list(self.kinds)
+            c, w = as_reduced(red)
+            if not kinds:
+                return BoundResult(lb=0, exceeded_k=0 > k)
+            res = eng.check(w, c, k, [x.id for x in kinds], _native.F_PHASED)
+            return _result_seq(res, kinds, k)
+        return _run_par(eng, red, k, self.kinds, self.cancellation)
+
+    def close(self) -> None:
+        with self._lock:
+            if self._engine is not None:
+                self._engine.close()
+                self._engine = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+
+class ParallelBoundEngine(GpuBoundEngine):
+    """Signature-compatible stand-in for parallel.py:140-174."""
+
+    def __init__(self, kinds: Sequence = DEFAULT_DFF_ORDER, workers: int | None = None,
+                 cancellation: bool = True):
+        self.workers = workers if workers is not None else default_workers()
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        super().__init__(kinds=kinds, cancellation=cancellation, mode="par")

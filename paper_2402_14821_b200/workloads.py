@@ -1,0 +1,150 @@
+"""Synthetic workloads of BASELINE.json's configs (definitions: SURVEY.md 8(d)).
+
+  cfg1  Falkenauer-U-shaped: r=120, w ~ U{20..100}, c=150 (rng(0))
+  cfg2  Scholl-1-shaped: n=500, w ~ U{20..100}, c=150 (seed 0); search-node
+        residual states (seed 1), bins k = L2(root) + 2
+  cfg3  AI/ANI-shaped: n=1000, c=1e5, triplets in (c/4, c/2) summing to c
+        (333 triplets + 1 extra item, seed 0); cfg3u: U{c/4+1..c/2-1} variant
+  cfg4  large: r=1e5, w ~ U{1..1e6}, c=1e6 (rng(0))
+  cfg5  search-node states of the cfg3 instance (seed 2), k = 334 bins
+
+Search-node generator (one node): draw depth d ~ U{0..n}; the d heaviest
+items (stable by index) are each committed to a uniformly random bin among
+those with load + w <= c (or stay open if none fits); the reduced instance is
+the open weights in item order followed by the positive bin loads in bin
+order -- exactly the layout of reduce_packing (instances.py:262-282).
+Nodes are generated in independent blocks (seeded by (seed, block)) so a
+rank can generate only its own shard.
+
+All workload code is data generation, not the bound path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = ["cfg1", "cfg2_instance", "cfg3", "cfg3u", "cfg4", "node_batch", "l2_host", "CONFIGS"]
+
+BLOCK = 1024
+
+
+def cfg1() -> tuple[int, np.ndarray]:
+    return 150, np.random.default_rng(0).integers(20, 101, 120).astype(np.int32)
+
+
+def cfg2_instance() -> tuple[int, np.ndarray]:
+    return 150, np.random.default_rng(0).integers(20, 101, 500).astype(np.int32)
+
+
+def cfg3(seed: int = 0, n: int = 1000, c: int = 100_000) -> tuple[int, np.ndarray]:
+    rng = np.random.default_rng(seed)
+    q = c // 4
+    items = []
+    for _ in range(n // 3):
+        a = int(rng.integers(q + 2, c // 2 - 1))
+        b_lo = max(q + 1, c // 2 - a + 1)
+        b_hi = min(c // 2 - 1, 3 * q - a - 1)
+        b = int(rng.integers(b_lo, b_hi + 1))
+        items += [a, b, c - a - b]
+    while len(items) < n:
+        items.append(int(rng.integers(q + 1, c // 2)))
+    w = np.array(items, dtype=np.int32)
+    rng.shuffle(w)
+    return c, w
+
+
+def cfg3u(seed: int = 0, n: int = 1000, c: int = 100_000) -> tuple[int, np.ndarray]:
+    rng = np.random.default_rng(seed)
+    return c, rng.integers(c // 4 + 1, c // 2, n).astype(np.int32)
+
+
+def cfg4() -> tuple[int, np.ndarray]:
+    return 1_000_000, np.random.default_rng(0).integers(1, 10**6 + 1, 10**5).astype(np.int32)
+
+
+def l2_host(c: int, w: np.ndarray) -> int:
+    """Martello-Toth L2 of a root instance (generator helper only: it picks
+    the bin count of the synthetic search nodes).  max over lambda of the
+    f_MT bound via prefix sums."""
+    w = np.asarray(w, dtype=np.int64)
+    if w.size == 0:
+        return 0
+    cnt = np.bincount(w, minlength=c + 1)
+    n_le = np.concatenate([[0], np.cumsum(cnt)])
+    w_le = np.concatenate([[0], np.cumsum(cnt * np.arange(c + 1))])
+    lam = np.arange(0, (c + 1) // 2 + 1, dtype=np.int64)
+    idx = lambda v: np.clip(v, -1, c) + 1  # noqa: E731
+    s = c * (w.size - n_le[idx(c - lam)]) + w_le[idx(c - lam)] - w_le[idx(lam - 1)]
+    return int(((s + c - 1) // c).max())
+
+
+def _node_block(w: np.ndarray, c: int, k: int, rng: np.random.Generator, nb: int):
+    n = w.size
+    order = np.argsort(-w.astype(np.int64), kind="stable")
+    ws = w[order].astype(np.int64)
+    d = rng.integers(0, n + 1, nb)
+    loads = np.zeros((nb, k), dtype=np.int64)
+    assign_sorted = np.full((nb, n), -1, dtype=np.int64)
+    for i in range(n):
+        rows = np.nonzero(d > i)[0]
+        if rows.size == 0:
+            break
+        fits = loads[rows] + ws[i] <= c
+        cnt = fits.sum(axis=1)
+        pick = (rng.random(rows.size) * cnt).astype(np.int64)
+        cs = np.cumsum(fits, axis=1)
+        j = np.argmax(cs > pick[:, None], axis=1)
+        ok = cnt > 0
+        rr, jj = rows[ok], j[ok]
+        loads[rr, jj] += ws[i]
+        assign_sorted[rr, i] = jj
+    assign = np.empty_like(assign_sorted)
+    assign[:, order] = assign_sorted
+    out = []
+    for b in range(nb):
+        open_w = w[assign[b] < 0]
+        ld = loads[b][loads[b] > 0]
+        out.append(np.concatenate([open_w.astype(np.int64), ld]).astype(np.int32))
+    return out
+
+
+def node_batch(w: np.ndarray, c: int, k: int, n_nodes: int, seed: int, first_node: int = 0):
+    """CSR (weights int32, offsets int64) of search-node states
+    [first_node, first_node + n_nodes) of the generator stream ``seed``."""
+    nodes = []
+    b0 = first_node // BLOCK
+    b1 = (first_node + n_nodes + BLOCK - 1) // BLOCK
+    for b in range(b0, b1):
+        rng = np.random.default_rng([seed, b])
+        blk = _node_block(w, c, k, rng, BLOCK)
+        lo = max(first_node, b * BLOCK) - b * BLOCK
+        hi = min(first_node + n_nodes, (b + 1) * BLOCK) - b * BLOCK
+        nodes.extend(blk[lo:hi])
+    lens = np.fromiter((x.size for x in nodes), dtype=np.int64, count=len(nodes))
+    off = np.zeros(len(nodes) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    flat = np.concatenate(nodes) if nodes else np.zeros(0, dtype=np.int32)
+    return flat.astype(np.int32), off
+
+
+def cfg2_nodes(n_nodes: int = 10_000, first_node: int = 0):
+    c, w = cfg2_instance()
+    k = l2_host(c, w) + 2
+    flat, off = node_batch(w, c, k, n_nodes, seed=1, first_node=first_node)
+    return c, k, flat, off
+
+
+def cfg5_nodes(n_nodes: int = 1_000_000, first_node: int = 0):
+    c, w = cfg3()
+    k = 334
+    flat, off = node_batch(w, c, k, n_nodes, seed=2, first_node=first_node)
+    return c, k, flat, off
+
+
+CONFIGS = {
+    "cfg1": "Falkenauer-U-shaped synthetic instance: 120 items, sizes U[20,100], capacity 150",
+    "cfg2": "Scholl-1-shaped instance: 500 items, capacity 150, batch of 10k search-node residual states",
+    "cfg3": "AI/ANI-shaped hard instance: 1000 items, capacity 1e5",
+    "cfg4": "large instance: 1e5 items, capacity 1e6, single check",
+    "cfg5": "batched search-node sweep of the 1000-item cfg3 instance",
+}

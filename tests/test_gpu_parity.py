@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI / drop-in API) against the
+golden vectors recorded from the reference and against the pinned C oracle
+on fresh seeded inputs.  Bit-exact equality everywhere (all integer)."""
+
+from __future__ import annotations
+
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_2402_14821_b200 as G
+from paper_2402_14821_b200 import DffKind, ReducedInstance, workloads as W
+from conftest import GOLDEN, random_reduced_pair
+
+pytestmark = pytest.mark.gpu
+KINDS = ("MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1")
+
+
+@pytest.fixture(scope="module")
+def small():
+    return np.load(os.path.join(GOLDEN, "small.npz"))
+
+
+@pytest.fixture(scope="module")
+def configs():
+    return np.load(os.path.join(GOLDEN, "configs.npz"))
+
+
+def _case(small, i):
+    off = small["offsets"]
+    return int(small["c"][i]), tuple(int(x) for x in small["weights"][off[i]:off[i + 1]])
+
+
+def test_small_vectors_golden(small):
+    meta, vals = small["vec_meta"], small["vec_vals"]
+    for case, kid, lo, hi, o in meta:
+        c, w = _case(small, case)
+        red = ReducedInstance(c, w)
+        got = G.dff_bound_batch(DffKind[KINDS[kid]], red, int(lo), int(hi))
+        np.testing.assert_array_equal(got, vals[o:o + hi - lo + 1], err_msg=f"case {case} {KINDS[kid]} c={c} w={w}")
+
+
+def test_small_seq_golden(small):
+    orders = json.loads(str(small["orders"]))
+    for row in small["seq_rows"]:
+        case, k, oi, lb, ex, evals, nd = (int(x) for x in row[:7])
+        per = [int(x) for x in row[7:7 + nd]]
+        c, w = _case(small, case)
+        kinds = [DffKind[KINDS[i]] for i in orders[oi]]
+        res = G.lower_bound_seq(ReducedInstance(c, w), k, kinds)
+        assert (res.lb, res.exceeded_k, res.evals) == (lb, bool(ex), evals), (case, k, oi)
+        assert list(res.per_dff) == kinds[:nd]
+        assert list(res.per_dff.values()) == per
+
+
+def test_small_par_golden(small):
+    for row in small["par_rows"]:
+        case, lb, evals, mask = (int(x) for x in row[:4])
+        c, w = _case(small, case)
+        res = G.lower_bound_par(ReducedInstance(c, w), 5, workers=1, cancellation=False)
+        assert res.lb == lb and res.evals == evals
+        want = {DffKind[KINDS[i]]: int(row[4 + i]) for i in range(6) if mask >> i & 1}
+        assert res.per_dff == want
+
+
+def test_batch_matches_single(small):
+    """All golden small cases as one CSR batch: per-node best == singles."""
+    n = len(small["c"])
+    # batch API needs one capacity: group by c
+    by_c: dict[int, list[int]] = {}
+    for i in range(n):
+        by_c.setdefault(int(small["c"][i]), []).append(i)
+    meta = small["vec_meta"]
+    vals = small["vec_vals"]
+    best_ref = {}
+    for case, kid, lo, hi, o in meta:
+        best_ref[(int(case), int(kid))] = int(vals[o:o + hi - lo + 1].max())
+    for c, cases in by_c.items():
+        nodes = [_case(small, i)[1] for i in cases]
+        w, off = G.csr_from_lists(nodes)
+        lb, ex, best, arg = G.lower_bound_batch(c, w, off, 2**62, want_best=True)
+        for j, case in enumerate(cases):
+            for kid in range(6):
+                assert best[j, kid] == best_ref.get((case, kid), 0), (case, kid, c)
+
+
+def test_cfg1(configs):
+    c, w = W.cfg1()
+    red = ReducedInstance.from_array(c, w)
+    res = G.lower_bound_seq(red, 2**62)
+    assert [res.per_dff[k] for k in G.DEFAULT_DFF_ORDER] == list(configs["cfg1_best"])
+    vec = np.concatenate([G.dff_bound_batch(k, red, *(lambda r: (r.lo, r.hi))(G.lambda_range(k, c, red)))
+                          for k in G.DEFAULT_DFF_ORDER])
+    np.testing.assert_array_equal(vec, configs["cfg1_vec"])
+    dec = G.lower_bound_seq(red, res.lb - 1)
+    assert dec.exceeded_k and dec.lb == int(configs["cfg1_l2m1"][0]) and list(dec.per_dff) == [DffKind.MT]
+
+
+@pytest.mark.parametrize("mode", ["full", "seq", "cancel"])
+def test_cfg2_nodes(configs, mode):
+    c, k, flat, off = W.cfg2_nodes(300)
+    if mode == "full":
+        lb, ex, best, arg = G.lower_bound_batch(c, flat, off, 2**62, want_best=True)
+        np.testing.assert_array_equal(best, configs["cfg2_best"])
+        np.testing.assert_array_equal(lb, configs["cfg2_best"].max(axis=1))
+    else:
+        lb, ex = G.lower_bound_batch(c, flat, off, k, mode=mode)
+        np.testing.assert_array_equal(ex, configs["cfg2_dec"][:, 1].astype(bool))
+        if mode == "seq":
+            np.testing.assert_array_equal(lb, configs["cfg2_dec"][:, 0])
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg3u"])
+def test_cfg3(configs, name):
+    w = configs[f"{name}_w"].astype(np.int32)
+    c = 100_000
+    red = ReducedInstance.from_array(c, w)
+    vals = configs[f"{name}_win_vals"]
+    for kid, lo, hi, o in configs[f"{name}_win_meta"]:
+        got = G.dff_bound_batch(DffKind[KINDS[kid]], red, int(lo), int(hi))
+        np.testing.assert_array_equal(got, vals[o:o + hi - lo + 1], err_msg=KINDS[kid])
+    res = G.lower_bound_seq(red, 2**62)
+    assert [res.per_dff[k] for k in G.DEFAULT_DFF_ORDER] == list(configs[f"{name}_best"])
+    par = G.lower_bound_par(red, 2**62, cancellation=False)
+    assert [par.per_dff[k] for k in G.DEFAULT_DFF_ORDER] == list(configs[f"{name}_best"])
+
+
+def test_cfg4(configs):
+    c, w = W.cfg4()
+    red = ReducedInstance.from_array(c, w)
+    vals = configs["cfg4_win_vals"]
+    for kid, lo, hi, o in configs["cfg4_win_meta"]:
+        got = G.dff_bound_batch(DffKind[KINDS[kid]], red, int(lo), int(hi))
+        np.testing.assert_array_equal(got, vals[o:o + hi - lo + 1], err_msg=KINDS[kid])
+    res = G.lower_bound_par(red, 2**62, cancellation=False)
+    best = configs["cfg4_best_nonvb2"]
+    for kid, kind in enumerate(G.DEFAULT_DFF_ORDER):
+        if kind is DffKind.VB2:
+            continue
+        assert res.per_dff[kind] == int(best[kid]), kind
+    vb2_path = os.path.join(GOLDEN, "cfg4_vb2.npz")
+    if os.path.exists(vb2_path):
+        vb = np.load(vb2_path)["cfg4_vb2_best"]
+        assert res.per_dff[DffKind.VB2] == int(vb[0])
+        assert res.arg[DffKind.VB2] == int(vb[1])
+
+
+def test_cfg5_nodes(configs):
+    c, k, flat, off = W.cfg5_nodes(12)
+    lb, ex, best, arg = G.lower_bound_batch(c, flat, off, 2**62, want_best=True)
+    np.testing.assert_array_equal(best, configs["cfg5_best"])
+
+
+# ---------------------------------------------------------------------------
+# Fresh seeded inputs against the pinned oracle
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("max_c,max_r,n", [(150, 40, 300), (5000, 300, 60), (200_000, 800, 12),
+                                           (4094, 2000, 20), (4096, 3000, 10)])
+def test_random_vs_oracle(oracle, max_c, max_r, n):
+    rng = random.Random(max_c * 7 + max_r)
+    for _ in range(n):
+        c, w = random_reduced_pair(rng, max_r, max_c)
+        red = ReducedInstance(c, w)
+        got = G.lower_bound_seq(red, 2**62)
+        want = oracle.lower_bound_seq(w, c, 2**62)
+        assert {k.name: v for k, v in got.per_dff.items()} == want.per_dff, (c, len(w))
+        assert {k.name: v for k, v in got.arg.items()} == want.arg, (c, len(w))
+
+
+def test_random_batch_vs_oracle(oracle):
+    rng = np.random.default_rng(7)
+    for c in (1, 2, 3, 7, 8, 150, 1000, 4094, 4095, 65536, 100_000, 999_983):
+        n = 64
+        lens = rng.integers(0, 300, n)
+        lens[0] = 0
+        nodes = []
+        for L in lens:
+            x = rng.integers(1, c + 1, L)
+            if L > 2:
+                x[0] = c
+                if c % 2 == 0:
+                    x[1] = c // 2
+            nodes.append(x)
+        w, off = G.csr_from_lists(nodes)
+        lb, ex, best, arg = G.lower_bound_batch(c, w, off, 2**62, want_best=True)
+        lbo, exo, besto = oracle.check_batch(w, off, c, 2**62, want_best=True)
+        np.testing.assert_array_equal(best, besto, err_msg=f"c={c}")
+        np.testing.assert_array_equal(lb, lbo)
+        kk = int(np.median(lbo))
+        lb2, ex2 = G.lower_bound_batch(c, w, off, kk, mode="seq")
+        lbo2, exo2 = oracle.check_batch(w, off, c, kk)
+        np.testing.assert_array_equal(lb2, lbo2)
+        np.testing.assert_array_equal(ex2, exo2)
+        lb3, ex3 = G.lower_bound_batch(c, w, off, kk, mode="cancel")
+        np.testing.assert_array_equal(ex3, exo2)
+        assert (lb3[~ex3] == lbo2[~exo2]).all()
+
+
+def test_invalid_weight_raises():
+    with pytest.raises(ValueError):
+        G.lower_bound_batch(10, np.array([3, 11], dtype=np.int32), np.array([0, 2]), 5)
+    with pytest.raises(ValueError):
+        G.dff_bound_batch(DffKind.MT, (10, np.array([0, 4], dtype=np.int32)), 0, 3)
+
+
+def test_launch_counter_moves():
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.default_engine()
+    before = eng.launch_count()
+    G.lower_bound_seq(ReducedInstance(10, (6, 6, 6)), 3)
+    assert eng.launch_count() > before
