@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""B200 LB-collection feasibility-check benchmark (BASELINE.json metric).
+
+One *step* = one batched feasibility check of this rank's search-node shard
+(default: the Scholl-1-shaped cfg2 workload, 10,000 reduced instances per
+GPU, c = 150, full collection: every kind over its full lambda range, k = 2^62).
+
+  value  device-resident throughput: inputs already in HBM, CUDA events around
+         the kernel on its stream, L2 flushed before every timed step
+         (a 256 MiB write), max over ranks -> whole-job checks/s
+  e2e    the same checks through the public API (lower_bound_batch) with
+         pinned HOST buffers: H2D of the CSR weights + offsets, kernel, D2H of
+         lb / exceeded, all inside the timed region
+  N > 1  weak scaling: each rank owns its own 10,000 nodes; the one exchange
+         step is an NCCL all-gather of the per-node verdicts (lb | exceeded).
+
+``--impl reference`` times the reference algorithm on the host cores instead:
+the C restatement in oracle/ (the reference package is Python and does not
+travel to the GPU box), all host threads, bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "feasibility checks/sec (LB collection: MT,RAD2,FS1,CCM1,VB2,BJ1 over full lambda ranges)"
+UNIT = "checks/s"
+# canonical integer-op model per (item, lambda) cell, SURVEY.md 8(d)
+I_K = {"MT": 5, "RAD2": 10, "FS1": 9, "CCM1": 12, "VB2": 15, "BJ1": 10}
+KINDS = ("MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1")
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def lambda_counts(c: int, r: np.ndarray, maxw: np.ndarray) -> dict:
+    """|Lambda_k| per node (bounds.py:253-273, VB2 cap per node)."""
+    mt = 1 + (0 if c == 1 else (c + 1) // 2)
+    rad2 = max(0, c // 3 - (c // 4 + 1) + 1)
+    prod = r.astype(object) * maxw.astype(object)
+    vb2_hi = np.array([c if rr == 0 else min(c, (2**64 - 1) // int(p)) for rr, p in zip(r, prod)],
+                      dtype=np.int64)
+    return {"MT": np.full(len(r), mt), "RAD2": np.full(len(r), rad2), "FS1": np.full(len(r), 100),
+            "CCM1": np.full(len(r), c // 2), "VB2": np.maximum(0, vb2_hi - 1), "BJ1": np.full(len(r), c)}
+
+
+def canonical_ops(c: int, flat: np.ndarray, off: np.ndarray) -> float:
+    r = np.diff(off)
+    maxw = np.maximum.reduceat(flat, off[:-1]) if len(flat) else np.zeros(len(r), dtype=np.int64)
+    maxw = np.where(r > 0, maxw, 0)
+    lc = lambda_counts(c, r, maxw)
+    return float(sum((r * lc[k]).sum() * I_K[k] for k in KINDS))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(c, k, flat, off, seconds: float = 12.0) -> dict:
+    """The reference algorithm (C port, oracle/) on this host's cores, on a
+    bounded sample of the same nodes."""
+    from oracle import oracle as O
+
+    threads = O.max_threads()
+    O.set_threads(threads)
+    n_total = len(off) - 1
+    n = min(n_total, 64)
+    t = time.perf_counter()
+    O.check_batch(flat[:off[n]], off[:n + 1], c, k)
+    dt = time.perf_counter() - t
+    n2 = int(min(n_total, max(n, n * seconds / max(dt, 1e-6))))
+    t = time.perf_counter()
+    O.check_batch(flat[:off[n2]], off[:n2 + 1] - off[0], c, k)
+    dt2 = time.perf_counter() - t
+    return {"value": n2 / dt2, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {n2} of the {n_total} cfg2 nodes of this shard, lower_bound_seq per node "
+                      f"(oracle/bplb_oracle.c, restating bounds.py), {dt2:.1f} s on {threads} threads"}
+
+
+def extra_latencies() -> dict:
+    """Single-check latencies of cfg1 / cfg3 / cfg4 through the public API."""
+    import paper_2402_14821_b200 as G
+    from paper_2402_14821_b200 import workloads as W
+
+    out = {}
+    for name, gen, reps in (("cfg1", W.cfg1, 200), ("cfg3", W.cfg3, 50), ("cfg4", W.cfg4, 8)):
+        c, w = gen()
+        red = G.ReducedInstance.from_array(c, w)
+        G.lower_bound_par(red, 2**62, cancellation=False)
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            res = G.lower_bound_par(red, 2**62, cancellation=False)
+            ts.append(time.perf_counter() - t)
+        out[name] = {"us_per_check_median": round(statistics.median(ts) * 1e6, 1),
+                     "checks_per_s": round(1.0 / statistics.median(ts), 1), "lb": res.lb,
+                     "r": int(w.size), "c": c}
+    return out
+
+
+def run_reference(args):
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2402_14821_b200 import workloads as W
+
+    c, k, flat, off = W.cfg2_nodes(args.nodes, first_node=0)
+    kk = 2**62
+    threads = O.max_threads()
+    O.set_threads(threads)
+    # each step: a bounded sample of the shard (sized so the whole run stays short)
+    n = min(args.nodes, args.ref_nodes_per_step)
+    fs, os_ = flat[:off[n]], off[:n + 1]
+    for _ in range(args.warmup):
+        O.check_batch(fs, os_, c, kk)
+    ts = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        O.check_batch(fs, os_, c, kk)
+        ts.append(time.perf_counter() - t)
+    total = sum(ts)
+    v = n * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": "cfg2: Scholl-1-shaped search-node states (n=500, c=150, k=2^62 full collection)",
+                   "nodes_per_step": n, "c": c},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{n} cfg2 nodes per step, oracle/bplb_oracle.c (C restatement of "
+                                   f"bounds.py lower_bound_seq), {threads} host threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2402_14821_b200 as G
+    from paper_2402_14821_b200 import _native, workloads as W
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    eng = _native.Engine(local)
+
+    c, k, flat, off = W.cfg2_nodes(args.nodes, first_node=rank * args.nodes)
+    kk = 2**62
+    n = len(off) - 1
+    max_r = int(np.diff(off).max())
+    kinds = list(range(6))
+    # device-resident copies (value) and pinned host copies (e2e)
+    d_w = torch.from_numpy(flat).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    d_lb = torch.empty(n, dtype=torch.int64, device=dev)
+    d_ex = torch.empty(n, dtype=torch.uint8, device=dev)
+    h_w = torch.from_numpy(flat).pin_memory().numpy()
+    h_off = torch.from_numpy(off).pin_memory().numpy()
+    h_lb = torch.empty(n, dtype=torch.int64).pin_memory().numpy()
+    h_ex = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    # a dedicated stream: the CUDA events, the L2 flush, the kernel and the
+    # NCCL gather are all ordered on it (the legacy default stream's handle
+    # is 0, which the C ABI reads as "the engine's own stream")
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    gathered = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(ws)] if ws > 1 else None
+
+    def device_step():
+        eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, max_r, c, kk, kinds, 0,
+                               d_lb.data_ptr(), d_ex.data_ptr(), stream_ptr=stream.cuda_stream)
+        if ws > 1:  # the exchange step: all-gather of per-node verdicts (lb | exceeded << 62)
+            verdict = d_lb | (d_ex.to(torch.int64) << 62)
+            dist.all_gather(gathered, verdict)
+
+    def e2e_step():
+        eng.check_batch(h_w, h_off, c, kk, kinds, 0, out=(h_lb, h_ex))
+        if ws > 1:
+            verdict = torch.from_numpy(h_lb).to(dev, non_blocking=True) | (
+                torch.from_numpy(h_ex).to(dev, non_blocking=True).to(torch.int64) << 62)
+            dist.all_gather(gathered, verdict)
+            torch.cuda.synchronize(dev)
+
+    # ---- parity spot-check of this shard against the oracle (rank 0, 64 nodes)
+    parity = None
+    if rank == 0:
+        from oracle import oracle as O
+
+        m = min(64, n)
+        lb_o, ex_o = O.check_batch(flat[:off[m]], off[:m + 1], c, kk)
+        eng.check_batch(h_w, h_off, c, kk, kinds, 0, out=(h_lb, h_ex))
+        parity = bool(np.array_equal(lb_o, h_lb[:m]))
+
+    for _ in range(args.warmup):
+        device_step()
+        e2e_step()
+    torch.cuda.synchronize(dev)
+
+    launches0 = eng.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.fill_(i)  # evict L2 (inputs are 16 MB < 126 MB L2)
+            ev[i][0].record(stream)
+            device_step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        launches = eng.launch_count() - launches0
+        # e2e: host buffers in, verdicts out, every step
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        te = []
+        for i in range(args.steps):
+            flush.fill_(i)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            e2e_step()
+            te.append(time.perf_counter() - t0)
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_ms = sum(step_ms)
+    e2e_ms = 1e3 * sum(te)
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    total_nodes = n * ws
+    value = total_nodes * args.steps / (dev_ms / 1e3)
+    e2e = total_nodes * args.steps / (e2e_ms / 1e3)
+
+    # kernel-only time of the dominant kernel (the whole step at N=1 is one launch)
+    kern_ms = None
+    if ws == 1:
+        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kt = []
+        for i in range(max(3, args.steps // 2)):
+            flush.fill_(i)
+            ka.record(stream)
+            eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, max_r, c, kk, kinds, 0,
+                                   d_lb.data_ptr(), d_ex.data_ptr(), stream_ptr=stream.cuda_stream)
+            kb.record(stream)
+            torch.cuda.synchronize(dev)
+            kt.append(ka.elapsed_time(kb))
+        kern_ms = statistics.mean(kt)
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    clocks = clk.summary()
+    ops = canonical_ops(c, flat, off)
+    sm_mhz = clocks.get("sm_max_mhz") or 1965.0
+    peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # Gop/s: 148 SMs x 128 int32 lanes x max clock
+    kms = kern_ms if kern_ms is not None else dev_ms / args.steps
+    achieved = ops / (kms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": "cfg2: Scholl-1-shaped instance (n=500, w~U{20..100}, c=150), batch of "
+                               "search-node residual states per GPU, full LB collection (k=2^62)",
+                   "nodes_per_gpu": n, "global_batch": total_nodes, "c": c, "bins_k_generator": k,
+                   "mean_r": float(np.diff(off).mean()), "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"node-shard x{ws}"},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(flat.nbytes + off.nbytes),
+                "d2h_bytes_per_step": int(n * 9)},
+        "us_per_check_e2e_amortized": 1e6 / e2e,
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "int32-issue", "achieved": achieved, "peak": peak, "unit": "Gop/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "note": "achieved = canonical integer ops (SURVEY.md 8(d): r x sum_k |Lambda_k| x I_k) / "
+                             "kernel time; peak = 148 SMs x 128 INT32 lanes x max SM clock (nominal, "
+                             "no measured int peak in MEASURED_PEAKS.json). The kernel computes the same "
+                             "bounds with histogram / distinct-value / harmonic shortcuts (as the reference's "
+                             "own sweeps do), so executed work is far below canonical and frac can exceed 1; "
+                             "executed-instruction issue utilisation is in profiles/."},
+        "kernel_ms": kms,
+        "clocks": clocks,
+        "parity_vs_oracle_64_nodes": parity,
+    }
+    if ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(c, kk, flat, off, seconds=args.cpu_seconds)
+    if ws == 1 and not args.no_extra:
+        line["extra_single_check_latency"] = extra_latencies()
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--nodes", type=int, default=10_000, help="search nodes per GPU")
+    ap.add_argument("--ref-nodes-per-step", type=int, default=2000)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -101,7 +101,8 @@ BPLB_API int bplb_check_batch(bplb_engine *eng, const int32_t *w_concat, const i
                      int64_t *best_out, int64_t *arg_out);
 
 /* Same as bplb_check_batch with every array already resident in device
- * memory (`stream` is a cudaStream_t, or NULL for the engine's stream).
+ * memory (`stream` is a cudaStream_t, or NULL for the engine's stream; pass
+ * cudaStreamLegacy, i.e. (void*)1, for the legacy default stream).
  * Asynchronous: returns after enqueueing; the caller synchronises.
  * d_best/d_arg may be NULL.  Work buffers are owned by the engine, so
  * concurrent device calls on one engine must be ordered on one stream. */

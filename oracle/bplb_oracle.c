@@ -164,14 +164,51 @@ int64_t or_dff_bound(int kind, const int64_t *w, int64_t r, int64_t c, int64_t l
 /* ---- _batch_matrix column sums: bounds.py:293-323 (dense r x L form) ----- */
 typedef struct { int kind; const int64_t *w; int64_t r, c, lo, maxw; int64_t *sums, *fc; const void *cu;
                  const int64_t *smalls, *mirrored; int64_t ns, nm, n_eq, n_big; int64_t *out; } sweep_ctx;
+/* One cell of _batch_matrix in numpy int64 semantics (bounds.py:293-323);
+ * every operand is non-negative, so C division equals numpy's floor division. */
+static int64_t bm_value(int kind, int64_t w, int64_t c, int64_t lam) {
+    switch (kind) {
+    case OR_MT: return w > c - lam ? c : (w < lam ? 0 : w);
+    case OR_RAD2: {
+        int64_t third = c / 3, half = c / 2;
+        int64_t v = w >= 2 * lam ? c - w : w;
+        int64_t base = v < lam ? 0 : (v <= c - 2 * lam ? third : half);
+        return w >= 2 * lam ? c - base : base;
+    }
+    case OR_FS1: {
+        int64_t num = w * (lam + 1);
+        return num % c == 0 ? w * lam : (num / c) * c;
+    }
+    case OR_CCM1: {
+        int64_t cq = c / lam;
+        if (2 * w > c) return 2 * (cq - (c - w) / lam);
+        return 2 * w == c ? cq : 2 * (w / lam);
+    }
+    case OR_VB2: {
+        int64_t pc = lam - 1 > 0 ? lam - 1 : 0;
+        if (2 * w > c) {
+            int64_t pv = ((c - w) * lam + c - 1) / c - 1;
+            return 2 * pc - 2 * (pv > 0 ? pv : 0);
+        }
+        if (2 * w == c) return pc;
+        int64_t pv = (w * lam + c - 1) / c - 1;
+        return 2 * (pv > 0 ? pv : 0);
+    }
+    default: {
+        int64_t cm = c % lam, base = (w / lam) * (lam - cm), wm = w % lam;
+        return wm <= cm ? base : base + wm - cm;
+    }
+    }
+}
+
 static void bm_range(void *p, int64_t b, int64_t e) {
     sweep_ctx *x = (sweep_ctx *)p;
     for (int64_t j = b; j < e; j++) {
         int64_t lam = x->lo + j;
         int64_t s = 0;
-        for (int64_t i = 0; i < x->r; i++) s += (int64_t)f_value(x->kind, x->w[i], x->c, lam);
+        for (int64_t i = 0; i < x->r; i++) s += bm_value(x->kind, x->w[i], x->c, lam);
         x->sums[j] = s;
-        x->fc[j] = (int64_t)f_value(x->kind, x->c, x->c, lam);
+        x->fc[j] = bm_value(x->kind, x->c, x->c, lam);
     }
 }
 static void batch_matrix_sums(int kind, const int64_t *w, int64_t r, int64_t c,

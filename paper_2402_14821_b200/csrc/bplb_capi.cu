@@ -14,6 +14,7 @@
 #include "bplb_core.h"
 #include "bplb_node.cuh"
 #include "bplb_wide.cuh"
+#include "bplb_warp.cuh"
 
 namespace {
 
@@ -136,8 +137,29 @@ void fill_params(bplb::KParams& p, int64_t c, int64_t k, const int* kinds, int n
     p.one = 1;
 }
 
+// Warp-per-node kernel for batches of small-capacity nodes.
+int launch_warp(bplb_engine* e, bplb::KParams& p, int64_t n_nodes) {
+    const size_t smem = bplb::warp_slice_bytes(p.c) * bplb::WNW;
+    CUDA_TRY(cudaFuncSetAttribute(bplb::warp_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::warp_node_kernel, bplb::WNT, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = std::min<int64_t>((n_nodes + bplb::WNW - 1) / bplb::WNW, (int64_t)per_sm * e->num_sms);
+    p.n_nodes = n_nodes;
+    bplb::warp_node_kernel<<<(unsigned)grid, bplb::WNT, smem, e->stream>>>(p);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+bool warp_path(const bplb::KParams& p, int64_t n_nodes) {
+    return p.lam_out == nullptr && p.c <= bplb::WARP_MAX_C && n_nodes >= 64 &&
+           bplb::warp_slice_bytes(p.c) * bplb::WNW <= 200 * 1024;
+}
+
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
 int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r, int grid_cap) {
+    if (grid_cap == 0 && warp_path(p, n_nodes)) return launch_warp(e, p, n_nodes);
     const bool table = p.c <= bplb::TABLE_MAX_C;
     if (max_r > (table ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT))
         return fail(BPLB_ERANGE, "node larger than the node-resident envelope");

@@ -185,6 +185,7 @@ BPLB_HD int64_t bplb_ccm1_part(const L& lk, const NodeStats& st, int64_t c, int6
     const int64_t hs = (c - 1) / 2, tmax = hs / lam;
     const int64_t base = (int64_t)st.n_small + (int64_t)st.r - (int64_t)st.n_big;
     int64_t acc = 0;
+#pragma unroll 4
     for (int64_t t = t0; t <= tmax; t += dt)
         acc += base - lk.n_le(t * lam - 1) - lk.n_le(c - t * lam);
     return acc;
@@ -206,6 +207,7 @@ BPLB_HD void bplb_bj1_part(const L& lk, const NodeStats& st, int64_t c, int64_t 
                            int64_t dt, int64_t* floor_part, int64_t* rem_part) {
     const int64_t r = st.r, cm = c % lam, tmax = st.maxw / lam;
     int64_t fl = 0, rem = 0;
+#pragma unroll 4
     for (int64_t t = t0; t <= tmax; t += dt) {
         const int64_t lo_v = lam * t + cm, hi_v = lam * (t + 1) - 1;
         int64_t nl, wl, nh, wh;

@@ -11,7 +11,7 @@ namespace bplb {
 
 constexpr int kWarp = 32;
 constexpr int LMOD = 128;   // lambdas per modular (VB2/FS1) unit
-constexpr int GMOD = 16;    // items per lane per modular group
+constexpr int GMOD_MAX = 16; // items per lane per modular group (max)
 constexpr int LLOOK = 32;   // lambdas per lookup unit (one per lane)
 constexpr int LDIV = 32;    // lambdas per division unit
 
@@ -42,6 +42,29 @@ struct LkSorted {  // sorted weights + prefix sums (shared memory)
     }
 };
 
+struct LkBucket {  // sorted weights + prefix sums + coarse value->index buckets
+    const int* sw;          // sorted weights [r]
+    const long long* pre;   // prefix sums [r+1]
+    const int* bidx;        // bidx[b] = #{w < (b << k)}, b in [0, nb]; bidx[nb] = r
+    int r;
+    int k;
+    int64_t c;
+    __device__ __forceinline__ int64_t n_le(int64_t x) const {
+        if (x < 0) return 0;
+        if (x >= c) return r;
+        const int b = (int)(x >> k);
+        int i = bidx[b];
+        const int e = bidx[b + 1];
+        while (i < e && (int64_t)sw[i] <= x) ++i;
+        return i;
+    }
+    __device__ __forceinline__ void both(int64_t x, int64_t* n, int64_t* w) const {
+        int64_t kk = n_le(x);
+        *n = kk;
+        *w = pre[kk];
+    }
+};
+
 struct LkTable {  // cumulative tables over values [-1, c] (index x+1)
     const int* cnt;
     const long long* wle;
@@ -57,18 +80,17 @@ struct LkTable {  // cumulative tables over values [-1, c] (index x+1)
     }
 };
 
-struct LkTableG {  // same, global-memory tables with 64-bit counts
-    const unsigned int* cnt;
-    const unsigned long long* wle;
+struct LkTableG {  // same, global memory (L2-resident), one 16-byte record per value
+    const ulonglong2* rec;  // {W<=(x), N<=(x)} at index x+1
     int64_t c;
     __device__ __forceinline__ int64_t idx(int64_t x) const {
         return (x < -1 ? -1 : (x > c ? c : x)) + 1;
     }
-    __device__ __forceinline__ int64_t n_le(int64_t x) const { return (int64_t)__ldg(cnt + idx(x)); }
+    __device__ __forceinline__ int64_t n_le(int64_t x) const { return (int64_t)__ldg(&rec[idx(x)].y); }
     __device__ __forceinline__ void both(int64_t x, int64_t* n, int64_t* w) const {
-        int64_t i = idx(x);
-        *n = (int64_t)__ldg(cnt + i);
-        *w = (int64_t)__ldg(wle + i);
+        const ulonglong2 v = __ldg(rec + idx(x));
+        *n = (int64_t)v.y;
+        *w = (int64_t)v.x;
     }
 };
 
@@ -120,18 +142,20 @@ __device__ __forceinline__ T reduce8_transposed(T v[8], int lane) {
 //
 // WIDE selects 64-bit lane partials (needed when 32 * GMOD * c >= 2^32).
 // ---------------------------------------------------------------------------
-template <bool FS1, bool WIDE>
-__device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_begin, int i_end,
-                                         uint32_t c, u64 cinv, int64_t lam_a, int L,
-                                         u64* tot, u64* ztot, uint32_t one) {
+template <bool FS1, bool WIDE, bool WEIGHTED, int GMOD>
+__device__ __forceinline__ void mod_group(const int* __restrict__ items, int g, int i_end,
+                                          uint32_t c, u64 cinv, int64_t lam_a, int L,
+                                          u64* tot, u64* ztot, uint32_t one,
+                                          const int* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
     const uint32_t negc = 0u - c;
-    for (int g = i_begin; g < i_end; g += kWarp * GMOD) {
-        uint32_t s[GMOD], u[GMOD], um[GMOD];
+    {
+        uint32_t s[GMOD], u[GMOD], um[GMOD], cw[WEIGHTED ? GMOD : 1];
 #pragma unroll
         for (int t = 0; t < GMOD; ++t) {
             int idx = g + lane + kWarp * t;
             uint32_t w = idx < i_end ? (uint32_t)items[idx] : 0u;
+            if (WEIGHTED) cw[t] = idx < i_end ? (uint32_t)counts[idx] : 0u;
             u[t] = w;
             um[t] = w + negc;
             if (w == 0) {
@@ -152,8 +176,20 @@ __device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_be
                 if (FS1) zac[j] = 0;
 #pragma unroll
                 for (int t = 0; t < GMOD; ++t) {
-                    acc[j] += (Acc)s[t];
-                    if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] : (Acc)0;
+                    if (WEIGHTED) {
+                        acc[j] += (Acc)s[t] * (Acc)cw[t];
+                        if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] * (Acc)cw[t] : (Acc)0;
+                    } else if (!WIDE && (t % 3) == 2) {
+                        // every third accumulate on the IMAD pipe: the walk is
+                        // ALU-bound (VIADDMNMX + IADD3), this balances the pipes
+                        uint32_t a = (uint32_t)acc[j];
+                        asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(a) : "r"(s[t]), "r"(one));
+                        acc[j] = (Acc)a;
+                        if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] : (Acc)0;
+                    } else {
+                        acc[j] += (Acc)s[t];
+                        if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] : (Acc)0;
+                    }
                     // s <- min(s + w, s + w - c)  (unsigned; exactly one is < c)
                     uint32_t b;
                     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(s[t]), "r"(one), "r"(um[t]));
@@ -188,6 +224,32 @@ __device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_be
     }
 }
 
+// Walk items [i_begin, i_end) in groups of 32 x G items, G chosen per group
+// so that short item lists are not padded to 512 slots.
+template <bool FS1, bool WIDE, bool WEIGHTED = false>
+__device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_begin, int i_end,
+                                         uint32_t c, u64 cinv, int64_t lam_a, int L,
+                                         u64* tot, u64* ztot, uint32_t one,
+                                         const int* __restrict__ counts = nullptr) {
+    int g = i_begin;
+    while (g < i_end) {
+        const int rem = i_end - g;
+        if (!WEIGHTED && rem > 8 * kWarp) {
+            mod_group<FS1, WIDE, WEIGHTED, 16>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
+            g += 16 * kWarp;
+        } else if (!WEIGHTED && rem > 4 * kWarp) {
+            mod_group<FS1, WIDE, WEIGHTED, 8>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
+            g += 8 * kWarp;
+        } else if (WEIGHTED || rem > 2 * kWarp) {
+            mod_group<FS1, WIDE, WEIGHTED, 4>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
+            g += 4 * kWarp;
+        } else {
+            mod_group<FS1, WIDE, WEIGHTED, 2>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
+            g += 2 * kWarp;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Division dense sums for one lambda (CCM1 / BJ1 at small lambda, where the
 // harmonic lookups would cost more than a pass over the items).
@@ -204,6 +266,23 @@ __device__ __forceinline__ int64_t ccm1_dense(const int* sw, const NodeStats& st
         ab += bplb_udiv31((uint32_t)(c - sw[i]), dv);
     int64_t A = (int64_t)warp_sum_u64(as) - (int64_t)warp_sum_u64(ab);
     int64_t cq = c / lam;
+    return 2 * A + (int64_t)st.n_eq * cq + 2 * (int64_t)st.n_big * cq;
+}
+
+// CCM1 over an unsorted item array (grid-wide path): classify per item.
+__device__ __forceinline__ int64_t ccm1_dense_raw(const int* w, int n, const NodeStats& st, int64_t c,
+                                                  int64_t lam) {
+    const int lane = threadIdx.x & 31;
+    const Div31 dv = bplb_div31((uint32_t)lam);
+    const uint32_t c32 = (uint32_t)c;
+    long long a = 0;
+    for (int i = lane; i < n; i += kWarp) {
+        const uint32_t x = (uint32_t)__ldg(w + i);
+        if (2ull * x < c32) a += bplb_udiv31(x, dv);
+        else if (2ull * x > c32) a -= bplb_udiv31(c32 - x, dv);
+    }
+    const int64_t A = (int64_t)warp_sum_u64((u64)a);
+    const int64_t cq = c / lam;
     return 2 * A + (int64_t)st.n_eq * cq + 2 * (int64_t)st.n_big * cq;
 }
 

@@ -4,10 +4,17 @@
 // as in the paper's calcDffLowerBound, but one launch covers
 // all six families, every lambda and every node of the batch.
 //
-// Work inside a CTA is cut into "units" taken from a shared-memory counter:
-//   T_LOOKUP  32 lambdas, one per lane, analytic sweep with histogram/sorted
-//             lookups (MT, RAD2, CCM1/BJ1 at large lambda)
-//   T_MOD     LMOD lambdas x all VB2 (or FS1) items, modular walk
+// Two shared-memory layouts, chosen per batch by capacity:
+//   TABLE (c <= TABLE_MAX_C): cumulative count / weight tables over the
+//     values [-1, c] (O(1) lookups) and the multiset compressed to distinct
+//     (value, count) pairs for the VB2/FS1 modular walks.
+//   SORT  (larger c): sorted weights + prefix sums + a coarse value->index
+//     bucket table (lookups = one bucket read + a ~1-item scan).
+//
+// Work inside a CTA is cut into "units" pulled from a shared counter:
+//   T_LOOKUP  32 lambdas, one per lane, analytic sweep (MT, RAD2, CCM1/BJ1)
+//   T_WLOOK   one lambda per warp, harmonic loop split across lanes
+//   T_MOD     up to LMOD lambdas x all VB2 (or FS1) items, modular walk
 //   T_DIV     LDIV lambdas, warp-cooperative item pass (CCM1/BJ1 small lambda)
 #pragma once
 #include <climits>
@@ -18,8 +25,11 @@ namespace bplb {
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
-constexpr int TABLE_MAX_C = 4094;  // node kernel uses cumulative tables when c <= this
-constexpr int MAX_SEGS = 2 * K_COUNT;
+constexpr int TABLE_MAX_C = 2046;   // node kernel uses cumulative tables when c <= this
+constexpr int NBMAX = 4096;         // SORT-mode bucket table entries
+constexpr int MAX_SEGS = 3 * K_COUNT;
+
+enum { T_WLOOK = 3 };
 
 struct Seg {
     int kind, type;
@@ -63,9 +73,27 @@ struct NodeCtl {
     int unit_next;
     int unit_end;
     int lb;
-    int n_vb2;
+    int n_vb2;     // SORT: VB2 item count; TABLE: distinct VB2 values
+    int n_dist;    // TABLE: distinct values
     int n_done;
     int bad;
+    int skip;
+    long long wsum[NW];
+    long long wsum2[NW];
+};
+
+struct NodeMem {  // shared-memory views of one node
+    int* sw;          // SORT: sorted weights (padded); TABLE: raw weights
+    long long* pre;   // SORT: prefix [r+1];  TABLE: W<=(x) table [c+2]
+    int* cnt;         // TABLE: N<=(x) table [c+2]
+    int* bidx;        // SORT: bucket index [NBMAX+1]
+    int* vb2;         // SORT: VB2 items; TABLE: distinct VB2 values
+    int* vb2c;        // TABLE: their counts
+    int* dval;        // TABLE: distinct values
+    int* dcnt;        // TABLE: their counts
+    u64* tot;
+    u64* ztot;
+    int bk;           // SORT: bucket shift
 };
 
 __device__ __forceinline__ bool kind_in(const KParams& p, int kind) {
@@ -74,23 +102,21 @@ __device__ __forceinline__ bool kind_in(const KParams& p, int kind) {
     return false;
 }
 
-// Threshold below which CCM1/BJ1 lambdas are summed densely instead of via
-// harmonic lookups (cost model in DESIGN.md).
+// Threshold below which CCM1/BJ1 lambdas are summed densely (SORT mode) --
+// harmonic lookups cost ~2 * 8 instructions per term, a dense pass ~3 (CCM1)
+// or ~5 (BJ1) per item.
 __device__ __forceinline__ int64_t div_split(int kind, const NodeStats& st, int64_t c) {
-    int lg = 1;
-    while ((1 << lg) <= st.r) ++lg;
-    int64_t n = st.r > 0 ? st.r : 1;
+    const int64_t n = st.r > 0 ? st.r : 1;
     if (kind == K_CCM1) {
-        int64_t hs = (c - 1) / 2;
-        return (8 * hs * (lg + 1)) / (3 * n) + 1;
+        const int64_t hs = (c - 1) / 2;
+        return (16 * hs) / (3 * n + 30) + 1;
     }
-    int64_t mw = st.maxw;
-    return (12 * mw * (lg + 1)) / (5 * n) + 1;
+    return (4 * (int64_t)st.maxw) / n + 1;
 }
 
 // Build the unit segments of one kind (thread 0).
 __device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c) {
-    int64_t lo = ctl.lo[kind], hi = ctl.hi[kind];
+    const int64_t lo = ctl.lo[kind], hi = ctl.hi[kind];
     ctl.kind_seg_first[kind] = ctl.nseg;
     ctl.kind_seg_count[kind] = 0;
     if (hi < lo) return;
@@ -109,24 +135,35 @@ __device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c) {
     };
     switch (kind) {
     case K_MT: case K_RAD2: push(T_LOOKUP, lo, hi, LLOOK); break;
-    case K_FS1: case K_VB2: push(T_MOD, lo, hi, LMOD); break;
+    case K_FS1: case K_VB2: {
+        // enough units to keep all warps busy on small nodes
+        int64_t ch = (hi - lo + 1 + 2 * NW - 1) / (2 * NW);
+        ch = (ch + 7) & ~7ll;
+        ch = ch < 32 ? 32 : (ch > LMOD ? LMOD : ch);
+        push(T_MOD, lo, hi, (int)ch);
+        break;
+    }
     default: {  // CCM1, BJ1
-        if (table) {
-            push(T_LOOKUP, lo, hi, LLOOK);
-        } else {
-            int64_t sp = div_split(kind, ctl.st, c);
+        const int64_t span = kind == K_CCM1 ? (c - 1) / 2 : (int64_t)ctl.st.maxw;
+        int64_t sp = lo;
+        if (!table) {
+            sp = div_split(kind, ctl.st, c);
             if (sp < lo) sp = lo;
             if (sp > hi + 1) sp = hi + 1;
             push(T_DIV, lo, sp - 1, LDIV);
-            push(T_LOOKUP, sp, hi, LLOOK);
         }
+        int64_t sw = span / 64 + 1;  // one warp per lambda while the loop is long
+        if (sw < sp) sw = sp;
+        if (sw > hi + 1) sw = hi + 1;
+        push(T_WLOOK, sp, sw - 1, 1);
+        push(T_LOOKUP, sw, hi, LLOOK);
     }
     }
 }
 
-template <class LK>
-__device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const int* sw,
-                         const int* vb2, u64* tot, u64* ztot, int u, bool single) {
+template <bool TABLE, class LK>
+__device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m, int u,
+                         bool single) {
     const int lane = threadIdx.x & 31;
     int si = 0;
     while (si + 1 < ctl.nseg && ctl.segs[si + 1].first <= u) ++si;
@@ -152,10 +189,26 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const int
         }
         int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
         wmax = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
+    } else if (sg.type == T_WLOOK) {
+        const int64_t lam = lam_a;
+        int64_t S;
+        if (kind == K_CCM1) {
+            int64_t part = bplb_ccm1_part(lk, st, c, lam, 1 + lane, 32);
+            part = (int64_t)warp_sum_u64((u64)part);
+            S = bplb_ccm1_from_part(st, c, lam, part);
+        } else {
+            int64_t fl, rem;
+            bplb_bj1_part(lk, st, c, lam, lane, 32, &fl, &rem);
+            fl = (int64_t)warp_sum_u64((u64)fl);
+            rem = (int64_t)warp_sum_u64((u64)rem);
+            S = bplb_bj1_from_parts(c, lam, fl, rem);
+        }
+        int64_t b = bplb_bound(S, bplb_fc(kind, c, lam));
+        wmax = emit_warp(lane == 0, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
     } else if (sg.type == T_DIV) {
         int64_t mine = 0;
         for (int64_t lam = lam_a; lam <= lam_b; ++lam) {
-            int64_t S = (kind == K_CCM1) ? ccm1_dense(sw, st, c, lam) : bj1_dense(sw, st.r, c, lam);
+            int64_t S = (kind == K_CCM1) ? ccm1_dense(m.sw, st, c, lam) : bj1_dense(m.sw, st.r, c, lam);
             if (lam - lam_a == lane) mine = S;
         }
         const int64_t lam = lam_a + lane;
@@ -164,20 +217,25 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const int
         wmax = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
     } else {
         const int warp = threadIdx.x >> 5;
-        u64* t = tot + warp * LMOD;
-        u64* z = ztot + warp * LMOD;
+        u64* t = m.tot + warp * LMOD;
+        u64* z = m.ztot + warp * LMOD;
         const int L = (int)(lam_b - lam_a + 1);
-        for (int j = lane; j < LMOD; j += kWarp) { t[j] = 0; z[j] = 0; }
+        for (int j = lane; j < L; j += kWarp) { t[j] = 0; z[j] = 0; }
         __syncwarp();
         const uint32_t c32 = (uint32_t)c;
         const u64 cinv = bplb_cinv(c32);
-        const bool wide = c >= (1 << 23);
-        if (kind == K_VB2) {
-            if (wide) mod_walk<false, true>(vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
-            else mod_walk<false, false>(vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
+        if (TABLE) {  // distinct values x counts (c small: never wide)
+            if (kind == K_VB2) mod_walk<false, false, true>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one, m.vb2c);
+            else mod_walk<true, false, true>(m.dval, 0, ctl.n_dist, c32, cinv, lam_a, L, t, z, p.one, m.dcnt);
         } else {
-            if (wide) mod_walk<true, true>(sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
-            else mod_walk<true, false>(sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
+            const bool wide = c >= (1 << 23);
+            if (kind == K_VB2) {
+                if (wide) mod_walk<false, true>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
+                else mod_walk<false, false>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
+            } else {
+                if (wide) mod_walk<true, true>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
+                else mod_walk<true, false>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
+            }
         }
         __syncwarp();
         wmax = -1;
@@ -189,8 +247,8 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const int
             if (valid)
                 S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j]) : bplb_fs1_sum(st, lam, t[j], z[j]);
             int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
-            int64_t m = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
-            wmax = m > wmax ? m : wmax;
+            int64_t mm = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
+            wmax = mm > wmax ? mm : wmax;
         }
     }
     if (lane == 0) {
@@ -201,9 +259,9 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const int
 }
 
 // Process units [ctl.unit_next, ctl.unit_end) with all warps.
-template <class LK>
-__device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const int* sw,
-                          const int* vb2, u64* tot, u64* ztot, bool single, bool cancel) {
+template <bool TABLE, class LK>
+__device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m,
+                          bool single, bool cancel) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         int u = 0;
@@ -214,7 +272,36 @@ __device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const in
             int cur = *(volatile int*)&ctl.lb;
             if ((int64_t)cur > p.k) continue;  // Alg. 4 guard
         }
-        run_unit(p, ctl, lk, sw, vb2, tot, ztot, u, single);
+        run_unit<TABLE>(p, ctl, lk, m, u, single);
+    }
+}
+
+// Kinds in order, one phase per kind (PHASED: stop after the first kind whose
+// best exceeds k -- bounds.py:523-525; CANCEL: skip later kinds once lb > k,
+// the Alg. 3/4 per-launch guard, and skip units inside a kind too).  Without
+// either flag all units of all kinds are pulled from one counter.
+template <bool TABLE, class LK>
+__device__ void sweep_node(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m,
+                           bool single, bool phased, bool cancel) {
+    if (phased || cancel) {
+        for (int i = 0; i < p.nk; ++i) {
+            const int kd = p.kinds[i];
+            if (threadIdx.x == 0) {
+                const int f = ctl.kind_seg_first[kd], n = ctl.kind_seg_count[kd];
+                ctl.unit_next = n ? ctl.segs[f].first : 0;
+                ctl.unit_end = n ? ctl.segs[f + n - 1].first + ctl.segs[f + n - 1].count : 0;
+                ctl.skip = cancel && (int64_t)ctl.lb > p.k;
+                if (!ctl.skip) ctl.n_done = i + 1;
+            }
+            __syncthreads();
+            if (!ctl.skip) run_units<TABLE>(p, ctl, lk, m, single, cancel);
+            __syncthreads();
+            if (phased && (int64_t)ctl.lb > p.k) break;
+        }
+    } else {
+        if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
+        __syncthreads();
+        run_units<TABLE>(p, ctl, lk, m, single, false);
     }
 }
 
@@ -234,23 +321,40 @@ __device__ __forceinline__ void block_sort(int* a, int n) {  // bitonic, n power
     }
 }
 
-// Exclusive-style inclusive scan helpers over shared arrays (one CTA).
-// out_n[i] = sum_{j < i} cnt_in[j]-style prefix is built by the callers.
-__device__ __forceinline__ void block_prefix_i64(const int* v, long long* pre, int n,
-                                                 long long* scratch /*NT*/) {
-    // pre[0] = 0, pre[i+1] = pre[i] + v[i]
+// Exclusive block-wide scan of one value per thread (warp shuffles + one
+// shared word per warp).  Returns the sum of v over threads < threadIdx.x.
+__device__ __forceinline__ long long block_excl_scan(long long v, long long* wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        long long t = lane < NW ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < NW; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < NW) wsum[lane] = t;
+    }
+    __syncthreads();
+    long long res = (warp ? wsum[warp - 1] : 0) + x - v;
+    __syncthreads();
+    return res;
+}
+
+// pre[0] = 0, pre[i+1] = pre[i] + v[i] over n elements.
+__device__ __forceinline__ void block_prefix_i64(const int* v, long long* pre, int n, long long* wsum) {
     const int per = (n + NT - 1) / NT;
     const int b = threadIdx.x * per, e = min(n, b + per);
     long long s = 0;
     for (int i = b; i < e; ++i) s += v[i];
-    scratch[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long run = 0;
-        for (int t = 0; t < NT; ++t) { long long x = scratch[t]; scratch[t] = run; run += x; }
-    }
-    __syncthreads();
-    long long run = scratch[threadIdx.x];
+    long long run = block_excl_scan(s, wsum);
     if (threadIdx.x == 0) pre[0] = 0;
     for (int i = b; i < e; ++i) { run += v[i]; pre[i + 1] = run; }
     __syncthreads();
@@ -258,25 +362,14 @@ __device__ __forceinline__ void block_prefix_i64(const int* v, long long* pre, i
 
 // cnt[i] holds the histogram count of value i-1 (i in [0, c+1]); converts in
 // place to cnt[i] = #{w <= i-1} and fills wle[i] = sum{w <= i-1}.
-__device__ __forceinline__ void block_table_scan(int* cnt, long long* wle, int n,
-                                                 long long* scratch /*2*NT*/) {
+__device__ __forceinline__ void block_table_scan(int* cnt, long long* wle, int n, long long* wsum,
+                                                 long long* wsum2) {
     const int per = (n + NT - 1) / NT;
     const int b = threadIdx.x * per, e = min(n, b + per);
     long long sc = 0, sw = 0;
     for (int i = b; i < e; ++i) { sc += cnt[i]; sw += (long long)cnt[i] * (i - 1); }
-    scratch[threadIdx.x] = sc;
-    scratch[NT + threadIdx.x] = sw;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        long long rc = 0, rw = 0;
-        for (int t = 0; t < NT; ++t) {
-            long long x = scratch[t], y = scratch[NT + t];
-            scratch[t] = rc; scratch[NT + t] = rw;
-            rc += x; rw += y;
-        }
-    }
-    __syncthreads();
-    long long rc = scratch[threadIdx.x], rw = scratch[NT + threadIdx.x];
+    long long rc = block_excl_scan(sc, wsum);
+    long long rw = block_excl_scan(sw, wsum2);
     for (int i = b; i < e; ++i) {
         int x = cnt[i];
         rc += x;
@@ -287,30 +380,59 @@ __device__ __forceinline__ void block_table_scan(int* cnt, long long* wle, int n
     __syncthreads();
 }
 
+__host__ __device__ inline int node_bucket_shift(int64_t c) {
+    int k = 0;
+    while ((c >> k) + 2 > NBMAX) ++k;
+    return k;
+}
+
 // Dynamic shared memory size of the node kernel.
 __host__ __device__ inline size_t node_smem_bytes(bool table, int rcap, int64_t c) {
     size_t s = 0;
-    s += (size_t)rcap * 4;                 // sw
-    s += (size_t)rcap * 4;                 // vb2
     s += (size_t)NW * LMOD * 8 * 2;        // tot, ztot
-    s += (size_t)2 * NT * 8;               // scratch
-    if (table) s += (size_t)(c + 2) * 8 + (size_t)(c + 2) * 4 + 8;
-    else s += (size_t)(rcap + 1) * 8;
-    return s;
+    s += (size_t)rcap * 4;                 // sw
+    if (table) {
+        const size_t dc = (size_t)(rcap < c + 1 ? rcap : c + 1);
+        s += (size_t)(c + 2) * 8;          // wle
+        s += (size_t)(c + 2) * 4;          // cnt
+        s += dc * 4 * 4;                   // dval, dcnt, vb2, vb2c
+    } else {
+        s += (size_t)(rcap + 1) * 8;       // pre
+        s += (size_t)rcap * 4;             // vb2
+        s += (size_t)(NBMAX + 1) * 4;      // bidx
+    }
+    return s + 64;
 }
 
 template <bool TABLE>
-__global__ void __launch_bounds__(NT) node_kernel(KParams p, int rcap) {
+__global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ NodeCtl ctl;
-    int* sw = (int*)smem;
-    int* vb2 = sw + rcap;
-    u64* tot = (u64*)(vb2 + rcap);
-    u64* ztot = tot + NW * LMOD;
-    long long* scratch = (long long*)(ztot + NW * LMOD);
-    long long* pre = scratch + 2 * NT;               // SORT: [rcap+1]; TABLE: wle [c+2]
-    int* cnt = (int*)(pre + (TABLE ? p.c + 2 : 0));  // TABLE only: [c+2]
     const int64_t c = p.c;
+    NodeMem m;
+    {
+        unsigned char* q = smem;
+        m.tot = (u64*)q; q += NW * LMOD * 8;
+        m.ztot = (u64*)q; q += NW * LMOD * 8;
+        if (TABLE) {
+            const int dc = (int)(rcap < c + 1 ? rcap : c + 1);
+            m.pre = (long long*)q; q += (c + 2) * 8;
+            m.cnt = (int*)q; q += (c + 2) * 4;
+            m.sw = (int*)q; q += (size_t)rcap * 4;
+            m.dval = (int*)q; q += dc * 4;
+            m.dcnt = (int*)q; q += dc * 4;
+            m.vb2 = (int*)q; q += dc * 4;
+            m.vb2c = (int*)q; q += dc * 4;
+            m.bidx = nullptr;
+        } else {
+            m.pre = (long long*)q; q += (size_t)(rcap + 1) * 8;
+            m.sw = (int*)q; q += (size_t)rcap * 4;
+            m.vb2 = (int*)q; q += (size_t)rcap * 4;
+            m.bidx = (int*)q;
+            m.cnt = m.dval = m.dcnt = m.vb2c = nullptr;
+        }
+        m.bk = TABLE ? 0 : node_bucket_shift(c);
+    }
     const bool single = p.lam_out != nullptr;
     const bool phased = p.flags & BPLB_F_PHASED;
     const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
@@ -325,31 +447,31 @@ __global__ void __launch_bounds__(NT) node_kernel(KParams p, int rcap) {
             for (int i = 0; i < K_COUNT; ++i) {
                 ctl.key[i] = 0; ctl.evals[i] = 0; ctl.evaluated[i] = 0;
             }
-            ctl.lb = 0; ctl.n_vb2 = 0; ctl.nseg = 0; ctl.nunits = 0; ctl.n_done = 0;
+            ctl.lb = 0; ctl.n_vb2 = 0; ctl.n_dist = 0; ctl.nseg = 0; ctl.nunits = 0; ctl.n_done = 0;
             ctl.bad = 0;
         }
         // ---- stage weights -------------------------------------------------
         int pw = 1;
         while (pw < r) pw <<= 1;
         if (TABLE) {
-            for (int i = threadIdx.x; i < c + 2; i += NT) cnt[i] = 0;
+            for (int i = threadIdx.x; i < c + 2; i += NT) m.cnt[i] = 0;
         }
         for (int i = threadIdx.x; i < (TABLE ? r : pw); i += NT)
-            sw[i] = i < r ? p.w[base + i] : INT_MAX;
+            m.sw[i] = i < r ? __ldg(p.w + base + i) : INT_MAX;
         __syncthreads();
         // ---- statistics ------------------------------------------------------
         {
             int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
             long long l_W = 0, l_Vs = 0, l_Vm = 0;
             for (int i = threadIdx.x; i < r; i += NT) {
-                int x = sw[i];
+                const int x = m.sw[i];
+                if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
                 l_max = max(l_max, x);
-                if (x < 1 || (int64_t)x > c) l_bad = 1;
                 l_W += x;
                 if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
                 else if (2 * (int64_t)x == c) l_e++;
                 else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
-                if (TABLE && x >= 1 && x <= c) atomicAdd(&cnt[x + 1], 1);
+                if (TABLE) atomicAdd(&m.cnt[x + 1], 1);
             }
             l_max = __reduce_max_sync(0xffffffffu, (unsigned)l_max);
             l_bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)l_bad);
@@ -375,19 +497,40 @@ __global__ void __launch_bounds__(NT) node_kernel(KParams p, int rcap) {
         __syncthreads();
         // ---- lookup structure -----------------------------------------------
         if (TABLE) {
-            block_table_scan(cnt, pre, (int)(c + 2), scratch);
-            // VB2 items: 2w != c and w < c (order irrelevant, G11)
-            for (int i = threadIdx.x; i < r; i += NT) {
-                int x = sw[i];
-                if (2 * (int64_t)x != c && x < c) vb2[atomicAdd(&ctl.n_vb2, 1)] = x;
+            // distinct (value, count) pairs for the modular walks (G11: order free)
+            for (int v = threadIdx.x + 1; v <= c; v += NT) {
+                const int n = m.cnt[v + 1];
+                if (n) {
+                    const int i = atomicAdd(&ctl.n_dist, 1);
+                    m.dval[i] = v;
+                    m.dcnt[i] = n;
+                    if (2 * (int64_t)v != c && v < c) {
+                        const int j = atomicAdd(&ctl.n_vb2, 1);
+                        m.vb2[j] = v;
+                        m.vb2c[j] = n;
+                    }
+                }
             }
+            __syncthreads();
+            block_table_scan(m.cnt, m.pre, (int)(c + 2), ctl.wsum, ctl.wsum2);
         } else {
-            block_sort(sw, pw);
-            block_prefix_i64(sw, pre, r, scratch);
+            block_sort(m.sw, pw);
+            block_prefix_i64(m.sw, m.pre, r, ctl.wsum);
             const NodeStats& st = ctl.st;
             const int nm = st.n_big - st.n_full;
             for (int i = threadIdx.x; i < st.n_small + nm; i += NT)
-                vb2[i] = i < st.n_small ? sw[i] : sw[i + st.n_eq];
+                m.vb2[i] = i < st.n_small ? m.sw[i] : m.sw[i + st.n_eq];
+            // bucket index: bidx[b] = #{w < b << k}
+            const int nb = (int)(c >> m.bk) + 1;
+            for (int b = threadIdx.x; b <= nb; b += NT) {
+                const int64_t v = (int64_t)b << m.bk;
+                int lo = 0, hi = r;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if ((int64_t)m.sw[mid] < v) lo = mid + 1; else hi = mid;
+                }
+                m.bidx[b] = b == nb ? r : lo;
+            }
             if (threadIdx.x == 0) ctl.n_vb2 = st.n_small + nm;
         }
         if (threadIdx.x == 0) {
@@ -402,7 +545,6 @@ __global__ void __launch_bounds__(NT) node_kernel(KParams p, int rcap) {
                 if (!kind_in(p, kd)) hi = lo - 1;
                 ctl.lo[kd] = lo; ctl.hi[kd] = hi;
             }
-            // segment order: kinds in p.kinds order
             for (int i = 0; i < p.nk; ++i) add_kind_segs(ctl, p.kinds[i], TABLE, c);
             if (ctl.bad) {
                 ctl.nunits = 0; ctl.nseg = 0;
@@ -412,49 +554,11 @@ __global__ void __launch_bounds__(NT) node_kernel(KParams p, int rcap) {
         __syncthreads();
         // ---- sweep -------------------------------------------------------------
         if (TABLE) {
-            LkTable lk{cnt, pre, c};
-            if (phased) {
-                for (int i = 0; i < p.nk; ++i) {
-                    const int kd = p.kinds[i];
-                    if (threadIdx.x == 0) {
-                        const int f = ctl.kind_seg_first[kd], n = ctl.kind_seg_count[kd];
-                        ctl.unit_next = n ? ctl.segs[f].first : 0;
-                        ctl.unit_end = n ? ctl.segs[f + n - 1].first + ctl.segs[f + n - 1].count : 0;
-                        ctl.n_done = i + 1;
-                    }
-                    __syncthreads();
-                    run_units(p, ctl, lk, sw, vb2, tot, ztot, single, false);
-                    __syncthreads();
-                    if ((int64_t)ctl.lb > p.k) break;
-                }
-            } else {
-                if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
-                __syncthreads();
-                run_units(p, ctl, lk, sw, vb2, tot, ztot, single, cancel);
-            }
+            LkTable lk{m.cnt, m.pre, c};
+            sweep_node<TABLE>(p, ctl, lk, m, single, phased, cancel);
         } else {
-            int top = 0;
-            if (r > 0) { top = 1; while (top * 2 <= r) top *= 2; }
-            LkSorted lk{sw, pre, r, top};
-            if (phased) {
-                for (int i = 0; i < p.nk; ++i) {
-                    const int kd = p.kinds[i];
-                    if (threadIdx.x == 0) {
-                        const int f = ctl.kind_seg_first[kd], n = ctl.kind_seg_count[kd];
-                        ctl.unit_next = n ? ctl.segs[f].first : 0;
-                        ctl.unit_end = n ? ctl.segs[f + n - 1].first + ctl.segs[f + n - 1].count : 0;
-                        ctl.n_done = i + 1;
-                    }
-                    __syncthreads();
-                    run_units(p, ctl, lk, sw, vb2, tot, ztot, single, false);
-                    __syncthreads();
-                    if ((int64_t)ctl.lb > p.k) break;
-                }
-            } else {
-                if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
-                __syncthreads();
-                run_units(p, ctl, lk, sw, vb2, tot, ztot, single, cancel);
-            }
+            LkBucket lk{m.sw, m.pre, m.bidx, r, m.bk, c};
+            sweep_node<TABLE>(p, ctl, lk, m, single, phased, cancel);
         }
         __syncthreads();
         // ---- outputs ----------------------------------------------------------

@@ -1,0 +1,320 @@
+// bplb_warp.cuh -- warp-per-node kernel for batches of small-capacity search
+// nodes (cfg2: c = 150, r ~ 400, 1e4 nodes).  Each warp owns one reduced
+// instance at a time: a histogram of its weights over [0, c] in the warp's
+// slice of shared memory, the cumulative count / weight tables (warp scan),
+// the multiset compressed to distinct (value, count) pairs, then every kind
+// in order -- lookups one lambda per lane, VB2/FS1 as the weighted modular
+// walk.  No block barriers; per-node fixed cost is a few hundred
+// instructions instead of a CTA-wide setup.
+#pragma once
+#include "bplb_node.cuh"
+
+namespace bplb {
+
+constexpr int WNT = 256;                 // threads per CTA
+constexpr int WNW = WNT / 32;            // warps (= nodes in flight) per CTA
+constexpr int WARP_MAX_C = 1024;         // capacity limit of the warp kernel
+
+// Per-warp shared-memory slice (bytes), 16-byte aligned.
+__host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t warp_slice_bytes(int64_t c) {
+    const size_t n = (size_t)(c + 2), d = (size_t)(c + 1);
+    return al16(n * 8) + al16(n * 4) + 4 * al16(d * 4) + 2 * al16(d * 8) + 256;
+}
+
+// lane-local running best for one kind: higher bound wins, lower lambda on ties
+struct Best {
+    int64_t b;
+    int64_t lam;
+    __device__ __forceinline__ void offer(int64_t bd, int64_t l) {
+        if (bd > b || (bd == b && l < lam)) { b = bd; lam = l; }
+    }
+};
+
+__device__ __forceinline__ Best warp_best(Best x) {
+    const uint32_t bv = x.b >= 0 ? (uint32_t)x.b + 1u : 0u;
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, bv);
+    const uint32_t lr = (bv == mx && mx) ? (uint32_t)x.lam : 0xFFFFFFFFu;
+    const uint32_t mn = __reduce_min_sync(0xffffffffu, lr);
+    Best r;
+    r.b = mx ? (int64_t)(mx - 1u) : -1;
+    r.lam = mx ? (int64_t)mn : -1;
+    return r;
+}
+
+// ceil(S / F) with a 32-bit divide when S fits (always for small c).
+__device__ __forceinline__ int64_t bound_fast(int64_t S, int64_t F) {
+    if (F <= 0) return 0;
+    if (((uint64_t)S >> 32) == 0 && ((uint64_t)F >> 32) == 0) {
+        const uint32_t s = (uint32_t)S, f = (uint32_t)F;
+        return (int64_t)(s / f + (s % f != 0));
+    }
+    return bplb_bound(S, F);
+}
+
+// 32-bit table lookups for c <= WARP_MAX_C (index x+1 for x in [-1, c]).
+struct Lk32 {
+    const int* cnt;
+    const long long* wle;
+    int c;
+    __device__ __forceinline__ int ix(int x) const { return (x < -1 ? -1 : (x > c ? c : x)) + 1; }
+    __device__ __forceinline__ int n(int x) const { return cnt[ix(x)]; }
+    __device__ __forceinline__ void both(int x, int* nn, long long* w) const {
+        const int i = ix(x);
+        *nn = cnt[i];
+        *w = wle[i];
+    }
+};
+
+// _sweep_mt / _sweep_rad2 (bounds.py:373-387) with 32-bit lookups
+__device__ __forceinline__ long long mt32(const Lk32& lk, int c, int r, int lam) {
+    int n1, n0;
+    long long w1, w0;
+    lk.both(c - lam, &n1, &w1);
+    lk.both(lam - 1, &n0, &w0);
+    return (long long)c * (r - n1) + w1 - w0;
+}
+__device__ __forceinline__ long long rad2_32(const Lk32& lk, int c, int r, int lam) {
+    const int third = c / 3, half = c / 2;
+    const int a = lk.n(lam - 1), b = lk.n(c - 2 * lam), d = lk.n(2 * lam - 1), e = lk.n(c - lam);
+    return (long long)(b - a) * third + (long long)(d - b) * half + (long long)(e - d) * (c - third) +
+           (long long)(r - e) * c;
+}
+// harmonic parts (bounds.py:390-407, 441-460), t = t0, t0+dt, ...
+__device__ __forceinline__ long long ccm1_part32(const Lk32& lk, const NodeStats& st, int c, int lam, int t0,
+                                                 int dt) {
+    const int tmax = ((c - 1) / 2) / lam;
+    const int base = st.n_small + st.r - st.n_big;
+    long long acc = 0;
+    for (int t = t0; t <= tmax; t += dt) acc += base - lk.n(t * lam - 1) - lk.n(c - t * lam);
+    return acc;
+}
+__device__ __forceinline__ void bj1_part32(const Lk32& lk, const NodeStats& st, int c, int lam, int t0, int dt,
+                                           long long* fl_out, long long* rem_out) {
+    const int cm = c % lam, tmax = st.maxw / lam;
+    long long fl = 0, rem = 0;
+    for (int t = t0; t <= tmax; t += dt) {
+        const int lo_v = lam * t + cm, hi_v = lam * (t + 1) - 1;
+        int nl, nh;
+        long long wl, wh;
+        lk.both(lo_v, &nl, &wl);
+        lk.both(hi_v, &nh, &wh);
+        rem += (wh - wl) - (long long)lo_v * (nh - nl);
+        if (t < tmax) fl += st.r - nh;
+    }
+    *fl_out = fl;
+    *rem_out = rem;
+}
+
+__device__ __forceinline__ void warp_kind_range(const KParams& p, int kd, int64_t c, int r, int maxw,
+                                                int64_t* lo, int64_t* hi) {
+    bplb_domain(kd, c, lo, hi);
+    if (kd == K_VB2) *hi = bplb_vb2_hi(c, r, maxw);
+    if (!kind_in(p, kd)) *hi = *lo - 1;
+}
+
+__global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c = p.c;
+    const int n2 = (int)c + 2, d1 = (int)c + 1;
+    unsigned char* q = smem + warp_slice_bytes(c) * warp;
+    long long* wle = (long long*)q; q += al16((size_t)n2 * 8);
+    int* cnt = (int*)q; q += al16((size_t)n2 * 4);
+    int* dval = (int*)q; q += al16((size_t)d1 * 4);
+    int* dcnt = (int*)q; q += al16((size_t)d1 * 4);
+    int* vval = (int*)q; q += al16((size_t)d1 * 4);
+    int* vcnt = (int*)q; q += al16((size_t)d1 * 4);
+    u64* tot = (u64*)q; q += al16((size_t)d1 * 8);
+    u64* ztot = (u64*)q; q += al16((size_t)d1 * 8);
+    long long* kres = (long long*)q;  // per-kind best / arg (lane 0)
+    const bool phased = p.flags & BPLB_F_PHASED;
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
+    const uint32_t c32 = (uint32_t)c;
+    const u64 cinv = bplb_cinv(c32);
+    const uint32_t lt_mask = (1u << lane) - 1u;
+
+    for (int64_t node = (int64_t)blockIdx.x * WNW + warp; node < p.n_nodes;
+         node += (int64_t)gridDim.x * WNW) {
+        const int64_t base = p.off[node];
+        const int r = (int)(p.off[node + 1] - base);
+        for (int i = lane; i < n2; i += 32) cnt[i] = 0;
+        __syncwarp();
+        // ---- histogram + statistics ---------------------------------------
+        int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
+        long long l_W = 0, l_Vs = 0, l_Vm = 0;
+        for (int i = lane; i < r; i += 32) {
+            const int x = __ldg(p.w + base + i);
+            if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
+            l_max = max(l_max, x);
+            l_W += x;
+            if (2 * x < c) { l_s++; l_Vs += x; }
+            else if (2 * x == c) l_e++;
+            else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
+            atomicAdd(&cnt[x + 1], 1);
+        }
+        NodeStats st;
+        st.r = r;
+        st.maxw = (int32_t)__reduce_max_sync(0xffffffffu, (unsigned)l_max);
+        const bool bad = __reduce_or_sync(0xffffffffu, (unsigned)l_bad) != 0;
+        st.n_small = __reduce_add_sync(0xffffffffu, l_s);
+        st.n_eq = __reduce_add_sync(0xffffffffu, l_e);
+        st.n_big = __reduce_add_sync(0xffffffffu, l_b);
+        st.n_full = __reduce_add_sync(0xffffffffu, l_f);
+        st.W = (int64_t)warp_sum_u64((u64)l_W);
+        st.Vs = (int64_t)warp_sum_u64((u64)l_Vs);
+        st.Vm = (int64_t)warp_sum_u64((u64)l_Vm);
+        bplb_stats_finish(&st, c);
+        __syncwarp();
+        // ---- distinct (value, count) lists (ballot compaction) --------------
+        int nd = 0, nv = 0;
+        for (int v0 = 1; v0 <= c; v0 += 32) {
+            const int v = v0 + lane;
+            const int n = v <= c ? cnt[v + 1] : 0;
+            const uint32_t m1 = __ballot_sync(0xffffffffu, n > 0);
+            const bool isv = n > 0 && 2 * v != c && v < c;
+            const uint32_t m2 = __ballot_sync(0xffffffffu, isv);
+            if (n > 0) { const int pos = nd + __popc(m1 & lt_mask); dval[pos] = v; dcnt[pos] = n; }
+            if (isv) { const int pos = nv + __popc(m2 & lt_mask); vval[pos] = v; vcnt[pos] = n; }
+            nd += __popc(m1);
+            nv += __popc(m2);
+        }
+        // ---- cumulative tables (warp scan, index x+1 for x in [-1, c]) -------
+        {
+            long long rc = 0, rw = 0;
+            for (int i0 = 0; i0 < n2; i0 += 32) {
+                const int i = i0 + lane;
+                long long x = i < n2 ? cnt[i] : 0;
+                long long y = x * (i - 1);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long xo = __shfl_up_sync(0xffffffffu, x, o);
+                    const long long yo = __shfl_up_sync(0xffffffffu, y, o);
+                    if (lane >= o) { x += xo; y += yo; }
+                }
+                __syncwarp();
+                if (i < n2) { cnt[i] = (int)(rc + x); wle[i] = rw + y; }
+                rc += __shfl_sync(0xffffffffu, x, 31);
+                rw += __shfl_sync(0xffffffffu, y, 31);
+            }
+        }
+        __syncwarp();
+        const Lk32 lk{cnt, wle, (int)c};
+        const int ci = (int)c;
+        // ---- kinds in order --------------------------------------------------
+        long long* kbest = kres;          // per kind (lane-0 copies; all lanes read)
+        long long* karg = kres + K_COUNT;
+        int* keval = (int*)(kres + 2 * K_COUNT);
+        if (lane < K_COUNT) {
+            int64_t lo, hi;
+            warp_kind_range(p, lane, c, r, st.maxw, &lo, &hi);
+            kbest[lane] = 0;
+            karg[lane] = lo;
+            keval[lane] = 0;
+        }
+        __syncwarp();
+        int64_t lb = 0;
+        int n_done = 0;
+        for (int i = 0; i < p.nk && !bad; ++i) {
+            const int kd = p.kinds[i];
+            if (cancel && lb > p.k) continue;  // Alg. 3/4 guard: later kinds skip
+            n_done = i + 1;
+            int64_t lo, hi;
+            warp_kind_range(p, kd, c, r, st.maxw, &lo, &hi);
+            if (hi < lo) {
+                if (phased && lb > p.k) break;
+                continue;
+            }
+            Best bl{-1, 0};
+            if (kd == K_VB2 || kd == K_FS1) {
+                for (int64_t la = lo; la <= hi; la += d1) {
+                    const int L = (int)min((int64_t)d1, hi - la + 1);
+                    for (int j = lane; j < L; j += 32) { tot[j] = 0; ztot[j] = 0; }
+                    __syncwarp();
+                    if (kd == K_VB2) mod_walk<false, false, true>(vval, 0, nv, c32, cinv, la, L, tot, ztot, p.one, vcnt);
+                    else mod_walk<true, false, true>(dval, 0, nd, c32, cinv, la, L, tot, ztot, p.one, dcnt);
+                    __syncwarp();
+                    for (int j = lane; j < L; j += 32) {
+                        const int64_t lam = la + j;
+                        const int64_t S = kd == K_VB2 ? bplb_vb2_sum(st, c, lam, tot[j])
+                                                      : bplb_fs1_sum(st, lam, tot[j], ztot[j]);
+                        bl.offer(bound_fast(S, bplb_fc(kd, c, lam)), lam);
+                    }
+                    __syncwarp();
+                }
+            } else {
+                int l0 = (int)lo;
+                if (kd == K_CCM1 || kd == K_BJ1) {
+                    // small lambda: long harmonic loop, split it across the lanes
+                    const int span = kd == K_CCM1 ? (ci - 1) / 2 : st.maxw;
+                    const int lw = min((int)hi + 1, span / 16 + 1);
+                    for (; l0 < lw; ++l0) {
+                        int64_t S;
+                        if (kd == K_CCM1) {
+                            const long long part = (long long)warp_sum_u64((u64)ccm1_part32(lk, st, ci, l0, 1 + lane, 32));
+                            S = bplb_ccm1_from_part(st, c, l0, part);
+                        } else {
+                            long long fl, rem;
+                            bj1_part32(lk, st, ci, l0, lane, 32, &fl, &rem);
+                            fl = (long long)warp_sum_u64((u64)fl);
+                            rem = (long long)warp_sum_u64((u64)rem);
+                            S = bplb_bj1_from_parts(c, l0, fl, rem);
+                        }
+                        if (lane == 0) bl.offer(bound_fast(S, bplb_fc(kd, c, l0)), l0);
+                    }
+                }
+                for (int lam = l0 + lane; lam <= (int)hi; lam += 32) {
+                    int64_t S;
+                    switch (kd) {
+                    case K_MT: S = mt32(lk, ci, r, lam); break;
+                    case K_RAD2: S = rad2_32(lk, ci, r, lam); break;
+                    case K_CCM1: S = bplb_ccm1_from_part(st, c, lam, ccm1_part32(lk, st, ci, lam, 1, 1)); break;
+                    default: {
+                        long long fl, rem;
+                        bj1_part32(lk, st, ci, lam, 0, 1, &fl, &rem);
+                        S = bplb_bj1_from_parts(c, lam, fl, rem);
+                    }
+                    }
+                    bl.offer(bound_fast(S, bplb_fc(kd, c, lam)), lam);
+                }
+            }
+            const Best wb = warp_best(bl);
+            if (lane == 0) { kbest[kd] = wb.b; karg[kd] = wb.lam; keval[kd] = 1; }
+            if (wb.b > lb) lb = wb.b;
+            if (phased && lb > p.k) break;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (bad && p.err_out) atomicExch(p.err_out, 1);
+            if (p.lb_out) p.lb_out[node] = lb;
+            if (p.ex_out) p.ex_out[node] = (uint8_t)(lb > p.k);
+            if (p.best_out)
+                for (int kd = 0; kd < K_COUNT; ++kd) p.best_out[node * K_COUNT + kd] = keval[kd] ? kbest[kd] : 0;
+            if (p.arg_out)
+                for (int kd = 0; kd < K_COUNT; ++kd) p.arg_out[node * K_COUNT + kd] = karg[kd];
+            if (p.res_out) {
+                bplb_result res;
+                int64_t et = 0;
+                for (int kd = 0; kd < K_COUNT; ++kd) {
+                    int64_t lo, hi;
+                    warp_kind_range(p, kd, c, r, st.maxw, &lo, &hi);
+                    const int64_t nl = hi >= lo ? hi - lo + 1 : 0;
+                    res.best[kd] = keval[kd] ? kbest[kd] : 0;
+                    res.arg_lambda[kd] = karg[kd];
+                    res.n_lambda[kd] = nl;
+                    res.evals[kd] = keval[kd] ? nl : 0;
+                    res.evaluated[kd] = keval[kd];
+                    et += res.evals[kd];
+                }
+                res.lb = lb;
+                res.exceeded = lb > p.k;
+                res.n_done = n_done;
+                res.evals_total = et;
+                p.res_out[node] = res;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace bplb

@@ -23,13 +23,12 @@
 namespace bplb {
 
 constexpr int WT = 256;              // threads per CTA (wide kernels)
-constexpr int ISLICE = 32 * GMOD * 8; // items per modular tile (4096)
+constexpr int ISLICE = 32 * GMOD_MAX * 8; // items per modular tile (4096)
 constexpr int LLW = 128;             // lambdas per lane-lookup unit (4 x 32)
 constexpr int WIDE_MAX_SEGS = 3 * K_COUNT;
 constexpr int64_t WIDE_MAX_C = (int64_t)1 << 27;
 constexpr int SCAN_TILE = 4096;      // entries per scan block
 
-enum { T_WLOOK = 3 };  // warp-cooperative harmonic lookup: one lambda per unit
 
 struct WSeg {
     int kind, type;
@@ -62,8 +61,7 @@ struct WideState {
 
 struct WideBufs {
     WideState* state;
-    unsigned int* cnt;          // [c+2] histogram -> N<=(x) at index x+1
-    unsigned long long* wle;    // [c+2] W<=(x)
+    ulonglong2* rec;            // [c+2] {W<=(x), N<=(x)} at index x+1 (one 16-byte load)
     unsigned long long* bsum;   // [2 * nblocks] block sums for the scan
     int* vb2;                   // [r]
     unsigned long long* acc;    // [c+1] VB2 per-lambda D (indexed by lambda)
@@ -77,8 +75,7 @@ inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
     size_t b = 0;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     b += al(sizeof(WideState));
-    b += al((size_t)n * 4);
-    b += al((size_t)n * 8);
+    b += al((size_t)n * 16);
     b += al((size_t)nb * 16);
     b += al((size_t)std::max<int64_t>(r, 1) * 4);
     b += al((size_t)(c + 1) * 8);
@@ -92,8 +89,7 @@ inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
     char* p = (char*)base;
     WideBufs w;
     w.state = (WideState*)p; p += al(sizeof(WideState));
-    w.cnt = (unsigned int*)p; p += al((size_t)n * 4);
-    w.wle = (unsigned long long*)p; p += al((size_t)n * 8);
+    w.rec = (ulonglong2*)p; p += al((size_t)n * 16);
     w.bsum = (unsigned long long*)p; p += al((size_t)nb * 16);
     w.vb2 = (int*)p; p += al((size_t)std::max<int64_t>(r, 1) * 4);
     w.acc = (unsigned long long*)p; p += al((size_t)(c + 1) * 8);
@@ -106,7 +102,7 @@ __global__ void wide_init(WideBufs b, int64_t c) {
     const int64_t n = c + 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = i0; i < n; i += stride) { b.cnt[i] = 0; }
+    for (int64_t i = i0; i < n; i += stride) b.rec[i] = make_ulonglong2(0ull, 0ull);
     for (int64_t i = i0; i < c + 1; i += stride) b.acc[i] = 0;
     for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
     if (i0 == 0) {
@@ -128,7 +124,7 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
         if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
         else if (2 * (int64_t)x == c) l_e++;
         else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
-        atomicAdd(&b.cnt[x + 1], 1u);
+        atomicAdd(&b.rec[x + 1].y, 1ull);
         if (2 * (int64_t)x != c && x < c) b.vb2[atomicAdd(&b.state->n_vb2, 1)] = x;
     }
     l_max = __reduce_max_sync(0xffffffffu, (unsigned)l_max);
@@ -155,11 +151,11 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
 }
 
 // Block-level inclusive scan of (count, count*(i-1)) over one SCAN_TILE tile.
-__device__ __forceinline__ void tile_sums(const unsigned int* cnt, int64_t n, int64_t t0,
+__device__ __forceinline__ void tile_sums(const ulonglong2* rec, int64_t n, int64_t t0,
                                           unsigned long long* sc, unsigned long long* sw) {
     unsigned long long a = 0, bw = 0;
     for (int64_t i = t0 + threadIdx.x; i < min(n, t0 + SCAN_TILE); i += WT) {
-        unsigned long long x = cnt[i];
+        unsigned long long x = rec[i].y;
         a += x;
         bw += x * (unsigned long long)(i - 1);
     }
@@ -184,7 +180,7 @@ __global__ void __launch_bounds__(WT) wide_scan_reduce(WideBufs b, int64_t c) {
     __shared__ unsigned long long red[WT / 32];
     const int64_t n = c + 2;
     unsigned long long sc, sw;
-    tile_sums(b.cnt, n, (int64_t)blockIdx.x * SCAN_TILE, &sc, &sw);
+    tile_sums(b.rec, n, (int64_t)blockIdx.x * SCAN_TILE, &sc, &sw);
     unsigned long long tc = block_sum_u64(sc, red);
     unsigned long long tw = block_sum_u64(sw, red);
     if (threadIdx.x == 0) {
@@ -213,7 +209,7 @@ __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
     const int64_t t1 = min(n, t0 + SCAN_TILE);
     for (int64_t s = t0; s < t1; s += WT) {
         const int64_t i = s + threadIdx.x;
-        unsigned long long x = i < t1 ? b.cnt[i] : 0;
+        unsigned long long x = i < t1 ? b.rec[i].y : 0;
         unsigned long long y = x * (unsigned long long)(i - 1);
         // inclusive warp scan
 #pragma unroll
@@ -229,10 +225,7 @@ __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
             for (int j = 1; j <= WT / 32; ++j) { carry_c[j] += carry_c[j - 1]; carry_w[j] += carry_w[j - 1]; }
         }
         __syncthreads();
-        if (i < t1) {
-            b.cnt[i] = (unsigned int)(rc + carry_c[warp] + x);
-            b.wle[i] = rw + carry_w[warp] + y;
-        }
+        if (i < t1) b.rec[i] = make_ulonglong2(rw + carry_w[warp] + y, rc + carry_c[warp] + x);
         rc += carry_c[WT / 32];
         rw += carry_w[WT / 32];
         __syncthreads();
@@ -275,7 +268,8 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
         s->kind_seg_count[kind]++;
     };
     // Heavy modular units first in concurrent mode (longest-processing-time
-    // order); kind order in PHASED mode.
+    // order); kind order in PHASED / CANCEL mode so cheap early kinds can
+    // raise lb before later units start.
     int order[K_COUNT];
     int no = 0;
     if (!phased) {
@@ -300,12 +294,19 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
             break;
         }
         default: {
-            // CCM1 / BJ1: one warp per lambda while the harmonic loop is long
+            // CCM1 / BJ1: a dense pass over the items at small lambda (the
+            // harmonic loop would be ~span/lambda L2 lookups), one warp per
+            // lambda while the loop is still long, one lane per lambda after.
             const int64_t span = kd == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
+            const int64_t n = st.r > 0 ? st.r : 1;
+            int64_t sd = kd == K_CCM1 ? (64 * span) / (3 * n + 30) + 1 : (16 * span) / n + 1;
+            if (sd < lo) sd = lo;
+            if (sd > hi + 1) sd = hi + 1;
             int64_t sp = span / 64 + 1;
-            if (sp < lo) sp = lo;
+            if (sp < sd) sp = sd;
             if (sp > hi + 1) sp = hi + 1;
-            push(kd, T_WLOOK, lo, sp - 1, 1, 1);
+            push(kd, T_DIV, lo, sd - 1, st.r > 8192 ? 1 : 8, 1);
+            push(kd, T_WLOOK, sd, sp - 1, 1, 1);
             push(kd, T_LOOKUP, sp, hi, LLW, 1);
         }
         }
@@ -350,6 +351,20 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
             int64_t m = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
             wmax = m > wmax ? m : wmax;
         }
+    } else if (sg.type == T_DIV) {
+        const int64_t lam_a = sg.lo + rel * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        n_eval = lam_b - lam_a + 1;
+        int64_t mine = 0;
+        for (int64_t lam = lam_a; lam <= lam_b; ++lam) {
+            const int64_t S = kind == K_CCM1 ? ccm1_dense_raw(p.w, st.r, st, c, lam)
+                                             : bj1_dense(p.w, st.r, c, lam);
+            if (lam - lam_a == lane) mine = S;
+        }
+        const int64_t lam = lam_a + lane;
+        const bool valid = lam <= lam_b;
+        int64_t bd = valid ? bplb_bound(mine, bplb_fc(kind, c, lam)) : 0;
+        wmax = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
     } else if (sg.type == T_WLOOK) {
         const int64_t lam = sg.lo + rel;
         n_eval = 1;
@@ -443,7 +458,7 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
     }
     __syncthreads();
     if (skip) return;
-    const LkTableG lk{b.cnt, b.wle, p.c};
+    const LkTableG lk{b.rec, p.c};
     const bool cancel = (p.flags & BPLB_F_CANCEL) && phase_kind < 0;
     const int lane = threadIdx.x & 31;
     for (;;) {
@@ -581,7 +596,7 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     wide_scan_reduce<<<(unsigned)nb, WT, 0, st>>>(b, c);
     wide_scan_apply<<<(unsigned)nb, WT, 0, st>>>(b, c);
     wide_plan<<<1, 1, 0, st>>>(b, c, p.nk, nullptr, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3],
-                               ks[4], ks[5], phased ? 1 : 0);
+                               ks[4], ks[5], (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0);
     *launches += 5;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_units, WT, 0);
