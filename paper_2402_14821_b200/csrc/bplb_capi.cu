@@ -168,7 +168,8 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
     else while (rcap < max_r) rcap <<= 1;
     size_t smem = bplb::node_smem_bytes(table, rcap, p.c);
     if (smem > e->smem_optin) return fail(BPLB_ERANGE, "node needs more shared memory than available");
-    auto kern = table ? bplb::node_kernel<true> : bplb::node_kernel<false>;
+    auto kern = table ? bplb::node_kernel<true, false>
+                      : (p.c >= (1 << 23) ? bplb::node_kernel<false, true> : bplb::node_kernel<false, false>);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::NT, smem));

@@ -129,6 +129,26 @@ BPLB_HD int64_t bplb_vb2_sum(const NodeStats& st, int64_t c, int64_t lam, uint64
     return 2 * dB + ((int64_t)st.n_eq + 2 * (int64_t)st.n_big) * (lam - 1);
 }
 
+// FS1 zero-remainder term Z(lambda) = sum of w with c | w(lambda+1).  Those
+// are exactly the multiples of m = c / gcd(c, lambda+1), so with cumulative
+// tables Z = sum_j W(j m) - W(j m - 1) over j <= max_w / m (<= 101 terms).
+BPLB_HD int64_t bplb_gcd(int64_t a, int64_t b) {
+    while (b) { int64_t t = a % b; a = b; b = t; }
+    return a;
+}
+template <class L>
+BPLB_HD int64_t bplb_fs1_zero(const L& lk, int64_t c, int64_t maxw, int64_t lam) {
+    const int64_t m = c / bplb_gcd(c, lam + 1);
+    int64_t z = 0;
+    for (int64_t v = m; v <= maxw; v += m) {
+        int64_t n1, w1, n0, w0;
+        lk.both(v, &n1, &w1);
+        lk.both(v - 1, &n0, &w0);
+        z += w1 - w0;
+    }
+    return z;
+}
+
 // FS1 per-lambda transformed sum from P = sum of (w(lambda+1) mod c) and
 // Z = sum of w over items with zero remainder:
 //   f(w) = c*floor(w(lambda+1)/c) - [rem == 0]*w    (bounds.py:173-178, 305-307)
@@ -149,8 +169,24 @@ BPLB_HD int64_t bplb_fc(int kind, int64_t c, int64_t lam) {
     }
 }
 
+#if defined(__CUDACC__)
+// 64-bit ceil-division kept out of line: it is rare (S >= 2^32) and large.
+__device__ __noinline__ static uint64_t bplb_ceil_div64_slow(uint64_t s, uint64_t f) {
+    return (s + f - 1) / f;
+}
+#endif
+
 BPLB_HD int64_t bplb_bound(int64_t S, int64_t F) {
-    return F > 0 ? (int64_t)bplb_ceil_div((uint64_t)S, (uint64_t)F) : 0;
+    if (F <= 0) return 0;
+#if defined(__CUDA_ARCH__)
+    if ((((uint64_t)S | (uint64_t)F) >> 32) == 0) {
+        const uint32_t s = (uint32_t)S, f = (uint32_t)F;
+        return (int64_t)(s / f + (s % f != 0));
+    }
+    return (int64_t)bplb_ceil_div64_slow((uint64_t)S, (uint64_t)F);
+#else
+    return (int64_t)bplb_ceil_div((uint64_t)S, (uint64_t)F);
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -132,120 +132,98 @@ __device__ __forceinline__ T reduce8_transposed(T v[8], int lane) {
 
 // ---------------------------------------------------------------------------
 // Modular dense walk (VB2 and FS1).  For every item with weight w the state
-//   s(lambda) = (w * lambda - delta) mod c           (VB2: delta = [2w < c])
-//   s(lambda) = (w * (lambda + 1)) mod c             (FS1)
-// advances by s <- (s + w) mod c per lambda step, i.e. one IMAD-add plus one
-// VIADDMNMX (min(s + w, s + w - c), unsigned) per (item, lambda) cell.  The
-// warp accumulates, per lambda, D = sum of s (and for FS1, Z = sum of w over
-// s == 0) into per-warp shared arrays tot[0..L) / ztot[0..L) (added to, not
-// overwritten, so several item slices may accumulate).
+//   s(lambda) = (w * (lambda + ofs) - delta) mod c
+// (VB2: ofs = 0, delta = [2w < c];  FS1: ofs = 1, delta = 0) advances by
+// s <- (s + w) mod c per lambda step: one IMAD-add plus one VIADDMNMX
+// (min(s + w, s + w - c), unsigned) per (item, lambda) cell.  The warp
+// accumulates, per lambda, D = sum of s (weighted by the item's count for
+// distinct-value lists) into the per-warp shared array tot[0..L) (added to,
+// not overwritten, so several item slices may accumulate).  FS1's
+// zero-remainder term is recovered from the lookup tables (bplb_fs1_zero),
+// so FS1 and VB2 share this one loop.
 //
-// WIDE selects 64-bit lane partials (needed when 32 * GMOD * c >= 2^32).
+// WIDE selects 64-bit lane partials (needed when 32 * G * c >= 2^32).
 // ---------------------------------------------------------------------------
-template <bool FS1, bool WIDE, bool WEIGHTED, int GMOD>
+template <bool WIDE, bool WEIGHTED, int GMOD>
 __device__ __forceinline__ void mod_group(const int* __restrict__ items, int g, int i_end,
-                                          uint32_t c, u64 cinv, int64_t lam_a, int L,
-                                          u64* tot, u64* ztot, uint32_t one,
-                                          const int* __restrict__ counts) {
+                                          uint32_t c, u64 cinv, int64_t lam_a, int L, u64* tot,
+                                          uint32_t one, const int* __restrict__ counts, int ofs,
+                                          bool vb2) {
     const int lane = threadIdx.x & 31;
     const uint32_t negc = 0u - c;
-    {
-        uint32_t s[GMOD], u[GMOD], um[GMOD], cw[WEIGHTED ? GMOD : 1];
+    uint32_t s[GMOD], u[GMOD], um[GMOD], cw[WEIGHTED ? GMOD : 1];
+    const uint32_t mult = (uint32_t)(lam_a + ofs);
 #pragma unroll
-        for (int t = 0; t < GMOD; ++t) {
-            int idx = g + lane + kWarp * t;
-            uint32_t w = idx < i_end ? (uint32_t)items[idx] : 0u;
-            if (WEIGHTED) cw[t] = idx < i_end ? (uint32_t)counts[idx] : 0u;
-            u[t] = w;
-            um[t] = w + negc;
-            if (w == 0) {
-                s[t] = 0;
-            } else if (FS1) {
-                s[t] = bplb_mulmod(w, (uint32_t)(lam_a + 1), 0, c, cinv);
-            } else {
-                s[t] = bplb_mulmod(w, (uint32_t)lam_a, (2 * w < c) ? 1u : 0u, c, cinv);
-            }
-        }
-        for (int sb = 0; sb < L; sb += 8) {
-            typedef typename std::conditional<WIDE, u64, uint32_t>::type Acc;
-            Acc acc[8];
-            Acc zac[8];
+    for (int t = 0; t < GMOD; ++t) {
+        const int idx = g + lane + kWarp * t;
+        const uint32_t w = idx < i_end ? (uint32_t)items[idx] : 0u;
+        if (WEIGHTED) cw[t] = idx < i_end ? (uint32_t)counts[idx] : 0u;
+        u[t] = w;
+        um[t] = w + negc;
+        s[t] = w == 0 ? 0u : bplb_mulmod(w, mult, (vb2 && 2 * w < c) ? 1u : 0u, c, cinv);
+    }
+    typedef typename std::conditional<WIDE, u64, uint32_t>::type Acc;
+    for (int sb = 0; sb < L; sb += 8) {
+        Acc acc[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                acc[j] = 0;
-                if (FS1) zac[j] = 0;
+        for (int j = 0; j < 8; ++j) {
+            acc[j] = 0;
 #pragma unroll
-                for (int t = 0; t < GMOD; ++t) {
-                    if (WEIGHTED) {
-                        acc[j] += (Acc)s[t] * (Acc)cw[t];
-                        if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] * (Acc)cw[t] : (Acc)0;
-                    } else if (!WIDE && (t % 3) == 2) {
-                        // every third accumulate on the IMAD pipe: the walk is
-                        // ALU-bound (VIADDMNMX + IADD3), this balances the pipes
-                        uint32_t a = (uint32_t)acc[j];
-                        asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(a) : "r"(s[t]), "r"(one));
-                        acc[j] = (Acc)a;
-                        if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] : (Acc)0;
-                    } else {
-                        acc[j] += (Acc)s[t];
-                        if (FS1) zac[j] += (s[t] == 0) ? (Acc)u[t] : (Acc)0;
-                    }
-                    // s <- min(s + w, s + w - c)  (unsigned; exactly one is < c)
-                    uint32_t b;
-                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(s[t]), "r"(one), "r"(um[t]));
-                    s[t] = __viaddmin_u32(s[t], u[t], b);
+            for (int t = 0; t < GMOD; ++t) {
+                if (WEIGHTED) {
+                    acc[j] += (Acc)s[t] * (Acc)cw[t];
+                } else if (!WIDE && (t % 3) == 2) {
+                    // every third accumulate on the IMAD pipe: the walk is
+                    // ALU-bound (VIADDMNMX + IADD3), this balances the pipes
+                    uint32_t a = (uint32_t)acc[j];
+                    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(a) : "r"(s[t]), "r"(one));
+                    acc[j] = (Acc)a;
+                } else {
+                    acc[j] += (Acc)s[t];
                 }
-            }
-            u64 tot_j;
-            if (WIDE) {
-                u64 v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = (u64)acc[j];
-                tot_j = reduce8_transposed<u64>(v, lane);
-            } else {
-                uint32_t v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = (uint32_t)acc[j];
-                tot_j = (u64)reduce8_transposed<uint32_t>(v, lane);
-            }
-            u64 z_j = 0;
-            if (FS1) {
-                u64 v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) v[j] = (u64)zac[j];
-                z_j = reduce8_transposed<u64>(v, lane);
-            }
-            const int jj = sb + ((lane >> 2) & 7);
-            if ((lane & 3) == 0 && jj < L) {
-                tot[jj] += tot_j;
-                if (FS1) ztot[jj] += z_j;
+                // s <- min(s + w, s + w - c)  (unsigned; exactly one is < c)
+                uint32_t b;
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(s[t]), "r"(one), "r"(um[t]));
+                s[t] = __viaddmin_u32(s[t], u[t], b);
             }
         }
+        u64 tot_j;
+        if (WIDE) {
+            u64 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = (u64)acc[j];
+            tot_j = reduce8_transposed<u64>(v, lane);
+        } else {
+            uint32_t v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = (uint32_t)acc[j];
+            tot_j = (u64)reduce8_transposed<uint32_t>(v, lane);
+        }
+        const int jj = sb + ((lane >> 2) & 7);
+        if ((lane & 3) == 0 && jj < L) tot[jj] += tot_j;
     }
 }
 
-// Walk items [i_begin, i_end) in groups of 32 x G items, G chosen per group
-// so that short item lists are not padded to 512 slots.
-template <bool FS1, bool WIDE, bool WEIGHTED = false>
+// Walk items [i_begin, i_end) in groups of 32 x G items (G = 16 or 8;
+// 4 for weighted distinct-value lists).  ofs / vb2 select FS1 or VB2.
+template <bool WIDE, bool WEIGHTED = false>
 __device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_begin, int i_end,
-                                         uint32_t c, u64 cinv, int64_t lam_a, int L,
-                                         u64* tot, u64* ztot, uint32_t one,
+                                         uint32_t c, u64 cinv, int64_t lam_a, int L, u64* tot,
+                                         uint32_t one, bool vb2,
                                          const int* __restrict__ counts = nullptr) {
+    const int ofs = vb2 ? 0 : 1;
     int g = i_begin;
     while (g < i_end) {
         const int rem = i_end - g;
-        if (!WEIGHTED && rem > 8 * kWarp) {
-            mod_group<FS1, WIDE, WEIGHTED, 16>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
-            g += 16 * kWarp;
-        } else if (!WEIGHTED && rem > 4 * kWarp) {
-            mod_group<FS1, WIDE, WEIGHTED, 8>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
-            g += 8 * kWarp;
-        } else if (WEIGHTED || rem > 2 * kWarp) {
-            mod_group<FS1, WIDE, WEIGHTED, 4>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
+        if (WEIGHTED) {
+            mod_group<WIDE, WEIGHTED, 4>(items, g, i_end, c, cinv, lam_a, L, tot, one, counts, ofs, vb2);
             g += 4 * kWarp;
+        } else if (rem > 8 * kWarp) {
+            mod_group<WIDE, WEIGHTED, 16>(items, g, i_end, c, cinv, lam_a, L, tot, one, counts, ofs, vb2);
+            g += 16 * kWarp;
         } else {
-            mod_group<FS1, WIDE, WEIGHTED, 2>(items, g, i_end, c, cinv, lam_a, L, tot, ztot, one, counts);
-            g += 2 * kWarp;
+            mod_group<WIDE, WEIGHTED, 8>(items, g, i_end, c, cinv, lam_a, L, tot, one, counts, ofs, vb2);
+            g += 8 * kWarp;
         }
     }
 }

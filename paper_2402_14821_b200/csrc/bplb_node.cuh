@@ -92,7 +92,6 @@ struct NodeMem {  // shared-memory views of one node
     int* dval;        // TABLE: distinct values
     int* dcnt;        // TABLE: their counts
     u64* tot;
-    u64* ztot;
     int bk;           // SORT: bucket shift
 };
 
@@ -161,7 +160,7 @@ __device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c) {
     }
 }
 
-template <bool TABLE, class LK>
+template <bool TABLE, bool WIDE, class LK>
 __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m, int u,
                          bool single) {
     const int lane = threadIdx.x & 31;
@@ -218,24 +217,17 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
     } else {
         const int warp = threadIdx.x >> 5;
         u64* t = m.tot + warp * LMOD;
-        u64* z = m.ztot + warp * LMOD;
         const int L = (int)(lam_b - lam_a + 1);
-        for (int j = lane; j < L; j += kWarp) { t[j] = 0; z[j] = 0; }
+        for (int j = lane; j < L; j += kWarp) t[j] = 0;
         __syncwarp();
         const uint32_t c32 = (uint32_t)c;
         const u64 cinv = bplb_cinv(c32);
         if (TABLE) {  // distinct values x counts (c small: never wide)
-            if (kind == K_VB2) mod_walk<false, false, true>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one, m.vb2c);
-            else mod_walk<true, false, true>(m.dval, 0, ctl.n_dist, c32, cinv, lam_a, L, t, z, p.one, m.dcnt);
+            if (kind == K_VB2) mod_walk<false, true>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, p.one, true, m.vb2c);
+            else mod_walk<false, true>(m.dval, 0, ctl.n_dist, c32, cinv, lam_a, L, t, p.one, false, m.dcnt);
         } else {
-            const bool wide = c >= (1 << 23);
-            if (kind == K_VB2) {
-                if (wide) mod_walk<false, true>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
-                else mod_walk<false, false>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, z, p.one);
-            } else {
-                if (wide) mod_walk<true, true>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
-                else mod_walk<true, false>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, z, p.one);
-            }
+            if (kind == K_VB2) mod_walk<WIDE>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, p.one, true);
+            else mod_walk<WIDE>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, p.one, false);
         }
         __syncwarp();
         wmax = -1;
@@ -245,7 +237,8 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
             const int64_t lam = lam_a + j;
             int64_t S = 0;
             if (valid)
-                S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j]) : bplb_fs1_sum(st, lam, t[j], z[j]);
+                S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j])
+                                    : bplb_fs1_sum(st, lam, t[j], (uint64_t)bplb_fs1_zero(lk, c, st.maxw, lam));
             int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
             int64_t mm = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
             wmax = mm > wmax ? mm : wmax;
@@ -259,7 +252,7 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
 }
 
 // Process units [ctl.unit_next, ctl.unit_end) with all warps.
-template <bool TABLE, class LK>
+template <bool TABLE, bool WIDE, class LK>
 __device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m,
                           bool single, bool cancel) {
     const int lane = threadIdx.x & 31;
@@ -272,7 +265,7 @@ __device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const No
             int cur = *(volatile int*)&ctl.lb;
             if ((int64_t)cur > p.k) continue;  // Alg. 4 guard
         }
-        run_unit<TABLE>(p, ctl, lk, m, u, single);
+        run_unit<TABLE, WIDE>(p, ctl, lk, m, u, single);
     }
 }
 
@@ -280,7 +273,7 @@ __device__ void run_units(const KParams& p, NodeCtl& ctl, const LK& lk, const No
 // best exceeds k -- bounds.py:523-525; CANCEL: skip later kinds once lb > k,
 // the Alg. 3/4 per-launch guard, and skip units inside a kind too).  Without
 // either flag all units of all kinds are pulled from one counter.
-template <bool TABLE, class LK>
+template <bool TABLE, bool WIDE, class LK>
 __device__ void sweep_node(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m,
                            bool single, bool phased, bool cancel) {
     if (phased || cancel) {
@@ -294,14 +287,14 @@ __device__ void sweep_node(const KParams& p, NodeCtl& ctl, const LK& lk, const N
                 if (!ctl.skip) ctl.n_done = i + 1;
             }
             __syncthreads();
-            if (!ctl.skip) run_units<TABLE>(p, ctl, lk, m, single, cancel);
+            if (!ctl.skip) run_units<TABLE, WIDE>(p, ctl, lk, m, single, cancel);
             __syncthreads();
             if (phased && (int64_t)ctl.lb > p.k) break;
         }
     } else {
         if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
         __syncthreads();
-        run_units<TABLE>(p, ctl, lk, m, single, false);
+        run_units<TABLE, WIDE>(p, ctl, lk, m, single, false);
     }
 }
 
@@ -389,7 +382,7 @@ __host__ __device__ inline int node_bucket_shift(int64_t c) {
 // Dynamic shared memory size of the node kernel.
 __host__ __device__ inline size_t node_smem_bytes(bool table, int rcap, int64_t c) {
     size_t s = 0;
-    s += (size_t)NW * LMOD * 8 * 2;        // tot, ztot
+    s += (size_t)NW * LMOD * 8;            // tot
     s += (size_t)rcap * 4;                 // sw
     if (table) {
         const size_t dc = (size_t)(rcap < c + 1 ? rcap : c + 1);
@@ -404,7 +397,8 @@ __host__ __device__ inline size_t node_smem_bytes(bool table, int rcap, int64_t 
     return s + 64;
 }
 
-template <bool TABLE>
+// WIDE: 64-bit lane partials in the modular walk, needed when c >= 2^23.
+template <bool TABLE, bool WIDE>
 __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ NodeCtl ctl;
@@ -413,7 +407,6 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
     {
         unsigned char* q = smem;
         m.tot = (u64*)q; q += NW * LMOD * 8;
-        m.ztot = (u64*)q; q += NW * LMOD * 8;
         if (TABLE) {
             const int dc = (int)(rcap < c + 1 ? rcap : c + 1);
             m.pre = (long long*)q; q += (c + 2) * 8;
@@ -555,10 +548,10 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
         // ---- sweep -------------------------------------------------------------
         if (TABLE) {
             LkTable lk{m.cnt, m.pre, c};
-            sweep_node<TABLE>(p, ctl, lk, m, single, phased, cancel);
+            sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
         } else {
             LkBucket lk{m.sw, m.pre, m.bidx, r, m.bk, c};
-            sweep_node<TABLE>(p, ctl, lk, m, single, phased, cancel);
+            sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
         }
         __syncthreads();
         // ---- outputs ----------------------------------------------------------

@@ -19,7 +19,7 @@ constexpr int WARP_MAX_C = 1024;         // capacity limit of the warp kernel
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
 __host__ __device__ inline size_t warp_slice_bytes(int64_t c) {
     const size_t n = (size_t)(c + 2), d = (size_t)(c + 1);
-    return al16(n * 8) + al16(n * 4) + 4 * al16(d * 4) + 2 * al16(d * 8) + 256;
+    return al16(n * 8) + al16(n * 4) + 4 * al16(d * 4) + al16(d * 8) + 256;
 }
 
 // lane-local running best for one kind: higher bound wins, lower lambda on ties
@@ -42,16 +42,6 @@ __device__ __forceinline__ Best warp_best(Best x) {
     return r;
 }
 
-// ceil(S / F) with a 32-bit divide when S fits (always for small c).
-__device__ __forceinline__ int64_t bound_fast(int64_t S, int64_t F) {
-    if (F <= 0) return 0;
-    if (((uint64_t)S >> 32) == 0 && ((uint64_t)F >> 32) == 0) {
-        const uint32_t s = (uint32_t)S, f = (uint32_t)F;
-        return (int64_t)(s / f + (s % f != 0));
-    }
-    return bplb_bound(S, F);
-}
-
 // 32-bit table lookups for c <= WARP_MAX_C (index x+1 for x in [-1, c]).
 struct Lk32 {
     const int* cnt;
@@ -66,44 +56,73 @@ struct Lk32 {
     }
 };
 
-// _sweep_mt / _sweep_rad2 (bounds.py:373-387) with 32-bit lookups
-__device__ __forceinline__ long long mt32(const Lk32& lk, int c, int r, int lam) {
-    int n1, n0;
-    long long w1, w0;
-    lk.both(c - lam, &n1, &w1);
-    lk.both(lam - 1, &n0, &w0);
-    return (long long)c * (r - n1) + w1 - w0;
-}
-__device__ __forceinline__ long long rad2_32(const Lk32& lk, int c, int r, int lam) {
-    const int third = c / 3, half = c / 2;
-    const int a = lk.n(lam - 1), b = lk.n(c - 2 * lam), d = lk.n(2 * lam - 1), e = lk.n(c - lam);
-    return (long long)(b - a) * third + (long long)(d - b) * half + (long long)(e - d) * (c - third) +
-           (long long)(r - e) * c;
-}
-// harmonic parts (bounds.py:390-407, 441-460), t = t0, t0+dt, ...
-__device__ __forceinline__ long long ccm1_part32(const Lk32& lk, const NodeStats& st, int c, int lam, int t0,
-                                                 int dt) {
-    const int tmax = ((c - 1) / 2) / lam;
-    const int base = st.n_small + st.r - st.n_big;
-    long long acc = 0;
-    for (int t = t0; t <= tmax; t += dt) acc += base - lk.n(t * lam - 1) - lk.n(c - t * lam);
-    return acc;
-}
-__device__ __forceinline__ void bj1_part32(const Lk32& lk, const NodeStats& st, int c, int lam, int t0, int dt,
-                                           long long* fl_out, long long* rem_out) {
-    const int cm = c % lam, tmax = st.maxw / lam;
-    long long fl = 0, rem = 0;
-    for (int t = t0; t <= tmax; t += dt) {
-        const int lo_v = lam * t + cm, hi_v = lam * (t + 1) - 1;
-        int nl, nh;
-        long long wl, wh;
-        lk.both(lo_v, &nl, &wl);
-        lk.both(hi_v, &nh, &wh);
-        rem += (wh - wl) - (long long)lo_v * (nh - nl);
-        if (t < tmax) fl += st.r - nh;
+// Partial transformed sums of the lookup kinds over a strided subset of the
+// harmonic terms t = t0, t0+dt, ... (MT / RAD2 have a single term, t0 == 0).
+// One out-of-line copy serves the lane-per-lambda and the warp-per-lambda
+// loops (keeps the warp kernel small enough for the instruction cache).
+//   MT   _sweep_mt   bounds.py:373-376    p1 = S
+//   RAD2 _sweep_rad2 bounds.py:379-387    p1 = S
+//   CCM1 _sweep_ccm1 bounds.py:390-407    p1 = sum_t (n_small - N(t l - 1)) - (N(c - t l) - (r - n_big))
+//   BJ1  _sweep_bj1  bounds.py:441-460    p1 = floor_sum part, p2 = rem_sum part
+__device__ __noinline__ void lookup_part(int kd, const Lk32& lk, const NodeStats& st, int c, int r, int lam,
+                                         int t0, int dt, long long* p1, long long* p2) {
+    long long a = 0, b = 0;
+    if (kd == K_MT) {
+        if (t0 == 0) {
+            int n1, n0;
+            long long w1, w0;
+            lk.both(c - lam, &n1, &w1);
+            lk.both(lam - 1, &n0, &w0);
+            a = (long long)c * (r - n1) + w1 - w0;
+        }
+    } else if (kd == K_RAD2) {
+        if (t0 == 0) {
+            const int third = c / 3, half = c / 2;
+            const int ia = lk.n(lam - 1), ib = lk.n(c - 2 * lam), id = lk.n(2 * lam - 1), ie = lk.n(c - lam);
+            a = (long long)(ib - ia) * third + (long long)(id - ib) * half + (long long)(ie - id) * (c - third) +
+                (long long)(r - ie) * c;
+        }
+    } else if (kd == K_CCM1) {
+        const int tmax = ((c - 1) / 2) / lam;
+        const int base = st.n_small + st.r - st.n_big;
+        for (int t = t0 + 1; t <= tmax; t += dt) a += base - lk.n(t * lam - 1) - lk.n(c - t * lam);
+    } else {
+        const int cm = c % lam, tmax = st.maxw / lam;
+        for (int t = t0; t <= tmax; t += dt) {
+            const int lo_v = lam * t + cm, hi_v = lam * (t + 1) - 1;
+            int nl, nh;
+            long long wl, wh;
+            lk.both(lo_v, &nl, &wl);
+            lk.both(hi_v, &nh, &wh);
+            b += (wh - wl) - (long long)lo_v * (nh - nl);
+            if (t < tmax) a += st.r - nh;
+        }
     }
-    *fl_out = fl;
-    *rem_out = rem;
+    *p1 = a;
+    *p2 = b;
+}
+
+__device__ __forceinline__ int64_t lookup_finish(int kd, const NodeStats& st, int64_t c, int64_t lam,
+                                                 long long p1, long long p2) {
+    if (kd == K_CCM1) return bplb_ccm1_from_part(st, c, lam, p1);
+    if (kd == K_BJ1) return bplb_bj1_from_parts(c, lam, p1, p2);
+    return p1;
+}
+
+// FS1 zero-remainder term with 32-bit lookups (see bplb_fs1_zero).
+__device__ __forceinline__ long long fs1_zero32(const Lk32& lk, int c, int maxw, int lam) {
+    int a = c, b = lam + 1;
+    while (b) { const int t = a % b; a = b; b = t; }
+    const int m = c / a;
+    long long z = 0;
+    for (int v = m; v <= maxw; v += m) {
+        int n1, n0;
+        long long w1, w0;
+        lk.both(v, &n1, &w1);
+        lk.both(v - 1, &n0, &w0);
+        z += w1 - w0;
+    }
+    return z;
 }
 
 __device__ __forceinline__ void warp_kind_range(const KParams& p, int kd, int64_t c, int r, int maxw,
@@ -126,7 +145,6 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
     int* vval = (int*)q; q += al16((size_t)d1 * 4);
     int* vcnt = (int*)q; q += al16((size_t)d1 * 4);
     u64* tot = (u64*)q; q += al16((size_t)d1 * 8);
-    u64* ztot = (u64*)q; q += al16((size_t)d1 * 8);
     long long* kres = (long long*)q;  // per-kind best / arg (lane 0)
     const bool phased = p.flags & BPLB_F_PHASED;
     const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
@@ -227,55 +245,42 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
             }
             Best bl{-1, 0};
             if (kd == K_VB2 || kd == K_FS1) {
+                const bool isv = kd == K_VB2;
                 for (int64_t la = lo; la <= hi; la += d1) {
                     const int L = (int)min((int64_t)d1, hi - la + 1);
-                    for (int j = lane; j < L; j += 32) { tot[j] = 0; ztot[j] = 0; }
+                    for (int j = lane; j < L; j += 32) tot[j] = 0;
                     __syncwarp();
-                    if (kd == K_VB2) mod_walk<false, false, true>(vval, 0, nv, c32, cinv, la, L, tot, ztot, p.one, vcnt);
-                    else mod_walk<true, false, true>(dval, 0, nd, c32, cinv, la, L, tot, ztot, p.one, dcnt);
+                    mod_walk<false, true>(isv ? vval : dval, 0, isv ? nv : nd, c32, cinv, la, L, tot, p.one,
+                                          isv, isv ? vcnt : dcnt);
                     __syncwarp();
                     for (int j = lane; j < L; j += 32) {
-                        const int64_t lam = la + j;
-                        const int64_t S = kd == K_VB2 ? bplb_vb2_sum(st, c, lam, tot[j])
-                                                      : bplb_fs1_sum(st, lam, tot[j], ztot[j]);
-                        bl.offer(bound_fast(S, bplb_fc(kd, c, lam)), lam);
+                        const int lam = (int)la + j;
+                        const int64_t S = isv ? bplb_vb2_sum(st, c, lam, tot[j])
+                                              : bplb_fs1_sum(st, lam, tot[j], (uint64_t)fs1_zero32(lk, ci, st.maxw, lam));
+                        bl.offer(bplb_bound(S, bplb_fc(kd, c, lam)), lam);
                     }
                     __syncwarp();
                 }
             } else {
-                int l0 = (int)lo;
-                if (kd == K_CCM1 || kd == K_BJ1) {
-                    // small lambda: long harmonic loop, split it across the lanes
-                    const int span = kd == K_CCM1 ? (ci - 1) / 2 : st.maxw;
-                    const int lw = min((int)hi + 1, span / 16 + 1);
-                    for (; l0 < lw; ++l0) {
-                        int64_t S;
-                        if (kd == K_CCM1) {
-                            const long long part = (long long)warp_sum_u64((u64)ccm1_part32(lk, st, ci, l0, 1 + lane, 32));
-                            S = bplb_ccm1_from_part(st, c, l0, part);
-                        } else {
-                            long long fl, rem;
-                            bj1_part32(lk, st, ci, l0, lane, 32, &fl, &rem);
-                            fl = (long long)warp_sum_u64((u64)fl);
-                            rem = (long long)warp_sum_u64((u64)rem);
-                            S = bplb_bj1_from_parts(c, l0, fl, rem);
-                        }
-                        if (lane == 0) bl.offer(bound_fast(S, bplb_fc(kd, c, l0)), l0);
+                // small lambda with a long harmonic loop: one lambda per warp,
+                // the t-loop split across lanes; afterwards one lambda per lane
+                const int span = kd == K_CCM1 ? (ci - 1) / 2 : (kd == K_BJ1 ? st.maxw : 0);
+                const int lw = min((int)hi + 1, span / 16 + 1);
+                int lam = (int)lo;
+                bool coop = lam < lw;
+                while (true) {
+                    const int my = coop ? lam : lam + lane;
+                    long long p1 = 0, p2 = 0;
+                    if (my <= (int)hi) lookup_part(kd, lk, st, ci, r, my, coop ? lane : 0, coop ? 32 : 1, &p1, &p2);
+                    if (coop) {
+                        p1 = (long long)warp_sum_u64((u64)p1);
+                        p2 = (long long)warp_sum_u64((u64)p2);
                     }
-                }
-                for (int lam = l0 + lane; lam <= (int)hi; lam += 32) {
-                    int64_t S;
-                    switch (kd) {
-                    case K_MT: S = mt32(lk, ci, r, lam); break;
-                    case K_RAD2: S = rad2_32(lk, ci, r, lam); break;
-                    case K_CCM1: S = bplb_ccm1_from_part(st, c, lam, ccm1_part32(lk, st, ci, lam, 1, 1)); break;
-                    default: {
-                        long long fl, rem;
-                        bj1_part32(lk, st, ci, lam, 0, 1, &fl, &rem);
-                        S = bplb_bj1_from_parts(c, lam, fl, rem);
-                    }
-                    }
-                    bl.offer(bound_fast(S, bplb_fc(kd, c, lam)), lam);
+                    if ((!coop || lane == 0) && my <= (int)hi)
+                        bl.offer(bplb_bound(lookup_finish(kd, st, c, my, p1, p2), bplb_fc(kd, c, my)), my);
+                    lam += coop ? 1 : 32;
+                    if (lam > (int)hi) break;
+                    coop = lam < lw;
                 }
             }
             const Best wb = warp_best(bl);

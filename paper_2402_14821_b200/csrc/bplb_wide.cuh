@@ -105,10 +105,8 @@ __global__ void wide_init(WideBufs b, int64_t c) {
     for (int64_t i = i0; i < n; i += stride) b.rec[i] = make_ulonglong2(0ull, 0ull);
     for (int64_t i = i0; i < c + 1; i += stride) b.acc[i] = 0;
     for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
-    if (i0 == 0) {
-        WideState* s = b.state;
-        memset(s, 0, sizeof(WideState));
-    }
+    unsigned int* st = (unsigned int*)b.state;  // zero the state word by word
+    for (int64_t i = i0; i < (int64_t)(sizeof(WideState) / 4); i += stride) st[i] = 0u;
 }
 
 __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restrict__ w, int64_t r,
@@ -320,8 +318,9 @@ __device__ __forceinline__ int find_wseg(const WideState* s, long long u) {
 }
 
 // One warp unit of the wide path.
+template <bool WIDE>
 __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkTableG& lk,
-                          long long u, u64* tot, u64* ztot) {
+                          long long u, u64* tot) {
     const int lane = threadIdx.x & 31;
     const WSeg sg = s->segs[find_wseg(s, u)];
     const int kind = sg.kind;
@@ -393,24 +392,16 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
         const int i0 = slice * ISLICE, i1 = min(n_items, i0 + ISLICE);
         const int warp = threadIdx.x >> 5;
         u64* t = tot + warp * LMOD;
-        u64* z = ztot + warp * LMOD;
-        for (int j = lane; j < LMOD; j += kWarp) { t[j] = 0; z[j] = 0; }
+        for (int j = lane; j < LMOD; j += kWarp) t[j] = 0;
         __syncwarp();
         const uint32_t c32 = (uint32_t)c;
         const u64 cinv = bplb_cinv(c32);
-        const bool wide = c >= (1 << 23);
-        if (kind == K_VB2) {
-            if (wide) mod_walk<false, true>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
-            else mod_walk<false, false>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
-        } else {
-            if (wide) mod_walk<true, true>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
-            else mod_walk<true, false>(items, i0, i1, c32, cinv, lam_a, L, t, z, p.one);
-        }
+        mod_walk<WIDE>(items, i0, i1, c32, cinv, lam_a, L, t, p.one, kind == K_VB2);
         __syncwarp();
         if (sg.nslice > 1) {
             for (int j = lane; j < L; j += kWarp) {
                 if (kind == K_VB2) atomicAdd(&b.acc[lam_a + j], t[j]);
-                else { atomicAdd(&b.pz[lam_a + j], t[j]); atomicAdd(&b.pz[101 + lam_a + j], z[j]); }
+                else atomicAdd(&b.pz[lam_a + j], t[j]);
             }
             n_eval = slice == 0 ? L : 0;  // count each lambda once
         } else {
@@ -421,7 +412,8 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
                 const int64_t lam = lam_a + j;
                 int64_t S = 0;
                 if (valid)
-                    S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j]) : bplb_fs1_sum(st, lam, t[j], z[j]);
+                    S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j])
+                                        : bplb_fs1_sum(st, lam, t[j], (uint64_t)bplb_fs1_zero(lk, c, st.maxw, lam));
                 int64_t bd = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
                 int64_t m = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
                 wmax = m > wmax ? m : wmax;
@@ -437,9 +429,9 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
 
 // Persistent warp-unit kernel.  phase_kind >= 0 restricts to that kind's
 // segments (PHASED mode) and applies the Alg. 4 entry guard lb <= k.
+template <bool WIDE>
 __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phase_kind) {
     __shared__ u64 tot[(WT / 32) * LMOD];
-    __shared__ u64 ztot[(WT / 32) * LMOD];
     __shared__ long long u_begin, u_end;
     __shared__ int skip;
     WideState* s = b.state;
@@ -467,7 +459,7 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= u_end) break;
         if (cancel && (int64_t)(*(volatile int*)&s->lb) > p.k) continue;
-        wide_unit(p, b, s, lk, u, tot, ztot);
+        wide_unit<WIDE>(p, b, s, lk, u, tot);
     }
 }
 
@@ -500,7 +492,8 @@ __global__ void __launch_bounds__(WT) wide_final(KParams p, WideBufs b, int only
             int64_t S = 0;
             if (valid)
                 S = kd == K_VB2 ? bplb_vb2_sum(s->st, p.c, lam, b.acc[lam])
-                                : bplb_fs1_sum(s->st, lam, b.pz[lam], b.pz[101 + lam]);
+                                : bplb_fs1_sum(s->st, lam, b.pz[lam],
+                                               (uint64_t)bplb_fs1_zero(LkTableG{b.rec, p.c}, p.c, s->st.maxw, lam));
             int64_t bd = valid ? bplb_bound(S, bplb_fc(kd, p.c, lam)) : 0;
             int64_t m = emit_warp(valid, lam, bd, lo, &s->key[kd], p.lam_out, p.out_lo, p.out_hi);
             wmax = m > wmax ? m : wmax;
@@ -599,20 +592,22 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
                                ks[4], ks[5], (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0);
     *launches += 5;
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_units, WT, 0);
+    const bool wide = c >= (1 << 23);
+    auto units = wide ? wide_units<true> : wide_units<false>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, units, WT, 0);
     if (per_sm < 1) per_sm = 1;
     const int grid = per_sm * num_sms;
     const int g_fin = num_sms * 2;
     if (phased) {
         for (int i = 0; i < p.nk; ++i) {
             wide_phase_begin<<<1, 1, 0, st>>>(b, i);
-            wide_units<<<grid, WT, 0, st>>>(p, b, p.kinds[i]);
+            units<<<grid, WT, 0, st>>>(p, b, p.kinds[i]);
             wide_final<<<g_fin, WT, 0, st>>>(p, b, p.kinds[i]);
             wide_phase_end<<<1, 1, 0, st>>>(b, p.k);
             *launches += 4;
         }
     } else {
-        wide_units<<<grid, WT, 0, st>>>(p, b, -1);
+        units<<<grid, WT, 0, st>>>(p, b, -1);
         wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
         *launches += 2;
     }

@@ -219,7 +219,15 @@ int main(int argc, char** argv) {
                         }
                     unsigned long long D = 0, Z = 0;
                     for (size_t i = 0; i < items.size(); ++i) { D += s[i]; if (s[i] == 0) Z += items[i]; }
-                    got_s = got_t = kind == K_VB2 ? bplb_vb2_sum(st, c, lam, D) : bplb_fs1_sum(st, lam, D, Z);
+                    if (kind == K_VB2) {
+                        got_s = got_t = bplb_vb2_sum(st, c, lam, D);
+                    } else {
+                        // the kernels take Z from the lookup tables (multiples of c/gcd)
+                        CHECK((unsigned long long)bplb_fs1_zero(ls, c, st.maxw, lam) == Z, "fs1 zero sorted");
+                        CHECK((unsigned long long)bplb_fs1_zero(lt, c, st.maxw, lam) == Z, "fs1 zero table");
+                        got_s = bplb_fs1_sum(st, lam, D, (uint64_t)bplb_fs1_zero(ls, c, st.maxw, lam));
+                        got_t = bplb_fs1_sum(st, lam, D, (uint64_t)bplb_fs1_zero(lt, c, st.maxw, lam));
+                    }
                     break;
                 }
                 }
