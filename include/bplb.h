@@ -100,6 +100,14 @@ BPLB_API int bplb_check_batch(bplb_engine *eng, const int32_t *w_concat, const i
                      int32_t nkinds, int32_t flags, int64_t *lb_out, uint8_t *exceeded_out,
                      int64_t *best_out, int64_t *arg_out);
 
+/* bplb_check_batch with a compact weight dtype: wbytes = 4 (int32),
+ * 2 (uint16, c <= 65535) or 1 (uint8, c <= 255).  Halves / quarters the
+ * host->device bytes of a batch; values are validated on the device. */
+BPLB_API int bplb_check_batch_ex(bplb_engine *eng, const void *w_concat, int32_t wbytes,
+                        const int64_t *offsets, int64_t n_nodes, int64_t c, int64_t k,
+                        const int32_t *kinds, int32_t nkinds, int32_t flags, int64_t *lb_out,
+                        uint8_t *exceeded_out, int64_t *best_out, int64_t *arg_out);
+
 /* Same as bplb_check_batch with every array already resident in device
  * memory (`stream` is a cudaStream_t, or NULL for the engine's stream; pass
  * cudaStreamLegacy, i.e. (void*)1, for the legacy default stream).
@@ -111,6 +119,13 @@ BPLB_API int bplb_check_batch_device(bplb_engine *eng, const int32_t *d_w_concat
                             int64_t c, int64_t k, const int32_t *kinds, int32_t nkinds,
                             int32_t flags, int64_t *d_lb, uint8_t *d_exceeded,
                             int64_t *d_best, int64_t *d_arg, void *stream);
+
+/* Device-resident variant with a compact weight dtype (see _ex above). */
+BPLB_API int bplb_check_batch_device_ex(bplb_engine *eng, const void *d_w_concat, int32_t wbytes,
+                               const int64_t *d_offsets, int64_t n_nodes, int64_t max_r,
+                               int64_t c, int64_t k, const int32_t *kinds, int32_t nkinds,
+                               int32_t flags, int64_t *d_lb, uint8_t *d_exceeded,
+                               int64_t *d_best, int64_t *d_arg, void *stream);
 
 /* Number of kernel launches issued by the engine since creation (for the
  * bench's gpu_launches claim), and device time of the last TIMING call. */

@@ -58,9 +58,15 @@ SIGNATURES = {
     "bplb_check_batch": (ctypes.c_int, [_vp, _i32p, _i64p, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_int64, _i32p, ctypes.c_int32, ctypes.c_int32,
                                         _i64p, _u8p, _i64p, _i64p]),
+    "bplb_check_batch_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _i64p, ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_int64, _i32p, ctypes.c_int32,
+                                           ctypes.c_int32, _i64p, _u8p, _i64p, _i64p]),
     "bplb_check_batch_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
                                                ctypes.c_int64, ctypes.c_int64, _i32p, ctypes.c_int32,
                                                ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "bplb_check_batch_device_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
+                                                  ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i32p,
+                                                  ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "bplb_launch_count": (ctypes.c_int64, [_vp]),
     "bplb_last_device_ms": (ctypes.c_double, [_vp]),
     "bplb_last_error": (ctypes.c_char_p, []),
@@ -179,7 +185,13 @@ class Engine:
 
     def check_batch(self, w: np.ndarray, offsets: np.ndarray, c: int, k: int, kinds, flags: int,
                     want_best: bool = False, out=None):
-        w = as_i32(w)
+        """CSR batch; ``w`` may be int32, or uint16 / uint8 (compact: half /
+        a quarter of the host->device bytes), used as-is when contiguous."""
+        if isinstance(w, np.ndarray) and w.dtype in (np.uint16, np.uint8) and w.flags.c_contiguous:
+            wbytes = w.itemsize
+        else:
+            w = as_i32(w)
+            wbytes = 4
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         n = len(off) - 1
         ks = np.ascontiguousarray(kinds, dtype=np.int32)
@@ -190,8 +202,8 @@ class Engine:
             lb, ex = out
         best = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
         arg = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
-        rc = self._lib.bplb_check_batch(
-            self.handle, w.ctypes.data_as(_i32p), off.ctypes.data_as(_i64p), n, int(c), _clamp_k(k),
+        rc = self._lib.bplb_check_batch_ex(
+            self.handle, _vp(w.ctypes.data), wbytes, off.ctypes.data_as(_i64p), n, int(c), _clamp_k(k),
             ks.ctypes.data_as(_i32p), len(ks), int(flags), lb.ctypes.data_as(_i64p),
             ex.ctypes.data_as(_u8p),
             best.ctypes.data_as(_i64p) if best is not None else None,
@@ -204,10 +216,10 @@ class Engine:
 
     def check_batch_device(self, w_ptr: int, off_ptr: int, n_nodes: int, max_r: int, c: int, k: int,
                            kinds, flags: int, lb_ptr: int, ex_ptr: int, best_ptr: int = 0,
-                           arg_ptr: int = 0, stream_ptr: int = 0) -> None:
+                           arg_ptr: int = 0, stream_ptr: int = 0, wbytes: int = 4) -> None:
         ks = np.ascontiguousarray(kinds, dtype=np.int32)
-        rc = self._lib.bplb_check_batch_device(
-            self.handle, _vp(w_ptr), _vp(off_ptr), int(n_nodes), int(max_r), int(c), _clamp_k(k),
+        rc = self._lib.bplb_check_batch_device_ex(
+            self.handle, _vp(w_ptr), int(wbytes), _vp(off_ptr), int(n_nodes), int(max_r), int(c), _clamp_k(k),
             ks.ctypes.data_as(_i32p), len(ks), int(flags), _vp(lb_ptr), _vp(ex_ptr),
             _vp(best_ptr or None), _vp(arg_ptr or None), _vp(stream_ptr or None))
         if rc != 0:

@@ -32,6 +32,9 @@ def lower_bound_batch(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
                       want_best: bool = False, engine: _native.Engine | None = None):
     """Evaluate the LB collection for every node of a CSR batch on the GPU.
 
+    ``weights`` may be int32, or -- to cut host->device bytes -- uint16
+    (c <= 65535) / uint8 (c <= 255); values are validated on the device.
+
     mode: ``"full"`` (every kind completes; lb = max over kinds),
           ``"seq"`` (kinds in order, early exit once lb > k -- per node
           identical to lower_bound_seq's lb/exceeded_k),

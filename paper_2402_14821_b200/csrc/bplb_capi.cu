@@ -135,11 +135,12 @@ void fill_params(bplb::KParams& p, int64_t c, int64_t k, const int* kinds, int n
     p.nk = nk;
     p.flags = flags;
     p.one = 1;
+    p.wbytes = 4;
 }
 
 // Warp-per-node kernel for batches of small-capacity nodes.
 int launch_warp(bplb_engine* e, bplb::KParams& p, int64_t n_nodes) {
-    const size_t smem = bplb::warp_slice_bytes(p.c) * bplb::WNW;
+    const size_t smem = bplb::warp_cta_bytes(p.c) + bplb::warp_slice_bytes(p.c) * bplb::WNW;
     CUDA_TRY(cudaFuncSetAttribute(bplb::warp_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::warp_node_kernel, bplb::WNT, smem));
@@ -154,7 +155,7 @@ int launch_warp(bplb_engine* e, bplb::KParams& p, int64_t n_nodes) {
 
 bool warp_path(const bplb::KParams& p, int64_t n_nodes) {
     return p.lam_out == nullptr && p.c <= bplb::WARP_MAX_C && n_nodes >= 64 &&
-           bplb::warp_slice_bytes(p.c) * bplb::WNW <= 200 * 1024;
+           bplb::warp_cta_bytes(p.c) + bplb::warp_slice_bytes(p.c) * bplb::WNW <= 200 * 1024;
 }
 
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
@@ -353,6 +354,15 @@ int bplb_check_batch_device(bplb_engine* e, const int32_t* d_w, const int64_t* d
                             int64_t n_nodes, int64_t max_r, int64_t c, int64_t k,
                             const int32_t* kinds, int32_t nkinds, int32_t flags, int64_t* d_lb,
                             uint8_t* d_ex, int64_t* d_best, int64_t* d_arg, void* stream) {
+    return bplb_check_batch_device_ex(e, d_w, 4, d_off, n_nodes, max_r, c, k, kinds, nkinds, flags,
+                                      d_lb, d_ex, d_best, d_arg, stream);
+}
+
+int bplb_check_batch_device_ex(bplb_engine* e, const void* d_w, int32_t wbytes, const int64_t* d_off,
+                               int64_t n_nodes, int64_t max_r, int64_t c, int64_t k,
+                               const int32_t* kinds, int32_t nkinds, int32_t flags, int64_t* d_lb,
+                               uint8_t* d_ex, int64_t* d_best, int64_t* d_arg, void* stream) {
+    if (wbytes != 4 && wbytes != 2 && wbytes != 1) return fail(BPLB_EINVAL, "wbytes must be 4, 2 or 1");
     if (!e) return fail(BPLB_EINVAL, "null engine");
     if (n_nodes < 0 || max_r < 0) return fail(BPLB_EINVAL, "bad batch shape");
     if (int rc = check_c(c)) return rc;
@@ -364,7 +374,8 @@ int bplb_check_batch_device(bplb_engine* e, const int32_t* d_w, const int64_t* d
     CUDA_TRY(cudaSetDevice(e->device));
     bplb::KParams p;
     fill_params(p, c, k, ks, nkinds, flags);
-    p.w = d_w;
+    p.w = (const int*)d_w;
+    p.wbytes = wbytes;
     p.off = d_off;
     p.lb_out = d_lb;
     p.ex_out = d_ex;
@@ -379,9 +390,11 @@ int bplb_check_batch_device(bplb_engine* e, const int32_t* d_w, const int64_t* d
     return rc;
 }
 
-int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64_t n_nodes,
-                     int64_t c, int64_t k, const int32_t* kinds, int32_t nkinds, int32_t flags,
-                     int64_t* lb_out, uint8_t* ex_out, int64_t* best_out, int64_t* arg_out) {
+int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int64_t* off,
+                        int64_t n_nodes, int64_t c, int64_t k, const int32_t* kinds, int32_t nkinds,
+                        int32_t flags, int64_t* lb_out, uint8_t* ex_out, int64_t* best_out,
+                        int64_t* arg_out) {
+    if (wbytes != 4 && wbytes != 2 && wbytes != 1) return fail(BPLB_EINVAL, "wbytes must be 4, 2 or 1");
     if (!e) return fail(BPLB_EINVAL, "null engine");
     if (n_nodes < 0 || (n_nodes > 0 && (!off || !lb_out || !ex_out)))
         return fail(BPLB_EINVAL, "bad batch arguments");
@@ -404,6 +417,7 @@ int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64
     int rc;
     const bool timing = flags & BPLB_F_TIMING;
     if ((rc = e->d_w.grow((size_t)std::max<int64_t>(total, 1) * 4 + 64))) return rc;
+    const size_t wsz = (size_t)total * (size_t)wbytes;
     if ((rc = e->d_off.grow((size_t)(n_nodes + 1) * 8))) return rc;
     if ((rc = e->d_lb.grow((size_t)n_nodes * 8))) return rc;
     if ((rc = e->d_ex.grow((size_t)n_nodes))) return rc;
@@ -411,12 +425,13 @@ int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64
     if (arg_out && (rc = e->d_arg.grow((size_t)n_nodes * 48))) return rc;
     if ((rc = e->d_err.grow(16))) return rc;
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
-    if ((rc = h2d(e, e->d_w.p, w, (size_t)total * 4))) return rc;
-    if ((rc = h2d(e, e->d_off.p, off, (size_t)(n_nodes + 1) * 8, (size_t)total * 4 + 64))) return rc;
+    if ((rc = h2d(e, e->d_w.p, w, wsz))) return rc;
+    if ((rc = h2d(e, e->d_off.p, off, (size_t)(n_nodes + 1) * 8, wsz + 64))) return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
     bplb::KParams p;
     fill_params(p, c, k, ks, nkinds, flags);
     p.w = (const int*)e->d_w.p;
+    p.wbytes = wbytes;
     p.off = (const int64_t*)e->d_off.p;
     p.lb_out = (int64_t*)e->d_lb.p;
     p.ex_out = (uint8_t*)e->d_ex.p;
@@ -426,6 +441,7 @@ int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64
     if (max_r <= ((c <= bplb::TABLE_MAX_C) ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT)) {
         if ((rc = launch_node(e, p, n_nodes, max_r, 0))) return rc;
     } else {
+        if (wbytes != 4) return fail(BPLB_ERANGE, "nodes above the node-resident envelope need int32 weights");
         // nodes beyond the node-resident envelope go one by one through the
         // grid-wide path (rare: r > 8192)
         for (int64_t i = 0; i < n_nodes; ++i) {
@@ -457,6 +473,13 @@ int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64
     }
     if (err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
     return 0;
+}
+
+int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64_t n_nodes,
+                     int64_t c, int64_t k, const int32_t* kinds, int32_t nkinds, int32_t flags,
+                     int64_t* lb_out, uint8_t* ex_out, int64_t* best_out, int64_t* arg_out) {
+    return bplb_check_batch_ex(e, w, 4, off, n_nodes, c, k, kinds, nkinds, flags, lb_out, ex_out,
+                               best_out, arg_out);
 }
 
 }  // extern "C"

@@ -39,7 +39,8 @@ struct Seg {
 };
 
 struct KParams {
-    const int* w;          // CSR weights
+    const int* w;          // CSR weights (int32; reinterpreted per wbytes)
+    int wbytes;            // 4 (int32), 2 (uint16) or 1 (uint8) bytes per weight
     const int64_t* off;    // CSR offsets [n_nodes + 1]
     int64_t n_nodes;
     int64_t c;
@@ -94,6 +95,13 @@ struct NodeMem {  // shared-memory views of one node
     u64* tot;
     int bk;           // SORT: bucket shift
 };
+
+// Weight i of the CSR batch in its storage dtype (uniform branch).
+__device__ __forceinline__ int load_w(const KParams& p, int64_t i) {
+    if (p.wbytes == 2) return (int)__ldg((const unsigned short*)p.w + i);
+    if (p.wbytes == 1) return (int)__ldg((const unsigned char*)p.w + i);
+    return __ldg(p.w + i);
+}
 
 __device__ __forceinline__ bool kind_in(const KParams& p, int kind) {
     for (int i = 0; i < p.nk; ++i)
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
             for (int i = threadIdx.x; i < c + 2; i += NT) m.cnt[i] = 0;
         }
         for (int i = threadIdx.x; i < (TABLE ? r : pw); i += NT)
-            m.sw[i] = i < r ? __ldg(p.w + base + i) : INT_MAX;
+            m.sw[i] = i < r ? load_w(p, base + i) : INT_MAX;
         __syncthreads();
         // ---- statistics ------------------------------------------------------
         {

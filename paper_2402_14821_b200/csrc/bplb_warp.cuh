@@ -17,9 +17,15 @@ constexpr int WARP_MAX_C = 1024;         // capacity limit of the warp kernel
 
 // Per-warp shared-memory slice (bytes), 16-byte aligned.
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
+// CTA-wide tables for the FS1 zero-remainder term (shared by all warps):
+// divisors of c (<= 32 for c <= 1024), the divisor index of m_v = c/gcd(c,v)
+// for every value v, and for every FS1 lambda the mask of divisors m | lambda+1.
+__host__ __device__ inline size_t warp_cta_bytes(int64_t c) {
+    return al16(32 * 4) + al16(100 * 4) + al16((size_t)(c + 1));
+}
 __host__ __device__ inline size_t warp_slice_bytes(int64_t c) {
     const size_t n = (size_t)(c + 2), d = (size_t)(c + 1);
-    return al16(n * 8) + al16(n * 4) + 4 * al16(d * 4) + al16(d * 8) + 256;
+    return al16(n * 8) + al16(n * 4) + 4 * al16(d * 4) + al16(d * 8) + al16(32 * 8) + 256;
 }
 
 // lane-local running best for one kind: higher bound wins, lower lambda on ties
@@ -109,18 +115,11 @@ __device__ __forceinline__ int64_t lookup_finish(int kd, const NodeStats& st, in
     return p1;
 }
 
-// FS1 zero-remainder term with 32-bit lookups (see bplb_fs1_zero).
-__device__ __forceinline__ long long fs1_zero32(const Lk32& lk, int c, int maxw, int lam) {
-    int a = c, b = lam + 1;
-    while (b) { const int t = a % b; a = b; b = t; }
-    const int m = c / a;
-    long long z = 0;
-    for (int v = m; v <= maxw; v += m) {
-        int n1, n0;
-        long long w1, w0;
-        lk.both(v, &n1, &w1);
-        lk.both(v - 1, &n0, &w0);
-        z += w1 - w0;
+__device__ __forceinline__ u64 fs1_z(const u64* zacc, unsigned int mask) {
+    u64 z = 0;
+    while (mask) {
+        z += zacc[__ffs(mask) - 1];
+        mask &= mask - 1;
     }
     return z;
 }
@@ -137,7 +136,36 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t c = p.c;
     const int n2 = (int)c + 2, d1 = (int)c + 1;
-    unsigned char* q = smem + warp_slice_bytes(c) * warp;
+    int* divs = (int*)smem;
+    unsigned int* dmask = (unsigned int*)(smem + al16(32 * 4));
+    unsigned char* mdiv = smem + al16(32 * 4) + al16(100 * 4);
+    {
+        __shared__ int n_div;
+        if (threadIdx.x == 0) {
+            int nd = 0;
+            for (int d = 1; d <= (int)c && nd < 32; ++d)
+                if ((int)c % d == 0) divs[nd++] = d;
+            n_div = nd;
+        }
+        __syncthreads();
+        const int ndv = n_div;
+        for (int v = threadIdx.x; v <= (int)c; v += blockDim.x) {
+            int a = (int)c, b = v;
+            while (b) { const int t = a % b; a = b; b = t; }
+            const int m = (int)c / a;
+            int i = 0;
+            while (i < ndv && divs[i] != m) ++i;
+            mdiv[v] = (unsigned char)i;
+        }
+        for (int l = threadIdx.x; l < 100; l += blockDim.x) {
+            unsigned int mk = 0;
+            for (int i = 0; i < ndv; ++i)
+                if ((l + 2) % divs[i] == 0) mk |= 1u << i;  // lambda = l + 1 -> lambda + 1 = l + 2
+            dmask[l] = mk;
+        }
+        __syncthreads();
+    }
+    unsigned char* q = smem + warp_cta_bytes(c) + warp_slice_bytes(c) * warp;
     long long* wle = (long long*)q; q += al16((size_t)n2 * 8);
     int* cnt = (int*)q; q += al16((size_t)n2 * 4);
     int* dval = (int*)q; q += al16((size_t)d1 * 4);
@@ -145,6 +173,7 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
     int* vval = (int*)q; q += al16((size_t)d1 * 4);
     int* vcnt = (int*)q; q += al16((size_t)d1 * 4);
     u64* tot = (u64*)q; q += al16((size_t)d1 * 8);
+    u64* zacc = (u64*)q; q += al16(32 * 8);  // FS1: sum of v*count per divisor class
     long long* kres = (long long*)q;  // per-kind best / arg (lane 0)
     const bool phased = p.flags & BPLB_F_PHASED;
     const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
@@ -162,7 +191,7 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
         int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
         long long l_W = 0, l_Vs = 0, l_Vm = 0;
         for (int i = lane; i < r; i += 32) {
-            const int x = __ldg(p.w + base + i);
+            const int x = load_w(p, base + i);
             if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
             l_max = max(l_max, x);
             l_W += x;
@@ -246,6 +275,17 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
             Best bl{-1, 0};
             if (kd == K_VB2 || kd == K_FS1) {
                 const bool isv = kd == K_VB2;
+                if (!isv) {
+                    // Z(lambda) = sum of w with c | w(lambda+1) = sum over the
+                    // divisor classes m = c/gcd(c, v) with m | lambda+1
+                    zacc[lane] = 0;
+                    __syncwarp();
+                    for (int i = lane; i < nd; i += 32) {
+                        const int v = dval[i];
+                        atomicAdd(&zacc[mdiv[v]], (u64)v * (u64)dcnt[i]);
+                    }
+                    __syncwarp();
+                }
                 for (int64_t la = lo; la <= hi; la += d1) {
                     const int L = (int)min((int64_t)d1, hi - la + 1);
                     for (int j = lane; j < L; j += 32) tot[j] = 0;
@@ -256,7 +296,7 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
                     for (int j = lane; j < L; j += 32) {
                         const int lam = (int)la + j;
                         const int64_t S = isv ? bplb_vb2_sum(st, c, lam, tot[j])
-                                              : bplb_fs1_sum(st, lam, tot[j], (uint64_t)fs1_zero32(lk, ci, st.maxw, lam));
+                                              : bplb_fs1_sum(st, lam, tot[j], fs1_z(zacc, dmask[lam - 1]));
                         bl.offer(bplb_bound(S, bplb_fc(kd, c, lam)), lam);
                     }
                     __syncwarp();

@@ -213,3 +213,22 @@ def test_launch_counter_moves():
     before = eng.launch_count()
     G.lower_bound_seq(ReducedInstance(10, (6, 6, 6)), 3)
     assert eng.launch_count() > before
+
+
+def test_compact_weight_dtypes(oracle):
+    """uint16 / uint8 CSR weights give the same verdicts as int32."""
+    c, k, flat, off = W.cfg2_nodes(300)
+    ref = G.lower_bound_batch(c, flat, off, 2**62, want_best=True)
+    for dt in (np.uint16, np.uint8):
+        got = G.lower_bound_batch(c, flat.astype(dt), off, 2**62, want_best=True)
+        for a, b in zip(ref, got):
+            np.testing.assert_array_equal(a, b)
+    rng = np.random.default_rng(3)
+    c2 = 60000
+    nodes = [rng.integers(1, c2 + 1, int(L)) for L in rng.integers(0, 400, 40)]
+    w, off2 = G.csr_from_lists(nodes)
+    lb16, ex16 = G.lower_bound_batch(c2, w.astype(np.uint16), off2, 2**62)
+    lbo, exo = oracle.check_batch(w, off2, c2, 2**62)
+    np.testing.assert_array_equal(lb16, lbo)
+    with pytest.raises(ValueError):  # 0 is not a valid weight
+        G.lower_bound_batch(10, np.array([0, 3], dtype=np.uint8), np.array([0, 2]), 5)
