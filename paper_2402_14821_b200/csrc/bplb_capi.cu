@@ -83,6 +83,10 @@ struct bplb_engine {
     int num_sms = 0;
     size_t smem_optin = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;            // batch uploads
+    cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};  // chunk kernels
+    cudaEvent_t ev_up[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_k[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::mutex mu;
     DevBuf d_w, d_off, d_res, d_lb, d_ex, d_best, d_arg, d_err, d_lam, d_wide;
@@ -95,16 +99,21 @@ namespace {
 
 // Copy host -> device (direct DMA when the source is pinned, through the
 // engine's pinned staging buffer otherwise).
-int h2d(bplb_engine* e, void* dst, const void* src, size_t bytes, size_t stage_off = 0) {
+int h2d(bplb_engine* e, void* dst, const void* src, size_t bytes, size_t stage_off = 0,
+        cudaStream_t s = nullptr, int pinned = -1) {
     if (bytes == 0) return 0;
-    if (bytes <= 65536 || is_pinned(src)) {
-        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, e->stream));
+    if (!s) s = e->stream;
+    if (pinned < 0) pinned = bytes > 65536 ? is_pinned(src) : 1;
+    if (bytes <= 65536 || pinned) {
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return 0;
     }
-    if (int rc = e->h_stage.grow(stage_off + bytes)) return rc;
+    // pageable source: stage through the engine's pinned buffer (the buffer
+    // is grown by the caller before any chunk is enqueued)
+    if (stage_off + bytes > e->h_stage.cap) return fail(BPLB_ENOMEM, "staging buffer too small");
     char* st = (char*)e->h_stage.p + stage_off;
     std::memcpy(st, src, bytes);
-    CUDA_TRY(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyHostToDevice, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(dst, st, bytes, cudaMemcpyHostToDevice, s));
     return 0;
 }
 
@@ -211,8 +220,14 @@ int bplb_engine_create(int device, bplb_engine** out) {
     e->device = device;
     e->num_sms = prop.multiProcessorCount;
     e->smem_optin = prop.sharedMemPerBlockOptin;
-    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&e->ev0) != cudaSuccess || cudaEventCreate(&e->ev1) != cudaSuccess) {
+    bool ok = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreate(&e->ev0) == cudaSuccess && cudaEventCreate(&e->ev1) == cudaSuccess;
+    for (int i = 0; i < 4 && ok; ++i)
+        ok = cudaStreamCreateWithFlags(&e->cstream[i], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&e->ev_up[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&e->ev_k[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
         delete e;
         return fail(BPLB_ECUDA, "stream/event creation failed");
     }
@@ -231,6 +246,12 @@ int bplb_engine_destroy(bplb_engine* e) {
     e->h_res.release();
     cudaEventDestroy(e->ev0);
     cudaEventDestroy(e->ev1);
+    for (int i = 0; i < 4; ++i) {
+        cudaEventDestroy(e->ev_up[i]);
+        cudaEventDestroy(e->ev_k[i]);
+        cudaStreamDestroy(e->cstream[i]);
+    }
+    cudaStreamDestroy(e->copy_stream);
     cudaStreamDestroy(e->stream);
     delete e;
     return 0;
@@ -255,6 +276,8 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     if (int rc = e->d_err.grow(16)) return rc;
     if (int rc = e->h_res.grow(sizeof(bplb_result) + 16)) return rc;
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+    if ((size_t)r * 4 > 65536)
+        if (int rc = e->h_stage.grow((size_t)r * 4 + 64)) return rc;
     if (int rc = h2d(e, e->d_w.p, w, (size_t)r * 4)) return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
     bplb::KParams p;
@@ -313,6 +336,7 @@ int bplb_dff_bound_batch(bplb_engine* e, int32_t kind, const int32_t* w, int64_t
     if ((rc = e->d_res.grow(sizeof(bplb_result) + 16))) return rc;
     if ((rc = e->d_err.grow(16))) return rc;
     if ((rc = e->d_lam.grow((size_t)L * 8))) return rc;
+    if ((size_t)r * 4 > 65536 && (rc = e->h_stage.grow((size_t)r * 4 + 64))) return rc;
     if ((rc = h2d(e, e->d_w.p, w, (size_t)r * 4))) return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
     bplb::KParams p;
@@ -424,10 +448,10 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
     if (best_out && (rc = e->d_best.grow((size_t)n_nodes * 48))) return rc;
     if (arg_out && (rc = e->d_arg.grow((size_t)n_nodes * 48))) return rc;
     if ((rc = e->d_err.grow(16))) return rc;
+    const bool node_path = max_r <= ((c <= bplb::TABLE_MAX_C) ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT);
+    const bool pinned = wsz <= 65536 || is_pinned(w);
+    if (!pinned && (rc = e->h_stage.grow(wsz + 64 + (size_t)(n_nodes + 1) * 8))) return rc;
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
-    if ((rc = h2d(e, e->d_w.p, w, wsz))) return rc;
-    if ((rc = h2d(e, e->d_off.p, off, (size_t)(n_nodes + 1) * 8, wsz + 64))) return rc;
-    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
     bplb::KParams p;
     fill_params(p, c, k, ks, nkinds, flags);
     p.w = (const int*)e->d_w.p;
@@ -438,9 +462,49 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
     p.best_out = best_out ? (int64_t*)e->d_best.p : nullptr;
     p.arg_out = arg_out ? (int64_t*)e->d_arg.p : nullptr;
     p.err_out = (int*)e->d_err.p;
-    if (max_r <= ((c <= bplb::TABLE_MAX_C) ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT)) {
-        if ((rc = launch_node(e, p, n_nodes, max_r, 0))) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    // Chunked upload on the copy stream, one kernel per chunk on its own
+    // stream as soon as its bytes have landed: the PCIe transfer of chunk
+    // i+1 overlaps the kernel of chunk i, and chunk kernels overlap each
+    // other's tails.  Small batches use a single chunk.
+    int nch = node_path && n_nodes >= 4096 && wsz >= (size_t)1 << 20 ? 4 : 1;
+    int64_t bounds_[5];
+    for (int i = 0; i <= nch; ++i) bounds_[i] = n_nodes * i / nch;
+    if (nch > 1) {
+        // a smaller first chunk starts the GPU sooner
+        bounds_[1] = n_nodes / 8;
+        bounds_[2] = n_nodes * 3 / 8;
+        bounds_[3] = n_nodes * 5 / 8;
+    }
+    CUDA_TRY(cudaEventRecord(e->ev_k[0], e->stream));  // memset done before uploads land
+    CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->ev_k[0], 0));
+    if ((rc = h2d(e, e->d_off.p, off, (size_t)(n_nodes + 1) * 8, wsz + 64, e->copy_stream, pinned ? 1 : 0)))
+        return rc;
+    for (int i = 0; i < nch; ++i) {
+        const int64_t a = off[bounds_[i]], b = off[bounds_[i + 1]];
+        if ((rc = h2d(e, (char*)e->d_w.p + a * wbytes, (const char*)w + a * wbytes, (size_t)(b - a) * wbytes,
+                      (size_t)a * wbytes, e->copy_stream, pinned ? 1 : 0)))
+            return rc;
+        CUDA_TRY(cudaEventRecord(e->ev_up[i], e->copy_stream));
+    }
+    if (node_path) {
+        cudaStream_t saved = e->stream;
+        for (int i = 0; i < nch; ++i) {
+            cudaStream_t cs = nch == 1 ? saved : e->cstream[i];
+            CUDA_TRY(cudaStreamWaitEvent(cs, e->ev_up[i], 0));
+            bplb::KParams q = p;
+            q.node0 = bounds_[i];
+            e->stream = cs;
+            rc = launch_node(e, q, bounds_[i + 1] - bounds_[i], max_r, 0);
+            e->stream = saved;
+            if (rc) return rc;
+            if (nch > 1) {
+                CUDA_TRY(cudaEventRecord(e->ev_k[i], cs));
+                CUDA_TRY(cudaStreamWaitEvent(saved, e->ev_k[i], 0));
+            }
+        }
     } else {
+        CUDA_TRY(cudaStreamWaitEvent(e->stream, e->ev_up[0], 0));
         if (wbytes != 4) return fail(BPLB_ERANGE, "nodes above the node-resident envelope need int32 weights");
         // nodes beyond the node-resident envelope go one by one through the
         // grid-wide path (rare: r > 8192)

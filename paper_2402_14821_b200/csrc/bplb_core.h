@@ -125,7 +125,14 @@ BPLB_HD int64_t bplb_vb2_sum(const NodeStats& st, int64_t c, int64_t lam, uint64
     int64_t dn = (int64_t)st.n_small - n_m;
     int64_t dR = (int64_t)D - n_m * (c - 1);
     int64_t num = lam * st.dr - dn - dR;  // exact multiple of c
+#if defined(__CUDA_ARCH__)
+    // 32-bit divide when it fits (always for small c): 64-bit division is emulated
+    const int64_t q = (num == (int64_t)(int32_t)num && c <= 0x7FFFFFFF) ? (int64_t)((int32_t)num / (int32_t)c)
+                                                                        : num / c;
+    int64_t dB = lam * st.dq + q;
+#else
     int64_t dB = lam * st.dq + num / c;
+#endif
     return 2 * dB + ((int64_t)st.n_eq + 2 * (int64_t)st.n_big) * (lam - 1);
 }
 

@@ -41,8 +41,9 @@ struct Seg {
 struct KParams {
     const int* w;          // CSR weights (int32; reinterpreted per wbytes)
     int wbytes;            // 4 (int32), 2 (uint16) or 1 (uint8) bytes per weight
-    const int64_t* off;    // CSR offsets [n_nodes + 1]
-    int64_t n_nodes;
+    const int64_t* off;    // CSR offsets (global node index)
+    int64_t node0;         // first node of this launch
+    int64_t n_nodes;       // nodes [node0, node0 + n_nodes)
     int64_t c;
     int64_t k;
     int kinds[K_COUNT];
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
     const bool phased = p.flags & BPLB_F_PHASED;
     const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
 
-    for (int64_t node = blockIdx.x; node < p.n_nodes; node += gridDim.x) {
+    for (int64_t node = p.node0 + blockIdx.x; node < p.node0 + p.n_nodes; node += gridDim.x) {
         const int64_t base = p.off[node];
         const int r = (int)(p.off[node + 1] - base);
         if (threadIdx.x == 0) {

@@ -108,11 +108,24 @@ __device__ __noinline__ void lookup_part(int kd, const Lk32& lk, const NodeStats
     *p2 = b;
 }
 
-__device__ __forceinline__ int64_t lookup_finish(int kd, const NodeStats& st, int64_t c, int64_t lam,
-                                                 long long p1, long long p2) {
-    if (kd == K_CCM1) return bplb_ccm1_from_part(st, c, lam, p1);
-    if (kd == K_BJ1) return bplb_bj1_from_parts(c, lam, p1, p2);
-    return p1;
+// Bound of one lookup-kind lambda from its partial sums, 32-bit divisions
+// only (c <= WARP_MAX_C): bounds.py:376, 387, 407, 460 for F.
+__device__ __forceinline__ int64_t lookup_bound32(int kd, const NodeStats& st, int c, int lam,
+                                                  long long p1, long long p2) {
+    long long S, F;
+    if (kd == K_CCM1) {
+        const int cq = c / lam;
+        S = 2 * p1 + (long long)st.n_eq * cq + 2ll * st.n_big * cq;
+        F = 2ll * cq;
+    } else if (kd == K_BJ1) {
+        const int cq = c / lam, cm = c - cq * lam;
+        S = (long long)(lam - cm) * p1 + p2;
+        F = (long long)cq * (lam - cm);
+    } else {
+        S = p1;
+        F = c;
+    }
+    return bplb_bound(S, F);
 }
 
 __device__ __forceinline__ u64 fs1_z(const u64* zacc, unsigned int mask) {
@@ -181,7 +194,7 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
     const u64 cinv = bplb_cinv(c32);
     const uint32_t lt_mask = (1u << lane) - 1u;
 
-    for (int64_t node = (int64_t)blockIdx.x * WNW + warp; node < p.n_nodes;
+    for (int64_t node = p.node0 + (int64_t)blockIdx.x * WNW + warp; node < p.node0 + p.n_nodes;
          node += (int64_t)gridDim.x * WNW) {
         const int64_t base = p.off[node];
         const int r = (int)(p.off[node + 1] - base);
@@ -297,7 +310,7 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
                         const int lam = (int)la + j;
                         const int64_t S = isv ? bplb_vb2_sum(st, c, lam, tot[j])
                                               : bplb_fs1_sum(st, lam, tot[j], fs1_z(zacc, dmask[lam - 1]));
-                        bl.offer(bplb_bound(S, bplb_fc(kd, c, lam)), lam);
+                        bl.offer(bplb_bound(S, isv ? 2ll * (lam - 1) : (long long)ci * lam), lam);
                     }
                     __syncwarp();
                 }
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(WNT, 3) warp_node_kernel(KParams p) {
                         p2 = (long long)warp_sum_u64((u64)p2);
                     }
                     if ((!coop || lane == 0) && my <= (int)hi)
-                        bl.offer(bplb_bound(lookup_finish(kd, st, c, my, p1, p2), bplb_fc(kd, c, my)), my);
+                        bl.offer(lookup_bound32(kd, st, ci, my, p1, p2), my);
                     lam += coop ? 1 : 32;
                     if (lam > (int)hi) break;
                     coop = lam < lw;
