@@ -89,7 +89,7 @@ struct bplb_engine {
     cudaEvent_t ev_k[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::mutex mu;
-    DevBuf d_w, d_off, d_res, d_lb, d_ex, d_best, d_arg, d_err, d_lam, d_wide;
+    DevBuf d_w, d_off, d_res, d_lb, d_ex, d_best, d_arg, d_err, d_lam, d_wide, d_multi;
     HostBuf h_stage, h_res;
     int64_t launches = 0;
     double last_ms = 0.0;
@@ -168,8 +168,15 @@ bool warp_path(const bplb::KParams& p, int64_t n_nodes) {
 }
 
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
-int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r, int grid_cap) {
-    if (grid_cap == 0 && warp_path(p, n_nodes)) return launch_warp(e, p, n_nodes);
+// multi: one node, every CTA of a co-resident grid sweeps part of it
+// (single-check latency path); p.ms must point at a zeroed MultiState.
+bool node_fits(int64_t r, int64_t c) {
+    return r <= (c <= bplb::TABLE_MAX_C ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT);
+}
+
+int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r, int grid_cap,
+                bool multi = false) {
+    if (!multi && grid_cap == 0 && warp_path(p, n_nodes)) return launch_warp(e, p, n_nodes);
     const bool table = p.c <= bplb::TABLE_MAX_C;
     if (max_r > (table ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT))
         return fail(BPLB_ERANGE, "node larger than the node-resident envelope");
@@ -185,6 +192,11 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::NT, smem));
     if (per_sm < 1) per_sm = 1;
     int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
+    if (multi) {  // co-resident grid (CTAs may wait on each other), sized by the work
+        const int64_t cells = std::max<int64_t>(max_r, 1) * (3 * std::min<int64_t>(p.c, 1 << 24) + 100);
+        grid = std::min<int64_t>((int64_t)std::min(per_sm, 2) * e->num_sms,
+                                 std::max<int64_t>(1, cells / 16384));
+    }
     if (grid_cap > 0) grid = std::min<int64_t>(grid, grid_cap);
     if (grid < 1) return 0;
     p.n_nodes = n_nodes;
@@ -240,7 +252,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
-                      &e->d_err, &e->d_lam, &e->d_wide})
+                      &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -268,6 +280,9 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     if (int rc = check_c(c)) return rc;
     int ks[K_COUNT];
     if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
+    // every bound is <= r (f(w) <= f(c) for w <= c), so with k >= r no kind
+    // can exceed k: the early-exit / cancellation guards are moot
+    if (k >= r) flags &= ~(BPLB_F_PHASED | BPLB_F_CANCEL);
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
     const bool timing = flags & BPLB_F_TIMING;
@@ -286,17 +301,20 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     p.res_out = (bplb_result*)e->d_res.p;
     p.err_out = (int*)e->d_err.p;
     int rc;
-    if (bplb::wide_preferred(r, c)) {
+    if (!node_fits(r, c)) {
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);
         if (rc) return fail(rc, bplb::wide_error());
     } else {
-        // single node: offsets live in the tail of the result buffer
+        // single node: offsets and the cross-CTA state
         int64_t off_h[2] = {0, r};
         if ((rc = e->d_off.grow(16))) return rc;
+        if ((rc = e->d_multi.grow(sizeof(bplb::MultiState)))) return rc;
         CUDA_TRY(cudaMemcpyAsync(e->d_off.p, off_h, 16, cudaMemcpyHostToDevice, e->stream));
+        CUDA_TRY(cudaMemsetAsync(e->d_multi.p, 0, sizeof(bplb::MultiState), e->stream));
         p.off = (const int64_t*)e->d_off.p;
-        if ((rc = launch_node(e, p, 1, r, 1))) return rc;
+        p.ms = (bplb::MultiState*)e->d_multi.p;
+        if ((rc = launch_node(e, p, 1, r, 0, true))) return rc;
     }
     CUDA_TRY(cudaMemcpyAsync(e->h_res.p, e->d_res.p, sizeof(bplb_result), cudaMemcpyDeviceToHost,
                              e->stream));
@@ -355,16 +373,19 @@ int bplb_dff_bound_batch(bplb_engine* e, int32_t kind, const int32_t* w, int64_t
     }
     if (r == 0) {  // bounds.py:478-479
         CUDA_TRY(cudaMemsetAsync(e->d_lam.p, 0, (size_t)L * 8, e->stream));
-    } else if (bplb::wide_preferred(r, c)) {
+    } else if (!node_fits(r, c)) {
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);
         if (rc) return fail(rc, bplb::wide_error());
     } else {
         int64_t off_h[2] = {0, r};
         if ((rc = e->d_off.grow(16))) return rc;
+        if ((rc = e->d_multi.grow(sizeof(bplb::MultiState)))) return rc;
         CUDA_TRY(cudaMemcpyAsync(e->d_off.p, off_h, 16, cudaMemcpyHostToDevice, e->stream));
+        CUDA_TRY(cudaMemsetAsync(e->d_multi.p, 0, sizeof(bplb::MultiState), e->stream));
         p.off = (const int64_t*)e->d_off.p;
-        if ((rc = launch_node(e, p, 1, r, 1))) return rc;
+        p.ms = (bplb::MultiState*)e->d_multi.p;
+        if ((rc = launch_node(e, p, 1, r, 0, true))) return rc;
     }
     int err = 0;
     CUDA_TRY(cudaMemcpyAsync(out, e->d_lam.p, (size_t)L * 8, cudaMemcpyDeviceToHost, e->stream));
@@ -434,6 +455,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         max_r = std::max(max_r, d);
     }
     if (max_r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items in a node for the GPU envelope");
+    if (k >= max_r) flags &= ~(BPLB_F_PHASED | BPLB_F_CANCEL);  // no node can exceed k
     const int64_t total = off[n_nodes];
     if (total > 0 && !w) return fail(BPLB_EINVAL, "null weights");
     std::lock_guard<std::mutex> lock(e->mu);

@@ -38,7 +38,21 @@ struct Seg {
     int first, count; // unit index range
 };
 
+// Cross-CTA state of the multi-CTA mode (one node, many CTAs): zeroed by the
+// host before the launch.
+struct MultiState {
+    u64 key[K_COUNT];
+    int kmax[K_COUNT];     // per-kind running max (PHASED guard at kind boundaries)
+    unsigned long long evals[K_COUNT];
+    int evaluated[K_COUNT];
+    int lb;
+    int unit_next;
+    int units_done;
+    int ctas_done;
+};
+
 struct KParams {
+    MultiState* ms;        // non-null: every CTA works on node node0 (single check)
     const int* w;          // CSR weights (int32; reinterpreted per wbytes)
     int wbytes;            // 4 (int32), 2 (uint16) or 1 (uint8) bytes per weight
     const int64_t* off;    // CSR offsets (global node index)
@@ -256,7 +270,60 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
     if (lane == 0) {
         atomicAdd(&ctl.evals[kind], (unsigned long long)(lam_b - lam_a + 1));
         ctl.evaluated[kind] = 1;
-        if (wmax >= 0) atomicMax(&ctl.lb, (int)wmax);
+        if (wmax >= 0) {
+            atomicMax(&ctl.lb, (int)wmax);
+            if (p.ms) {
+                atomicMax(&p.ms->lb, (int)wmax);
+                atomicMax(&p.ms->kmax[kind], (int)wmax);
+            }
+        }
+    }
+}
+
+// Multi-CTA sweep of one node: units come from a global counter in kind
+// order.  PHASED / CANCEL: before the first unit of a later kind, wait until
+// every earlier unit has completed, then apply the guard lb <= k (a skipped
+// unit still counts as completed).  No CTA waits while holding an unfinished
+// unit (one unit per warp at a time) and the grid is co-resident, so the
+// waits cannot deadlock.
+template <bool TABLE, bool WIDE, class LK>
+__device__ void sweep_multi(const KParams& p, NodeCtl& ctl, const LK& lk, const NodeMem& m,
+                            bool single, bool guard, bool phased) {
+    const int lane = threadIdx.x & 31;
+    MultiState* ms = p.ms;
+    for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&ms->unit_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= ctl.nunits) break;
+        bool skip = false;
+        if (guard) {
+            int si = 0;
+            while (si + 1 < ctl.nseg && ctl.segs[si + 1].first <= u) ++si;
+            const int kd = ctl.segs[si].kind;
+            const int first = ctl.segs[ctl.kind_seg_first[kd]].first;  // first unit of this kind
+            if (lane == 0) {
+                while (*(volatile int*)&ms->units_done < first) __nanosleep(200);
+            }
+            __syncwarp();
+            __threadfence();
+            if (phased) {
+                // Alg. 2: a kind runs to completion; stop at the first kind
+                // boundary where the earlier kinds' max exceeds k
+                int prev = 0;
+                for (int i = 0; i < p.nk && p.kinds[i] != kd; ++i)
+                    prev = max(prev, *(volatile int*)&ms->kmax[p.kinds[i]]);
+                skip = (int64_t)prev > p.k;
+            } else {
+                skip = (int64_t)(*(volatile int*)&ms->lb) > p.k;  // Alg. 4 guard
+            }
+        }
+        if (!skip) run_unit<TABLE, WIDE>(p, ctl, lk, m, u, single);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(&ms->units_done, 1);
+        }
     }
 }
 
@@ -439,7 +506,9 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
     const bool phased = p.flags & BPLB_F_PHASED;
     const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
 
-    for (int64_t node = p.node0 + blockIdx.x; node < p.node0 + p.n_nodes; node += gridDim.x) {
+    const bool multi = p.ms != nullptr;
+    for (int64_t node = p.node0 + (multi ? 0 : blockIdx.x); node < p.node0 + p.n_nodes;
+         node += (multi ? p.n_nodes : gridDim.x)) {
         const int64_t base = p.off[node];
         const int r = (int)(p.off[node + 1] - base);
         if (threadIdx.x == 0) {
@@ -557,13 +626,51 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
         // ---- sweep -------------------------------------------------------------
         if (TABLE) {
             LkTable lk{m.cnt, m.pre, c};
-            sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
+            if (multi) sweep_multi<TABLE, WIDE>(p, ctl, lk, m, single, phased || (p.flags & BPLB_F_CANCEL), phased);
+            else sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
         } else {
             LkBucket lk{m.sw, m.pre, m.bidx, r, m.bk, c};
-            sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
+            if (multi) sweep_multi<TABLE, WIDE>(p, ctl, lk, m, single, phased || (p.flags & BPLB_F_CANCEL), phased);
+            else sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
         }
         __syncthreads();
         // ---- outputs ----------------------------------------------------------
+        if (multi) {
+            __shared__ int last;
+            if (threadIdx.x == 0) {
+                MultiState* ms = p.ms;
+                for (int kd = 0; kd < K_COUNT; ++kd) {
+                    if (ctl.evaluated[kd]) {
+                        atomicMax(&ms->key[kd], ctl.key[kd]);
+                        atomicAdd(&ms->evals[kd], ctl.evals[kd]);
+                        atomicOr(&ms->evaluated[kd], 1);
+                    }
+                }
+                __threadfence();
+                last = atomicAdd(&ms->ctas_done, 1) == (int)gridDim.x - 1;
+                if (last) {
+                    __threadfence();
+                    for (int kd = 0; kd < K_COUNT; ++kd) {
+                        ctl.key[kd] = *(volatile u64*)&ms->key[kd];
+                        ctl.evals[kd] = *(volatile unsigned long long*)&ms->evals[kd];
+                        ctl.evaluated[kd] = *(volatile int*)&ms->evaluated[kd];
+                    }
+                    // kinds processed in order until the running max exceeds k
+                    int nd = p.nk;
+                    if (phased) {
+                        int64_t run = 0;
+                        for (int i = 0; i < p.nk; ++i) {
+                            const int kd = p.kinds[i];
+                            if (ctl.evaluated[kd]) run = max(run, (int64_t)(ctl.key[kd] >> 32));
+                            if (run > p.k) { nd = i + 1; break; }
+                        }
+                    }
+                    ctl.n_done = nd;
+                }
+            }
+            __syncthreads();
+            if (!last) break;
+        }
         if (threadIdx.x == 0) {
             if (ctl.bad && p.err_out) atomicExch(p.err_out, 1);
             int64_t lb = 0;
