@@ -53,6 +53,8 @@ extern "C" {
 #define BPLB_F_CANCEL 0x2   /* Alg. 4 guard "if lb <= k" per work unit
                                (parallel.py:76-77): units observing lb > k skip */
 #define BPLB_F_TIMING 0x4   /* record device time of the last call (bplb_last_device_ms) */
+#define BPLB_F_NOTAB  0x8   /* batched calls: do not use the histogram x table kernel
+                               (selects the warp-per-node kernel; parity testing) */
 
 typedef struct bplb_engine bplb_engine;
 

@@ -21,6 +21,7 @@ NKINDS = 6
 F_PHASED = 0x1
 F_CANCEL = 0x2
 F_TIMING = 0x4
+F_NOTAB = 0x8  # batched: skip the histogram x table kernel (parity testing)
 
 E_INVAL, E_RANGE, E_CUDA, E_NOMEM, E_NODEV = -1, -2, -3, -4, -5
 

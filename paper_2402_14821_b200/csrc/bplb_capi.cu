@@ -15,6 +15,8 @@
 #include "bplb_node.cuh"
 #include "bplb_wide.cuh"
 #include "bplb_warp.cuh"
+#include "bplb_tab.cuh"
+#include <vector>
 
 namespace {
 
@@ -91,6 +93,11 @@ struct bplb_engine {
     std::mutex mu;
     DevBuf d_w, d_off, d_res, d_lb, d_ex, d_best, d_arg, d_err, d_lam, d_wide, d_multi;
     HostBuf h_stage, h_res;
+    // batched small-c path: cached table of transformed values for (tab_c, tab_kmask)
+    DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist;
+    int64_t tab_c = -1;
+    int tab_kmask = -1, tab_KV = 0, tab_nsub = 0, tab_spp = 0, tab_P = 0;
+    int64_t tab_nodes = 0;  // capacity of d_tabkeys / d_tabhist (nodes)
     int64_t launches = 0;
     double last_ms = 0.0;
 };
@@ -167,6 +174,170 @@ bool warp_path(const bplb::KParams& p, int64_t n_nodes) {
            bplb::warp_cta_bytes(p.c) + bplb::warp_slice_bytes(p.c) * bplb::WNW <= 200 * 1024;
 }
 
+
+// ---- batched small-capacity path (bplb_tab.cuh) ------------------------------
+int tab_kmask(const bplb::KParams& p) {
+    int m = 0;
+    for (int i = 0; i < p.nk; ++i) m |= 1 << p.kinds[i];
+    return m;
+}
+
+// Shared memory of one tab CTA for a part of spp sub-chunks.
+size_t tab_smem(int spp, int KV) {
+    return bplb::tab_part_bytes(spp, KV) + bplb::tab_warp_bytes(KV) * bplb::TAB_NW;
+}
+
+// Tabulate f_k(w, lambda) for capacity c and the requested kinds (cached).
+int tab_ensure(bplb_engine* e, const bplb::KParams& p) {
+    const int kmask = tab_kmask(p);
+    if (e->tab_c == p.c && e->tab_kmask == kmask) return 0;
+    const int c = (int)p.c;
+    std::vector<int4> meta;
+    std::vector<int2> cols;
+    auto pad_col = [&](int kind) {
+        meta.push_back(int4{(int)0x80000000u, (int)(0u - 0x96000000u), 0, kind << 16});  // F = 1, S = 0
+        cols.push_back(int2{-1, kind});
+    };
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        if (!(kmask >> kd & 1)) continue;
+        int64_t lo, hi;
+        bplb_domain(kd, c, &lo, &hi);  // VB2 uncapped: the cap is >= c in this envelope
+        const int64_t n = hi - lo + 1;
+        if (n <= 0) continue;
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t lam = lo + i;
+            const int64_t F = bplb_fc(kd, c, lam);
+            if (F <= 0) return fail(BPLB_ERANGE, "f(c, lambda) <= 0 inside the table path");  // never for c >= 1
+            int l = 0;
+            while ((1ll << l) < F) ++l;
+            const uint64_t m = ((1ull << (31 + l)) + (uint64_t)F - 1) / (uint64_t)F;  // < 2^32
+            const uint32_t K = (uint32_t)(2 * F - 2) - 0x96000000u;
+            meta.push_back(int4{(int)(uint32_t)m, (int)K, l, (int)(511 - lam) | (kd << 16)});
+            cols.push_back(int2{(int)lam, kd});
+        }
+        while (meta.size() % 4) pad_col(kd);  // one kind per 4-column lane group
+    }
+    while (meta.size() % bplb::TAB_SUB || meta.empty()) pad_col(K_COUNT);
+    const int KV = (c + 3) / 4 * 4;
+    const int nsub = (int)(meta.size() / bplb::TAB_SUB);
+    const size_t budget = e->smem_optin - bplb::tab_warp_bytes(KV) * bplb::TAB_NW;
+    const int spp_max = (int)(budget / bplb::tab_part_bytes(1, KV));
+    if (spp_max < 1) return fail(BPLB_ERANGE, "capacity too large for the table path");
+    const int P = (nsub + spp_max - 1) / spp_max;
+    const int spp = (nsub + P - 1) / P;
+    int rc;
+    if ((rc = e->d_tab.grow((size_t)nsub * (KV + 2) * bplb::TAB_SUB * 4))) return rc;
+    if ((rc = e->d_tabmeta.grow(meta.size() * (sizeof(int4) + sizeof(int2))))) return rc;
+    int2* d_cols = (int2*)((int4*)e->d_tabmeta.p + meta.size());
+    CUDA_TRY(cudaMemcpyAsync(e->d_tabmeta.p, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice,
+                             e->stream));
+    CUDA_TRY(cudaMemcpyAsync(d_cols, cols.data(), cols.size() * sizeof(int2), cudaMemcpyHostToDevice, e->stream));
+    const int64_t n = (int64_t)nsub * (KV + 2) * bplb::TAB_SUB;
+    bplb::tab_build_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4 * e->num_sms), 256, 0, e->stream>>>(
+        (float*)e->d_tab.p, d_cols, KV + 2, nsub, p.c);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(e->stream));  // meta / cols are host vectors; the table is cached
+    e->tab_c = p.c;
+    e->tab_kmask = kmask;
+    e->tab_KV = KV;
+    e->tab_nsub = nsub;
+    e->tab_spp = spp;
+    e->tab_P = P;
+    return 0;
+}
+
+// Per-node key / per-tile counter arrays (zero between launches; the kernel
+// clears what it used) for nodes [0, n).
+int tab_reserve(bplb_engine* e, int64_t n) {
+    if (n <= e->tab_nodes) return 0;
+    int rc;
+    if ((rc = e->d_tabkeys.grow((size_t)n * bplb::TAB_KSLOT * 4))) return rc;
+    // histogram tiles: a launch over nodes [node0, ...) on chunk slot s uses
+    // tiles from node0 / 16 + s on (disjoint across the chunk launches)
+    if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 9) * ((bplb::TAB_MAX_C + 3) / 4 * 4) * bplb::TAB_TM * 4)))
+        return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_tabkeys.p, 0, (size_t)n * bplb::TAB_KSLOT * 4, e->stream));
+    e->tab_nodes = n;
+    return 0;
+}
+
+// The table path applies to batches of small-capacity nodes whose
+// transformed sums stay exact in fp32 below 2^23 (the epilogue reads S from
+// the bits of S + 2^23): max_r * max f < 2^23 (MT, RAD2, BJ1 <= c; CCM1,
+// VB2 <= 2c; FS1 <= 101c).
+bool tab_path(const bplb_engine* e, const bplb::KParams& p, int64_t n_nodes, int64_t max_r) {
+    if (p.lam_out || p.ms || p.c > bplb::TAB_MAX_C || n_nodes < 256 || max_r > 65535) return false;
+    if (n_nodes > ((int64_t)1 << 30)) return false;  // 32-bit item indices (ntiles * sub-chunks)
+    if ((uintptr_t)p.w & 15) return false;  // the histogram pass reads aligned 16-byte vectors
+    const int KV = ((int)p.c + 3) / 4 * 4;
+    if (tab_smem(1, KV) > e->smem_optin) return false;
+    const int64_t maxf = (tab_kmask(p) >> K_FS1 & 1) ? 101 * p.c : 2 * p.c;
+    return max_r * maxf < (1ll << 23);
+}
+
+// Launch with programmatic dependent launch: the kernel may start while the
+// previous one on the stream drains; it waits in cudaGridDependencySynchronize.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// hist pass -> contraction -> per-node results (three launches, PDL-chained).
+int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
+    int rc;
+    if ((rc = tab_ensure(e, p))) return rc;
+    if ((rc = tab_reserve(e, p.node0 + n_nodes))) return rc;
+    const int KV = e->tab_KV, P = e->tab_P;
+    const size_t smem = tab_smem(e->tab_spp, KV);
+    CUDA_TRY(cudaFuncSetAttribute(bplb::tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::tab_kernel, bplb::TAB_NT, smem));
+    if (per_sm < 1) per_sm = 1;
+    bplb::TabDev t;
+    t.T = (const float*)e->d_tab.p;
+    t.meta = (const int4*)e->d_tabmeta.p;
+    t.KV = KV;
+    t.nsub = e->tab_nsub;
+    t.spp = e->tab_spp;
+    t.P = P;
+    t.gkeys = (unsigned*)e->d_tabkeys.p;
+    t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
+    t.H = (const float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM + (slot & 3)) * KV * bplb::TAB_TM;
+    // the whole GPU, but no more CTAs per part than its warps have items
+    const int64_t items = t.ntiles * t.spp;
+    const int64_t cpp = std::max<int64_t>(1, std::min<int64_t>(((int64_t)per_sm * e->num_sms + P - 1) / P,
+                                                              (items + bplb::TAB_NW - 1) / bplb::TAB_NW));
+    const int64_t grid = std::min<int64_t>((int64_t)per_sm * e->num_sms, cpp * P);
+    p.n_nodes = n_nodes;
+    {
+        const size_t hs = (size_t)(KV + 1) * bplb::TAB_HN * 4;
+        CUDA_TRY(cudaFuncSetAttribute(bplb::tab_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
+        bplb::tab_hist_kernel<<<(unsigned)(2 * t.ntiles), bplb::TAB_HNT, hs, e->stream>>>(p, KV, (float*)t.H);
+        e->launches++;
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(launch_pdl(bplb::tab_kernel, dim3((unsigned)std::max<int64_t>(grid, P)), dim3(bplb::TAB_NT), smem,
+                        e->stream, p, t));
+    e->launches++;
+    CUDA_TRY(launch_pdl(bplb::tab_fin_kernel, dim3((unsigned)((n_nodes + 63) / 64)), dim3(64), 0, e->stream, p,
+                        t.gkeys));
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
 // multi: one node, every CTA of a co-resident grid sweeps part of it
 // (single-check latency path); p.ms must point at a zeroed MultiState.
@@ -175,7 +346,9 @@ bool node_fits(int64_t r, int64_t c) {
 }
 
 int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r, int grid_cap,
-                bool multi = false) {
+                bool multi = false, int slot = 0) {
+    if (!multi && grid_cap == 0 && !(p.flags & BPLB_F_NOTAB) && tab_path(e, p, n_nodes, max_r))
+        return launch_tab(e, p, n_nodes, slot);
     if (!multi && grid_cap == 0 && warp_path(p, n_nodes)) return launch_warp(e, p, n_nodes);
     const bool table = p.c <= bplb::TABLE_MAX_C;
     if (max_r > (table ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT))
@@ -252,7 +425,8 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
-                      &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi})
+                      &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
+                      &e->d_tabkeys, &e->d_tabhist})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -485,6 +659,11 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
     p.arg_out = arg_out ? (int64_t*)e->d_arg.p : nullptr;
     p.err_out = (int*)e->d_err.p;
     CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    if (node_path && tab_path(e, p, n_nodes, max_r) && !(flags & BPLB_F_NOTAB)) {
+        // table and key arrays for the whole batch before concurrent chunk launches
+        if ((rc = tab_ensure(e, p))) return rc;
+        if ((rc = tab_reserve(e, n_nodes))) return rc;
+    }
     // Chunked upload on the copy stream, one kernel per chunk on its own
     // stream as soon as its bytes have landed: the PCIe transfer of chunk
     // i+1 overlaps the kernel of chunk i, and chunk kernels overlap each
@@ -517,7 +696,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             bplb::KParams q = p;
             q.node0 = bounds_[i];
             e->stream = cs;
-            rc = launch_node(e, q, bounds_[i + 1] - bounds_[i], max_r, 0);
+            rc = launch_node(e, q, bounds_[i + 1] - bounds_[i], max_r, 0, false, i);
             e->stream = saved;
             if (rc) return rc;
             if (nch > 1) {

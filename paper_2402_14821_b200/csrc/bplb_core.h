@@ -176,6 +176,46 @@ BPLB_HD int64_t bplb_fc(int kind, int64_t c, int64_t lam) {
     }
 }
 
+// One transformed item f_k(w) for 1 <= w <= c, lambda in the kind's domain:
+// the scalar transforms _mt/_rad2/_fs1/_ccm1/_vb2/_bj1 (bounds.py:155-206),
+// used to tabulate f over (lambda, w) once per capacity (batched small-c
+// path).  piece(v) = max(0, ceil(v*lambda/c) - 1) as in _vb2.
+BPLB_HD int64_t bplb_vb2_piece(int64_t v, int64_t c, int64_t lam) {
+    const int64_t q = (v * lam + c - 1) / c - 1;
+    return q > 0 ? q : 0;
+}
+BPLB_HD int64_t bplb_cell(int kind, int64_t w, int64_t c, int64_t lam) {
+    switch (kind) {
+    case K_MT:  // bounds.py:155-160
+        return c - lam < w ? c : (w < lam ? 0 : w);
+    case K_RAD2: {  // bounds.py:163-170; lambda > c/4 makes the recursion depth <= 1
+        const bool mirror = w >= 2 * lam;
+        const int64_t x = mirror ? c - w : w;
+        int64_t f;
+        if (x < lam) f = 0;
+        else if (x <= c - 2 * lam) f = c / 3;
+        else f = c / 2;
+        return mirror ? c - f : f;
+    }
+    case K_FS1: {  // bounds.py:173-178
+        const int64_t num = w * (lam + 1), q = num / c;
+        return num - q * c == 0 ? w * lam : q * c;
+    }
+    case K_CCM1:  // bounds.py:181-186
+        if (2 * w > c) return 2 * (c / lam - (c - w) / lam);
+        if (2 * w == c) return c / lam;
+        return 2 * (w / lam);
+    case K_VB2:  // bounds.py:189-197
+        if (2 * w > c) return 2 * bplb_vb2_piece(c, c, lam) - 2 * bplb_vb2_piece(c - w, c, lam);
+        if (2 * w == c) return bplb_vb2_piece(c, c, lam);
+        return 2 * bplb_vb2_piece(w, c, lam);
+    default: {  // K_BJ1, bounds.py:200-206
+        const int64_t cm = c % lam, base = (w / lam) * (lam - cm), wm = w % lam;
+        return wm <= cm ? base : base + wm - cm;
+    }
+    }
+}
+
 #if defined(__CUDACC__)
 // 64-bit ceil-division kept out of line: it is rare (S >= 2^32) and large.
 __device__ __noinline__ static uint64_t bplb_ceil_div64_slow(uint64_t s, uint64_t f) {

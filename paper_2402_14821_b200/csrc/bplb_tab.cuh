@@ -1,0 +1,392 @@
+// bplb_tab.cuh -- batched small-capacity path: the LB collection of many
+// search nodes as a contraction of per-node weight histograms with a table
+// of transformed values.
+//
+// Every node of a batch shares the capacity c, so f_k(w, lambda) -- the
+// reference's scalar transforms (bounds.py:155-206) -- is the same for every
+// node.  It is tabulated once per capacity (tab_build_kernel, cached by the
+// engine): T[lambda column][w] for every requested kind and every lambda of
+// its range.  A node's transformed sum for column j is then
+//     S_j = sum_w hist[w] * T[j][w]          (bounds.py:276-290, 463-501)
+// an (items-histogram x table) product, evaluated on the FP32 pipe with
+// packed FFMA2 and exact integer arithmetic: every operand and partial sum
+// is an integer < 2^23 (host check: max_r * max T < 2^23), so nothing is
+// rounded.  The per-column bound ceil(S/F) (F = f(c, lambda)) is an exact
+// multiply-high division and the max over lambda (lowest lambda on ties) a
+// segmented warp REDUX, both fused into the epilogue.
+//
+// Layout: tab_hist_kernel first builds the per-node histograms (u16 counts,
+// tile-major [16-node tile][w][16 nodes], L2-resident).  In tab_kernel one
+// CTA per SM holds one *part* of the table (a run of 64-column sub-chunks,
+// [sub][w][64] fp32) in shared memory for the whole launch.  A work item is
+// (16-node tile, sub-chunk of this part); each warp pulls items from a
+// per-CTA counter, prefetches the next item's histogram into registers
+// while it sweeps the current one, and sweeps the sub-chunk with an 8-node x
+// 4-column register tile per lane (lanes: 2 node groups x 16 column groups;
+// histogram reads are warp broadcasts).  Per-(node, kind) best keys meet in
+// a global u32 atomicMax array; tab_fin_kernel (PDL-chained) then writes
+// the node results (mode replay as in warp_node_kernel) and clears the keys.
+#pragma once
+#include "bplb_node.cuh"
+
+namespace bplb {
+
+constexpr int TAB_NT = 256;         // threads per CTA
+constexpr int TAB_NW = TAB_NT / 32; // warps per CTA
+constexpr int TAB_TM = 16;          // nodes per warp tile
+constexpr int TAB_SUB = 64;         // columns per sub-chunk (16 lanes x 4)
+constexpr int TAB_MAX_C = 288;      // capacity limit (smem budget; VB2 cap >= c)
+constexpr int TAB_PF = 20;          // uint4 (4 fp32 counts) per lane prefetched: a whole tile for KV <= 160
+constexpr int TAB_KSLOT = 8;        // key slots per node (6 kinds; 6 = padding sink)
+
+// Per-column epilogue constants (host-computed, TabCol):
+//   m, l : exact division floor(n/F) = umulhi(n2, m) >> l with n2 = 2n
+//          (l = ceil(log2 F), m = ceil(2^(31+l)/F); bplb_core.h proof)
+//   K    : n2 = 2*(S + F - 1) computed from the fp32 bits of S + 2^23 as
+//          2*bits + K, K = 2F - 2 - 2*0x4B000000 (mod 2^32)
+//   lk   : 511 - lambda (0 for a padding column), key = bound << 9 | lk
+//   kind : kind id (6 for a padding group)
+struct TabDev {
+    const float* T;               // [nsub][KV + 2][64]
+    const int4* meta;             // [nsub * 64] {m, K, l, lk | kind << 16}
+    int KV;                       // rows swept (w = 1..KV, KV = c rounded up to 4); the table
+                                  // and the histogram buffers hold KV + 2 rows (zero) so the
+                                  // two-stage k pipeline reads ahead without a bound check
+    int nsub;                     // 64-column sub-chunks in the whole table
+    int spp;                      // sub-chunks per part
+    int P;                        // parts (CTA b works on part b % P)
+    unsigned* gkeys;              // [node * 8 + kind], zero between launches
+    int64_t ntiles;
+    const float* H;               // [tile][KV][16] histogram counts (fp32) of this launch's tiles
+};
+
+__host__ __device__ inline size_t tab_warp_bytes(int KV) { return (size_t)(KV + 2) * TAB_TM * 4; }
+__host__ __device__ inline size_t tab_part_bytes(int spp, int KV) {
+    return (size_t)spp * (KV + 2) * TAB_SUB * 4 + (size_t)spp * TAB_SUB * 16;
+}
+
+// T[sub][w-1][j] = f_kind(w, c, lambda) for column (sub*64 + j), rows up to
+// KV + 2 (zero past c); cols[] = {lambda, kind} (lambda < 0: padding, zero).
+__global__ void tab_build_kernel(float* T, const int2* cols, int KVR, int nsub, int64_t c) {
+    const int KV = KVR;  // rows per sub-chunk (KV + 2)
+    const int64_t n = (int64_t)nsub * KV * TAB_SUB;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(i % TAB_SUB);
+        const int64_t sk = i / TAB_SUB;
+        const int w = (int)(sk % KV) + 1;
+        const int s = (int)(sk / KV);
+        const int2 m = cols[s * TAB_SUB + j];
+        float v = 0.0f;
+        if (m.x >= 0 && w <= c) v = (float)bplb_cell(m.y, w, c, m.x);
+        T[i] = v;
+    }
+}
+
+// Histograms of the launch's 16-node tiles: a CTA per half tile, warp j
+// counts node j into its own smem row (node-major, row stride KV + 1 so the
+// transposed read-out is conflict-free), written out as u16 counts in the
+// tile-major [w][16 nodes] layout tab_kernel consumes.  The node's weights
+// are read as aligned 16-byte vectors (one per lane covers a whole cfg2
+// node of uint8 weights), elements outside the node masked off.  Weights
+// outside [1, c] raise the error flag (ValueError on the host).
+constexpr int TAB_HN = 8;            // nodes per histogram CTA (half a tile)
+constexpr int TAB_HNT = TAB_HN * 32;
+template <int WB>
+__device__ __forceinline__ void tab_hist_node(const KParams& p, int64_t b, int r, unsigned* row, int c, int* bad) {
+    constexpr int PER = 16 / WB;
+    const int lane = threadIdx.x & 31;
+    const int64_t e0 = b & ~(int64_t)(PER - 1);  // first element of the first vector
+    const int lead = (int)(b - e0);              // elements of vector 0 before the node
+    const int nv = (lead + r + PER - 1) / PER;   // vectors covering [b, b + r)
+    const uint4* src = (const uint4*)((const unsigned char*)p.w + e0 * WB);
+    for (int v = lane; v < nv; v += 32) {
+        const uint4 x = __ldg(src + v);
+        const unsigned wds[4] = {x.x, x.y, x.z, x.w};
+        const int elo = v * PER - lead;  // node-relative index of element 0 of this vector
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const unsigned word = wds[(e * WB) >> 2];
+            const int val = WB == 4 ? (int)word
+                                    : (int)((word >> (((e * WB) & 3) * 8)) & (WB == 1 ? 0xffu : 0xffffu));
+            if ((unsigned)(elo + e) >= (unsigned)r) continue;  // outside [b, b + r)
+            if ((unsigned)(val - 1) >= (unsigned)c) { *bad = 1; continue; }
+            atomicAdd(row + (val - 1), 1u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, int KV, float* H) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned* Hs = (unsigned*)smem;  // [8][KV + 1]
+    const int j = threadIdx.x >> 5;
+    const int c = (int)p.c;
+    const int ld = KV + 1;
+    const int64_t tile = blockIdx.x >> 1, half = blockIdx.x & 1;  // this CTA: nodes 8 half .. + 7 of the tile
+    for (int i = threadIdx.x; i < ld * TAB_HN; i += TAB_HNT) Hs[i] = 0u;
+    __syncthreads();
+    const int64_t node = p.node0 + tile * TAB_TM + half * TAB_HN + j;
+    int bad = 0;
+    if (node < p.node0 + p.n_nodes) {
+        const int64_t b = p.off[node];
+        const int r = (int)(p.off[node + 1] - b);
+        unsigned* row = Hs + j * ld;
+        if (p.wbytes == 1) tab_hist_node<1>(p, b, r, row, c, &bad);
+        else if (p.wbytes == 2) tab_hist_node<2>(p, b, r, row, c, &bad);
+        else tab_hist_node<4>(p, b, r, row, c, &bad);
+    }
+    if (bad && p.err_out) atomicExch(p.err_out, 1);
+    __syncthreads();
+    // out[w][16] fp32 of the tile: this CTA writes nodes 8 half .. + 7 of every row
+    float4* dst = (float4*)(H + tile * KV * TAB_TM);
+    for (int i = threadIdx.x; i < KV * 2; i += TAB_HNT) {
+        const int w = i >> 1, q4 = i & 1;
+        const unsigned* a = Hs + q4 * 4 * ld + w;
+        dst[w * 4 + half * 2 + q4] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
+    }
+}
+
+// acc(2 columns) += h * f(2 columns): one packed FFMA2 with h broadcast.
+__device__ __forceinline__ void tab_ffma2(unsigned long long& acc, float h, unsigned long long f) {
+    asm("{\n\t.reg .b64 hh;\n\tmov.b64 hh, {%2, %2};\n\tfma.rn.f32x2 %0, hh, %1, %0;\n\t}"
+        : "+l"(acc)
+        : "l"(f), "r"(__float_as_uint(h)));
+}
+
+__global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int part = blockIdx.x % t.P;
+    const int s0 = part * t.spp;
+    const int ns = min(t.spp, t.nsub - s0);
+    if (ns <= 0) return;
+    const int KV = t.KV;
+    float* Fs = (float*)smem;
+    int4* Ms = (int4*)(smem + (size_t)t.spp * (KV + 2) * TAB_SUB * 4);
+    float* H = (float*)(smem + tab_part_bytes(t.spp, KV) + tab_warp_bytes(KV) * warp);
+    __shared__ int s_next;
+    // ---- this CTA's part of the table, resident for the whole launch ----------
+    // (independent of the histogram pass: loaded before the PDL wait)
+    {
+        const int4* src = (const int4*)(t.T + (size_t)s0 * (KV + 2) * TAB_SUB);
+        int4* dst = (int4*)Fs;
+        const int n4 = ns * (KV + 2) * (TAB_SUB / 4);
+#pragma unroll 8
+        for (int i = threadIdx.x; i < n4; i += TAB_NT) dst[i] = __ldg(src + i);
+        for (int i = threadIdx.x; i < ns * TAB_SUB; i += TAB_NT) Ms[i] = __ldg(t.meta + s0 * TAB_SUB + i);
+    }
+    // this CTA's static range of (tile, sub-chunk) items of its part; warps
+    // take items from it through a shared counter
+    const int rank = blockIdx.x / t.P;
+    const int cpp = ((int)gridDim.x - part + t.P - 1) / t.P;  // CTAs of this part
+    const int nitems = (int)t.ntiles * ns;  // < 2^31 (host-checked)
+    const int base = nitems / cpp, rem = nitems % cpp;
+    const int it0 = rank * base + min(rank, rem);
+    const int it1 = it0 + base + (rank < rem ? 1 : 0);
+    if (threadIdx.x == 0) s_next = TAB_NW;
+    if (lane < 2 * TAB_TM / 4) ((float4*)(H + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+#if __CUDA_ARCH__ >= 900
+    cudaGridDependencySynchronize();  // the histogram pass has completed
+#endif
+    const int ng = lane >> 4, lc = lane & 15;
+
+    const int n4 = KV * TAB_TM / 4;  // float4 per tile histogram
+    float4 pf[TAB_PF];
+    auto fetch = [&](int tl) {
+        const float4* src = (const float4*)(t.H + (int64_t)tl * KV * TAB_TM);
+#pragma unroll
+        for (int u = 0; u < TAB_PF; ++u) {
+            const int i = lane + 32 * u;
+            if (i < n4) pf[u] = __ldcg(src + i);
+        }
+    };
+    int item = it0 + warp;
+    int have = -1;  // tile whose histogram is in H
+    if (item < it1) fetch(item / ns);
+
+    while (item < it1) {
+        const int tile = item / ns;
+        const int s = item - tile * ns;
+        const int64_t n0 = p.node0 + (int64_t)tile * TAB_TM;
+        const int nn = (int)min((int64_t)TAB_TM, p.node0 + p.n_nodes - n0);
+        // ---- this item's histogram (prefetched) -> fp32 [w][16] -----------------
+        if (tile != have) {
+            __syncwarp();
+            float4* d = (float4*)H;
+#pragma unroll
+            for (int u = 0; u < TAB_PF; ++u) {
+                const int i = lane + 32 * u;
+                if (i < n4) d[i] = pf[u];
+            }
+            // KV > 160: the rest of the tile is read here (not prefetched)
+            const float4* src = (const float4*)(t.H + (int64_t)tile * KV * TAB_TM);
+            for (int i = lane + 32 * TAB_PF; i < n4; i += 32) d[i] = __ldcg(src + i);
+            have = tile;
+        }
+        // next item: claim it and start its loads now, they land during the sweep
+        int nx = 0;
+        if (lane == 0) nx = atomicAdd(&s_next, 1);
+        const int nxt = it0 + __shfl_sync(FULL, nx, 0);
+        if (nxt < it1 && nxt / ns != tile) fetch(nxt / ns);
+        __syncwarp();
+        // ---- contraction: acc[a][b2] = columns (2 b2, 2 b2 + 1) of node a -----
+        unsigned long long acc[8][2];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0ull;
+        {
+            const float* Fp = Fs + (size_t)s * (KV + 2) * TAB_SUB + lc * 4;
+            const float* Hp = H + ng * 8;
+            // two-stage register pipeline: operands of step k+1 are loaded
+            // while the 16 FFMA2 of step k issue (KV is a multiple of 4;
+            // rows KV, KV + 1 are zero padding, read ahead harmlessly)
+            ulonglong2 fa = *(const ulonglong2*)Fp, fb;
+            float4 ha0 = *(const float4*)Hp, ha1 = *(const float4*)(Hp + 4), hb0, hb1;
+#define TAB_FMA_BLOCK(F_, H0_, H1_)                                                  \
+    {                                                                                \
+        const float hv[8] = {H0_.x, H0_.y, H0_.z, H0_.w, H1_.x, H1_.y, H1_.z, H1_.w}; \
+        _Pragma("unroll") for (int a = 0; a < 8; ++a) {                              \
+            tab_ffma2(acc[a][0], hv[a], F_.x);                                       \
+            tab_ffma2(acc[a][1], hv[a], F_.y);                                       \
+        }                                                                            \
+    }
+#pragma unroll 2
+            for (int k = 0; k < KV; k += 2) {
+                fb = *(const ulonglong2*)(Fp + (k + 1) * TAB_SUB);
+                hb0 = *(const float4*)(Hp + (k + 1) * TAB_TM);
+                hb1 = *(const float4*)(Hp + (k + 1) * TAB_TM + 4);
+                TAB_FMA_BLOCK(fa, ha0, ha1)
+                fa = *(const ulonglong2*)(Fp + (k + 2) * TAB_SUB);
+                ha0 = *(const float4*)(Hp + (k + 2) * TAB_TM);
+                ha1 = *(const float4*)(Hp + (k + 2) * TAB_TM + 4);
+                TAB_FMA_BLOCK(fb, hb0, hb1)
+            }
+#undef TAB_FMA_BLOCK
+        }
+        // ---- epilogue: exact ceil-div, key, segmented max per (node, kind) ------
+        {
+            int4 m[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) m[b] = Ms[s * TAB_SUB + lc * 4 + b];
+            const int kind = m[0].w >> 16;  // kinds are padded to 4 columns: one kind per lane
+            // lanes of one kind form a contiguous run within each 16-lane node
+            // group: a segmented max by shfl_down leaves each run's maximum in
+            // its first lane (the head), which folds it into the global key
+            bool seg[4];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int ko = __shfl_down_sync(FULL, kind, 1 << o, 16);
+                seg[o] = lc + (1 << o) < 16 && ko == kind;
+            }
+            const int kprev = __shfl_up_sync(FULL, kind, 1, 16);
+            const bool head = lc == 0 || kprev != kind;
+            unsigned best[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                best[a] = 0u;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const unsigned long long pr = acc[a][b >> 1];
+                    const float S = __uint_as_float((unsigned)(b & 1 ? pr >> 32 : pr));
+                    const unsigned bits = __float_as_uint(S + 8388608.0f);  // 0x4B000000 + S (S < 2^23)
+                    const unsigned n2 = 2u * bits + (unsigned)m[b].y;       // 2 (S + F - 1)
+                    const unsigned q = __umulhi(n2, (unsigned)m[b].x) >> m[b].z;
+                    best[a] = max(best[a], (q << 9) | (unsigned)(m[b].w & 0xffff));
+                }
+            }
+#pragma unroll
+            for (int o = 0; o < 4; ++o)
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    const unsigned v = __shfl_down_sync(FULL, best[a], 1 << o, 16);
+                    if (seg[o]) best[a] = max(best[a], v);
+                }
+            if (head && kind < K_COUNT) {
+                unsigned* g = t.gkeys + (n0 + ng * 8) * TAB_KSLOT + kind;
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+                    if (ng * 8 + a < nn) atomicMax(g + a * TAB_KSLOT, best[a]);
+            }
+        }
+        item = nxt;
+    }
+}
+
+// Per-node results from the best keys (key = bound << 9 | 511 - lambda),
+// with the kinds replayed in order as warp_node_kernel evaluates them: full
+// collection, PHASED (stop after the first kind whose running max exceeds
+// k, bounds.py:512-526) or CANCEL (later kinds skip once lb > k, Alg. 4).
+// One thread per node; the keys are cleared for the next launch.
+__global__ void __launch_bounds__(64) tab_fin_kernel(KParams p, unsigned* gkeys) {
+#if __CUDA_ARCH__ >= 900
+    cudaGridDependencySynchronize();  // every tab_kernel item has landed
+#endif
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p.n_nodes) return;
+    const int64_t node = p.node0 + i;
+    const int c = (int)p.c;
+    const bool phased = p.flags & BPLB_F_PHASED;
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
+    unsigned* g = gkeys + node * TAB_KSLOT;
+    const uint4 k0 = *(const uint4*)g;
+    const uint2 k1 = *(const uint2*)(g + 4);
+    *(uint4*)g = make_uint4(0u, 0u, 0u, 0u);
+    *(uint2*)(g + 4) = make_uint2(0u, 0u);
+    // kind domains (bplb_domain, 32-bit: c <= 288); the VB2 cap
+    // floor((2^64-1)/(r*max_w)) is >= 2^30 > c here, so VB2 is [2, c]
+    const int lo[K_COUNT] = {0, c / 4 + 1, 1, 1, 2, 1};
+    const int hi[K_COUNT] = {c == 1 ? 0 : (c + 1) / 2, c / 3, 100, c / 2, c, c};
+    const unsigned key[K_COUNT] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y};
+    unsigned ev = 0;  // evaluated kinds (bit mask)
+    int64_t lb = 0;
+    int n_done = 0;
+    for (int j = 0; j < p.nk; ++j) {
+        const int kd = p.kinds[j];
+        if (cancel && lb > p.k) continue;  // Alg. 3/4 guard: later kinds skip
+        n_done = j + 1;
+        int l = 0, h = -1;
+        unsigned kk = 0;
+#pragma unroll
+        for (int x = 0; x < K_COUNT; ++x)
+            if (x == kd) { l = lo[x]; h = hi[x]; kk = key[x]; }
+        if (h < l) {
+            if (phased && lb > p.k) break;
+            continue;
+        }
+        ev |= 1u << kd;
+        lb = max(lb, (int64_t)(kk >> 9));
+        if (phased && lb > p.k) break;
+    }
+    if (p.lb_out) p.lb_out[node] = lb;
+    if (p.ex_out) p.ex_out[node] = (uint8_t)(lb > p.k);
+#pragma unroll
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        const bool e = ev >> kd & 1;
+        const int64_t b = e ? (int64_t)(key[kd] >> 9) : 0;
+        const int64_t a = e ? (int64_t)(511u - (key[kd] & 511u)) : lo[kd];
+        if (p.best_out) p.best_out[node * K_COUNT + kd] = b;
+        if (p.arg_out) p.arg_out[node * K_COUNT + kd] = a;
+    }
+    if (p.res_out) {
+        bplb_result res;
+        int64_t et = 0;
+#pragma unroll
+        for (int kd = 0; kd < K_COUNT; ++kd) {
+            const bool e = ev >> kd & 1;
+            const int64_t nl = kind_in(p, kd) && hi[kd] >= lo[kd] ? hi[kd] - lo[kd] + 1 : 0;
+            res.best[kd] = e ? (int64_t)(key[kd] >> 9) : 0;
+            res.arg_lambda[kd] = e ? (int64_t)(511u - (key[kd] & 511u)) : lo[kd];
+            res.n_lambda[kd] = nl;
+            res.evals[kd] = e ? nl : 0;
+            res.evaluated[kd] = e;
+            et += res.evals[kd];
+        }
+        res.lb = lb;
+        res.exceeded = lb > p.k;
+        res.n_done = n_done;
+        res.evals_total = et;
+        p.res_out[node] = res;
+    }
+}
+
+}  // namespace bplb

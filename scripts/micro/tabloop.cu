@@ -1,0 +1,66 @@
+// Microbenchmark: the tab_kernel contraction loop in isolation (smem F
+// sub-chunk [KV+2][64], per-warp H [KV+2][16], 8 warps, FFMA2), variants:
+//  V=0: lanes 2 node-groups x 16 col-groups, tile 8 nodes x 4 cols (current)
+//  V=1: lanes 32 col-groups, tile 16 nodes x 4 cols (warp-uniform H), 128 cols
+#include <cstdio>
+#include <cuda_runtime.h>
+__device__ __forceinline__ void ffma2(unsigned long long& acc, float h, unsigned long long f) {
+    asm("{\n\t.reg .b64 hh;\n\tmov.b64 hh, {%2, %2};\n\tfma.rn.f32x2 %0, hh, %1, %0;\n\t}" : "+l"(acc) : "l"(f), "r"(__float_as_uint(h)));
+}
+constexpr int KV = 152;
+template <int V>
+__global__ void __launch_bounds__(256, 1) k(float* out, int reps) {
+    extern __shared__ __align__(16) float sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int SUB = V == 0 ? 64 : 128;
+    float* F = sm;                                   // [KV+2][SUB]
+    float* H = sm + (KV + 2) * SUB + warp * (KV + 2) * 16;
+    for (int i = threadIdx.x; i < (KV + 2) * SUB; i += 256) F[i] = (i % 7) * 0.5f;
+    for (int i = lane; i < (KV + 2) * 16; i += 32) H[i] = (i % 5);
+    __syncthreads();
+    constexpr int NA = V == 0 ? 8 : 16;
+    unsigned long long acc[NA][2];
+    for (int a = 0; a < NA; ++a) acc[a][0] = acc[a][1] = 0;
+    const int lc = V == 0 ? (lane & 15) : lane, ng = V == 0 ? lane >> 4 : 0;
+    const float* Fp = F + lc * 4;
+    const float* Hp = H + ng * 8;
+    for (int r = 0; r < reps; ++r) {
+        ulonglong2 fa = *(const ulonglong2*)Fp, fb;
+        float hA[NA], hB[NA];
+#pragma unroll
+        for (int a = 0; a < NA; a += 4) *(float4*)&hA[a] = *(const float4*)(Hp + a);
+#pragma unroll 2
+        for (int kk = 0; kk < KV; kk += 2) {
+            fb = *(const ulonglong2*)(Fp + (kk + 1) * SUB);
+#pragma unroll
+            for (int a = 0; a < NA; a += 4) *(float4*)&hB[a] = *(const float4*)(Hp + (kk + 1) * 16 + a);
+#pragma unroll
+            for (int a = 0; a < NA; ++a) { ffma2(acc[a][0], hA[a], fa.x); ffma2(acc[a][1], hA[a], fa.y); }
+            fa = *(const ulonglong2*)(Fp + (kk + 2) * SUB);
+#pragma unroll
+            for (int a = 0; a < NA; a += 4) *(float4*)&hA[a] = *(const float4*)(Hp + (kk + 2) * 16 + a);
+#pragma unroll
+            for (int a = 0; a < NA; ++a) { ffma2(acc[a][0], hB[a], fb.x); ffma2(acc[a][1], hB[a], fb.y); }
+        }
+    }
+    float s = 0;
+    for (int a = 0; a < NA; ++a) s += __uint_as_float((unsigned)acc[a][0]) + __uint_as_float((unsigned)(acc[a][1] >> 32));
+    if (s == 1.2345f) out[0] = s;
+}
+template <int V> void run(float* d) {
+    constexpr int SUB = V == 0 ? 64 : 128;
+    size_t smem = ((KV + 2) * SUB + 8 * (KV + 2) * 16) * 4;
+    cudaFuncSetAttribute(k<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    int reps = 200;
+    k<V><<<148, 256, smem>>>(d, 2);
+    cudaEventRecord(e0);
+    k<V><<<148, 256, smem>>>(d, reps);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double nodes = V == 0 ? 8 * 2 : 16, cols = V == 0 ? 4 * 16 : 4 * 32;
+    double fma = 148.0 * 8 * nodes * cols * KV * reps;
+    printf("V=%d: %.1f FMA/clk/SM  (%s)\n", V, fma / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
+}
+int main() { float* d; cudaMalloc(&d, 4); run<0>(d); run<1>(d); return 0; }

@@ -21,12 +21,13 @@ import sys
 import tempfile
 
 
-def sass_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+def sass_rows(rep, kernel_sub=""):
+    flt = ["--kernel-name", f"regex:{kernel_sub}"] if kernel_sub else []
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", *flt],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    return [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+    return [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr) and r != hdr]
 
 
 def line_table(lib, kernel_sub):
@@ -53,16 +54,20 @@ def line_table(lib, kernel_sub):
 
 
 def main(rep, kernel_sub, lib="paper_2402_14821_b200/libbplb.so"):
-    rows = sass_rows(rep)
+    rows = sass_rows(rep, kernel_sub)
     base = int(rows[0]["Address"], 16)
     table = line_table(lib, kernel_sub)
     S, I = "Warp Stall Sampling (All Samples)", "Instructions Executed"
     agg_s, agg_i = collections.Counter(), collections.Counter()
+    reasons = collections.defaultdict(collections.Counter)
     for d in rows:
         off = int(d["Address"], 16) - base
         key = table.get(off, ("?", 0))
         agg_s[key] += int(d[S] or 0)
         agg_i[key] += int(d[I] or 0)
+        for col, v in d.items():
+            if col.startswith("stall_") and "Not Issued" not in col and v and v.isdigit():
+                reasons[key][col[6:]] += int(v)
     ts, ti = sum(agg_s.values()) or 1, sum(agg_i.values()) or 1
     srcs = {}
     for (f, ln) in agg_s:
@@ -75,7 +80,8 @@ def main(rep, kernel_sub, lib="paper_2402_14821_b200/libbplb.so"):
     for key, s in sorted(agg_s.items(), key=lambda kv: -kv[1])[:45]:
         f, ln = key
         text = srcs.get(f, [""] * (ln + 1))[ln - 1].strip() if ln and f in srcs else ""
-        print(f"{100 * s / ts:7.1f}% {100 * agg_i[key] / ti:6.1f}%  {f}:{ln}  {text[:90]}")
+        top = ",".join(f"{r}:{100 * n / max(s, 1):.0f}" for r, n in reasons[key].most_common(3))
+        print(f"{100 * s / ts:7.1f}% {100 * agg_i[key] / ti:6.1f}%  {f}:{ln}  {text[:70]:70s} [{top}]")
 
 
 if __name__ == "__main__":

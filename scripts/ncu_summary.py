@@ -1,7 +1,7 @@
 """Summarise an ncu report (.ncu-rep) as markdown: duration, issue/pipe
 utilisation, occupancy, DRAM traffic, top stall reasons, instruction mix.
 
-    python scripts/ncu_summary.py gpurun_out/prof.ncu-rep [title] > profiles/x.md
+    python scripts/ncu_summary.py gpurun_out/prof.ncu-rep [title] [kernel-regex] > profiles/x.md
 """
 
 from __future__ import annotations
@@ -18,8 +18,9 @@ def _csv(path, *args):
     return list(csv.reader(io.StringIO(out)))
 
 
-def main(path, title=""):
-    raw = _csv(path, "--page", "raw")
+def main(path, title="", kernel=""):
+    flt = ["--kernel-name", f"regex:{kernel}"] if kernel else []
+    raw = _csv(path, "--page", "raw", *flt)
     hdr, units, vals = raw[0], raw[1], raw[2]
     m = {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
@@ -62,10 +63,11 @@ def main(path, title=""):
     print("\nwarp-state samples (top):\n")
     for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]:
         print(f"- {k}: {100 * v / tot:.1f}%")
-    src = _csv(path, "--page", "source", "--print-source", "sass")
+    src = _csv(path, "--page", "source", "--print-source", "sass", *flt)
     if len(src) > 2:
         h = src[1]
-        data = [dict(zip(h, r)) for r in src[2:] if len(r) == len(h)]
+        data = [dict(zip(h, r)) for r in src[2:] if len(r) == len(h) and r != h]
+        data = [d for d in data if (d.get("Instructions Executed") or "0").isdigit()]
         key = "Instructions Executed"
         tot_i = sum(int(d.get(key) or 0) for d in data) or 1
         op = collections.Counter()
@@ -79,4 +81,4 @@ def main(path, title=""):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "", sys.argv[3] if len(sys.argv) > 3 else "")

@@ -232,3 +232,103 @@ def test_compact_weight_dtypes(oracle):
     np.testing.assert_array_equal(lb16, lbo)
     with pytest.raises(ValueError):  # 0 is not a valid weight
         G.lower_bound_batch(10, np.array([0, 3], dtype=np.uint8), np.array([0, 2]), 5)
+
+
+# ---------------------------------------------------------------------------
+# Batched small-capacity path (histogram x table kernel, bplb_tab.cuh)
+# ---------------------------------------------------------------------------
+def _tab_batch(rng, c, n, max_r):
+    lens = rng.integers(0, max_r + 1, n)
+    lens[:3] = [0, 1, max_r]
+    nodes = []
+    for L in lens:
+        x = rng.integers(1, c + 1, L)
+        if L > 2:
+            x[0] = c
+            if c % 2 == 0:
+                x[1] = c // 2
+        nodes.append(x)
+    return G.csr_from_lists(nodes)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 7, 8, 100, 150, 151, 255, 280])
+def test_tab_batch_vs_oracle(oracle, c):
+    """The table kernel (>= 256 nodes, small c) against the oracle in all
+    three modes, with ragged node sizes (r = 0 included) and a partial tile."""
+    from paper_2402_14821_b200 import _native
+
+    rng = np.random.default_rng(c)
+    max_r = min(500, (1 << 24) // (101 * c))
+    w, off = _tab_batch(rng, c, 517, max_r)
+    lb, ex, best, arg = G.lower_bound_batch(c, w, off, 2**62, want_best=True)
+    lbo, exo, besto = oracle.check_batch(w, off, c, 2**62, want_best=True)
+    np.testing.assert_array_equal(best, besto, err_msg=f"c={c}")
+    np.testing.assert_array_equal(lb, lbo)
+    # same arg-lambdas as the warp-per-node kernel
+    eng = _native.default_engine()
+    lbw, exw, bestw, argw = eng.check_batch(w, off, c, 2**62, list(range(6)), _native.F_NOTAB, want_best=True)
+    np.testing.assert_array_equal(arg, argw)
+    np.testing.assert_array_equal(best, bestw)
+    kk = int(np.median(lbo))
+    for mode, fl in (("seq", _native.F_PHASED), ("cancel", _native.F_CANCEL)):
+        lb2, ex2 = G.lower_bound_batch(c, w, off, kk, mode=mode)
+        lbo2, exo2 = oracle.check_batch(w, off, c, kk)
+        np.testing.assert_array_equal(ex2, exo2)
+        if mode == "seq":
+            np.testing.assert_array_equal(lb2, lbo2)
+        got = eng.check_batch(w, off, c, kk, list(range(6)), fl, want_best=True)
+        ref = eng.check_batch(w, off, c, kk, list(range(6)), fl | _native.F_NOTAB, want_best=True)
+        for a, b in zip(got, ref):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_tab_kind_subsets_and_orders():
+    """Kind subsets / orders (the table is re-tabulated per kind mask) match
+    the warp-per-node kernel, every output."""
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.default_engine()
+    rng = np.random.default_rng(11)
+    w, off = _tab_batch(rng, 150, 300, 400)
+    for kinds in ([4], [2, 0], [5, 3, 1], [1], [3, 4, 5, 0, 1, 2]):
+        for fl in (0, _native.F_PHASED, _native.F_CANCEL):
+            got = eng.check_batch(w, off, 150, 190, kinds, fl, want_best=True)
+            ref = eng.check_batch(w, off, 150, 190, kinds, fl | _native.F_NOTAB, want_best=True)
+            for a, b in zip(got, ref):
+                np.testing.assert_array_equal(a, b, err_msg=f"{kinds} {fl}")
+
+
+def test_tab_exactness_envelope_fallback(oracle):
+    """Nodes too large for exact fp32 sums (max_r * 101 c > 2^24) take the
+    integer kernels; results are unchanged."""
+    rng = np.random.default_rng(5)
+    c = 250
+    nodes = [rng.integers(1, c + 1, 700) for _ in range(260)]
+    w, off = G.csr_from_lists(nodes)
+    lb, ex = G.lower_bound_batch(c, w, off, 2**62)
+    lbo, exo = oracle.check_batch(w, off, c, 2**62)
+    np.testing.assert_array_equal(lb, lbo)
+
+
+def test_tab_large_batch_device_api(oracle):
+    """10^4 cfg2 nodes through the device-resident entry (the bench path)."""
+    import torch
+
+    from paper_2402_14821_b200 import _native
+
+    c, k, flat, off = W.cfg2_nodes(10_000)
+    eng = _native.default_engine()
+    dev = torch.device("cuda", 0)
+    d_w = torch.from_numpy(flat.astype(np.uint8)).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    d_lb = torch.empty(len(off) - 1, dtype=torch.int64, device=dev)
+    d_ex = torch.empty(len(off) - 1, dtype=torch.uint8, device=dev)
+    eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), len(off) - 1, int(np.diff(off).max()), c,
+                           2**62, list(range(6)), 0, d_lb.data_ptr(), d_ex.data_ptr(), wbytes=1)
+    torch.cuda.synchronize()
+    lb = d_lb.cpu().numpy()
+    m = 1500
+    lbo, _ = oracle.check_batch(flat[:off[m]], off[:m + 1], c, 2**62)
+    np.testing.assert_array_equal(lb[:m], lbo)
+    lbh, _ = G.lower_bound_batch(c, flat, off, 2**62)
+    np.testing.assert_array_equal(lb, lbh)
