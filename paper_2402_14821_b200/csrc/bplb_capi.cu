@@ -95,6 +95,8 @@ struct bplb_engine {
     HostBuf h_stage, h_res;
     // batched small-c path: cached table of transformed values for (tab_c, tab_kmask)
     DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist;
+    size_t tab_attr_smem = 0;
+    int tab_per_sm = 1;
     int64_t tab_c = -1;
     int tab_kmask = -1, tab_KV = 0, tab_nsub = 0, tab_spp = 0, tab_P = 0;
     int64_t tab_nodes = 0;  // capacity of d_tabkeys / d_tabhist (nodes)
@@ -182,9 +184,12 @@ int tab_kmask(const bplb::KParams& p) {
     return m;
 }
 
-// Shared memory of one tab CTA for a part of spp sub-chunks.
-size_t tab_smem(int spp, int KV) {
-    return bplb::tab_part_bytes(spp, KV) + bplb::tab_warp_bytes(KV) * bplb::TAB_NW;
+// Warps per tab_kernel CTA: 8, fewer when the histogram buffers of large
+// capacities do not fit (0: the table path does not apply).
+int tab_warps(const bplb_engine* e, int KV) {
+    for (int nw = bplb::TAB_NW; nw >= 2; --nw)
+        if (bplb::tab_cta_bytes(nw, KV) + 64 <= e->smem_optin) return nw;
+    return 0;
 }
 
 // Tabulate f_k(w, lambda) for capacity c and the requested kinds (cached).
@@ -220,11 +225,8 @@ int tab_ensure(bplb_engine* e, const bplb::KParams& p) {
     while (meta.size() % bplb::TAB_SUB || meta.empty()) pad_col(K_COUNT);
     const int KV = (c + 3) / 4 * 4;
     const int nsub = (int)(meta.size() / bplb::TAB_SUB);
-    const size_t budget = e->smem_optin - bplb::tab_warp_bytes(KV) * bplb::TAB_NW;
-    const int spp_max = (int)(budget / bplb::tab_part_bytes(1, KV));
-    if (spp_max < 1) return fail(BPLB_ERANGE, "capacity too large for the table path");
-    const int P = (nsub + spp_max - 1) / spp_max;
-    const int spp = (nsub + P - 1) / P;
+    if (tab_warps(e, KV) < 1) return fail(BPLB_ERANGE, "capacity too large for the table path");
+    const int P = nsub, spp = 1;  // one 64-column sub-chunk per CTA
     int rc;
     if ((rc = e->d_tab.grow((size_t)nsub * (KV + 2) * bplb::TAB_SUB * 4))) return rc;
     if ((rc = e->d_tabmeta.grow(meta.size() * (sizeof(int4) + sizeof(int2))))) return rc;
@@ -258,6 +260,7 @@ int tab_reserve(bplb_engine* e, int64_t n) {
     if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 9) * ((bplb::TAB_MAX_C + 3) / 4 * 4) * bplb::TAB_TM * 4)))
         return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_tabkeys.p, 0, (size_t)n * bplb::TAB_KSLOT * 4, e->stream));
+
     e->tab_nodes = n;
     return 0;
 }
@@ -271,7 +274,7 @@ bool tab_path(const bplb_engine* e, const bplb::KParams& p, int64_t n_nodes, int
     if (n_nodes > ((int64_t)1 << 30)) return false;  // 32-bit item indices (ntiles * sub-chunks)
     if ((uintptr_t)p.w & 15) return false;  // the histogram pass reads aligned 16-byte vectors
     const int KV = ((int)p.c + 3) / 4 * 4;
-    if (tab_smem(1, KV) > e->smem_optin) return false;
+    if (tab_warps(e, KV) < 2) return false;
     const int64_t maxf = (tab_kmask(p) >> K_FS1 & 1) ? 101 * p.c : 2 * p.c;
     return max_r * maxf < (1ll << 23);
 }
@@ -294,42 +297,42 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// hist pass -> contraction -> per-node results (three launches, PDL-chained).
+// Histograms -> contraction -> per-node results: three launches, the last
+// two PDL-chained (their prologues overlap the previous kernel's tail).
 int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
     int rc;
     if ((rc = tab_ensure(e, p))) return rc;
     if ((rc = tab_reserve(e, p.node0 + n_nodes))) return rc;
     const int KV = e->tab_KV, P = e->tab_P;
-    const size_t smem = tab_smem(e->tab_spp, KV);
-    CUDA_TRY(cudaFuncSetAttribute(bplb::tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::tab_kernel, bplb::TAB_NT, smem));
-    if (per_sm < 1) per_sm = 1;
+    const int nw = tab_warps(e, KV);
+    const size_t smem = bplb::tab_cta_bytes(nw, KV);
+    if (e->tab_attr_smem != smem) {  // once per table shape (cudaFuncSetAttribute is not free)
+        CUDA_TRY(cudaFuncSetAttribute(bplb::tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::tab_kernel, nw * 32, smem));
+        e->tab_per_sm = per_sm < 1 ? 1 : per_sm;
+        e->tab_attr_smem = smem;
+    }
     bplb::TabDev t;
     t.T = (const float*)e->d_tab.p;
     t.meta = (const int4*)e->d_tabmeta.p;
     t.KV = KV;
     t.nsub = e->tab_nsub;
-    t.spp = e->tab_spp;
     t.P = P;
     t.gkeys = (unsigned*)e->d_tabkeys.p;
     t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
-    t.H = (const float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM + (slot & 3)) * KV * bplb::TAB_TM;
-    // the whole GPU, but no more CTAs per part than its warps have items
-    const int64_t items = t.ntiles * t.spp;
-    const int64_t cpp = std::max<int64_t>(1, std::min<int64_t>(((int64_t)per_sm * e->num_sms + P - 1) / P,
-                                                              (items + bplb::TAB_NW - 1) / bplb::TAB_NW));
-    const int64_t grid = std::min<int64_t>((int64_t)per_sm * e->num_sms, cpp * P);
+    t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM + (slot & 3)) * KV * bplb::TAB_TM;
+    // every SM, at least one CTA per table sub-chunk, no more CTAs per
+    // sub-chunk than its warps have tiles
+    const int64_t cpp = std::max<int64_t>(1, std::min<int64_t>(((int64_t)e->tab_per_sm * e->num_sms + P - 1) / P,
+                                                              (t.ntiles + nw - 1) / nw));
+    const int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
     p.n_nodes = n_nodes;
-    {
-        const size_t hs = (size_t)(KV + 1) * bplb::TAB_HN * 4;
-        CUDA_TRY(cudaFuncSetAttribute(bplb::tab_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
-        bplb::tab_hist_kernel<<<(unsigned)(2 * t.ntiles), bplb::TAB_HNT, hs, e->stream>>>(p, KV, (float*)t.H);
-        e->launches++;
-        CUDA_TRY(cudaGetLastError());
-    }
-    CUDA_TRY(launch_pdl(bplb::tab_kernel, dim3((unsigned)std::max<int64_t>(grid, P)), dim3(bplb::TAB_NT), smem,
-                        e->stream, p, t));
+    const size_t hs = (size_t)bplb::TAB_TM * (KV + 1) * 4;  // <= 18.5 KB (KV <= 288)
+    bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_pdl(bplb::tab_kernel, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
     e->launches++;
     CUDA_TRY(launch_pdl(bplb::tab_fin_kernel, dim3((unsigned)((n_nodes + 63) / 64)), dim3(64), 0, e->stream, p,
                         t.gkeys));
@@ -688,10 +691,13 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             return rc;
         CUDA_TRY(cudaEventRecord(e->ev_up[i], e->copy_stream));
     }
+    const bool tab = node_path && !(flags & BPLB_F_NOTAB) && tab_path(e, p, n_nodes, max_r);
     if (node_path) {
         cudaStream_t saved = e->stream;
         for (int i = 0; i < nch; ++i) {
-            cudaStream_t cs = nch == 1 ? saved : e->cstream[i];
+            // the table kernel occupies every SM: its chunk launches stay on
+            // one stream (PDL-chained), each behind its upload
+            cudaStream_t cs = (nch == 1 || tab) ? saved : e->cstream[i];
             CUDA_TRY(cudaStreamWaitEvent(cs, e->ev_up[i], 0));
             bplb::KParams q = p;
             q.node0 = bounds_[i];
@@ -699,7 +705,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             rc = launch_node(e, q, bounds_[i + 1] - bounds_[i], max_r, 0, false, i);
             e->stream = saved;
             if (rc) return rc;
-            if (nch > 1) {
+            if (nch > 1 && !tab) {
                 CUDA_TRY(cudaEventRecord(e->ev_k[i], cs));
                 CUDA_TRY(cudaStreamWaitEvent(saved, e->ev_k[i], 0));
             }

@@ -15,17 +15,19 @@
 // multiply-high division and the max over lambda (lowest lambda on ties) a
 // segmented warp REDUX, both fused into the epilogue.
 //
-// Layout: tab_hist_kernel first builds the per-node histograms (u16 counts,
-// tile-major [16-node tile][w][16 nodes], L2-resident).  In tab_kernel one
-// CTA per SM holds one *part* of the table (a run of 64-column sub-chunks,
-// [sub][w][64] fp32) in shared memory for the whole launch.  A work item is
-// (16-node tile, sub-chunk of this part); each warp pulls items from a
-// per-CTA counter, prefetches the next item's histogram into registers
-// while it sweeps the current one, and sweeps the sub-chunk with an 8-node x
-// 4-column register tile per lane (lanes: 2 node groups x 16 column groups;
-// histogram reads are warp broadcasts).  Per-(node, kind) best keys meet in
-// a global u32 atomicMax array; tab_fin_kernel (PDL-chained) then writes
-// the node results (mode replay as in warp_node_kernel) and clears the keys.
+// Three PDL-chained launches per batch:
+//   A  tab_hist_kernel: one CTA per 16-node tile, one warp per node, counts
+//      the CSR weights into a smem scratch and writes them as fp32
+//      [tile][w][16 nodes] (L2-resident)
+//   B  tab_kernel, one CTA per SM: each CTA holds one 64-column sub-chunk of the table
+//      ([w][64] fp32, loaded by TMA while phase A runs) and sweeps a static
+//      range of tiles; each warp double-buffers tile histograms in smem with
+//      TMA bulk copies and runs an 8-node x 4-column register tile per lane
+//      (lanes: 2 node groups x 16 column groups; histogram reads are
+//      broadcasts).  Per-(node, kind) best keys meet in a global u32
+//      atomicMax array.
+//   C  tab_fin_kernel: one thread per node replays the kinds in order (modes
+//      as in warp_node_kernel), writes the outputs and clears its keys.
 #pragma once
 #include "bplb_node.cuh"
 
@@ -36,7 +38,6 @@ constexpr int TAB_NW = TAB_NT / 32; // warps per CTA
 constexpr int TAB_TM = 16;          // nodes per warp tile
 constexpr int TAB_SUB = 64;         // columns per sub-chunk (16 lanes x 4)
 constexpr int TAB_MAX_C = 288;      // capacity limit (smem budget; VB2 cap >= c)
-constexpr int TAB_PF = 20;          // uint4 (4 fp32 counts) per lane prefetched: a whole tile for KV <= 160
 constexpr int TAB_KSLOT = 8;        // key slots per node (6 kinds; 6 = padding sink)
 
 // Per-column epilogue constants (host-computed, TabCol):
@@ -53,16 +54,20 @@ struct TabDev {
                                   // and the histogram buffers hold KV + 2 rows (zero) so the
                                   // two-stage k pipeline reads ahead without a bound check
     int nsub;                     // 64-column sub-chunks in the whole table
-    int spp;                      // sub-chunks per part
-    int P;                        // parts (CTA b works on part b % P)
+    int P;                        // = nsub: CTA b holds sub-chunk b % P
     unsigned* gkeys;              // [node * 8 + kind], zero between launches
     int64_t ntiles;
-    const float* H;               // [tile][KV][16] histogram counts (fp32) of this launch's tiles
+    float* H;                     // [tile][KV][16] histogram counts (fp32) of this launch's tiles
 };
 
 __host__ __device__ inline size_t tab_warp_bytes(int KV) { return (size_t)(KV + 2) * TAB_TM * 4; }
 __host__ __device__ inline size_t tab_part_bytes(int spp, int KV) {
     return (size_t)spp * (KV + 2) * TAB_SUB * 4 + (size_t)spp * TAB_SUB * 16;
+}
+// Dynamic smem of a tab_kernel CTA with nw warps: one sub-chunk + metadata,
+// per warp two histogram buffers and three mbarriers.
+__host__ __device__ inline size_t tab_cta_bytes(int nw, int KV) {
+    return tab_part_bytes(1, KV) + (size_t)nw * (2 * tab_warp_bytes(KV) + 24);
 }
 
 // T[sub][w-1][j] = f_kind(w, c, lambda) for column (sub*64 + j), rows up to
@@ -82,69 +87,6 @@ __global__ void tab_build_kernel(float* T, const int2* cols, int KVR, int nsub, 
     }
 }
 
-// Histograms of the launch's 16-node tiles: a CTA per half tile, warp j
-// counts node j into its own smem row (node-major, row stride KV + 1 so the
-// transposed read-out is conflict-free), written out as u16 counts in the
-// tile-major [w][16 nodes] layout tab_kernel consumes.  The node's weights
-// are read as aligned 16-byte vectors (one per lane covers a whole cfg2
-// node of uint8 weights), elements outside the node masked off.  Weights
-// outside [1, c] raise the error flag (ValueError on the host).
-constexpr int TAB_HN = 8;            // nodes per histogram CTA (half a tile)
-constexpr int TAB_HNT = TAB_HN * 32;
-template <int WB>
-__device__ __forceinline__ void tab_hist_node(const KParams& p, int64_t b, int r, unsigned* row, int c, int* bad) {
-    constexpr int PER = 16 / WB;
-    const int lane = threadIdx.x & 31;
-    const int64_t e0 = b & ~(int64_t)(PER - 1);  // first element of the first vector
-    const int lead = (int)(b - e0);              // elements of vector 0 before the node
-    const int nv = (lead + r + PER - 1) / PER;   // vectors covering [b, b + r)
-    const uint4* src = (const uint4*)((const unsigned char*)p.w + e0 * WB);
-    for (int v = lane; v < nv; v += 32) {
-        const uint4 x = __ldg(src + v);
-        const unsigned wds[4] = {x.x, x.y, x.z, x.w};
-        const int elo = v * PER - lead;  // node-relative index of element 0 of this vector
-#pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            const unsigned word = wds[(e * WB) >> 2];
-            const int val = WB == 4 ? (int)word
-                                    : (int)((word >> (((e * WB) & 3) * 8)) & (WB == 1 ? 0xffu : 0xffffu));
-            if ((unsigned)(elo + e) >= (unsigned)r) continue;  // outside [b, b + r)
-            if ((unsigned)(val - 1) >= (unsigned)c) { *bad = 1; continue; }
-            atomicAdd(row + (val - 1), 1u);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, int KV, float* H) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    unsigned* Hs = (unsigned*)smem;  // [8][KV + 1]
-    const int j = threadIdx.x >> 5;
-    const int c = (int)p.c;
-    const int ld = KV + 1;
-    const int64_t tile = blockIdx.x >> 1, half = blockIdx.x & 1;  // this CTA: nodes 8 half .. + 7 of the tile
-    for (int i = threadIdx.x; i < ld * TAB_HN; i += TAB_HNT) Hs[i] = 0u;
-    __syncthreads();
-    const int64_t node = p.node0 + tile * TAB_TM + half * TAB_HN + j;
-    int bad = 0;
-    if (node < p.node0 + p.n_nodes) {
-        const int64_t b = p.off[node];
-        const int r = (int)(p.off[node + 1] - b);
-        unsigned* row = Hs + j * ld;
-        if (p.wbytes == 1) tab_hist_node<1>(p, b, r, row, c, &bad);
-        else if (p.wbytes == 2) tab_hist_node<2>(p, b, r, row, c, &bad);
-        else tab_hist_node<4>(p, b, r, row, c, &bad);
-    }
-    if (bad && p.err_out) atomicExch(p.err_out, 1);
-    __syncthreads();
-    // out[w][16] fp32 of the tile: this CTA writes nodes 8 half .. + 7 of every row
-    float4* dst = (float4*)(H + tile * KV * TAB_TM);
-    for (int i = threadIdx.x; i < KV * 2; i += TAB_HNT) {
-        const int w = i >> 1, q4 = i & 1;
-        const unsigned* a = Hs + q4 * 4 * ld + w;
-        dst[w * 4 + half * 2 + q4] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
-    }
-}
-
 // acc(2 columns) += h * f(2 columns): one packed FFMA2 with h broadcast.
 __device__ __forceinline__ void tab_ffma2(unsigned long long& acc, float h, unsigned long long f) {
     asm("{\n\t.reg .b64 hh;\n\tmov.b64 hh, {%2, %2};\n\tfma.rn.f32x2 %0, hh, %1, %0;\n\t}"
@@ -152,84 +94,232 @@ __device__ __forceinline__ void tab_ffma2(unsigned long long& acc, float h, unsi
         : "l"(f), "r"(__float_as_uint(h)));
 }
 
-__global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
+// mbarrier / bulk-copy helpers (TMA 1-D bulk copy global -> shared)
+__device__ __forceinline__ unsigned tab_smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tab_bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tab_smem_addr(bar)));
+}
+// lane 0: fence the warp's earlier generic reads of dst against the async
+// proxy, then copy `bytes` from global src to shared dst, completing on bar.
+__device__ __forceinline__ void tab_bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tab_smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            tab_smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(tab_smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tab_bar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(tab_smem_addr(bar)), "r"(parity)
+            : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Phase A (tab_hist_kernel): one CTA per 16-node tile, warp j counts node j.
+// The node's weights are read as aligned 16-byte vectors (one per lane
+// covers a whole cfg2 node of uint8 weights); each element is counted
+// branch-free into the warp's row of a node-major u32 scratch [16][KV + 1]
+// -- elements outside the node or outside [1, c] land in the row's spare
+// slot KV (the latter also raise the error flag, ValueError on the host).
+// The tile is written as fp32 [w][16].
+template <int WB>
+__device__ __forceinline__ void tab_hist_node(const KParams& p, int64_t b, int r, unsigned* row, int c, int KV,
+                                              unsigned* bad) {
+    constexpr int PER = 16 / WB;
+    const int lane = threadIdx.x & 31;
+    const int64_t e0 = b & ~(int64_t)(PER - 1);  // first element of the first vector
+    const int lead = (int)(b - e0);              // elements of vector 0 before the node
+    const int nv = (lead + r + PER - 1) / PER;   // vectors covering [b, b + r)
+    const uint4* src = (const uint4*)((const unsigned char*)p.w + e0 * WB);
+    unsigned bd = 0;
+    for (int v = lane; v < nv; v += 32) {
+        const uint4 x = __ldg(src + v);
+        const unsigned wds[4] = {x.x, x.y, x.z, x.w};
+        const int elo = v * PER - lead;  // node-relative index of element 0 of this vector
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const unsigned word = wds[(e * WB) >> 2];
+            const unsigned val = WB == 4 ? word : (word >> (((e * WB) & 3) * 8)) & (WB == 1 ? 0xffu : 0xffffu);
+            const bool in = (unsigned)(elo + e) < (unsigned)r;
+            const bool ok = val - 1u < (unsigned)c;
+            bd |= in & !ok;
+            atomicAdd(row + (in && ok ? (int)val - 1 : KV), 1u);
+        }
+    }
+    *bad |= bd;
+}
+
+constexpr int TAB_HNT = TAB_TM * 32;
+__global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const int KV = t.KV, ld = KV + 1, c = (int)p.c;
+    unsigned* Hs = (unsigned*)smem;  // [16][KV + 1]
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+    const int tile = blockIdx.x;
+    for (int i = threadIdx.x; i < TAB_TM * ld; i += TAB_HNT) Hs[i] = 0u;
+    __syncthreads();
+    const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
+    unsigned bad = 0;
+    if (node < p.node0 + p.n_nodes) {
+        const int64_t o = lane < 2 ? p.off[node + lane] : 0;
+        const int64_t b = __shfl_sync(0xffffffffu, o, 0), e = __shfl_sync(0xffffffffu, o, 1);
+        unsigned* row = Hs + j * ld;
+        if (p.wbytes == 1) tab_hist_node<1>(p, b, (int)(e - b), row, c, KV, &bad);
+        else if (p.wbytes == 2) tab_hist_node<2>(p, b, (int)(e - b), row, c, KV, &bad);
+        else tab_hist_node<4>(p, b, (int)(e - b), row, c, KV, &bad);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
+    __syncthreads();
+    // fp32 [w][16]: float4 i holds w = i / 4, nodes 4 (i & 3) .. + 3
+    float4* dst = (float4*)(t.H + (int64_t)tile * KV * TAB_TM);
+    for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT) {
+        const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
+        dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
+    }
+    // the histograms are read back by TMA (async proxy) in tab_kernel
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Phase C: per-node results from the best keys (key = bound << 9 | 511 -
+// lambda), with the kinds replayed in order as warp_node_kernel evaluates
+// them: full collection, PHASED (stop after the first kind whose running max
+// exceeds k, bounds.py:512-526) or CANCEL (later kinds skip once lb > k,
+// Alg. 4).  The node's keys are cleared for the next launch.
+__device__ __forceinline__ void tab_node_result(const KParams& p, unsigned* gkeys, int64_t node) {
+    const int c = (int)p.c;
+    const bool phased = p.flags & BPLB_F_PHASED;
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
+    unsigned* g = gkeys + node * TAB_KSLOT;
+    const uint4 k0 = __ldcg((const uint4*)g);  // written by atomics (L2) in phase B
+    const uint2 k1 = __ldcg((const uint2*)(g + 4));
+    *(uint4*)g = make_uint4(0u, 0u, 0u, 0u);
+    *(uint2*)(g + 4) = make_uint2(0u, 0u);
+    // kind domains (bplb_domain, 32-bit: c <= 288); the VB2 cap
+    // floor((2^64-1)/(r*max_w)) is >= 2^30 > c here, so VB2 is [2, c]
+    const int lo[K_COUNT] = {0, c / 4 + 1, 1, 1, 2, 1};
+    const int hi[K_COUNT] = {c == 1 ? 0 : (c + 1) / 2, c / 3, 100, c / 2, c, c};
+    const unsigned key[K_COUNT] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y};
+    unsigned ev = 0;  // evaluated kinds (bit mask)
+    int64_t lb = 0;
+    int n_done = 0;
+    for (int j = 0; j < p.nk; ++j) {
+        const int kd = p.kinds[j];
+        if (cancel && lb > p.k) continue;  // Alg. 3/4 guard: later kinds skip
+        n_done = j + 1;
+        int l = 0, h = -1;
+        unsigned kk = 0;
+#pragma unroll
+        for (int x = 0; x < K_COUNT; ++x)
+            if (x == kd) { l = lo[x]; h = hi[x]; kk = key[x]; }
+        if (h < l) {
+            if (phased && lb > p.k) break;
+            continue;
+        }
+        ev |= 1u << kd;
+        lb = max(lb, (int64_t)(kk >> 9));
+        if (phased && lb > p.k) break;
+    }
+    if (p.lb_out) p.lb_out[node] = lb;
+    if (p.ex_out) p.ex_out[node] = (uint8_t)(lb > p.k);
+#pragma unroll
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        const bool e = ev >> kd & 1;
+        const int64_t b = e ? (int64_t)(key[kd] >> 9) : 0;
+        const int64_t a = e ? (int64_t)(511u - (key[kd] & 511u)) : lo[kd];
+        if (p.best_out) p.best_out[node * K_COUNT + kd] = b;
+        if (p.arg_out) p.arg_out[node * K_COUNT + kd] = a;
+    }
+    if (p.res_out) {
+        bplb_result res;
+        int64_t et = 0;
+#pragma unroll
+        for (int kd = 0; kd < K_COUNT; ++kd) {
+            const bool e = ev >> kd & 1;
+            const int64_t nl = kind_in(p, kd) && hi[kd] >= lo[kd] ? hi[kd] - lo[kd] + 1 : 0;
+            res.best[kd] = e ? (int64_t)(key[kd] >> 9) : 0;
+            res.arg_lambda[kd] = e ? (int64_t)(511u - (key[kd] & 511u)) : lo[kd];
+            res.n_lambda[kd] = nl;
+            res.evals[kd] = e ? nl : 0;
+            res.evaluated[kd] = e;
+            et += res.evals[kd];
+        }
+        res.lb = lb;
+        res.exceeded = lb > p.k;
+        res.n_done = n_done;
+        res.evals_total = et;
+        p.res_out[node] = res;
+    }
+}
+
+__global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
+    extern __shared__ __align__(128) unsigned char smem[];
     const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int part = blockIdx.x % t.P;
-    const int s0 = part * t.spp;
-    const int ns = min(t.spp, t.nsub - s0);
-    if (ns <= 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int part = blockIdx.x % t.P;  // = sub-chunk (one per CTA)
     const int KV = t.KV;
     float* Fs = (float*)smem;
-    int4* Ms = (int4*)(smem + (size_t)t.spp * (KV + 2) * TAB_SUB * 4);
-    float* H = (float*)(smem + tab_part_bytes(t.spp, KV) + tab_warp_bytes(KV) * warp);
+    int4* Ms = (int4*)(smem + (size_t)(KV + 2) * TAB_SUB * 4);
+    const size_t hb = tab_warp_bytes(KV);  // one histogram buffer
+    float* Hbuf = (float*)(smem + tab_part_bytes(1, KV) + 2 * hb * warp);
+    unsigned long long* bars = (unsigned long long*)(smem + tab_part_bytes(1, KV) + 2 * hb * nw) + 3 * warp;
     __shared__ int s_next;
-    // ---- this CTA's part of the table, resident for the whole launch ----------
-    // (independent of the histogram pass: loaded before the PDL wait)
-    {
-        const int4* src = (const int4*)(t.T + (size_t)s0 * (KV + 2) * TAB_SUB);
-        int4* dst = (int4*)Fs;
-        const int n4 = ns * (KV + 2) * (TAB_SUB / 4);
-#pragma unroll 8
-        for (int i = threadIdx.x; i < n4; i += TAB_NT) dst[i] = __ldg(src + i);
-        for (int i = threadIdx.x; i < ns * TAB_SUB; i += TAB_NT) Ms[i] = __ldg(t.meta + s0 * TAB_SUB + i);
+    // ---- phase 0: barriers; this CTA's table sub-chunk by TMA (overlaps A) ------
+    if (lane == 0) {
+        tab_bar_init(bars);
+        tab_bar_init(bars + 1);
+        tab_bar_init(bars + 2);
     }
-    // this CTA's static range of (tile, sub-chunk) items of its part; warps
-    // take items from it through a shared counter
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned long long* tbar = (unsigned long long*)(smem + tab_part_bytes(1, KV) + 2 * hb * nw) + 2;  // warp 0's third
+    __syncthreads();  // barrier inits visible to the CTA
+    if (warp == 0 && lane == 0)
+        tab_bulk_load(Fs, t.T + (size_t)part * (KV + 2) * TAB_SUB, (unsigned)((KV + 2) * TAB_SUB * 4), tbar);
+    if (threadIdx.x < TAB_SUB) Ms[threadIdx.x] = __ldg(t.meta + part * TAB_SUB + threadIdx.x);
+#if __CUDA_ARCH__ >= 900
+    cudaGridDependencySynchronize();  // the histogram pass is complete
+#endif
+    // ---- phase B: contraction -------------------------------------------------
+    // this CTA's static range of tiles of its part
     const int rank = blockIdx.x / t.P;
     const int cpp = ((int)gridDim.x - part + t.P - 1) / t.P;  // CTAs of this part
-    const int nitems = (int)t.ntiles * ns;  // < 2^31 (host-checked)
-    const int base = nitems / cpp, rem = nitems % cpp;
+    const int ntl = (int)t.ntiles;  // < 2^31 (host-checked)
+    const int base = ntl / cpp, rem = ntl % cpp;
     const int it0 = rank * base + min(rank, rem);
     const int it1 = it0 + base + (rank < rem ? 1 : 0);
-    if (threadIdx.x == 0) s_next = TAB_NW;
-    if (lane < 2 * TAB_TM / 4) ((float4*)(H + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (threadIdx.x == 0) s_next = nw;
+    // zero padding rows KV, KV + 1 of both buffers (never written by the copies)
+    if (lane < 2 * TAB_TM / 4) {
+        ((float4*)(Hbuf + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ((float4*)(Hbuf + (KV + 2) * TAB_TM + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     __syncthreads();
-#if __CUDA_ARCH__ >= 900
-    cudaGridDependencySynchronize();  // the histogram pass has completed
-#endif
+    tab_bar_wait(tbar, 0);  // the table sub-chunk has landed
     const int ng = lane >> 4, lc = lane & 15;
-
-    const int n4 = KV * TAB_TM / 4;  // float4 per tile histogram
-    float4 pf[TAB_PF];
-    auto fetch = [&](int tl) {
-        const float4* src = (const float4*)(t.H + (int64_t)tl * KV * TAB_TM);
-#pragma unroll
-        for (int u = 0; u < TAB_PF; ++u) {
-            const int i = lane + 32 * u;
-            if (i < n4) pf[u] = __ldcg(src + i);
-        }
-    };
-    int item = it0 + warp;
-    int have = -1;  // tile whose histogram is in H
-    if (item < it1) fetch(item / ns);
-
-    while (item < it1) {
-        const int tile = item / ns;
-        const int s = item - tile * ns;
+    const unsigned hbytes = (unsigned)(KV * TAB_TM * 4);
+    const int s = 0;
+    int tile = it0 + warp;
+    if (tile < it1 && lane == 0) tab_bulk_load(Hbuf, t.H + (int64_t)tile * KV * TAB_TM, hbytes, bars);
+    unsigned phase = 0;  // bit b: parity of buffer b's next completion
+    int b = 0;
+    while (tile < it1) {
         const int64_t n0 = p.node0 + (int64_t)tile * TAB_TM;
         const int nn = (int)min((int64_t)TAB_TM, p.node0 + p.n_nodes - n0);
-        // ---- this item's histogram (prefetched) -> fp32 [w][16] -----------------
-        if (tile != have) {
-            __syncwarp();
-            float4* d = (float4*)H;
-#pragma unroll
-            for (int u = 0; u < TAB_PF; ++u) {
-                const int i = lane + 32 * u;
-                if (i < n4) d[i] = pf[u];
-            }
-            // KV > 160: the rest of the tile is read here (not prefetched)
-            const float4* src = (const float4*)(t.H + (int64_t)tile * KV * TAB_TM);
-            for (int i = lane + 32 * TAB_PF; i < n4; i += 32) d[i] = __ldcg(src + i);
-            have = tile;
-        }
-        // next item: claim it and start its loads now, they land during the sweep
+        // next tile: claim it and start its copy into the other buffer
         int nx = 0;
         if (lane == 0) nx = atomicAdd(&s_next, 1);
         const int nxt = it0 + __shfl_sync(FULL, nx, 0);
-        if (nxt < it1 && nxt / ns != tile) fetch(nxt / ns);
-        __syncwarp();
+        if (nxt < it1 && lane == 0)
+            tab_bulk_load(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, t.H + (int64_t)nxt * KV * TAB_TM, hbytes, bars + (b ^ 1));
+        const float* H = Hbuf + b * (KV + 2) * TAB_TM;
+        tab_bar_wait(bars + b, (phase >> b) & 1);
+        phase ^= 1u << b;
         // ---- contraction: acc[a][b2] = columns (2 b2, 2 b2 + 1) of node a -----
         unsigned long long acc[8][2];
 #pragma unroll
@@ -308,85 +398,19 @@ __global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
                     if (ng * 8 + a < nn) atomicMax(g + a * TAB_KSLOT, best[a]);
             }
         }
-        item = nxt;
+        __syncwarp();  // every lane is done with buffer b before it is refilled
+        tile = nxt;
+        b ^= 1;
     }
 }
 
-// Per-node results from the best keys (key = bound << 9 | 511 - lambda),
-// with the kinds replayed in order as warp_node_kernel evaluates them: full
-// collection, PHASED (stop after the first kind whose running max exceeds
-// k, bounds.py:512-526) or CANCEL (later kinds skip once lb > k, Alg. 4).
-// One thread per node; the keys are cleared for the next launch.
+// Per-node results (PDL-chained after tab_kernel): one thread per node.
 __global__ void __launch_bounds__(64) tab_fin_kernel(KParams p, unsigned* gkeys) {
 #if __CUDA_ARCH__ >= 900
-    cudaGridDependencySynchronize();  // every tab_kernel item has landed
+    cudaGridDependencySynchronize();  // every tab_kernel tile has landed
 #endif
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= p.n_nodes) return;
-    const int64_t node = p.node0 + i;
-    const int c = (int)p.c;
-    const bool phased = p.flags & BPLB_F_PHASED;
-    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
-    unsigned* g = gkeys + node * TAB_KSLOT;
-    const uint4 k0 = *(const uint4*)g;
-    const uint2 k1 = *(const uint2*)(g + 4);
-    *(uint4*)g = make_uint4(0u, 0u, 0u, 0u);
-    *(uint2*)(g + 4) = make_uint2(0u, 0u);
-    // kind domains (bplb_domain, 32-bit: c <= 288); the VB2 cap
-    // floor((2^64-1)/(r*max_w)) is >= 2^30 > c here, so VB2 is [2, c]
-    const int lo[K_COUNT] = {0, c / 4 + 1, 1, 1, 2, 1};
-    const int hi[K_COUNT] = {c == 1 ? 0 : (c + 1) / 2, c / 3, 100, c / 2, c, c};
-    const unsigned key[K_COUNT] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y};
-    unsigned ev = 0;  // evaluated kinds (bit mask)
-    int64_t lb = 0;
-    int n_done = 0;
-    for (int j = 0; j < p.nk; ++j) {
-        const int kd = p.kinds[j];
-        if (cancel && lb > p.k) continue;  // Alg. 3/4 guard: later kinds skip
-        n_done = j + 1;
-        int l = 0, h = -1;
-        unsigned kk = 0;
-#pragma unroll
-        for (int x = 0; x < K_COUNT; ++x)
-            if (x == kd) { l = lo[x]; h = hi[x]; kk = key[x]; }
-        if (h < l) {
-            if (phased && lb > p.k) break;
-            continue;
-        }
-        ev |= 1u << kd;
-        lb = max(lb, (int64_t)(kk >> 9));
-        if (phased && lb > p.k) break;
-    }
-    if (p.lb_out) p.lb_out[node] = lb;
-    if (p.ex_out) p.ex_out[node] = (uint8_t)(lb > p.k);
-#pragma unroll
-    for (int kd = 0; kd < K_COUNT; ++kd) {
-        const bool e = ev >> kd & 1;
-        const int64_t b = e ? (int64_t)(key[kd] >> 9) : 0;
-        const int64_t a = e ? (int64_t)(511u - (key[kd] & 511u)) : lo[kd];
-        if (p.best_out) p.best_out[node * K_COUNT + kd] = b;
-        if (p.arg_out) p.arg_out[node * K_COUNT + kd] = a;
-    }
-    if (p.res_out) {
-        bplb_result res;
-        int64_t et = 0;
-#pragma unroll
-        for (int kd = 0; kd < K_COUNT; ++kd) {
-            const bool e = ev >> kd & 1;
-            const int64_t nl = kind_in(p, kd) && hi[kd] >= lo[kd] ? hi[kd] - lo[kd] + 1 : 0;
-            res.best[kd] = e ? (int64_t)(key[kd] >> 9) : 0;
-            res.arg_lambda[kd] = e ? (int64_t)(511u - (key[kd] & 511u)) : lo[kd];
-            res.n_lambda[kd] = nl;
-            res.evals[kd] = e ? nl : 0;
-            res.evaluated[kd] = e;
-            et += res.evals[kd];
-        }
-        res.lb = lb;
-        res.exceeded = lb > p.k;
-        res.n_done = n_done;
-        res.evals_total = et;
-        p.res_out[node] = res;
-    }
+    if (i < p.n_nodes) tab_node_result(p, gkeys, p.node0 + i);
 }
 
 }  // namespace bplb

@@ -22,12 +22,14 @@ n = len(off) - 1
 d_lb = torch.empty(n, dtype=torch.int64, device=dev)
 d_ex = torch.empty(n, dtype=torch.uint8, device=dev)
 fl = _native.F_NOTAB if a.notab else 0
+st = torch.cuda.Stream()  # a real stream handle (the legacy default stream reads as "engine stream")
+torch.cuda.set_stream(st)
 for i in range(a.reps):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
+    s.record(st)
     eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, int(np.diff(off).max()), c, 2**62,
                            list(range(6)), fl, d_lb.data_ptr(), d_ex.data_ptr(), wbytes=np.dtype(wdt).itemsize,
-                           stream_ptr=torch.cuda.current_stream().cuda_stream)
-    e.record()
+                           stream_ptr=st.cuda_stream)
+    e.record(st)
     torch.cuda.synchronize()
     print(f"{a.cfg} nodes={n} rep={i} ms={s.elapsed_time(e):.4f}", flush=True)
