@@ -186,9 +186,9 @@ int tab_kmask(const bplb::KParams& p) {
 
 // Warps per tab_kernel CTA: 8, fewer when the histogram buffers of large
 // capacities do not fit (0: the table path does not apply).
-int tab_warps(const bplb_engine* e, int KV) {
+int tab_warps(const bplb_engine* e, int KV, int nb = 2) {
     for (int nw = bplb::TAB_NW; nw >= 2; --nw)
-        if (bplb::tab_cta_bytes(nw, KV) + 64 <= e->smem_optin) return nw;
+        if (bplb::tab_cta_bytes(nw, KV, nb) + 64 <= e->smem_optin) return nw;
     return 0;
 }
 
@@ -261,6 +261,7 @@ int tab_reserve(bplb_engine* e, int64_t n) {
         return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_tabkeys.p, 0, (size_t)n * bplb::TAB_KSLOT * 4, e->stream));
 
+
     e->tab_nodes = n;
     return 0;
 }
@@ -304,12 +305,21 @@ int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
     if ((rc = tab_ensure(e, p))) return rc;
     if ((rc = tab_reserve(e, p.node0 + n_nodes))) return rc;
     const int KV = e->tab_KV, P = e->tab_P;
-    const int nw = tab_warps(e, KV);
-    const size_t smem = bplb::tab_cta_bytes(nw, KV);
+    static const int variant = getenv("BPLB_TAB_V") ? atoi(getenv("BPLB_TAB_V")) : 1;    // experiments
+    static const int want_nw = getenv("BPLB_TAB_NW") ? atoi(getenv("BPLB_TAB_NW")) : 8;  // experiments
+    int nb = 2, nw = tab_warps(e, KV, 2);
+    if (want_nw > nw) {  // more warps, one histogram buffer each
+        nb = 1;
+        nw = want_nw;
+        while (nw > 2 && bplb::tab_cta_bytes(nw, KV, 1) + 64 > e->smem_optin) --nw;
+    }
+    const size_t smem = bplb::tab_cta_bytes(nw, KV, nb);
+    auto kern = variant == 1 ? (nb == 2 ? bplb::tab_kernel<1, 2> : bplb::tab_kernel<1, 1>)
+                             : (nb == 2 ? bplb::tab_kernel<0, 2> : bplb::tab_kernel<0, 1>);
     if (e->tab_attr_smem != smem) {  // once per table shape (cudaFuncSetAttribute is not free)
-        CUDA_TRY(cudaFuncSetAttribute(bplb::tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::tab_kernel, nw * 32, smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
         e->tab_per_sm = per_sm < 1 ? 1 : per_sm;
         e->tab_attr_smem = smem;
     }
@@ -320,19 +330,35 @@ int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
     t.nsub = e->tab_nsub;
     t.P = P;
     t.gkeys = (unsigned*)e->d_tabkeys.p;
+    static unsigned long long* dbg = nullptr;
+    if (getenv("BPLB_TAB_DBG") && !dbg) { cudaMalloc(&dbg, 64); cudaMemset(dbg, 0, 64); }
+    t.dbg = dbg;
+    if (dbg) {
+        unsigned long long h[8];
+        cudaMemcpy(h, dbg, 64, cudaMemcpyDeviceToHost);
+        if (h[3]) fprintf(stderr, "tab dbg: tiles %llu  wait %.0f  loop %.0f  epi %.0f cyc/tile;  warp total %.0f cyc\n",
+                          h[3], (double)h[0] / h[3], (double)h[1] / h[3], (double)h[2] / h[3], (double)h[4] / h[5]);
+        cudaMemset(dbg, 0, 64);
+    }
     t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
     t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM + (slot & 3)) * KV * bplb::TAB_TM;
     // every SM, at least one CTA per table sub-chunk, no more CTAs per
     // sub-chunk than its warps have tiles
     const int64_t cpp = std::max<int64_t>(1, std::min<int64_t>(((int64_t)e->tab_per_sm * e->num_sms + P - 1) / P,
                                                               (t.ntiles + nw - 1) / nw));
-    const int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
+    int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
+    static const int even = getenv("BPLB_TAB_EVEN") ? atoi(getenv("BPLB_TAB_EVEN")) : 0;  // experiments
+    if (even && grid > P) grid = grid / P * P;  // equal CTAs per sub-chunk
     p.n_nodes = n_nodes;
-    const size_t hs = (size_t)bplb::TAB_TM * (KV + 1) * 4;  // <= 18.5 KB (KV <= 288)
+    // histogram pass, then the contraction PDL-chained behind it (no
+    // cross-kernel waiting: stream order is the only dependency)
+    t.ready = nullptr;
+    t.epoch = 0;
+    const size_t hs = ((size_t)bplb::TAB_TM * (KV + 1) + 2 * bplb::TAB_HPAD) * 4;  // <= 20.5 KB (KV <= 288)
     bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
     e->launches++;
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(launch_pdl(bplb::tab_kernel, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
+    CUDA_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
     e->launches++;
     CUDA_TRY(launch_pdl(bplb::tab_fin_kernel, dim3((unsigned)((n_nodes + 63) / 64)), dim3(64), 0, e->stream, p,
                         t.gkeys));
@@ -409,6 +435,7 @@ int bplb_engine_create(int device, bplb_engine** out) {
     e->num_sms = prop.multiProcessorCount;
     e->smem_optin = prop.sharedMemPerBlockOptin;
     bool ok = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) == cudaSuccess &&
+
               cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
               cudaEventCreate(&e->ev0) == cudaSuccess && cudaEventCreate(&e->ev1) == cudaSuccess;
     for (int i = 0; i < 4 && ok; ++i)
@@ -441,6 +468,7 @@ int bplb_engine_destroy(bplb_engine* e) {
         cudaStreamDestroy(e->cstream[i]);
     }
     cudaStreamDestroy(e->copy_stream);
+
     cudaStreamDestroy(e->stream);
     delete e;
     return 0;

@@ -57,6 +57,9 @@ struct TabDev {
     int P;                        // = nsub: CTA b holds sub-chunk b % P
     unsigned* gkeys;              // [node * 8 + kind], zero between launches
     int64_t ntiles;
+    unsigned long long* dbg;      // experiment: per-phase clock totals (null = off)
+    int* ready;                   // unused (null)
+    int epoch;
     float* H;                     // [tile][KV][16] histogram counts (fp32) of this launch's tiles
 };
 
@@ -65,9 +68,9 @@ __host__ __device__ inline size_t tab_part_bytes(int spp, int KV) {
     return (size_t)spp * (KV + 2) * TAB_SUB * 4 + (size_t)spp * TAB_SUB * 16;
 }
 // Dynamic smem of a tab_kernel CTA with nw warps: one sub-chunk + metadata,
-// per warp two histogram buffers and three mbarriers.
-__host__ __device__ inline size_t tab_cta_bytes(int nw, int KV) {
-    return tab_part_bytes(1, KV) + (size_t)nw * (2 * tab_warp_bytes(KV) + 24);
+// per warp nb histogram buffers and three mbarriers.
+__host__ __device__ inline size_t tab_cta_bytes(int nw, int KV, int nb) {
+    return tab_part_bytes(1, KV) + (size_t)nw * (nb * tab_warp_bytes(KV) + 24);
 }
 
 // T[sub][w-1][j] = f_kind(w, c, lambda) for column (sub*64 + j), rows up to
@@ -156,14 +159,53 @@ __device__ __forceinline__ void tab_hist_node(const KParams& p, int64_t b, int r
     *bad |= bd;
 }
 
+// uint8 weights: one code path for every vector (no divergence at the node's
+// boundary vectors): a 16-bit mask marks the elements inside the node,
+// validity is tested four bytes at a time with SIMD byte compares, and an
+// element outside the node or invalid is counted into the row's spare slot
+// KV (invalid ones also raise the error flag).
+__device__ __forceinline__ void tab_hist_node_u8(const KParams& p, int64_t b, int r, unsigned* row, int c, int KV,
+                                                 unsigned* bad) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e0 = b & ~(int64_t)15;
+    const int lead = (int)(b - e0);
+    const int nv = (lead + r + 15) / 16;
+    const uint4* src = (const uint4*)((const unsigned char*)p.w + e0);
+    const unsigned cc = c >= 255 ? 0xffffffffu : (unsigned)c * 0x01010101u;
+    unsigned bd = 0;
+    for (int v = lane; v < nv; v += 32) {
+        const uint4 x = __ldg(src + v);
+        const unsigned wds[4] = {x.x, x.y, x.z, x.w};
+        const int elo = v * 16 - lead;  // node-relative index of element 0
+        // in-node elements: [max(0, -elo), min(16, r - elo))
+        const int a0 = max(0, -elo), a1 = min(16, r - elo);
+        const unsigned inm = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned wd = wds[q];
+            // per byte: 0xff where the byte is 0 or > c
+            const unsigned badb = __vcmpeq4(wd, 0u) | __vcmpgtu4(wd, cc);
+            const unsigned in4 = (inm >> (4 * q)) & 0xfu;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const bool use = ((in4 >> e) & 1u) && !((badb >> (8 * e)) & 1u);
+                bd |= ((in4 >> e) & 1u) & ((badb >> (8 * e)) & 1u);
+                atomicAdd(row + (use ? (int)((wd >> (8 * e)) & 0xffu) - 1 : KV), 1u);
+            }
+        }
+    }
+    *bad |= bd;
+}
+
 constexpr int TAB_HNT = TAB_TM * 32;
+constexpr int TAB_HPAD = 0;
 __global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int KV = t.KV, ld = KV + 1, c = (int)p.c;
-    unsigned* Hs = (unsigned*)smem;  // [16][KV + 1]
+    unsigned* Hs = (unsigned*)smem + TAB_HPAD;  // [16][KV + 1]
     const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
     const int tile = blockIdx.x;
-    for (int i = threadIdx.x; i < TAB_TM * ld; i += TAB_HNT) Hs[i] = 0u;
+    for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
     unsigned bad = 0;
@@ -171,7 +213,7 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) 
         const int64_t o = lane < 2 ? p.off[node + lane] : 0;
         const int64_t b = __shfl_sync(0xffffffffu, o, 0), e = __shfl_sync(0xffffffffu, o, 1);
         unsigned* row = Hs + j * ld;
-        if (p.wbytes == 1) tab_hist_node<1>(p, b, (int)(e - b), row, c, KV, &bad);
+        if (p.wbytes == 1) tab_hist_node_u8(p, b, (int)(e - b), row, c, KV, &bad);
         else if (p.wbytes == 2) tab_hist_node<2>(p, b, (int)(e - b), row, c, KV, &bad);
         else tab_hist_node<4>(p, b, (int)(e - b), row, c, KV, &bad);
     }
@@ -258,7 +300,8 @@ __device__ __forceinline__ void tab_node_result(const KParams& p, unsigned* gkey
     }
 }
 
-__global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
+template <int V, int NB>
+__global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     extern __shared__ __align__(128) unsigned char smem[];
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -267,8 +310,8 @@ __global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
     float* Fs = (float*)smem;
     int4* Ms = (int4*)(smem + (size_t)(KV + 2) * TAB_SUB * 4);
     const size_t hb = tab_warp_bytes(KV);  // one histogram buffer
-    float* Hbuf = (float*)(smem + tab_part_bytes(1, KV) + 2 * hb * warp);
-    unsigned long long* bars = (unsigned long long*)(smem + tab_part_bytes(1, KV) + 2 * hb * nw) + 3 * warp;
+    float* Hbuf = (float*)(smem + tab_part_bytes(1, KV) + NB * hb * warp);
+    unsigned long long* bars = (unsigned long long*)(smem + tab_part_bytes(1, KV) + NB * hb * nw) + 3 * warp;
     __shared__ int s_next;
     // ---- phase 0: barriers; this CTA's table sub-chunk by TMA (overlaps A) ------
     if (lane == 0) {
@@ -277,7 +320,7 @@ __global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
         tab_bar_init(bars + 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    unsigned long long* tbar = (unsigned long long*)(smem + tab_part_bytes(1, KV) + 2 * hb * nw) + 2;  // warp 0's third
+    unsigned long long* tbar = (unsigned long long*)(smem + tab_part_bytes(1, KV) + NB * hb * nw) + 2;  // warp 0's third
     __syncthreads();  // barrier inits visible to the CTA
     if (warp == 0 && lane == 0)
         tab_bulk_load(Fs, t.T + (size_t)part * (KV + 2) * TAB_SUB, (unsigned)((KV + 2) * TAB_SUB * 4), tbar);
@@ -285,41 +328,54 @@ __global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
 #if __CUDA_ARCH__ >= 900
     cudaGridDependencySynchronize();  // the histogram pass is complete
 #endif
-    // ---- phase B: contraction -------------------------------------------------
-    // this CTA's static range of tiles of its part
+    // ---- contraction ----------------------------------------------------------
+    // this CTA's tiles of its part: rank, rank + cpp, ... (strided)
     const int rank = blockIdx.x / t.P;
     const int cpp = ((int)gridDim.x - part + t.P - 1) / t.P;  // CTAs of this part
     const int ntl = (int)t.ntiles;  // < 2^31 (host-checked)
-    const int base = ntl / cpp, rem = ntl % cpp;
-    const int it0 = rank * base + min(rank, rem);
-    const int it1 = it0 + base + (rank < rem ? 1 : 0);
+    const int it0 = 0, it1 = rank < ntl ? (ntl - rank + cpp - 1) / cpp : 0;  // local tile indices
+    // lane 0: wait for the tile's histogram, then copy it into buf by TMA
+    auto load_tile = [&](float* buf, int k, unsigned long long* bar) {
+        const int tl = rank + k * cpp;
+        if (t.ready) {
+            int st;
+            do {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(st) : "l"(t.ready + tl) : "memory");
+            } while (st != t.epoch && (__nanosleep(100), true));
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        tab_bulk_load(buf, t.H + (int64_t)tl * KV * TAB_TM, (unsigned)(KV * TAB_TM * 4), bar);
+    };
     if (threadIdx.x == 0) s_next = nw;
-    // zero padding rows KV, KV + 1 of both buffers (never written by the copies)
-    if (lane < 2 * TAB_TM / 4) {
-        ((float4*)(Hbuf + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ((float4*)(Hbuf + (KV + 2) * TAB_TM + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    // zero padding rows KV, KV + 1 of the buffers (never written by the copies)
+    if (lane < 2 * TAB_TM / 4)
+        for (int u = 0; u < NB; ++u)
+            ((float4*)(Hbuf + u * (KV + 2) * TAB_TM + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     tab_bar_wait(tbar, 0);  // the table sub-chunk has landed
+    const long long cstart = clock64();
     const int ng = lane >> 4, lc = lane & 15;
-    const unsigned hbytes = (unsigned)(KV * TAB_TM * 4);
     const int s = 0;
-    int tile = it0 + warp;
-    if (tile < it1 && lane == 0) tab_bulk_load(Hbuf, t.H + (int64_t)tile * KV * TAB_TM, hbytes, bars);
+    int kt = it0 + warp;  // local tile index
+    if (kt < it1 && lane == 0) load_tile(Hbuf, kt, bars);
     unsigned phase = 0;  // bit b: parity of buffer b's next completion
     int b = 0;
-    while (tile < it1) {
+    while (kt < it1) {
+        const int tile = rank + kt * cpp;
         const int64_t n0 = p.node0 + (int64_t)tile * TAB_TM;
         const int nn = (int)min((int64_t)TAB_TM, p.node0 + p.n_nodes - n0);
-        // next tile: claim it and start its copy into the other buffer
+        // next tile: claim it; with two buffers its copy starts now (lands
+        // during this sweep), with one buffer right after the sweep (lands
+        // during the epilogue, the other warps cover the rest)
         int nx = 0;
         if (lane == 0) nx = atomicAdd(&s_next, 1);
         const int nxt = it0 + __shfl_sync(FULL, nx, 0);
-        if (nxt < it1 && lane == 0)
-            tab_bulk_load(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, t.H + (int64_t)nxt * KV * TAB_TM, hbytes, bars + (b ^ 1));
+        if (NB == 2 && nxt < it1 && lane == 0) load_tile(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, nxt, bars + (b ^ 1));
         const float* H = Hbuf + b * (KV + 2) * TAB_TM;
+        long long c0 = clock64();
         tab_bar_wait(bars + b, (phase >> b) & 1);
         phase ^= 1u << b;
+        long long c1 = clock64();
         // ---- contraction: acc[a][b2] = columns (2 b2, 2 b2 + 1) of node a -----
         unsigned long long acc[8][2];
 #pragma unroll
@@ -340,18 +396,40 @@ __global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
             tab_ffma2(acc[a][1], hv[a], F_.y);                                       \
         }                                                                            \
     }
+            if (V == 0) {
 #pragma unroll 2
-            for (int k = 0; k < KV; k += 2) {
-                fb = *(const ulonglong2*)(Fp + (k + 1) * TAB_SUB);
-                hb0 = *(const float4*)(Hp + (k + 1) * TAB_TM);
-                hb1 = *(const float4*)(Hp + (k + 1) * TAB_TM + 4);
-                TAB_FMA_BLOCK(fa, ha0, ha1)
-                fa = *(const ulonglong2*)(Fp + (k + 2) * TAB_SUB);
-                ha0 = *(const float4*)(Hp + (k + 2) * TAB_TM);
-                ha1 = *(const float4*)(Hp + (k + 2) * TAB_TM + 4);
-                TAB_FMA_BLOCK(fb, hb0, hb1)
+                for (int k = 0; k < KV; k += 2) {
+                    fb = *(const ulonglong2*)(Fp + (k + 1) * TAB_SUB);
+                    hb0 = *(const float4*)(Hp + (k + 1) * TAB_TM);
+                    hb1 = *(const float4*)(Hp + (k + 1) * TAB_TM + 4);
+                    TAB_FMA_BLOCK(fa, ha0, ha1)
+                    fa = *(const ulonglong2*)(Fp + (k + 2) * TAB_SUB);
+                    ha0 = *(const float4*)(Hp + (k + 2) * TAB_TM);
+                    ha1 = *(const float4*)(Hp + (k + 2) * TAB_TM + 4);
+                    TAB_FMA_BLOCK(fb, hb0, hb1)
+                }
+            } else {
+                // operands of 4 steps loaded up front; the other warp of the
+                // SMSP covers the load latency
+                for (int k = 0; k < KV; k += 4) {
+                    ulonglong2 f[4];
+                    float4 h[4][2];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        f[u] = *(const ulonglong2*)(Fp + (k + u) * TAB_SUB);
+                        h[u][0] = *(const float4*)(Hp + (k + u) * TAB_TM);
+                        h[u][1] = *(const float4*)(Hp + (k + u) * TAB_TM + 4);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) TAB_FMA_BLOCK(f[u], h[u][0], h[u][1])
+                }
             }
 #undef TAB_FMA_BLOCK
+        }
+        long long c2 = clock64();
+        if (NB == 1) {
+            __syncwarp();  // every lane is done with the buffer
+            if (nxt < it1 && lane == 0) load_tile(Hbuf, nxt, bars);
         }
         // ---- epilogue: exact ceil-div, key, segmented max per (node, kind) ------
         {
@@ -399,8 +477,19 @@ __global__ void __launch_bounds__(TAB_NT, 1) tab_kernel(KParams p, TabDev t) {
             }
         }
         __syncwarp();  // every lane is done with buffer b before it is refilled
-        tile = nxt;
-        b ^= 1;
+        if (t.dbg && lane == 0) {
+            long long c3 = clock64();
+            atomicAdd(t.dbg + 0, (unsigned long long)(c1 - c0));
+            atomicAdd(t.dbg + 1, (unsigned long long)(c2 - c1));
+            atomicAdd(t.dbg + 2, (unsigned long long)(c3 - c2));
+            atomicAdd(t.dbg + 3, 1ull);
+        }
+        kt = nxt;
+        if (NB == 2) b ^= 1;
+    }
+    if (t.dbg && lane == 0) {
+        atomicAdd(t.dbg + 4, (unsigned long long)(clock64() - cstart));
+        atomicAdd(t.dbg + 5, 1ull);
     }
 }
 
