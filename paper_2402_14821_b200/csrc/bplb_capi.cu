@@ -255,9 +255,8 @@ int tab_reserve(bplb_engine* e, int64_t n) {
     if (n <= e->tab_nodes) return 0;
     int rc;
     if ((rc = e->d_tabkeys.grow((size_t)n * bplb::TAB_KSLOT * 4))) return rc;
-    // histogram tiles: a launch over nodes [node0, ...) on chunk slot s uses
-    // tiles from node0 / 16 + s on (disjoint across the chunk launches)
-    if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 9) * ((bplb::TAB_MAX_C + 3) / 4 * 4) * bplb::TAB_TM * 4)))
+    // histogram tiles, indexed by absolute tile (node / 16)
+    if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 1) * ((bplb::TAB_MAX_C + 3) / 4 * 4) * bplb::TAB_TM * 4)))
         return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_tabkeys.p, 0, (size_t)n * bplb::TAB_KSLOT * 4, e->stream));
 
@@ -298,24 +297,39 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// Histograms -> contraction -> per-node results: three launches, the last
-// two PDL-chained (their prologues overlap the previous kernel's tail).
-int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
-    int rc;
-    if ((rc = tab_ensure(e, p))) return rc;
-    if ((rc = tab_reserve(e, p.node0 + n_nodes))) return rc;
+// The table path in three launches over nodes [p.node0, p.node0 + n):
+// histograms, contraction (PDL), per-node results (PDL).  Tiles are indexed
+// absolutely (tile = node / 16), so sub-ranges must start on a multiple of 16.
+bplb::TabDev tab_dev(bplb_engine* e, const bplb::KParams& p, int64_t n_nodes) {
+    bplb::TabDev t;
+    t.T = (const float*)e->d_tab.p;
+    t.meta = (const int4*)e->d_tabmeta.p;
+    t.KV = e->tab_KV;
+    t.nsub = e->tab_nsub;
+    t.P = e->tab_P;
+    t.gkeys = (unsigned*)e->d_tabkeys.p;
+    t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
+    t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM) * t.KV * bplb::TAB_TM;
+    return t;
+}
+
+int tab_hist(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
+    p.n_nodes = n_nodes;
+    const bplb::TabDev t = tab_dev(e, p, n_nodes);
+    const size_t hs = ((size_t)bplb::TAB_TM * (t.KV + 1) + 2 * bplb::TAB_HPAD) * 4;  // <= 20.5 KB (KV <= 288)
+    bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int tab_contract(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     const int KV = e->tab_KV, P = e->tab_P;
-    static const int variant = getenv("BPLB_TAB_V") ? atoi(getenv("BPLB_TAB_V")) : 1;    // experiments
-    static const int want_nw = getenv("BPLB_TAB_NW") ? atoi(getenv("BPLB_TAB_NW")) : 8;  // experiments
-    int nb = 2, nw = tab_warps(e, KV, 2);
-    if (want_nw > nw) {  // more warps, one histogram buffer each
-        nb = 1;
-        nw = want_nw;
-        while (nw > 2 && bplb::tab_cta_bytes(nw, KV, 1) + 64 > e->smem_optin) --nw;
-    }
+    // 8 warps with two histogram buffers each (8 / 12 / 16 warps with one
+    // buffer measured no faster on cfg2)
+    const int nb = 2, nw = tab_warps(e, KV, 2);
     const size_t smem = bplb::tab_cta_bytes(nw, KV, nb);
-    auto kern = variant == 1 ? (nb == 2 ? bplb::tab_kernel<1, 2> : bplb::tab_kernel<1, 1>)
-                             : (nb == 2 ? bplb::tab_kernel<0, 2> : bplb::tab_kernel<0, 1>);
+    auto kern = bplb::tab_kernel<2>;
     if (e->tab_attr_smem != smem) {  // once per table shape (cudaFuncSetAttribute is not free)
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
@@ -323,48 +337,37 @@ int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
         e->tab_per_sm = per_sm < 1 ? 1 : per_sm;
         e->tab_attr_smem = smem;
     }
-    bplb::TabDev t;
-    t.T = (const float*)e->d_tab.p;
-    t.meta = (const int4*)e->d_tabmeta.p;
-    t.KV = KV;
-    t.nsub = e->tab_nsub;
-    t.P = P;
-    t.gkeys = (unsigned*)e->d_tabkeys.p;
-    static unsigned long long* dbg = nullptr;
-    if (getenv("BPLB_TAB_DBG") && !dbg) { cudaMalloc(&dbg, 64); cudaMemset(dbg, 0, 64); }
-    t.dbg = dbg;
-    if (dbg) {
-        unsigned long long h[8];
-        cudaMemcpy(h, dbg, 64, cudaMemcpyDeviceToHost);
-        if (h[3]) fprintf(stderr, "tab dbg: tiles %llu  wait %.0f  loop %.0f  epi %.0f cyc/tile;  warp total %.0f cyc\n",
-                          h[3], (double)h[0] / h[3], (double)h[1] / h[3], (double)h[2] / h[3], (double)h[4] / h[5]);
-        cudaMemset(dbg, 0, 64);
-    }
-    t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
-    t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM + (slot & 3)) * KV * bplb::TAB_TM;
+    p.n_nodes = n_nodes;
+    bplb::TabDev t = tab_dev(e, p, n_nodes);
     // every SM, at least one CTA per table sub-chunk, no more CTAs per
     // sub-chunk than its warps have tiles
     const int64_t cpp = std::max<int64_t>(1, std::min<int64_t>(((int64_t)e->tab_per_sm * e->num_sms + P - 1) / P,
                                                               (t.ntiles + nw - 1) / nw));
     int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
-    static const int even = getenv("BPLB_TAB_EVEN") ? atoi(getenv("BPLB_TAB_EVEN")) : 0;  // experiments
-    if (even && grid > P) grid = grid / P * P;  // equal CTAs per sub-chunk
-    p.n_nodes = n_nodes;
-    // histogram pass, then the contraction PDL-chained behind it (no
-    // cross-kernel waiting: stream order is the only dependency)
-    t.ready = nullptr;
-    t.epoch = 0;
-    const size_t hs = ((size_t)bplb::TAB_TM * (KV + 1) + 2 * bplb::TAB_HPAD) * 4;  // <= 20.5 KB (KV <= 288)
-    bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
-    e->launches++;
-    CUDA_TRY(cudaGetLastError());
     CUDA_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
-    e->launches++;
-    CUDA_TRY(launch_pdl(bplb::tab_fin_kernel, dim3((unsigned)((n_nodes + 63) / 64)), dim3(64), 0, e->stream, p,
-                        t.gkeys));
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     return 0;
+}
+
+int tab_fin(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
+    p.n_nodes = n_nodes;
+    CUDA_TRY(launch_pdl(bplb::tab_fin_kernel, dim3((unsigned)((n_nodes + 63) / 64)), dim3(64), 0, e->stream, p,
+                        (unsigned*)e->d_tabkeys.p));
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
+    (void)slot;
+    int rc;
+    if ((rc = tab_ensure(e, p))) return rc;
+    if ((rc = tab_reserve(e, p.node0 + n_nodes))) return rc;
+    if (p.node0 % bplb::TAB_TM) return fail(BPLB_EINVAL, "table path sub-range must start on a 16-node tile");
+    if ((rc = tab_hist(e, p, n_nodes))) return rc;
+    if ((rc = tab_contract(e, p, n_nodes))) return rc;
+    return tab_fin(e, p, n_nodes);
 }
 
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
@@ -708,6 +711,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         bounds_[2] = n_nodes * 3 / 8;
         bounds_[3] = n_nodes * 5 / 8;
     }
+    for (int i = 1; i < nch; ++i) bounds_[i] = bounds_[i] / 16 * 16;  // table path: whole 16-node tiles
     CUDA_TRY(cudaEventRecord(e->ev_k[0], e->stream));  // memset done before uploads land
     CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, e->ev_k[0], 0));
     if ((rc = h2d(e, e->d_off.p, off, (size_t)(n_nodes + 1) * 8, wsz + 64, e->copy_stream, pinned ? 1 : 0)))
@@ -755,14 +759,15 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             if (rc) return fail(rc, bplb::wide_error());
         }
     }
-    int err = 0;
+    if ((rc = e->h_res.grow(sizeof(bplb_result) + 16))) return rc;
+    int* h_err = (int*)((char*)e->h_res.p + sizeof(bplb_result));  // pinned: no synchronous copy
     CUDA_TRY(cudaMemcpyAsync(lb_out, e->d_lb.p, (size_t)n_nodes * 8, cudaMemcpyDeviceToHost, e->stream));
     CUDA_TRY(cudaMemcpyAsync(ex_out, e->d_ex.p, (size_t)n_nodes, cudaMemcpyDeviceToHost, e->stream));
     if (best_out)
         CUDA_TRY(cudaMemcpyAsync(best_out, e->d_best.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
     if (arg_out)
         CUDA_TRY(cudaMemcpyAsync(arg_out, e->d_arg.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
-    CUDA_TRY(cudaMemcpyAsync(&err, e->d_err.p, 4, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(h_err, e->d_err.p, 4, cudaMemcpyDeviceToHost, e->stream));
     if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
     CUDA_TRY(cudaStreamSynchronize(e->stream));
     if (timing) {
@@ -770,7 +775,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         cudaEventElapsedTime(&ms, e->ev0, e->ev1);
         e->last_ms = ms;
     }
-    if (err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+    if (*h_err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
     return 0;
 }
 

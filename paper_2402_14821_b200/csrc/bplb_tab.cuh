@@ -57,9 +57,6 @@ struct TabDev {
     int P;                        // = nsub: CTA b holds sub-chunk b % P
     unsigned* gkeys;              // [node * 8 + kind], zero between launches
     int64_t ntiles;
-    unsigned long long* dbg;      // experiment: per-phase clock totals (null = off)
-    int* ready;                   // unused (null)
-    int epoch;
     float* H;                     // [tile][KV][16] histogram counts (fp32) of this launch's tiles
 };
 
@@ -300,7 +297,7 @@ __device__ __forceinline__ void tab_node_result(const KParams& p, unsigned* gkey
     }
 }
 
-template <int V, int NB>
+template <int NB>
 __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     extern __shared__ __align__(128) unsigned char smem[];
     const unsigned FULL = 0xffffffffu;
@@ -334,16 +331,9 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     const int cpp = ((int)gridDim.x - part + t.P - 1) / t.P;  // CTAs of this part
     const int ntl = (int)t.ntiles;  // < 2^31 (host-checked)
     const int it0 = 0, it1 = rank < ntl ? (ntl - rank + cpp - 1) / cpp : 0;  // local tile indices
-    // lane 0: wait for the tile's histogram, then copy it into buf by TMA
+    // lane 0: copy local tile k's histogram into buf by TMA
     auto load_tile = [&](float* buf, int k, unsigned long long* bar) {
         const int tl = rank + k * cpp;
-        if (t.ready) {
-            int st;
-            do {
-                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(st) : "l"(t.ready + tl) : "memory");
-            } while (st != t.epoch && (__nanosleep(100), true));
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
         tab_bulk_load(buf, t.H + (int64_t)tl * KV * TAB_TM, (unsigned)(KV * TAB_TM * 4), bar);
     };
     if (threadIdx.x == 0) s_next = nw;
@@ -353,7 +343,6 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
             ((float4*)(Hbuf + u * (KV + 2) * TAB_TM + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     tab_bar_wait(tbar, 0);  // the table sub-chunk has landed
-    const long long cstart = clock64();
     const int ng = lane >> 4, lc = lane & 15;
     const int s = 0;
     int kt = it0 + warp;  // local tile index
@@ -372,10 +361,8 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
         const int nxt = it0 + __shfl_sync(FULL, nx, 0);
         if (NB == 2 && nxt < it1 && lane == 0) load_tile(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, nxt, bars + (b ^ 1));
         const float* H = Hbuf + b * (KV + 2) * TAB_TM;
-        long long c0 = clock64();
         tab_bar_wait(bars + b, (phase >> b) & 1);
         phase ^= 1u << b;
-        long long c1 = clock64();
         // ---- contraction: acc[a][b2] = columns (2 b2, 2 b2 + 1) of node a -----
         unsigned long long acc[8][2];
 #pragma unroll
@@ -383,11 +370,7 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
         {
             const float* Fp = Fs + (size_t)s * (KV + 2) * TAB_SUB + lc * 4;
             const float* Hp = H + ng * 8;
-            // two-stage register pipeline: operands of step k+1 are loaded
-            // while the 16 FFMA2 of step k issue (KV is a multiple of 4;
-            // rows KV, KV + 1 are zero padding, read ahead harmlessly)
-            ulonglong2 fa = *(const ulonglong2*)Fp, fb;
-            float4 ha0 = *(const float4*)Hp, ha1 = *(const float4*)(Hp + 4), hb0, hb1;
+            // KV is a multiple of 4 (rows past c are zero)
 #define TAB_FMA_BLOCK(F_, H0_, H1_)                                                  \
     {                                                                                \
         const float hv[8] = {H0_.x, H0_.y, H0_.z, H0_.w, H1_.x, H1_.y, H1_.z, H1_.w}; \
@@ -396,37 +379,22 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
             tab_ffma2(acc[a][1], hv[a], F_.y);                                       \
         }                                                                            \
     }
-            if (V == 0) {
-#pragma unroll 2
-                for (int k = 0; k < KV; k += 2) {
-                    fb = *(const ulonglong2*)(Fp + (k + 1) * TAB_SUB);
-                    hb0 = *(const float4*)(Hp + (k + 1) * TAB_TM);
-                    hb1 = *(const float4*)(Hp + (k + 1) * TAB_TM + 4);
-                    TAB_FMA_BLOCK(fa, ha0, ha1)
-                    fa = *(const ulonglong2*)(Fp + (k + 2) * TAB_SUB);
-                    ha0 = *(const float4*)(Hp + (k + 2) * TAB_TM);
-                    ha1 = *(const float4*)(Hp + (k + 2) * TAB_TM + 4);
-                    TAB_FMA_BLOCK(fb, hb0, hb1)
-                }
-            } else {
-                // operands of 4 steps loaded up front; the other warp of the
-                // SMSP covers the load latency
-                for (int k = 0; k < KV; k += 4) {
-                    ulonglong2 f[4];
-                    float4 h[4][2];
+            // operands of 4 steps loaded up front; the other warp of the
+            // SMSP covers the load latency
+            for (int k = 0; k < KV; k += 4) {
+                ulonglong2 f[4];
+                float4 h[4][2];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        f[u] = *(const ulonglong2*)(Fp + (k + u) * TAB_SUB);
-                        h[u][0] = *(const float4*)(Hp + (k + u) * TAB_TM);
-                        h[u][1] = *(const float4*)(Hp + (k + u) * TAB_TM + 4);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) TAB_FMA_BLOCK(f[u], h[u][0], h[u][1])
+                for (int u = 0; u < 4; ++u) {
+                    f[u] = *(const ulonglong2*)(Fp + (k + u) * TAB_SUB);
+                    h[u][0] = *(const float4*)(Hp + (k + u) * TAB_TM);
+                    h[u][1] = *(const float4*)(Hp + (k + u) * TAB_TM + 4);
                 }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) TAB_FMA_BLOCK(f[u], h[u][0], h[u][1])
             }
 #undef TAB_FMA_BLOCK
         }
-        long long c2 = clock64();
         if (NB == 1) {
             __syncwarp();  // every lane is done with the buffer
             if (nxt < it1 && lane == 0) load_tile(Hbuf, nxt, bars);
@@ -477,19 +445,8 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
             }
         }
         __syncwarp();  // every lane is done with buffer b before it is refilled
-        if (t.dbg && lane == 0) {
-            long long c3 = clock64();
-            atomicAdd(t.dbg + 0, (unsigned long long)(c1 - c0));
-            atomicAdd(t.dbg + 1, (unsigned long long)(c2 - c1));
-            atomicAdd(t.dbg + 2, (unsigned long long)(c3 - c2));
-            atomicAdd(t.dbg + 3, 1ull);
-        }
         kt = nxt;
         if (NB == 2) b ^= 1;
-    }
-    if (t.dbg && lane == 0) {
-        atomicAdd(t.dbg + 4, (unsigned long long)(clock64() - cstart));
-        atomicAdd(t.dbg + 5, 1ull);
     }
 }
 
