@@ -40,6 +40,9 @@ UNIT = "checks/s"
 # canonical integer-op model per (item, lambda) cell, SURVEY.md 8(d)
 I_K = {"MT": 5, "RAD2": 10, "FS1": 9, "CCM1": 12, "VB2": 15, "BJ1": 10}
 KINDS = ("MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1")
+# DRAM bytes (read + write) of one tab_kernel launch on the 10^4-node cfg2
+# batch, from the ncu --set full capture summarised in profiles/round1_tab_ncu.md
+TAB_TRAFFIC_BYTES = 6788608
 
 
 def _dist():
@@ -114,26 +117,30 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(c, k, flat, off, seconds: float = 12.0) -> dict:
+def cpu_baseline(c, k, flat, off, seconds: float = 15.0) -> dict:
     """The reference algorithm (C port, oracle/) on this host's cores, on a
-    bounded sample of the same nodes."""
+    bounded sample of the same nodes: whole passes over the shard (or a
+    prefix of it) repeated until about `seconds` of CPU time."""
     from oracle import oracle as O
 
     threads = O.max_threads()
     O.set_threads(threads)
     n_total = len(off) - 1
+    flat = flat.astype(np.int64)
     n = min(n_total, 64)
     t = time.perf_counter()
-    flat = flat.astype(np.int64)
     O.check_batch(flat[:off[n]], off[:n + 1], c, k)
-    dt = time.perf_counter() - t
-    n2 = int(min(n_total, max(n, n * seconds / max(dt, 1e-6))))
+    per_node = (time.perf_counter() - t) / n
+    n2 = int(min(n_total, max(n, seconds / max(per_node, 1e-9))))
+    passes = max(1, int(seconds / max(per_node * n2, 1e-9)))
     t = time.perf_counter()
-    O.check_batch(flat[:off[n2]], off[:n2 + 1] - off[0], c, k)
+    for _ in range(passes):
+        O.check_batch(flat[:off[n2]], off[:n2 + 1], c, k)
     dt2 = time.perf_counter() - t
-    return {"value": n2 / dt2, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {n2} of the {n_total} cfg2 nodes of this shard, lower_bound_seq per node "
-                      f"(oracle/bplb_oracle.c, restating bounds.py), {dt2:.1f} s on {threads} threads"}
+    return {"value": n2 * passes / dt2, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{passes} pass(es) over the first {n2} of the {n_total} cfg2 nodes of this shard, "
+                      f"lower_bound_seq per node (oracle/bplb_oracle.c, restating bounds.py), "
+                      f"{dt2:.1f} s on {threads} threads"}
 
 
 def extra_latencies() -> dict:
@@ -308,21 +315,20 @@ def run_ours(args):
     value = total_nodes * args.steps / (dev_ms / 1e3)
     e2e = total_nodes * args.steps / (e2e_ms / 1e3)
 
-    # kernel-only time of the dominant kernel (the whole step at N=1 is one launch)
+    # kernel-only time of the dominant kernel (the histogram x table
+    # contraction), CUDA events around its launch on the same stream
     kern_ms = None
     if ws == 1:
-        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kt = []
+        eng.profile_kernel(True)
         for i in range(max(3, args.steps // 2)):
             flush.fill_(i)
-            ka.record(stream)
             eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, max_r, c, kk, kinds, 0,
                                    d_lb.data_ptr(), d_ex.data_ptr(), stream_ptr=stream.cuda_stream,
                                    wbytes=wbytes)
-            kb.record(stream)
-            torch.cuda.synchronize(dev)
-            kt.append(ka.elapsed_time(kb))
-        kern_ms = statistics.mean(kt)
+            kt.append(eng.last_kernel_ms())
+        eng.profile_kernel(False)
+        kern_ms = statistics.mean(kt) if all(kt) else None
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -330,9 +336,16 @@ def run_ours(args):
     clocks = clk.summary()
     ops = canonical_ops(c, flat, off)
     sm_mhz = clocks.get("sm_max_mhz") or 1965.0
-    peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # Gop/s: 148 SMs x 128 int32 lanes x max clock
+    int_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # Gop/s: 148 SMs x 128 int32 lanes x max clock
     kms = kern_ms if kern_ms is not None else dev_ms / args.steps
-    achieved = ops / (kms / 1e3) / 1e9
+    # the dominant kernel's algorithmic work: the (node histogram) x (table of
+    # transformed values) product over every lambda column and weight value,
+    # 2 flops per multiply-add: 2 * n * sum_k |Lambda_k| * c (padding excluded)
+    r_arr = np.diff(off)
+    lam_total = int(sum(v[0] for v in lambda_counts(c, r_arr[:1], np.array([c])).values()))
+    alg_flops = 2.0 * n * lam_total * c
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s nominal (128 FP32 FMA/clk/SM)
+    achieved = alg_flops / (kms / 1e3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -347,14 +360,20 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(n * 9)},
         "us_per_check_e2e_amortized": 1e6 / e2e,
         "gpu_launches": int(launches),
-        "roofline": {"bound": "int32-issue", "achieved": achieved, "peak": peak, "unit": "Gop/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "note": "achieved = canonical integer ops (SURVEY.md 8(d): r x sum_k |Lambda_k| x I_k) / "
-                             "kernel time; peak = 148 SMs x 128 INT32 lanes x max SM clock (nominal, "
-                             "no measured int peak in MEASURED_PEAKS.json). The kernel computes the same "
-                             "bounds with histogram / distinct-value / harmonic shortcuts (as the reference's "
-                             "own sweeps do), so executed work is far below canonical and frac can exceed 1; "
-                             "executed-instruction issue utilisation is in profiles/."},
+        "roofline": {"bound": "fp32-fma", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp32_peak, "traffic": TAB_TRAFFIC_BYTES,
+                     "kernel": "tab_kernel (histogram x transformed-value table contraction, packed FFMA2)",
+                     "note": "achieved = 2 * nodes * sum_k |Lambda_k| * c algorithmic flops per launch / the "
+                             "kernel's CUDA-event duration; peak = nominal FP32 FMA rate (148 SMs x 128 "
+                             "FMA/clk x 2 flop x max SM clock; no FP32 figure in MEASURED_PEAKS.json -- a "
+                             "packed-FFMA2 microbenchmark, scripts/micro/ffma2_test.cu, reaches 89% of it); "
+                             "traffic = DRAM bytes of one launch from the committed ncu capture "
+                             "(profiles/round1_tab_ncu.md); compute-bound, not HBM: the kernel reads its "
+                             "L2-resident histograms once per table sub-chunk"},
+        "canonical_int_ops": {"achieved_gops": ops / (kms / 1e3) / 1e9, "peak_gops": int_peak,
+                              "frac": ops / (kms / 1e3) / 1e9 / int_peak,
+                              "note": "SURVEY.md 8(d) canonical count r x sum_k |Lambda_k| x I_k; the table "
+                                      "formulation does far less executed work, so this exceeds 1"},
         "kernel_ms": kms,
         "clocks": clocks,
         "parity_vs_oracle_64_nodes": parity,
@@ -377,7 +396,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--nodes", type=int, default=10_000, help="search nodes per GPU")
     ap.add_argument("--ref-nodes-per-step", type=int, default=2000)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     args = ap.parse_args()

@@ -134,6 +134,13 @@ BPLB_API int bplb_check_batch_device_ex(bplb_engine *eng, const void *d_w_concat
 BPLB_API int64_t bplb_launch_count(bplb_engine *eng);
 BPLB_API double bplb_last_device_ms(bplb_engine *eng);
 
+/* Measurement hook: with on != 0 the engine brackets every launch of its
+ * dominant batched kernel (the histogram x table contraction) with CUDA
+ * events on the launching stream; bplb_last_kernel_ms waits for the last
+ * one and returns its duration (0 if none was recorded). */
+BPLB_API int bplb_profile_kernel(bplb_engine *eng, int on);
+BPLB_API double bplb_last_kernel_ms(bplb_engine *eng);
+
 /* Thread-local message describing the last error on this thread. */
 BPLB_API const char *bplb_last_error(void);
 

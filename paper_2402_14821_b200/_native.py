@@ -70,6 +70,8 @@ SIGNATURES = {
                                                   ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "bplb_launch_count": (ctypes.c_int64, [_vp]),
     "bplb_last_device_ms": (ctypes.c_double, [_vp]),
+    "bplb_profile_kernel": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "bplb_last_kernel_ms": (ctypes.c_double, [_vp]),
     "bplb_last_error": (ctypes.c_char_p, []),
     "bplb_version": (ctypes.c_char_p, []),
 }
@@ -161,6 +163,15 @@ class Engine:
 
     def last_device_ms(self) -> float:
         return float(self._lib.bplb_last_device_ms(self.handle))
+
+    def profile_kernel(self, on: bool) -> None:
+        """Bracket the dominant batched kernel with CUDA events (bench)."""
+        rc = self._lib.bplb_profile_kernel(self.handle, int(bool(on)))
+        if rc != 0:
+            _raise(rc, "bplb_profile_kernel")
+
+    def last_kernel_ms(self) -> float:
+        return float(self._lib.bplb_last_kernel_ms(self.handle))
 
     def check(self, w: np.ndarray, c: int, k: int, kinds, flags: int) -> BplbResult:
         w = as_i32(w)

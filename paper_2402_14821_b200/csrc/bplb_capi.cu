@@ -102,6 +102,9 @@ struct bplb_engine {
     int64_t tab_nodes = 0;  // capacity of d_tabkeys / d_tabhist (nodes)
     int64_t launches = 0;
     double last_ms = 0.0;
+    int prof_kernel = 0;       // bracket the contraction kernel with ev_pk0 / ev_pk1
+    int prof_recorded = 0;
+    cudaEvent_t ev_pk0 = nullptr, ev_pk1 = nullptr;
 };
 
 namespace {
@@ -344,7 +347,12 @@ int tab_contract(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     const int64_t cpp = std::max<int64_t>(1, std::min<int64_t>(((int64_t)e->tab_per_sm * e->num_sms + P - 1) / P,
                                                               (t.ntiles + nw - 1) / nw));
     int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
+    if (e->prof_kernel) CUDA_TRY(cudaEventRecord(e->ev_pk0, e->stream));
     CUDA_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
+    if (e->prof_kernel) {
+        CUDA_TRY(cudaEventRecord(e->ev_pk1, e->stream));
+        e->prof_recorded = 1;
+    }
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -465,6 +473,8 @@ int bplb_engine_destroy(bplb_engine* e) {
     e->h_res.release();
     cudaEventDestroy(e->ev0);
     cudaEventDestroy(e->ev1);
+    if (e->ev_pk0) cudaEventDestroy(e->ev_pk0);
+    if (e->ev_pk1) cudaEventDestroy(e->ev_pk1);
     for (int i = 0; i < 4; ++i) {
         cudaEventDestroy(e->ev_up[i]);
         cudaEventDestroy(e->ev_k[i]);
@@ -478,6 +488,29 @@ int bplb_engine_destroy(bplb_engine* e) {
 }
 
 int64_t bplb_launch_count(bplb_engine* e) { return e ? e->launches : 0; }
+
+int bplb_profile_kernel(bplb_engine* e, int on) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    if (on && !e->ev_pk0) {
+        CUDA_TRY(cudaEventCreate(&e->ev_pk0));
+        CUDA_TRY(cudaEventCreate(&e->ev_pk1));
+    }
+    e->prof_kernel = on != 0;
+    e->prof_recorded = 0;
+    return 0;
+}
+
+double bplb_last_kernel_ms(bplb_engine* e) {
+    if (!e || !e->prof_recorded) return 0.0;
+    std::lock_guard<std::mutex> lock(e->mu);
+    cudaSetDevice(e->device);
+    if (cudaEventSynchronize(e->ev_pk1) != cudaSuccess) return 0.0;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e->ev_pk0, e->ev_pk1);
+    return ms;
+}
 double bplb_last_device_ms(bplb_engine* e) { return e ? e->last_ms : 0.0; }
 
 int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k,
