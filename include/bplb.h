@@ -129,6 +129,30 @@ BPLB_API int bplb_check_batch_device_ex(bplb_engine *eng, const void *d_w_concat
                                int32_t flags, int64_t *d_lb, uint8_t *d_exceeded,
                                int64_t *d_best, int64_t *d_arg, void *stream);
 
+/* Device-side reduction of search-node states + batched check.
+ * Node states are bin assignments: assign[node * n_items + i] is the bin
+ * (0 <= b < n_bins) item i is committed to, or the all-ones value of the
+ * element type (0xFF for abytes = 1, 0xFFFF for abytes = 2) while item i is
+ * still open.  Each node is reduced on the GPU exactly as reduce_packing
+ * (instances.py:262-282): open items' weights in item order, then the
+ * positive committed bin loads in bin order; a load above c fails with
+ * BPLB_EINVAL ("committed load exceeds capacity", ValueError in Python), as
+ * does a bin id >= n_bins.  inst_w[n_items] are the instance weights.
+ * Replaces, for a batch of nodes: reduce_packing + engine(red, k) in the
+ * feasibility check (propagator.py:266-276).  Outputs as bplb_check_batch. */
+BPLB_API int bplb_check_batch_assign(bplb_engine *eng, const int32_t *inst_w, int64_t n_items,
+                            int64_t n_bins, const void *assign, int32_t abytes, int64_t n_nodes,
+                            int64_t c, int64_t k, const int32_t *kinds, int32_t nkinds,
+                            int32_t flags, int64_t *lb_out, uint8_t *exceeded_out,
+                            int64_t *best_out, int64_t *arg_out);
+
+/* The reduction alone (parity surface): writes the reduced CSR to host
+ * arrays offsets_out[n_nodes + 1] and weights_out[total] (int32, capacity
+ * n_nodes * n_items).  Same errors as bplb_check_batch_assign. */
+BPLB_API int bplb_reduce_batch(bplb_engine *eng, const int32_t *inst_w, int64_t n_items,
+                      int64_t n_bins, const void *assign, int32_t abytes, int64_t n_nodes,
+                      int64_t c, int64_t *offsets_out, int32_t *weights_out);
+
 /* Number of kernel launches issued by the engine since creation (for the
  * bench's gpu_launches claim), and device time of the last TIMING call. */
 BPLB_API int64_t bplb_launch_count(bplb_engine *eng);

@@ -22,7 +22,8 @@ from .bounds import (
 )
 from .instances import ArrayReducedInstance, ReducedInstance, reduce_packing_arrays
 from .parallel import GpuBoundEngine, ParallelBoundEngine, SharedMax, default_workers, lower_bound_par
-from .batch import csr_from_lists, lower_bound_batch
+from .batch import (csr_from_lists, lower_bound_batch, lower_bound_batch_assign, open_marker,
+                    reduce_packing_batch)
 
 __version__ = "0.1.0"
 
@@ -49,6 +50,9 @@ __all__ = [
     "l2_value",
     "lambda_range",
     "lower_bound_batch",
+    "lower_bound_batch_assign",
+    "open_marker",
+    "reduce_packing_batch",
     "lower_bound_par",
     "lower_bound_seq",
     "reduce_packing_arrays",

@@ -68,6 +68,11 @@ SIGNATURES = {
     "bplb_check_batch_device_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
                                                   ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i32p,
                                                   ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "bplb_check_batch_assign": (ctypes.c_int, [_vp, _i32p, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
+                                               ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i32p,
+                                               ctypes.c_int32, ctypes.c_int32, _i64p, _u8p, _i64p, _i64p]),
+    "bplb_reduce_batch": (ctypes.c_int, [_vp, _i32p, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
+                                         ctypes.c_int64, ctypes.c_int64, _i64p, _i32p]),
     "bplb_launch_count": (ctypes.c_int64, [_vp]),
     "bplb_last_device_ms": (ctypes.c_double, [_vp]),
     "bplb_profile_kernel": (ctypes.c_int, [_vp, ctypes.c_int]),
@@ -225,6 +230,51 @@ class Engine:
         if want_best:
             return lb, ex.view(bool), best, arg
         return lb, ex.view(bool)
+
+    @staticmethod
+    def _assign_args(inst_w, assign):
+        inst = as_i32(inst_w)
+        a = np.ascontiguousarray(assign)
+        if a.dtype not in (np.uint8, np.uint16):
+            raise ValueError("assignments must be uint8 or uint16 (open = all ones)")
+        if a.ndim != 2 or a.shape[1] != len(inst):
+            raise ValueError("assignments must be [n_nodes, n_items]")
+        return inst, a
+
+    def check_batch_assign(self, inst_w, assign: np.ndarray, n_bins: int, c: int, k: int, kinds, flags: int,
+                           want_best: bool = False):
+        """Device-side reduce_packing + LB collection for node states given
+        as bin assignments (see bplb_check_batch_assign)."""
+        inst, a = self._assign_args(inst_w, assign)
+        n = a.shape[0]
+        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        lb = np.empty(n, dtype=np.int64)
+        ex = np.empty(n, dtype=np.uint8)
+        best = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        arg = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        rc = self._lib.bplb_check_batch_assign(
+            self.handle, inst.ctypes.data_as(_i32p), len(inst), int(n_bins), _vp(a.ctypes.data), a.itemsize, n,
+            int(c), _clamp_k(k), ks.ctypes.data_as(_i32p), len(ks), int(flags), lb.ctypes.data_as(_i64p),
+            ex.ctypes.data_as(_u8p), best.ctypes.data_as(_i64p) if best is not None else None,
+            arg.ctypes.data_as(_i64p) if arg is not None else None)
+        if rc != 0:
+            _raise(rc, "bplb_check_batch_assign")
+        if want_best:
+            return lb, ex.view(bool), best, arg
+        return lb, ex.view(bool)
+
+    def reduce_batch(self, inst_w, assign: np.ndarray, n_bins: int, c: int):
+        """Device-side reduce_packing only: the reduced CSR (int32 weights, int64 offsets)."""
+        inst, a = self._assign_args(inst_w, assign)
+        n = a.shape[0]
+        off = np.empty(n + 1, dtype=np.int64)
+        w = np.empty(max(1, n * len(inst)), dtype=np.int32)
+        rc = self._lib.bplb_reduce_batch(self.handle, inst.ctypes.data_as(_i32p), len(inst), int(n_bins),
+                                         _vp(a.ctypes.data), a.itemsize, n, int(c), off.ctypes.data_as(_i64p),
+                                         w.ctypes.data_as(_i32p))
+        if rc != 0:
+            _raise(rc, "bplb_reduce_batch")
+        return w[:off[-1]].copy(), off
 
     def check_batch_device(self, w_ptr: int, off_ptr: int, n_nodes: int, max_r: int, c: int, k: int,
                            kinds, flags: int, lb_ptr: int, ex_ptr: int, best_ptr: int = 0,

@@ -47,3 +47,32 @@ def lower_bound_batch(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
     flags = {"full": 0, "seq": _native.F_PHASED, "cancel": _native.F_CANCEL}[mode]
     eng = engine or _native.default_engine()
     return eng.check_batch(weights, offsets, c, k, kind_ids(kinds), flags, want_best=want_best)
+
+
+def open_marker(dtype) -> int:
+    """Assignment value of an open item (all ones of the element type)."""
+    return int(np.iinfo(np.dtype(dtype)).max)
+
+
+def lower_bound_batch_assign(c: int, inst_weights, assign: np.ndarray, n_bins: int, k: int,
+                             kinds: Sequence = DEFAULT_DFF_ORDER, *, mode: str = "full",
+                             want_best: bool = False, engine: _native.Engine | None = None):
+    """The feasibility check of many search nodes given as bin assignments.
+
+    ``assign[node, i]`` is the bin item ``i`` is committed to, or
+    ``open_marker(assign.dtype)`` (uint8: 255, uint16: 65535) while it is
+    open.  Each node is reduced on the GPU exactly as ``reduce_packing``
+    (instances.py:262-282) -- open weights in item order, then positive bin
+    loads in bin order; a load above ``c`` raises ValueError -- and checked as
+    in :func:`lower_bound_batch` (same modes and outputs)."""
+    flags = {"full": 0, "seq": _native.F_PHASED, "cancel": _native.F_CANCEL}[mode]
+    eng = engine or _native.default_engine()
+    return eng.check_batch_assign(inst_weights, assign, n_bins, c, k, kind_ids(kinds), flags, want_best=want_best)
+
+
+def reduce_packing_batch(c: int, inst_weights, assign: np.ndarray, n_bins: int,
+                         engine: _native.Engine | None = None):
+    """Device-side ``reduce_packing`` of a batch of node states: the reduced
+    instances as CSR (int32 weights, int64 offsets), reference order."""
+    eng = engine or _native.default_engine()
+    return eng.reduce_batch(inst_weights, assign, n_bins, c)

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libbplb.so")
 SOURCES = ["bplb_capi.cu"]
-HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh"]
+HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh", "bplb_reduce.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -16,6 +16,7 @@
 #include "bplb_wide.cuh"
 #include "bplb_warp.cuh"
 #include "bplb_tab.cuh"
+#include "bplb_reduce.cuh"
 #include <vector>
 
 namespace {
@@ -95,6 +96,7 @@ struct bplb_engine {
     HostBuf h_stage, h_res;
     // batched small-c path: cached table of transformed values for (tab_c, tab_kmask)
     DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist;
+    DevBuf d_inst, d_assign, d_redr;  // device-side reduction of node states
     size_t tab_attr_smem = 0;
     int tab_per_sm = 1;
     int64_t tab_c = -1;
@@ -419,6 +421,64 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
     return 0;
 }
 
+
+// Device-side reduce_packing of a batch of node states (bplb_reduce.cuh):
+// uploads the instance and the assignments, leaves the reduced CSR in
+// d_w (obytes per weight) / d_off and the error flags in d_err[1].
+int reduce_device(bplb_engine* e, const int32_t* inst_w, int64_t n_items, int64_t n_bins, const void* assign,
+                  int32_t abytes, int64_t n_nodes, int64_t c, int* obytes) {
+    if (abytes != 1 && abytes != 2) return fail(BPLB_EINVAL, "assignment element must be 1 or 2 bytes");
+    if (n_items < 0 || n_bins < 0 || n_nodes < 0) return fail(BPLB_EINVAL, "bad shape");
+    if (n_bins > bplb::RED_MAX_BINS) return fail(BPLB_ERANGE, "more bins than the device reduction supports");
+    if (n_bins >= (abytes == 1 ? 255 : 65535)) return fail(BPLB_EINVAL, "bin ids collide with the open marker");
+    if (n_items > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items for the GPU envelope");
+    *obytes = c <= 255 ? 1 : (c <= 65535 ? 2 : 4);
+    int rc;
+    const size_t asz = (size_t)n_nodes * (size_t)n_items * (size_t)abytes;
+    if ((rc = e->d_inst.grow((size_t)std::max<int64_t>(n_items, 1) * 4))) return rc;
+    if ((rc = e->d_assign.grow(std::max<size_t>(asz, 16)))) return rc;
+    if ((rc = e->d_w.grow((size_t)std::max<int64_t>(n_nodes * n_items, 1) * 4 + 64))) return rc;
+    if ((rc = e->d_off.grow((size_t)(n_nodes + 1) * 8))) return rc;
+    if ((rc = e->d_redr.grow(16))) return rc;
+    if ((rc = e->d_err.grow(16))) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 8, e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->d_redr.p, 0, 8, e->stream));
+    if (asz > 65536 && !is_pinned(assign) && (rc = e->h_stage.grow(asz + 64))) return rc;
+    if ((rc = h2d(e, e->d_inst.p, inst_w, (size_t)n_items * 4, 0, e->stream, 1))) return rc;
+    if ((rc = h2d(e, e->d_assign.p, assign, asz))) return rc;
+    bplb::ReduceArgs a;
+    a.w = (const int*)e->d_inst.p;
+    a.assign = e->d_assign.p;
+    a.abytes = abytes;
+    a.n_items = n_items;
+    a.n_bins = n_bins;
+    a.n_nodes = n_nodes;
+    a.c = c;
+    a.r = (int64_t*)e->d_off.p;
+    a.out_w = e->d_w.p;
+    a.obytes = *obytes;
+    a.err = (int*)e->d_err.p + 1;
+    a.max_r = (unsigned long long*)e->d_redr.p;
+    const size_t smem = (size_t)(bplb::RED_NT / 32) * std::max<int64_t>(n_bins, 1) * 8;
+    if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(bplb::reduce_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(bplb::reduce_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = (unsigned)std::min<int64_t>((n_nodes + 7) / 8, (int64_t)8 * e->num_sms);
+    if (n_nodes > 0) {
+        bplb::reduce_count_kernel<<<grid, bplb::RED_NT, smem, e->stream>>>(a);
+        bplb::reduce_scan_kernel<<<1, 1024, 0, e->stream>>>(a.r, n_nodes);
+        bplb::reduce_write_kernel<<<grid, bplb::RED_NT, smem, e->stream>>>(a);
+        e->launches += 3;
+        CUDA_TRY(cudaGetLastError());
+    }
+    return 0;
+}
+
+const char* reduce_error(int err) {
+    return (err & 1) ? "committed bin load exceeds capacity (reduce_packing)" : "bin id out of range";
+}
+
 }  // namespace
 
 extern "C" {
@@ -467,7 +527,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
                       &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
-                      &e->d_tabkeys, &e->d_tabhist})
+                      &e->d_tabkeys, &e->d_tabhist, &e->d_inst, &e->d_assign, &e->d_redr})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -809,6 +869,92 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         e->last_ms = ms;
     }
     if (*h_err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+    return 0;
+}
+
+int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_items, int64_t n_bins,
+                            const void* assign, int32_t abytes, int64_t n_nodes, int64_t c, int64_t k,
+                            const int32_t* kinds, int32_t nkinds, int32_t flags, int64_t* lb_out,
+                            uint8_t* ex_out, int64_t* best_out, int64_t* arg_out) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (n_nodes < 0 || (n_nodes > 0 && (!lb_out || !ex_out || !assign || (n_items > 0 && !inst_w))))
+        return fail(BPLB_EINVAL, "bad batch arguments");
+    if (int rc = check_c(c)) return rc;
+    int ks[K_COUNT];
+    if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
+    if (n_nodes == 0) return 0;
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    const bool timing = flags & BPLB_F_TIMING;
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+    int obytes = 4, rc;
+    if ((rc = reduce_device(e, inst_w, n_items, n_bins, assign, abytes, n_nodes, c, &obytes))) return rc;
+    // r <= n_items for every node: the kernel choice uses that bound (no sync)
+    const int64_t max_r = std::max<int64_t>(n_items, 1);
+    if (k >= max_r) flags &= ~(BPLB_F_PHASED | BPLB_F_CANCEL);
+    if ((rc = e->d_lb.grow((size_t)n_nodes * 8))) return rc;
+    if ((rc = e->d_ex.grow((size_t)n_nodes))) return rc;
+    if (best_out && (rc = e->d_best.grow((size_t)n_nodes * 48))) return rc;
+    if (arg_out && (rc = e->d_arg.grow((size_t)n_nodes * 48))) return rc;
+    bplb::KParams p;
+    fill_params(p, c, k, ks, nkinds, flags);
+    p.w = (const int*)e->d_w.p;
+    p.wbytes = obytes;
+    p.off = (const int64_t*)e->d_off.p;
+    p.lb_out = (int64_t*)e->d_lb.p;
+    p.ex_out = (uint8_t*)e->d_ex.p;
+    p.best_out = best_out ? (int64_t*)e->d_best.p : nullptr;
+    p.arg_out = arg_out ? (int64_t*)e->d_arg.p : nullptr;
+    p.err_out = (int*)e->d_err.p;
+    if (!node_fits(max_r, c)) return fail(BPLB_ERANGE, "instance larger than the node-resident envelope");
+    if ((rc = launch_node(e, p, n_nodes, max_r, 0))) return rc;
+    if ((rc = e->h_res.grow(sizeof(bplb_result) + 16))) return rc;
+    int* h_err = (int*)((char*)e->h_res.p + sizeof(bplb_result));
+    CUDA_TRY(cudaMemcpyAsync(lb_out, e->d_lb.p, (size_t)n_nodes * 8, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(ex_out, e->d_ex.p, (size_t)n_nodes, cudaMemcpyDeviceToHost, e->stream));
+    if (best_out)
+        CUDA_TRY(cudaMemcpyAsync(best_out, e->d_best.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
+    if (arg_out)
+        CUDA_TRY(cudaMemcpyAsync(arg_out, e->d_arg.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(h_err, e->d_err.p, 8, cudaMemcpyDeviceToHost, e->stream));
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (timing) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+        e->last_ms = ms;
+    }
+    if (h_err[1]) return fail(BPLB_EINVAL, reduce_error(h_err[1]));
+    if (h_err[0]) return fail(BPLB_EINVAL, "instance weight outside [1, c]");
+    return 0;
+}
+
+int bplb_reduce_batch(bplb_engine* e, const int32_t* inst_w, int64_t n_items, int64_t n_bins,
+                      const void* assign, int32_t abytes, int64_t n_nodes, int64_t c, int64_t* off_out,
+                      int32_t* w_out) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (n_nodes < 0 || !off_out || (n_nodes > 0 && (!assign || !w_out || (n_items > 0 && !inst_w))))
+        return fail(BPLB_EINVAL, "bad batch arguments");
+    if (int rc = check_c(c)) return rc;
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    off_out[0] = 0;
+    if (n_nodes == 0) return 0;
+    int obytes = 4, rc;
+    if ((rc = reduce_device(e, inst_w, n_items, n_bins, assign, abytes, n_nodes, c, &obytes))) return rc;
+    std::vector<int64_t> off((size_t)n_nodes + 1);
+    int err[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(off.data(), e->d_off.p, off.size() * 8, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaMemcpyAsync(err, e->d_err.p, 8, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (err[1]) return fail(BPLB_EINVAL, reduce_error(err[1]));
+    const int64_t total = off[(size_t)n_nodes];
+    std::vector<unsigned char> buf((size_t)std::max<int64_t>(total, 1) * obytes);
+    CUDA_TRY(cudaMemcpy(buf.data(), e->d_w.p, (size_t)total * obytes, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < total; ++i)
+        w_out[i] = obytes == 1 ? buf[(size_t)i] : obytes == 2 ? ((const uint16_t*)buf.data())[i]
+                                                              : ((const int32_t*)buf.data())[i];
+    std::memcpy(off_out, off.data(), off.size() * 8);
     return 0;
 }
 

@@ -105,7 +105,7 @@ def _node_block(w: np.ndarray, c: int, k: int, rng: np.random.Generator, nb: int
         open_w = w[assign[b] < 0]
         ld = loads[b][loads[b] > 0]
         out.append(np.concatenate([open_w.astype(np.int64), ld]).astype(np.int32))
-    return out
+    return out, assign
 
 
 def node_batch(w: np.ndarray, c: int, k: int, n_nodes: int, seed: int, first_node: int = 0):
@@ -116,7 +116,7 @@ def node_batch(w: np.ndarray, c: int, k: int, n_nodes: int, seed: int, first_nod
     b1 = (first_node + n_nodes + BLOCK - 1) // BLOCK
     for b in range(b0, b1):
         rng = np.random.default_rng([seed, b])
-        blk = _node_block(w, c, k, rng, BLOCK)
+        blk, _ = _node_block(w, c, k, rng, BLOCK)
         lo = max(first_node, b * BLOCK) - b * BLOCK
         hi = min(first_node + n_nodes, (b + 1) * BLOCK) - b * BLOCK
         nodes.extend(blk[lo:hi])
@@ -125,6 +125,32 @@ def node_batch(w: np.ndarray, c: int, k: int, n_nodes: int, seed: int, first_nod
     np.cumsum(lens, out=off[1:])
     flat = np.concatenate(nodes) if nodes else np.zeros(0, dtype=np.int32)
     return flat.astype(np.int32), off
+
+
+def node_assignments(w: np.ndarray, c: int, k: int, n_nodes: int, seed: int, first_node: int = 0):
+    """The same node states as :func:`node_batch`, as bin assignments
+    (uint8 when k < 255, else uint16; open items = all ones): the input of
+    the device-side reduction (``lower_bound_batch_assign``)."""
+    dt = np.uint8 if k < 255 else np.uint16
+    openv = np.iinfo(dt).max
+    rows = []
+    b0 = first_node // BLOCK
+    b1 = (first_node + n_nodes + BLOCK - 1) // BLOCK
+    for b in range(b0, b1):
+        rng = np.random.default_rng([seed, b])
+        _, assign = _node_block(w, c, k, rng, BLOCK)
+        lo = max(first_node, b * BLOCK) - b * BLOCK
+        hi = min(first_node + n_nodes, (b + 1) * BLOCK) - b * BLOCK
+        rows.append(assign[lo:hi])
+    a = np.concatenate(rows) if rows else np.zeros((0, w.size), dtype=np.int64)
+    return np.where(a < 0, openv, a).astype(dt)
+
+
+def cfg2_assignments(n_nodes: int = 10_000, first_node: int = 0):
+    """cfg2 search nodes as (c, k, instance weights, bin assignments)."""
+    c, w = cfg2_instance()
+    k = l2_host(c, w) + 2
+    return c, k, w, node_assignments(w, c, k, n_nodes, seed=1, first_node=first_node)
 
 
 def cfg2_nodes(n_nodes: int = 10_000, first_node: int = 0):

@@ -332,3 +332,67 @@ def test_tab_large_batch_device_api(oracle):
     np.testing.assert_array_equal(lb[:m], lbo)
     lbh, _ = G.lower_bound_batch(c, flat, off, 2**62)
     np.testing.assert_array_equal(lb, lbh)
+
+
+# ---------------------------------------------------------------------------
+# Device-side reduce_packing of node states (bplb_reduce.cuh)
+# ---------------------------------------------------------------------------
+def _random_assignments(rng, n, k, c, n_nodes, dtype=np.uint8):
+    w = rng.integers(1, c // 3 + 1, n)
+    openv = np.iinfo(dtype).max
+    a = np.full((n_nodes, n), openv, dtype=dtype)
+    for r in range(n_nodes):
+        loads = np.zeros(k, dtype=np.int64)
+        depth = rng.integers(0, n + 1)
+        for i in rng.permutation(n)[:depth]:
+            j = rng.integers(0, k)
+            if loads[j] + w[i] <= c:
+                loads[j] += w[i]
+                a[r, i] = j
+    return w.astype(np.int32), a
+
+
+@pytest.mark.parametrize("c,n,k,dt", [(150, 500, 209, np.uint8), (1000, 300, 120, np.uint8),
+                                      (100_000, 200, 300, np.uint16), (7, 40, 30, np.uint8)])
+def test_reduce_batch_matches_reduce_packing(c, n, k, dt):
+    """Device reduction == reduce_packing_arrays (reference order) per node."""
+    from paper_2402_14821_b200.instances import reduce_packing_arrays
+
+    rng = np.random.default_rng(c + n)
+    w, a = _random_assignments(rng, n, k, c, 120, dt)
+    flat, off = G.reduce_packing_batch(c, w, a, k)
+    openv = np.iinfo(dt).max
+    for i in range(a.shape[0]):
+        asg = np.where(a[i] == openv, -1, a[i].astype(np.int64))
+        np.testing.assert_array_equal(flat[off[i]:off[i + 1]], reduce_packing_arrays(w, asg, k, c))
+
+
+def test_check_batch_assign_matches_csr_path(oracle):
+    """cfg2 nodes as assignments through the device reduction give the same
+    verdicts / per-kind bests as the CSR path and the oracle."""
+    c, k, w, a = W.cfg2_assignments(600)
+    _, _, flat, off = W.cfg2_nodes(600)
+    got = G.lower_bound_batch_assign(c, w, a, k, 2**62, want_best=True)
+    ref = G.lower_bound_batch(c, flat, off, 2**62, want_best=True)
+    for x, y in zip(got, ref):
+        np.testing.assert_array_equal(x, y)
+    lbo, _ = oracle.check_batch(flat[:off[100]], off[:101], c, 2**62)
+    np.testing.assert_array_equal(got[0][:100], lbo)
+    for mode in ("seq", "cancel"):
+        g = G.lower_bound_batch_assign(c, w, a, k, 209, mode=mode)
+        r = G.lower_bound_batch(c, flat, off, 209, mode=mode)
+        np.testing.assert_array_equal(g[1], r[1])
+
+
+def test_reduce_errors():
+    """A committed load above c and an out-of-range bin id raise ValueError."""
+    w = np.array([60, 60, 40], dtype=np.int32)
+    a = np.array([[0, 0, 255]], dtype=np.uint8)  # bin 0 holds 120 > 100
+    with pytest.raises(ValueError):
+        G.lower_bound_batch_assign(100, w, a, 4, 5)
+    a2 = np.array([[7, 255, 255]], dtype=np.uint8)  # bin 7 >= n_bins = 4
+    with pytest.raises(ValueError):
+        G.reduce_packing_batch(100, w, a2, 4)
+    # all open: the reduced instance is the instance itself
+    flat, off = G.reduce_packing_batch(100, w, np.full((2, 3), 255, dtype=np.uint8), 4)
+    np.testing.assert_array_equal(flat, np.concatenate([w, w]))

@@ -8,6 +8,7 @@ from __future__ import annotations
 import random
 import threading
 
+import numpy as np
 import pytest
 
 from paper_2402_14821_b200 import (DffKind, ParallelBoundEngine, ReducedInstance, SharedMax,
@@ -140,3 +141,18 @@ def test_workloads_deterministic():
     assert (f3 == f1[o1[10]:o1[15]]).all()
     c3, w3 = W.cfg3()
     assert w3.size == 1000 and ((w3 > c3 // 4) & (w3 < c3 // 2)).all() and -(-int(w3.sum()) // c3) == 334
+
+
+def test_node_assignments_reduce_to_node_batch():
+    """The assignment form of the cfg2 node generator reduces (reduce_packing
+    semantics) to exactly the CSR nodes the benchmark uses."""
+    from paper_2402_14821_b200 import workloads as W
+    from paper_2402_14821_b200.instances import reduce_packing_arrays
+
+    c, k, w, a = W.cfg2_assignments(40, first_node=3)
+    _, _, flat, off = W.cfg2_nodes(40, first_node=3)
+    openv = np.iinfo(a.dtype).max
+    for i in range(40):
+        asg = np.where(a[i] == openv, -1, a[i].astype(np.int64))
+        red = reduce_packing_arrays(w, asg, k, c)
+        np.testing.assert_array_equal(red, flat[off[i]:off[i + 1]])
