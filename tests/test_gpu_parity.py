@@ -396,3 +396,39 @@ def test_reduce_errors():
     # all open: the reduced instance is the instance itself
     flat, off = G.reduce_packing_batch(100, w, np.full((2, 3), 255, dtype=np.uint8), 4)
     np.testing.assert_array_equal(flat, np.concatenate([w, w]))
+
+
+# ---------------------------------------------------------------------------
+# Solver integration: GPU bound mode and batched dffstats
+# ---------------------------------------------------------------------------
+def _dffstats_golden():
+    with open(os.path.join(GOLDEN, "dffstats.json")) as f:
+        return json.load(f)
+
+
+def test_dffstats_batched_matches_reference():
+    """Root bounds and the dffstats table of 60 instances (3 capacities, one
+    batched launch each) equal the reference's cli._root_bounds / dffstats_table."""
+    from paper_2402_14821_b200 import solver
+
+    g = _dffstats_golden()
+    insts = [(x["c"], x["weights"], x["name"]) for x in g["instances"]]
+    roots = solver.root_bounds_batch(insts)
+    assert [{k.name: v for k, v in r.items()} for r in roots] == g["root_bounds"]
+    assert solver.dffstats_table(insts, g["optima"]) == g["table"]
+
+
+def test_gpu_bound_mode_engine():
+    """make_gpu_bound_engine gives a BoundEngine with lower_bound_seq semantics."""
+    from paper_2402_14821_b200 import solver
+
+    eng, close = solver.make_gpu_bound_engine(mode="seq")
+    rng = random.Random(3)
+    for _ in range(20):
+        c, w = random_reduced_pair(rng, 60, 300)
+        red = ReducedInstance(c, w)
+        k = rng.randint(0, 40)
+        got, want = eng(red, k), G.lower_bound_seq(red, k)
+        assert (got.lb, got.exceeded_k, got.evals, list(got.per_dff.items())) == \
+            (want.lb, want.exceeded_k, want.evals, list(want.per_dff.items()))
+    close()

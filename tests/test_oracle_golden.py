@@ -127,3 +127,18 @@ def test_oracle_known_answers(oracle):
     assert res.exceeded_k and list(res.per_dff) == ["MT"]
     res = oracle.lower_bound_seq((6, 6, 6), 10, 3)
     assert res.lb == 3 and not res.exceeded_k
+
+
+def test_oracle_pins_dffstats_golden(oracle):
+    """The C oracle's per-kind maxima equal the reference's root bounds in
+    tests/golden/dffstats.json (the fixture of the batched dffstats test)."""
+    import json
+    import os
+
+    with open(os.path.join(GOLDEN, "dffstats.json")) as f:
+        g = json.load(f)
+    kinds = ("MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1")
+    for x, roots in zip(g["instances"], g["root_bounds"]):
+        w = np.asarray(x["weights"], dtype=np.int64)
+        _, _, best = oracle.check_batch(w, np.array([0, len(w)]), x["c"], 2**62, want_best=True)
+        assert {k: int(best[0, i]) for i, k in enumerate(kinds)} == roots, x["name"]
