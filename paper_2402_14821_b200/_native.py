@@ -52,8 +52,10 @@ _vp = ctypes.c_void_p
 SIGNATURES = {
     "bplb_engine_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
     "bplb_engine_destroy": (ctypes.c_int, [_vp]),
-    "bplb_check": (ctypes.c_int, [_vp, _i32p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
-                                  _i32p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BplbResult)]),
+    # pointers as plain addresses: this is the per-node drop-in call, and
+    # ctypes' data_as/byref conversions cost microseconds each
+    "bplb_check": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                  _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
     "bplb_dff_bound_batch": (ctypes.c_int, [_vp, ctypes.c_int32, _i32p, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int64, _i64p]),
     "bplb_check_batch": (ctypes.c_int, [_vp, _i32p, _i64p, ctypes.c_int64, ctypes.c_int64,
@@ -145,6 +147,7 @@ class Engine:
             _raise(rc, "bplb_engine_create")
         self._h = h
         self.device = int(device)
+        self._kinds_cache: dict = {}
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -180,10 +183,13 @@ class Engine:
 
     def check(self, w: np.ndarray, c: int, k: int, kinds, flags: int) -> BplbResult:
         w = as_i32(w)
-        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        key = tuple(kinds)
+        ks = self._kinds_cache.get(key)
+        if ks is None:
+            ks = self._kinds_cache[key] = (ctypes.c_int32 * len(key))(*key)
         res = BplbResult()
-        rc = self._lib.bplb_check(self.handle, w.ctypes.data_as(_i32p), len(w), int(c), _clamp_k(k),
-                                  ks.ctypes.data_as(_i32p), len(ks), int(flags), ctypes.byref(res))
+        rc = self._lib.bplb_check(self.handle, w.ctypes.data if len(w) else None, len(w), int(c), _clamp_k(k),
+                                  ctypes.addressof(ks), len(key), int(flags), ctypes.addressof(res))
         if rc != 0:
             _raise(rc, "bplb_check")
         return res

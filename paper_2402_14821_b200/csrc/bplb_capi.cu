@@ -70,6 +70,27 @@ struct HostBuf {
     void release() { if (p) cudaFreeHost(p); p = nullptr; cap = 0; }
 };
 
+// Pinned host memory mapped into the device address space: the single-check
+// kernel reads its weights and writes its result through it (no separate
+// copy operations on the stream for a few hundred bytes each way).
+struct MappedBuf {
+    void* h = nullptr;
+    void* d = nullptr;
+    size_t cap = 0;
+    int grow(size_t bytes) {
+        if (bytes <= cap) return 0;
+        if (h) cudaFreeHost(h);
+        h = d = nullptr;
+        cap = 0;
+        size_t n = std::max<size_t>(bytes, 4096);
+        if (cudaHostAlloc(&h, n, cudaHostAllocMapped) != cudaSuccess) return fail(BPLB_ENOMEM, "cudaHostAlloc failed");
+        if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return fail(BPLB_ECUDA, "cudaHostGetDevicePointer failed");
+        cap = n;
+        return 0;
+    }
+    void release() { if (h) cudaFreeHost(h); h = d = nullptr; cap = 0; }
+};
+
 bool is_pinned(const void* ptr) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -97,6 +118,9 @@ struct bplb_engine {
     // batched small-c path: cached table of transformed values for (tab_c, tab_kmask)
     DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist;
     DevBuf d_inst, d_assign, d_redr;  // device-side reduction of node states
+    DevBuf d_skeys;                   // single-check table path: keys[8] + CTA counter
+    MappedBuf m_single;               // single-check table path: weights in, result out
+    bool skeys_zeroed = false;
     size_t tab_attr_smem = 0;
     int tab_per_sm = 1;
     int64_t tab_c = -1;
@@ -527,10 +551,11 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
                       &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
-                      &e->d_tabkeys, &e->d_tabhist, &e->d_inst, &e->d_assign, &e->d_redr})
+                      &e->d_tabkeys, &e->d_tabhist, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys})
         b->release();
     e->h_stage.release();
     e->h_res.release();
+    e->m_single.release();
     cudaEventDestroy(e->ev0);
     cudaEventDestroy(e->ev1);
     if (e->ev_pk0) cudaEventDestroy(e->ev_pk0);
@@ -592,16 +617,55 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     if (int rc = e->d_err.grow(16)) return rc;
     if (int rc = e->h_res.grow(sizeof(bplb_result) + 16)) return rc;
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
-    if ((size_t)r * 4 > 65536)
-        if (int rc = e->h_stage.grow((size_t)r * 4 + 64)) return rc;
-    if (int rc = h2d(e, e->d_w.p, w, (size_t)r * 4)) return rc;
-    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
     bplb::KParams p;
     fill_params(p, c, k, ks, nkinds, flags);
+    int rc;
+    const int64_t maxf = (tab_kmask(p) >> K_FS1 & 1) ? 101 * c : 2 * c;
+    const bool small_tab = c <= bplb::TAB_MAX_C && r <= 65535 && r * maxf < (1ll << 23) &&
+                           !(flags & BPLB_F_NOTAB) && tab_warps(e, ((int)c + 3) / 4 * 4) >= 2;
+    if (small_tab) {
+        // small capacity: the cached table, one CTA per 64-column sub-chunk;
+        // weights and result travel through mapped pinned memory
+        if ((rc = tab_ensure(e, p))) return rc;
+        if ((rc = e->d_skeys.grow(64))) return rc;
+        if (!e->skeys_zeroed) {
+            CUDA_TRY(cudaMemsetAsync(e->d_skeys.p, 0, 64, e->stream));
+            e->skeys_zeroed = true;
+        }
+        const size_t woff = 256 + sizeof(bplb_result);  // [result][err] [weights]
+        if ((rc = e->m_single.grow(woff + (size_t)r * 4))) return rc;
+        if (r > 0) std::memcpy((char*)e->m_single.h + woff, w, (size_t)r * 4);
+        p.w = (const int*)((char*)e->m_single.d + woff);
+        p.res_out = (bplb_result*)e->m_single.d;
+        p.err_out = (int*)((char*)e->m_single.d + sizeof(bplb_result));
+        bplb::TabDev t = tab_dev(e, p, 1);
+        const int KV = e->tab_KV;
+        bplb::tab_single_kernel<<<(unsigned)e->tab_nsub, bplb::TAB_SNT, (size_t)KV * 4 + 16 * 64 * 4, e->stream>>>(
+            p, t, (int)r, (unsigned*)e->d_skeys.p, (int*)e->d_skeys.p + 8);
+        e->launches++;
+        CUDA_TRY(cudaGetLastError());
+        if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+        if (timing) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+            e->last_ms = ms;
+        }
+        if (*(volatile int*)((char*)e->m_single.h + sizeof(bplb_result)))
+            return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+        std::memcpy(out, e->m_single.h, sizeof(bplb_result));
+        return 0;
+    }
+    // weights through the pinned staging buffer (the copy stays asynchronous)
+    if (int rc2 = e->h_stage.grow((size_t)r * 4 + 64)) return rc2;
+    if (r > 0) {
+        std::memcpy(e->h_stage.p, w, (size_t)r * 4);
+        CUDA_TRY(cudaMemcpyAsync(e->d_w.p, e->h_stage.p, (size_t)r * 4, cudaMemcpyHostToDevice, e->stream));
+    }
     p.w = (const int*)e->d_w.p;
     p.res_out = (bplb_result*)e->d_res.p;
-    p.err_out = (int*)e->d_err.p;
-    int rc;
+    p.err_out = (int*)((char*)e->d_res.p + sizeof(bplb_result));  // copied back with the result
+    CUDA_TRY(cudaMemsetAsync(p.err_out, 0, 4, e->stream));
     if (!node_fits(r, c)) {
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);
@@ -617,10 +681,8 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
         p.ms = (bplb::MultiState*)e->d_multi.p;
         if ((rc = launch_node(e, p, 1, r, 0, true))) return rc;
     }
-    CUDA_TRY(cudaMemcpyAsync(e->h_res.p, e->d_res.p, sizeof(bplb_result), cudaMemcpyDeviceToHost,
+    CUDA_TRY(cudaMemcpyAsync(e->h_res.p, e->d_res.p, sizeof(bplb_result) + 4, cudaMemcpyDeviceToHost,
                              e->stream));
-    CUDA_TRY(cudaMemcpyAsync((char*)e->h_res.p + sizeof(bplb_result), e->d_err.p, 4,
-                             cudaMemcpyDeviceToHost, e->stream));
     if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
     CUDA_TRY(cudaStreamSynchronize(e->stream));
     if (timing) {

@@ -459,4 +459,73 @@ __global__ void __launch_bounds__(64) tab_fin_kernel(KParams p, unsigned* gkeys)
     if (i < p.n_nodes) tab_node_result(p, gkeys, p.node0 + i);
 }
 
+// One small check on the cached table (the drop-in single-node call,
+// propagator.py:274-276, for c <= 288): one CTA per 64-column sub-chunk
+// builds the node's histogram in smem, sums its 64 columns (4 row quarters
+// per column, exact fp32 partial sums), applies the same exact ceil-div /
+// key epilogue and folds per-kind maxima into keys[8]; the last CTA writes
+// the result (mode replay of tab_node_result) and clears keys / counter.
+constexpr int TAB_SNT = 1024;  // 64 columns x 16 row groups
+__global__ void __launch_bounds__(TAB_SNT) tab_single_kernel(KParams p, TabDev t, int r, unsigned* keys, int* done) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int KV = t.KV, c = (int)p.c, sub = blockIdx.x, tid = threadIdx.x;
+    unsigned* Hu = (unsigned*)smem;                    // [KV] counts -> fp32
+    float* part = (float*)(smem + (size_t)KV * 4);     // [16][64]
+    __shared__ unsigned skey[TAB_KSLOT];
+    __shared__ int sbad;
+    for (int i = tid; i < KV; i += TAB_SNT) Hu[i] = 0u;
+    if (tid < TAB_KSLOT) skey[tid] = 0u;
+    if (tid == 0) sbad = 0;
+    __syncthreads();
+    int bad = 0;
+    for (int i = tid; i < r; i += TAB_SNT) {
+        const int x = p.w[i];  // int32, possibly mapped host memory (plain load)
+        if (x < 1 || x > c) { bad = 1; continue; }
+        atomicAdd(&Hu[x - 1], 1u);
+    }
+    if (bad) sbad = 1;
+    __syncthreads();
+    for (int i = tid; i < KV; i += TAB_SNT) ((float*)Hu)[i] = (float)Hu[i];
+    __syncthreads();
+    const float* H = (const float*)Hu;
+    const int col = tid & 63, q = tid >> 6, rq = (KV + 15) / 16;
+    const float* T = t.T + (size_t)sub * (KV + 2) * TAB_SUB + col;
+    // this thread's rows (<= 18 for KV <= 288): loads first, then the sums
+    float tv[18];
+    const int w0 = q * rq, w1 = min(KV, w0 + rq);
+#pragma unroll
+    for (int u = 0; u < 18; ++u) tv[u] = w0 + u < w1 ? __ldg(T + (size_t)(w0 + u) * TAB_SUB) : 0.0f;
+    float S = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 18; ++u) S = fmaf(w0 + u < w1 ? H[w0 + u] : 0.0f, tv[u], S);
+    part[q * 64 + col] = S;
+    __syncthreads();
+    if (tid < 64) {
+        float Sf = 0.0f;  // integers < 2^23: every partial sum is exact
+#pragma unroll
+        for (int g = 0; g < 16; ++g) Sf += part[g * 64 + col];
+        const int4 m = __ldg(t.meta + sub * TAB_SUB + col);
+        const int kind = m.w >> 16;
+        const unsigned bits = __float_as_uint(Sf + 8388608.0f);
+        const unsigned n2 = 2u * bits + (unsigned)m.y;
+        const unsigned qd = __umulhi(n2, (unsigned)m.x) >> m.z;
+        const unsigned key = (qd << 9) | (unsigned)(m.w & 0xffff);
+        if (kind < K_COUNT && (m.w & 0xffff)) atomicMax(&skey[kind], key);
+    }
+    __syncthreads();
+    if (tid < K_COUNT && skey[tid]) atomicMax(&keys[tid], skey[tid]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const bool last = atomicAdd(done, 1) == (int)gridDim.x - 1;
+        if (last) {
+            __threadfence();
+            *done = 0;
+            if (p.err_out) *p.err_out = sbad;  // every CTA sees the same weights
+            tab_node_result(p, keys, 0);
+            __threadfence_system();  // result may live in mapped host memory
+        }
+    }
+}
+
 }  // namespace bplb
