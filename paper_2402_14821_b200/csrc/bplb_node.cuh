@@ -449,6 +449,64 @@ __device__ __forceinline__ void block_table_scan(int* cnt, long long* wle, int n
     __syncthreads();
 }
 
+// Sort the r weights of sw by a counting sort on their bucket (v >> bk),
+// producing the bucket index bidx[b] = #{w < b << bk} (bidx[nb] = r) on the
+// way; tmp holds rcap ints.  Buckets hold few weights on typical inputs (insertion sort per
+// bucket); returns false (sw / bidx unspecified, tmp clobbered) when a
+// bucket exceeds 32 weights -- the caller then falls back to block_sort.
+__device__ __forceinline__ bool block_bucket_sort(int* sw, int* tmp, int* bidx, int r, int nb, int bk,
+                                                  int* s_maxb, long long* wsum) {
+    for (int b = threadIdx.x; b <= nb; b += NT) bidx[b] = 0;
+    if (threadIdx.x == 0) *s_maxb = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < r; i += NT) {
+        const int n = atomicAdd(&bidx[sw[i] >> bk], 1);
+        if (n >= 32) atomicMax(s_maxb, n + 1);
+    }
+    __syncthreads();
+    if (*s_maxb > 32) return false;
+    // exclusive scan of the nb + 1 bucket counts (bidx[nb] = 0 -> r)
+    {
+        const int per = (nb + 1 + NT - 1) / NT, b0 = threadIdx.x * per, b1 = min(nb + 1, b0 + per);
+        int s = 0;
+        for (int b = b0; b < b1; ++b) s += bidx[b];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        int x = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        long long off = 0;
+        for (int w = 0; w < warp; ++w) off += wsum[w];
+        int run = (int)off + x - s;  // inclusive scan: bidx[b] = end of bucket b
+        for (int b = b0; b < b1; ++b) {
+            run += bidx[b];
+            bidx[b] = run;
+        }
+    }
+    __syncthreads();
+    // scatter from each bucket's end (bidx moves back to the bucket's start)
+    for (int i = threadIdx.x; i < r; i += NT) {
+        const int v = sw[i];
+        tmp[atomicSub(&bidx[v >> bk], 1) - 1] = v;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += NT) {
+        const int s0 = bidx[b], e = bidx[b + 1];
+        for (int i = s0; i < e; ++i) {  // insertion sort of the bucket into sw
+            const int v = tmp[i];
+            int j = i;
+            while (j > s0 && sw[j - 1] > v) { sw[j] = sw[j - 1]; --j; }
+            sw[j] = v;
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
 __host__ __device__ inline int node_bucket_shift(int64_t c) {
     int k = 0;
     while ((c >> k) + 2 > NBMAX) ++k;
@@ -585,22 +643,31 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
             __syncthreads();
             block_table_scan(m.cnt, m.pre, (int)(c + 2), ctl.wsum, ctl.wsum2);
         } else {
-            block_sort(m.sw, pw);
+            // sorted weights + bucket index bidx[b] = #{w < b << k}: counting
+            // sort by bucket (O(r + nb)); bitonic sort when a bucket is crowded
+            const int nb = (int)(c >> m.bk) + 1;
+            __shared__ int s_maxb;
+            const bool bucketed = !ctl.bad && block_bucket_sort(m.sw, m.vb2, m.bidx, r, nb, m.bk, &s_maxb, ctl.wsum);
+            if (!bucketed) {
+                for (int i = threadIdx.x; i < pw; i += NT) m.sw[i] = i < r ? load_w(p, base + i) : INT_MAX;
+                __syncthreads();
+                block_sort(m.sw, pw);
+            }
             block_prefix_i64(m.sw, m.pre, r, ctl.wsum);
             const NodeStats& st = ctl.st;
             const int nm = st.n_big - st.n_full;
             for (int i = threadIdx.x; i < st.n_small + nm; i += NT)
                 m.vb2[i] = i < st.n_small ? m.sw[i] : m.sw[i + st.n_eq];
-            // bucket index: bidx[b] = #{w < b << k}
-            const int nb = (int)(c >> m.bk) + 1;
-            for (int b = threadIdx.x; b <= nb; b += NT) {
-                const int64_t v = (int64_t)b << m.bk;
-                int lo = 0, hi = r;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if ((int64_t)m.sw[mid] < v) lo = mid + 1; else hi = mid;
+            if (!bucketed) {
+                for (int b = threadIdx.x; b <= nb; b += NT) {
+                    const int64_t v = (int64_t)b << m.bk;
+                    int lo = 0, hi = r;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if ((int64_t)m.sw[mid] < v) lo = mid + 1; else hi = mid;
+                    }
+                    m.bidx[b] = b == nb ? r : lo;
                 }
-                m.bidx[b] = b == nb ? r : lo;
             }
             if (threadIdx.x == 0) ctl.n_vb2 = st.n_small + nm;
         }

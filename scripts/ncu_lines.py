@@ -4,7 +4,7 @@ ncu's CSV source export carries no per-line metrics here, so this joins the
 per-instruction SASS page (exec counts, warp-state samples) with nvdisasm's
 line table of the SAME build (-lineinfo):
 
-    python scripts/ncu_lines.py gpurun_out/prof.ncu-rep <kernel-substring> [libbplb.so]
+    python scripts/ncu_lines.py gpurun_out/prof.ncu-rep <kernel-regex> [libbplb.so] [mangled-substring]
 
 Only valid when the report was captured from the library passed in.
 """
@@ -53,10 +53,12 @@ def line_table(lib, kernel_sub):
     return table
 
 
-def main(rep, kernel_sub, lib="paper_2402_14821_b200/libbplb.so"):
+def main(rep, kernel_sub, lib="paper_2402_14821_b200/libbplb.so", mangled=None):
+    """kernel_sub filters the ncu report (demangled name regex); mangled (or
+    kernel_sub) selects the function in the library's line table."""
     rows = sass_rows(rep, kernel_sub)
     base = int(rows[0]["Address"], 16)
-    table = line_table(lib, kernel_sub)
+    table = line_table(lib, mangled or kernel_sub)
     S, I = "Warp Stall Sampling (All Samples)", "Instructions Executed"
     agg_s, agg_i = collections.Counter(), collections.Counter()
     reasons = collections.defaultdict(collections.Counter)
