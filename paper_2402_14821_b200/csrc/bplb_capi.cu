@@ -285,7 +285,7 @@ int tab_reserve(bplb_engine* e, int64_t n) {
     int rc;
     if ((rc = e->d_tabkeys.grow((size_t)n * bplb::TAB_KSLOT * 4))) return rc;
     // histogram tiles, indexed by absolute tile (node / 16)
-    if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 1) * ((bplb::TAB_MAX_C + 3) / 4 * 4) * bplb::TAB_TM * 4)))
+    if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 1) * ((bplb::TAB_MAX_C + 3) / 4 * 4 + 1) * bplb::TAB_TM * 4)))
         return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_tabkeys.p, 0, (size_t)n * bplb::TAB_KSLOT * 4, e->stream));
 
@@ -338,7 +338,7 @@ bplb::TabDev tab_dev(bplb_engine* e, const bplb::KParams& p, int64_t n_nodes) {
     t.P = e->tab_P;
     t.gkeys = (unsigned*)e->d_tabkeys.p;
     t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
-    t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM) * t.KV * bplb::TAB_TM;
+    t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM) * (t.KV + 1) * bplb::TAB_TM;
     return t;
 }
 

@@ -57,7 +57,8 @@ struct TabDev {
     int P;                        // = nsub: CTA b holds sub-chunk b % P
     unsigned* gkeys;              // [node * 8 + kind], zero between launches
     int64_t ntiles;
-    float* H;                     // [tile][KV][16] histogram counts (fp32) of this launch's tiles
+    float* H;                     // [tile][KV + 1][16] fp32 counts of this launch's tiles; row KV
+                                  // holds the tile's occupied row range {lo, hi} (int bits)
 };
 
 __host__ __device__ inline size_t tab_warp_bytes(int KV) { return (size_t)(KV + 2) * TAB_TM * 4; }
@@ -215,12 +216,23 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) 
         else tab_hist_node<4>(p, b, (int)(e - b), row, c, KV, &bad);
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
+    __shared__ int s_lo, s_hi;
+    if (threadIdx.x == 0) { s_lo = KV; s_hi = 0; }
     __syncthreads();
-    // fp32 [w][16]: float4 i holds w = i / 4, nodes 4 (i & 3) .. + 3
-    float4* dst = (float4*)(t.H + (int64_t)tile * KV * TAB_TM);
+    // fp32 [w][16]: float4 i holds w = i / 4, nodes 4 (i & 3) .. + 3; plus the
+    // rows that hold any count, [lo, hi) rounded to 4, in header row KV
+    float4* dst = (float4*)(t.H + (int64_t)tile * (KV + 1) * TAB_TM);
+    int lo = KV, hi = 0;
     for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT) {
         const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
         dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
+        if (a[0] | a[ld] | a[2 * ld] | a[3 * ld]) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
+    }
+    if (lo < hi) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
+        dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
     }
     // the histograms are read back by TMA (async proxy) in tab_kernel
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -334,13 +346,9 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     // lane 0: copy local tile k's histogram into buf by TMA
     auto load_tile = [&](float* buf, int k, unsigned long long* bar) {
         const int tl = rank + k * cpp;
-        tab_bulk_load(buf, t.H + (int64_t)tl * KV * TAB_TM, (unsigned)(KV * TAB_TM * 4), bar);
+        tab_bulk_load(buf, t.H + (int64_t)tl * (KV + 1) * TAB_TM, (unsigned)((KV + 1) * TAB_TM * 4), bar);
     };
     if (threadIdx.x == 0) s_next = nw;
-    // zero padding rows KV, KV + 1 of the buffers (never written by the copies)
-    if (lane < 2 * TAB_TM / 4)
-        for (int u = 0; u < NB; ++u)
-            ((float4*)(Hbuf + u * (KV + 2) * TAB_TM + KV * TAB_TM))[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     tab_bar_wait(tbar, 0);  // the table sub-chunk has landed
     const int ng = lane >> 4, lc = lane & 15;
@@ -381,7 +389,9 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     }
             // operands of 4 steps loaded up front; the other warp of the
             // SMSP covers the load latency
-            for (int k = 0; k < KV; k += 4) {
+            // only the rows holding a count in this tile (header row KV)
+            const int klo = __float_as_int(H[KV * TAB_TM]), khi = __float_as_int(H[KV * TAB_TM + 1]);
+            for (int k = klo; k < khi; k += 4) {
                 ulonglong2 f[4];
                 float4 h[4][2];
 #pragma unroll
