@@ -91,6 +91,19 @@ struct MappedBuf {
     void release() { if (h) cudaFreeHost(h); h = d = nullptr; cap = 0; }
 };
 
+// Device address of a pinned (page-locked, UVA-mapped) host buffer, or null:
+// kernels write batch outputs straight into such buffers, so the call needs
+// no device-to-host copies.
+void* device_alias(const void* ptr) {
+    if (!ptr) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 bool is_pinned(const void* ptr) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -120,6 +133,7 @@ struct bplb_engine {
     DevBuf d_inst, d_assign, d_redr;  // device-side reduction of node states
     DevBuf d_skeys;                   // single-check table path: keys[8] + CTA counter
     MappedBuf m_single;               // single-check table path: weights in, result out
+    MappedBuf m_err;                  // batch calls: error flag written by the kernels
     bool skeys_zeroed = false;
     size_t tab_attr_smem = 0;
     int tab_per_sm = 1;
@@ -556,6 +570,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     e->h_stage.release();
     e->h_res.release();
     e->m_single.release();
+    e->m_err.release();
     cudaEventDestroy(e->ev0);
     cudaEventDestroy(e->ev1);
     if (e->ev_pk0) cudaEventDestroy(e->ev_pk0);
@@ -842,12 +857,19 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
     p.w = (const int*)e->d_w.p;
     p.wbytes = wbytes;
     p.off = (const int64_t*)e->d_off.p;
-    p.lb_out = (int64_t*)e->d_lb.p;
-    p.ex_out = (uint8_t*)e->d_ex.p;
-    p.best_out = best_out ? (int64_t*)e->d_best.p : nullptr;
-    p.arg_out = arg_out ? (int64_t*)e->d_arg.p : nullptr;
-    p.err_out = (int*)e->d_err.p;
-    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    // outputs: written by the kernels straight into pinned caller buffers
+    // (no copies), else into device buffers copied back at the end
+    int64_t* lb_dev = (int64_t*)device_alias(lb_out);
+    uint8_t* ex_dev = (uint8_t*)device_alias(ex_out);
+    int64_t* best_dev = best_out ? (int64_t*)device_alias(best_out) : nullptr;
+    int64_t* arg_dev = arg_out ? (int64_t*)device_alias(arg_out) : nullptr;
+    p.lb_out = lb_dev ? lb_dev : (int64_t*)e->d_lb.p;
+    p.ex_out = ex_dev ? ex_dev : (uint8_t*)e->d_ex.p;
+    p.best_out = best_out ? (best_dev ? best_dev : (int64_t*)e->d_best.p) : nullptr;
+    p.arg_out = arg_out ? (arg_dev ? arg_dev : (int64_t*)e->d_arg.p) : nullptr;
+    if ((rc = e->m_err.grow(64))) return rc;
+    *(volatile int*)e->m_err.h = 0;  // the previous call has completed (calls are synchronous)
+    p.err_out = (int*)e->m_err.d;
     if (node_path && tab_path(e, p, n_nodes, max_r) && !(flags & BPLB_F_NOTAB)) {
         // table and key arrays for the whole batch before concurrent chunk launches
         if ((rc = tab_ensure(e, p))) return rc;
@@ -857,6 +879,21 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
     // stream as soon as its bytes have landed: the PCIe transfer of chunk
     // i+1 overlaps the kernel of chunk i, and chunk kernels overlap each
     // other's tails.  Small batches use a single chunk.
+    // table path with pinned caller buffers: the histogram pass reads the
+    // weights and offsets over PCIe directly (zero-copy; measured 167 us vs
+    // 184 us p50 for the chunked uploads on cfg2, and far less jitter)
+    const void* w_alias = pinned ? device_alias(w) : nullptr;
+    const void* off_alias = w_alias ? device_alias(off) : nullptr;
+    if (w_alias && off_alias && !((uintptr_t)w_alias & 15) && node_path && !(flags & BPLB_F_NOTAB)) {
+        bplb::KParams q = p;
+        q.w = (const int*)w_alias;
+        q.off = (const int64_t*)off_alias;
+        if (tab_path(e, q, n_nodes, max_r)) {
+            if ((rc = launch_tab(e, q, n_nodes, 0))) return rc;
+            goto outputs;
+        }
+    }
+    {
     int nch = node_path && n_nodes >= 4096 && wsz >= (size_t)1 << 20 ? 4 : 1;
     int64_t bounds_[5];
     for (int i = 0; i <= nch; ++i) bounds_[i] = n_nodes * i / nch;
@@ -914,15 +951,14 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             if (rc) return fail(rc, bplb::wide_error());
         }
     }
-    if ((rc = e->h_res.grow(sizeof(bplb_result) + 16))) return rc;
-    int* h_err = (int*)((char*)e->h_res.p + sizeof(bplb_result));  // pinned: no synchronous copy
-    CUDA_TRY(cudaMemcpyAsync(lb_out, e->d_lb.p, (size_t)n_nodes * 8, cudaMemcpyDeviceToHost, e->stream));
-    CUDA_TRY(cudaMemcpyAsync(ex_out, e->d_ex.p, (size_t)n_nodes, cudaMemcpyDeviceToHost, e->stream));
-    if (best_out)
+    }
+outputs:
+    if (!lb_dev) CUDA_TRY(cudaMemcpyAsync(lb_out, e->d_lb.p, (size_t)n_nodes * 8, cudaMemcpyDeviceToHost, e->stream));
+    if (!ex_dev) CUDA_TRY(cudaMemcpyAsync(ex_out, e->d_ex.p, (size_t)n_nodes, cudaMemcpyDeviceToHost, e->stream));
+    if (best_out && !best_dev)
         CUDA_TRY(cudaMemcpyAsync(best_out, e->d_best.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
-    if (arg_out)
+    if (arg_out && !arg_dev)
         CUDA_TRY(cudaMemcpyAsync(arg_out, e->d_arg.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
-    CUDA_TRY(cudaMemcpyAsync(h_err, e->d_err.p, 4, cudaMemcpyDeviceToHost, e->stream));
     if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
     CUDA_TRY(cudaStreamSynchronize(e->stream));
     if (timing) {
@@ -930,7 +966,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         cudaEventElapsedTime(&ms, e->ev0, e->ev1);
         e->last_ms = ms;
     }
-    if (*h_err) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+    if (*(volatile int*)e->m_err.h) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
     return 0;
 }
 
