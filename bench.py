@@ -143,13 +143,22 @@ def cpu_baseline(c, k, flat, off, seconds: float = 15.0) -> dict:
                       f"{dt2:.1f} s on {threads} threads"}
 
 
-def extra_latencies() -> dict:
-    """Single-check latencies of cfg1 / cfg3 / cfg4 through the public API."""
+def extra_configs(with_cpu: bool = True) -> dict:
+    """The other BASELINE.json configs through the public API, each beside the
+    CPU reference port (oracle/, restating bounds.py) timed on a bounded
+    sample in the same run:
+      cfg1, cfg3, cfg4  single drop-in checks (lower_bound_par, no cancellation)
+      cfg5              batched search nodes of the cfg3 instance (2048 nodes)
+      cfg2_assign       cfg2 nodes given as bin assignments (device-side
+                        reduce_packing + check), pinned host buffers."""
+    import torch
+
     import paper_2402_14821_b200 as G
+    from oracle import oracle as O
     from paper_2402_14821_b200 import workloads as W
 
     out = {}
-    for name, gen, reps in (("cfg1", W.cfg1, 200), ("cfg3", W.cfg3, 50), ("cfg4", W.cfg4, 8)):
+    for name, gen, reps, cpu_reps in (("cfg1", W.cfg1, 200, 200), ("cfg3", W.cfg3, 50, 3), ("cfg4", W.cfg4, 8, 0)):
         c, w = gen()
         red = G.ReducedInstance.from_array(c, w)
         G.lower_bound_par(red, 2**62, cancellation=False)
@@ -158,9 +167,51 @@ def extra_latencies() -> dict:
             t = time.perf_counter()
             res = G.lower_bound_par(red, 2**62, cancellation=False)
             ts.append(time.perf_counter() - t)
-        out[name] = {"us_per_check_median": round(statistics.median(ts) * 1e6, 1),
-                     "checks_per_s": round(1.0 / statistics.median(ts), 1), "lb": res.lb,
-                     "r": int(w.size), "c": c}
+        d = {"us_per_check_median": round(statistics.median(ts) * 1e6, 1),
+             "checks_per_s": round(1.0 / statistics.median(ts), 1), "lb": res.lb, "r": int(w.size), "c": c}
+        if with_cpu and cpu_reps:
+            O.set_threads(1)
+            tc = []
+            for _ in range(cpu_reps):
+                t = time.perf_counter()
+                O.lower_bound_seq(w.astype(np.int64), c, 2**62)
+                tc.append(time.perf_counter() - t)
+            d["cpu_port_1thread_us_median"] = round(statistics.median(tc) * 1e6, 1)
+        elif cpu_reps == 0:
+            d["cpu_reference"] = "DNF: lower_bound_seq raises MemoryError (VB2 dense matrix, 373 GiB); " \
+                                 "~729 core-s chunked + extrapolated (SURVEY.md 6.3)"
+        out[name] = d
+    # cfg5: batched nodes of the cfg3 instance (c = 10^5), host buffers
+    c, k, flat, off = W.cfg5_nodes(2048)
+    G.lower_bound_batch(c, flat, off, 2**62)
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        G.lower_bound_batch(c, flat, off, 2**62)
+        ts.append(time.perf_counter() - t)
+    d = {"nodes": 2048, "ms_per_batch_median": round(statistics.median(ts) * 1e3, 2),
+         "checks_per_s": round(2048 / statistics.median(ts), 1), "mean_r": float(np.diff(off).mean()), "c": c}
+    if with_cpu:
+        O.set_threads(O.max_threads())
+        m = 32
+        t = time.perf_counter()
+        O.check_batch(flat[:off[m]].astype(np.int64), off[:m + 1], c, 2**62)
+        d["cpu_port_checks_per_s"] = round(m / (time.perf_counter() - t), 1)
+        d["cpu_port_threads"] = O.max_threads()
+        d["cpu_sample"] = f"first {m} nodes"
+    out["cfg5"] = d
+    # cfg2 from bin assignments (device-side reduce_packing), pinned buffers
+    c, k, w, a = W.cfg2_assignments(10_000)
+    ha = torch.from_numpy(a).pin_memory().numpy()
+    G.lower_bound_batch_assign(c, w, ha, k, 2**62)
+    ts = []
+    for _ in range(10):
+        t = time.perf_counter()
+        G.lower_bound_batch_assign(c, w, ha, k, 2**62)
+        ts.append(time.perf_counter() - t)
+    out["cfg2_assign"] = {"nodes": 10_000, "us_per_batch_median": round(statistics.median(ts) * 1e6, 1),
+                          "checks_per_s": round(10_000 / statistics.median(ts), 1),
+                          "h2d_bytes": int(a.nbytes + w.nbytes)}
     return out
 
 
@@ -384,7 +435,7 @@ def run_ours(args):
     if ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(c, kk, flat, off, seconds=args.cpu_seconds)
     if ws == 1 and not args.no_extra:
-        line["extra_single_check_latency"] = extra_latencies()
+        line["extra_configs"] = extra_configs(with_cpu=not args.no_cpu)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

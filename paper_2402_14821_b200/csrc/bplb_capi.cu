@@ -986,6 +986,76 @@ int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_ite
     const bool timing = flags & BPLB_F_TIMING;
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
     int obytes = 4, rc;
+    if ((rc = e->m_err.grow(64))) return rc;
+    // table path: histograms straight from the assignments (no reduced CSR);
+    // pinned assignments are read across PCIe (zero-copy), outputs written
+    // into pinned caller buffers
+    {
+        bplb::KParams q;
+        fill_params(q, c, k, ks, nkinds, flags);
+        const int64_t maxf = (tab_kmask(q) >> K_FS1 & 1) ? 101 * c : 2 * c;
+        const bool tab = !(flags & BPLB_F_NOTAB) && (abytes == 1 || abytes == 2) && c <= bplb::TAB_MAX_C &&
+                         n_items <= 65535 && std::max<int64_t>(n_items, 1) * maxf < (1ll << 23) &&
+                         n_bins <= bplb::TAB_ASSIGN_MAX_BINS && n_bins < (abytes == 1 ? 255 : 65535) &&
+                         n_nodes >= 256 && n_nodes <= ((int64_t)1 << 30) && tab_warps(e, ((int)c + 3) / 4 * 4) >= 2;
+        if (tab) {
+            const void* a_dev = device_alias(assign);
+            const size_t asz = (size_t)n_nodes * (size_t)n_items * (size_t)abytes;
+            if (!a_dev || ((uintptr_t)a_dev & 15)) {
+                if ((rc = e->d_assign.grow(std::max<size_t>(asz, 16)))) return rc;
+                if (asz > 65536 && !is_pinned(assign) && (rc = e->h_stage.grow(asz + 64))) return rc;
+                if ((rc = h2d(e, e->d_assign.p, assign, asz))) return rc;
+                a_dev = e->d_assign.p;
+            }
+            if ((rc = e->d_inst.grow((size_t)std::max<int64_t>(n_items, 1) * 4))) return rc;
+            if ((rc = h2d(e, e->d_inst.p, inst_w, (size_t)n_items * 4, 0, e->stream, 1))) return rc;
+            if ((rc = tab_ensure(e, q))) return rc;
+            if ((rc = tab_reserve(e, n_nodes))) return rc;
+            int64_t* lb_dev = (int64_t*)device_alias(lb_out);
+            uint8_t* ex_dev = (uint8_t*)device_alias(ex_out);
+            int64_t* best_dev = best_out ? (int64_t*)device_alias(best_out) : nullptr;
+            int64_t* arg_dev = arg_out ? (int64_t*)device_alias(arg_out) : nullptr;
+            if ((rc = e->d_lb.grow((size_t)n_nodes * 8))) return rc;
+            if ((rc = e->d_ex.grow((size_t)n_nodes))) return rc;
+            if (best_out && !best_dev && (rc = e->d_best.grow((size_t)n_nodes * 48))) return rc;
+            if (arg_out && !arg_dev && (rc = e->d_arg.grow((size_t)n_nodes * 48))) return rc;
+            q.lb_out = lb_dev ? lb_dev : (int64_t*)e->d_lb.p;
+            q.ex_out = ex_dev ? ex_dev : (uint8_t*)e->d_ex.p;
+            q.best_out = best_out ? (best_dev ? best_dev : (int64_t*)e->d_best.p) : nullptr;
+            q.arg_out = arg_out ? (arg_dev ? arg_dev : (int64_t*)e->d_arg.p) : nullptr;
+            int* herr = (int*)e->m_err.h;
+            herr[0] = herr[1] = 0;
+            q.err_out = (int*)e->m_err.d;
+            q.n_nodes = n_nodes;
+            const bplb::TabDev t = tab_dev(e, q, n_nodes);
+            const int KV = e->tab_KV;
+            const size_t hs = ((size_t)bplb::TAB_TM * (KV + 1) + ((n_items + 3) & ~3) + (size_t)bplb::TAB_TM * n_bins) * 4;
+            auto hk = abytes == 1 ? bplb::tab_hist_assign_kernel<1> : bplb::tab_hist_assign_kernel<2>;
+            if (hs > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
+            hk<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(q, t, (const int*)e->d_inst.p, (int)n_items,
+                                                                    (int)n_bins, a_dev, (int*)e->m_err.d);
+            e->launches++;
+            CUDA_TRY(cudaGetLastError());
+            if ((rc = tab_contract(e, q, n_nodes))) return rc;
+            if ((rc = tab_fin(e, q, n_nodes))) return rc;
+            if (!lb_dev) CUDA_TRY(cudaMemcpyAsync(lb_out, e->d_lb.p, (size_t)n_nodes * 8, cudaMemcpyDeviceToHost, e->stream));
+            if (!ex_dev) CUDA_TRY(cudaMemcpyAsync(ex_out, e->d_ex.p, (size_t)n_nodes, cudaMemcpyDeviceToHost, e->stream));
+            if (best_out && !best_dev)
+                CUDA_TRY(cudaMemcpyAsync(best_out, e->d_best.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
+            if (arg_out && !arg_dev)
+                CUDA_TRY(cudaMemcpyAsync(arg_out, e->d_arg.p, (size_t)n_nodes * 48, cudaMemcpyDeviceToHost, e->stream));
+            if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+            CUDA_TRY(cudaStreamSynchronize(e->stream));
+            if (timing) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+                e->last_ms = ms;
+            }
+            if (herr[1]) return fail(BPLB_EINVAL, reduce_error(herr[1]));
+            if (herr[0]) return fail(BPLB_EINVAL, "instance weight outside [1, c]");
+            return 0;
+        }
+    }
     if ((rc = reduce_device(e, inst_w, n_items, n_bins, assign, abytes, n_nodes, c, &obytes))) return rc;
     // r <= n_items for every node: the kernel choice uses that bound (no sync)
     const int64_t max_r = std::max<int64_t>(n_items, 1);

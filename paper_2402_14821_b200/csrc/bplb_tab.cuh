@@ -238,6 +238,96 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) 
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Phase A from node states given as bin assignments (bplb_check_batch_assign
+// on the table path): the histogram of each node's reduced instance --
+// reduce_packing (instances.py:262-282): the open items' weights plus one
+// virtual item per bin with a positive committed load -- is built directly,
+// without materialising the reduced CSR (every bound depends on the
+// multiset only, G11).  One CTA per 16-node tile, warp j = node j: its
+// assignment row read as aligned 16-byte vectors, open items counted into
+// the node's histogram row, committed weights summed per bin in smem, then
+// the positive loads counted.  err[0]: instance weight outside [1, c];
+// err[1]: bit 1 = a committed load above c, bit 2 = a bin id >= n_bins.
+constexpr int TAB_ASSIGN_MAX_BINS = 512;
+template <int AB>
+__global__ void __launch_bounds__(TAB_HNT) tab_hist_assign_kernel(KParams p, TabDev t, const int* inst_w, int n_items,
+                                                                   int n_bins, const void* assign, int* err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int KV = t.KV, ld = KV + 1, c = (int)p.c;
+    unsigned* Hs = (unsigned*)smem;                                  // [16][KV + 1]
+    int* iw = (int*)(Hs + TAB_TM * ld);                              // [n_items]
+    unsigned* loads = (unsigned*)(iw + ((n_items + 3) & ~3));        // [16][n_bins]
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+    const int tile = blockIdx.x;
+    const unsigned openv = AB == 1 ? 0xffu : 0xffffu;
+    __shared__ int s_bad, s_rerr;
+    if (threadIdx.x == 0) { s_bad = 0; s_rerr = 0; }
+    for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = threadIdx.x; i < TAB_TM * n_bins; i += TAB_HNT) loads[i] = 0u;
+    for (int i = threadIdx.x; i < n_items; i += TAB_HNT) {
+        const int x = __ldg(inst_w + i);
+        if (x < 1 || x > c) s_bad = 1;
+        iw[i] = x;
+    }
+    __syncthreads();
+    const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
+    int rerr = 0;
+    if (node < p.node0 + p.n_nodes && !s_bad) {
+        unsigned* row = Hs + j * ld;
+        unsigned* ld_ = loads + j * n_bins;
+        constexpr int PER = 16 / AB;
+        const int64_t b0 = node * (int64_t)n_items;
+        const int64_t e0 = b0 & ~(int64_t)(PER - 1);
+        const int lead = (int)(b0 - e0);
+        const int nv = (lead + n_items + PER - 1) / PER;
+        const uint4* src = (const uint4*)((const unsigned char*)assign + e0 * AB);
+        for (int v = lane; v < nv; v += 32) {
+            const uint4 x = src[v];  // possibly mapped host memory (zero-copy)
+            const unsigned wds[4] = {x.x, x.y, x.z, x.w};
+            const int elo = v * PER - lead;  // item index of element 0
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int i = elo + e;
+                if ((unsigned)i >= (unsigned)n_items) continue;
+                const unsigned word = wds[(e * AB) >> 2];
+                const unsigned b = (word >> (((e * AB) & 3) * 8)) & openv;
+                if (b == openv) atomicAdd(row + iw[i] - 1, 1u);
+                else if (b < (unsigned)n_bins) atomicAdd(ld_ + b, (unsigned)iw[i]);
+                else rerr |= 2;
+            }
+        }
+        __syncwarp();
+        for (int b = lane; b < n_bins; b += 32) {
+            const unsigned L = ld_[b];
+            if (L > (unsigned)c) rerr |= 1;
+            else if (L > 0u) atomicAdd(row + L - 1, 1u);
+        }
+    }
+    if (rerr) atomicOr(&s_rerr, rerr);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_bad) atomicExch(err, 1);
+        if (s_rerr) atomicOr(err + 1, s_rerr);
+    }
+    __shared__ int s_lo, s_hi;
+    if (threadIdx.x == 0) { s_lo = KV; s_hi = 0; }
+    __syncthreads();
+    float4* dst = (float4*)(t.H + (int64_t)tile * (KV + 1) * TAB_TM);
+    int lo = KV, hi = 0;
+    for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT) {
+        const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
+        dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
+        if (a[0] | a[ld] | a[2 * ld] | a[3 * ld]) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
+    }
+    if (lo < hi) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
+        dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Phase C: per-node results from the best keys (key = bound << 9 | 511 -
 // lambda), with the kinds replayed in order as warp_node_kernel evaluates
 // them: full collection, PHASED (stop after the first kind whose running max

@@ -432,3 +432,25 @@ def test_gpu_bound_mode_engine():
         assert (got.lb, got.exceeded_k, got.evals, list(got.per_dff.items())) == \
             (want.lb, want.exceeded_k, want.evals, list(want.per_dff.items()))
     close()
+
+
+def test_assign_table_path_errors_and_modes(oracle):
+    """>= 256 nodes from assignments take the table path (histograms straight
+    from the assignments): errors as reduce_packing, uint16 assignments, and
+    all modes against the CSR path."""
+    c, k, w, a = W.cfg2_assignments(300)
+    _, _, flat, off = W.cfg2_nodes(300)
+    a16 = np.where(a == 255, 65535, a.astype(np.uint16)).astype(np.uint16)
+    for mode, kk in (("full", 2**62), ("seq", 209), ("cancel", 209)):
+        got = G.lower_bound_batch_assign(c, w, a16, k, kk, mode=mode, want_best=True)
+        ref = G.lower_bound_batch(c, flat, off, kk, mode=mode, want_best=True)
+        for x, y in zip(got, ref):
+            np.testing.assert_array_equal(x, y)
+    bad = a.copy()
+    bad[17, :] = 0  # every item committed to bin 0: load far above c
+    with pytest.raises(ValueError):
+        G.lower_bound_batch_assign(c, w, bad, k, 2**62)
+    bad = a.copy()
+    bad[5, 3] = k + 2  # bin id >= n_bins
+    with pytest.raises(ValueError):
+        G.lower_bound_batch_assign(c, w, bad, k, 2**62)
