@@ -138,7 +138,7 @@ struct bplb_engine {
     size_t tab_attr_smem = 0;
     int tab_per_sm = 1;
     int64_t tab_c = -1;
-    int tab_kmask = -1, tab_KV = 0, tab_nsub = 0, tab_spp = 0, tab_P = 0;
+    int tab_kmask = -1, tab_KV = 0, tab_nsub = 0, tab_P = 0;
     int64_t tab_nodes = 0;  // capacity of d_tabkeys / d_tabhist (nodes)
     int64_t launches = 0;
     double last_ms = 0.0;
@@ -269,7 +269,7 @@ int tab_ensure(bplb_engine* e, const bplb::KParams& p) {
     const int KV = (c + 3) / 4 * 4;
     const int nsub = (int)(meta.size() / bplb::TAB_SUB);
     if (tab_warps(e, KV) < 1) return fail(BPLB_ERANGE, "capacity too large for the table path");
-    const int P = nsub, spp = 1;  // one 64-column sub-chunk per CTA
+    const int P = nsub;  // one 64-column sub-chunk per CTA
     int rc;
     if ((rc = e->d_tab.grow((size_t)nsub * (KV + 2) * bplb::TAB_SUB * 4))) return rc;
     if ((rc = e->d_tabmeta.grow(meta.size() * (sizeof(int4) + sizeof(int2))))) return rc;
@@ -287,7 +287,6 @@ int tab_ensure(bplb_engine* e, const bplb::KParams& p) {
     e->tab_kmask = kmask;
     e->tab_KV = KV;
     e->tab_nsub = nsub;
-    e->tab_spp = spp;
     e->tab_P = P;
     return 0;
 }

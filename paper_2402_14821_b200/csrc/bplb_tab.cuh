@@ -50,9 +50,9 @@ constexpr int TAB_KSLOT = 8;        // key slots per node (6 kinds; 6 = padding 
 struct TabDev {
     const float* T;               // [nsub][KV + 2][64]
     const int4* meta;             // [nsub * 64] {m, K, l, lk | kind << 16}
-    int KV;                       // rows swept (w = 1..KV, KV = c rounded up to 4); the table
-                                  // and the histogram buffers hold KV + 2 rows (zero) so the
-                                  // two-stage k pipeline reads ahead without a bound check
+    int KV;                       // rows swept (w = 1..KV, KV = c rounded up to 4); table
+                                  // sub-chunks and histogram buffers are KV + 2 rows long
+                                  // (row KV of a histogram tile: its occupied row range)
     int nsub;                     // 64-column sub-chunks in the whole table
     int P;                        // = nsub: CTA b holds sub-chunk b % P
     unsigned* gkeys;              // [node * 8 + kind], zero between launches
