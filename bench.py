@@ -400,7 +400,9 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "int (exact: uint8 weights, fp32 FFMA2 sums of integers < 2^23, int32/int64 bounds)",
+        "data": "synthetic",
         "config": {"workload": "cfg2: Scholl-1-shaped instance (n=500, w~U{20..100}, c=150), batch of "
                                "search-node residual states per GPU, full LB collection (k=2^62)",
                    "nodes_per_gpu": n, "global_batch": total_nodes, "c": c, "bins_k_generator": k,
