@@ -454,3 +454,36 @@ def test_assign_table_path_errors_and_modes(oracle):
     bad[5, 3] = k + 2  # bin id >= n_bins
     with pytest.raises(ValueError):
         G.lower_bound_batch_assign(c, w, bad, k, 2**62)
+
+
+def test_pinned_zero_copy_batch_paths(oracle):
+    """Pinned caller buffers take the zero-copy path (the histogram pass reads
+    the weights across PCIe, kernels write the outputs into the pinned
+    arrays); results equal the pageable path, errors still raise."""
+    import torch
+
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.default_engine()
+    c, k, flat, off = W.cfg2_nodes(2000)
+    w8 = flat.astype(np.uint8)
+    ref = eng.check_batch(w8, off, c, 2**62, list(range(6)), 0, want_best=True)
+    pw = torch.from_numpy(w8).pin_memory().numpy()
+    po = torch.from_numpy(off).pin_memory().numpy()
+    n = len(off) - 1
+    lb = torch.empty(n, dtype=torch.int64).pin_memory().numpy()
+    ex = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
+    for inputs in ((pw, po), (w8, off)):
+        for outputs in ((lb, ex), None):
+            got = eng.check_batch(inputs[0], inputs[1], c, 2**62, list(range(6)), 0, out=outputs)
+            np.testing.assert_array_equal(got[0], ref[0])
+            np.testing.assert_array_equal(got[1], ref[1])
+    got = eng.check_batch(pw, po, c, 209, list(range(6)), _native.F_PHASED, want_best=True)
+    want = eng.check_batch(w8, off, c, 209, list(range(6)), _native.F_PHASED, want_best=True)
+    for a, b in zip(got, want):
+        np.testing.assert_array_equal(a, b)
+    bad = pw.copy()
+    bad[off[7] + 3] = 0  # weight 0 is outside [1, c]
+    pbad = torch.from_numpy(bad).pin_memory().numpy()
+    with pytest.raises(ValueError):
+        eng.check_batch(pbad, po, c, 2**62, list(range(6)), 0, out=(lb, ex))
