@@ -359,7 +359,10 @@ int tab_hist(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     p.n_nodes = n_nodes;
     const bplb::TabDev t = tab_dev(e, p, n_nodes);
     const size_t hs = ((size_t)bplb::TAB_TM * (t.KV + 1) + 2 * bplb::TAB_HPAD) * 4;  // <= 20.5 KB (KV <= 288)
-    bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
+    if (p.wbytes == 1 && !((uintptr_t)p.w & 15))
+        bplb::tab_hist_u8_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT8, hs, e->stream>>>(p, t);
+    else
+        bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     return 0;

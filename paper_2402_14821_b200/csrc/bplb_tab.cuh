@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) 
         const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
         dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
     }
-    // the histograms are read back by TMA (async proxy) in tab_kernel
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+    // (read back by TMA in tab_kernel after the PDL grid-dependency wait,
+    // which orders this grid's completed writes before the copies)
 }
 
 // Phase A from node states given as bin assignments (bplb_check_batch_assign
@@ -325,7 +325,80 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_assign_kernel(KParams p, Tab
         const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
         dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// uint8 weights: one CTA of 8 warps per 16-node tile, a half-warp per node
+// (all of a lane's vector loads issued before any is counted), so a 10^4-node
+// batch's tiles are resident in one wave (same output as tab_hist_kernel).
+constexpr int TAB_HNT8 = 256;
+__global__ void __launch_bounds__(TAB_HNT8) tab_hist_u8_kernel(KParams p, TabDev t) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int KV = t.KV, ld = KV + 1, c = (int)p.c;
+    unsigned* Hs = (unsigned*)smem;  // [16][KV + 1]
+    const int lane = threadIdx.x & 31, hl = lane & 15, j = threadIdx.x >> 4;  // node j of the tile
+    const int tile = blockIdx.x;
+    for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT8) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
+    unsigned bad = 0;
+    const bool live = node < p.node0 + p.n_nodes;
+    const int64_t o = live && hl < 2 ? p.off[node + hl] : 0;
+    const int64_t b = __shfl_sync(0xffffffffu, o, lane & 16), e = __shfl_sync(0xffffffffu, o, (lane & 16) + 1);
+    if (live) {
+        const int r = (int)(e - b);
+        unsigned* row = Hs + j * ld;
+        const int64_t e0 = b & ~(int64_t)15;
+        const int lead = (int)(b - e0);
+        const int nv = (lead + r + 15) / 16;
+        const uint4* src = (const uint4*)((const unsigned char*)p.w + e0);
+        const unsigned cc = c >= 255 ? 0xffffffffu : (unsigned)c * 0x01010101u;
+        for (int v0 = 0; v0 < nv; v0 += 32) {
+            uint4 x[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int v = v0 + hl + 16 * u;
+                x[u] = v < nv ? src[v] : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int v = v0 + hl + 16 * u;
+                if (v >= nv) continue;
+                const unsigned wds[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+                const int elo = v * 16 - lead;
+                const int a0 = max(0, -elo), a1 = min(16, r - elo);
+                const unsigned inm = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned wd = wds[q];
+                    const unsigned badb = __vcmpeq4(wd, 0u) | __vcmpgtu4(wd, cc);
+                    const unsigned in4 = (inm >> (4 * q)) & 0xfu;
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const bool use = ((in4 >> e2) & 1u) && !((badb >> (8 * e2)) & 1u);
+                        bad |= ((in4 >> e2) & 1u) & ((badb >> (8 * e2)) & 1u);
+                        atomicAdd(row + (use ? (int)((wd >> (8 * e2)) & 0xffu) - 1 : KV), 1u);
+                    }
+                }
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
+    __shared__ int s_lo, s_hi;
+    if (threadIdx.x == 0) { s_lo = KV; s_hi = 0; }
+    __syncthreads();
+    float4* dst = (float4*)(t.H + (int64_t)tile * (KV + 1) * TAB_TM);
+    int lo = KV, hi = 0;
+    for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT8) {
+        const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
+        dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
+        if (a[0] | a[ld] | a[2 * ld] | a[3 * ld]) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
+    }
+    if (lo < hi) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
+        dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
+    }
 }
 
 // Phase C: per-node results from the best keys (key = bound << 9 | 511 -
