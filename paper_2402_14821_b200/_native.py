@@ -68,7 +68,7 @@ SIGNATURES = {
                                                ctypes.c_int64, ctypes.c_int64, _i32p, ctypes.c_int32,
                                                ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "bplb_check_batch_device_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
-                                                  ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i32p,
+                                                  ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _vp,
                                                   ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "bplb_check_batch_assign": (ctypes.c_int, [_vp, _i32p, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
                                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i32p,
@@ -285,11 +285,14 @@ class Engine:
     def check_batch_device(self, w_ptr: int, off_ptr: int, n_nodes: int, max_r: int, c: int, k: int,
                            kinds, flags: int, lb_ptr: int, ex_ptr: int, best_ptr: int = 0,
                            arg_ptr: int = 0, stream_ptr: int = 0, wbytes: int = 4) -> None:
-        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        key = tuple(kinds)
+        ks = self._kinds_cache.get(key)
+        if ks is None:
+            ks = self._kinds_cache[key] = (ctypes.c_int32 * len(key))(*key)
+        # plain ints for every pointer: this call sits inside device-timed loops
         rc = self._lib.bplb_check_batch_device_ex(
-            self.handle, _vp(w_ptr), int(wbytes), _vp(off_ptr), int(n_nodes), int(max_r), int(c), _clamp_k(k),
-            ks.ctypes.data_as(_i32p), len(ks), int(flags), _vp(lb_ptr), _vp(ex_ptr),
-            _vp(best_ptr or None), _vp(arg_ptr or None), _vp(stream_ptr or None))
+            self.handle, w_ptr, wbytes, off_ptr, n_nodes, max_r, c, _clamp_k(k), ctypes.addressof(ks), len(key),
+            flags, lb_ptr, ex_ptr, best_ptr or None, arg_ptr or None, stream_ptr or None)
         if rc != 0:
             _raise(rc, "bplb_check_batch_device")
 

@@ -487,3 +487,45 @@ def test_pinned_zero_copy_batch_paths(oracle):
     pbad = torch.from_numpy(bad).pin_memory().numpy()
     with pytest.raises(ValueError):
         eng.check_batch(pbad, po, c, 2**62, list(range(6)), 0, out=(lb, ex))
+
+
+def test_device_batch_graph_replay(oracle):
+    """Repeated device-resident calls with the same arguments replay a
+    captured CUDA graph: new buffer contents are picked up, and a changed
+    argument (node count) re-captures."""
+    import torch
+
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.Engine(0)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream()
+    c, k, flat, off = W.cfg2_nodes(1200)
+    n = len(off) - 1
+    d_w = torch.from_numpy(flat.astype(np.uint8)).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    d_lb = torch.zeros(n, dtype=torch.int64, device=dev)
+    d_ex = torch.zeros(n, dtype=torch.uint8, device=dev)
+    mr = int(np.diff(off).max())
+
+    def run(nn):
+        eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), nn, mr, c, 2**62, list(range(6)), 0,
+                               d_lb.data_ptr(), d_ex.data_ptr(), stream_ptr=st.cuda_stream, wbytes=1)
+        st.synchronize()
+        return d_lb.cpu().numpy().copy()
+
+    first = run(n)
+    lbo, _ = oracle.check_batch(flat, off, c, 2**62)
+    np.testing.assert_array_equal(first, lbo)
+    # same arguments, new contents: nodes shifted by one (weights rotated)
+    flat2, off2 = flat.copy(), off.copy()
+    perm = np.roll(np.arange(n), 1)
+    nodes = [flat[off[i]:off[i + 1]] for i in perm]
+    flat2, off2 = G.csr_from_lists(nodes)
+    d_w.copy_(torch.from_numpy(flat2.astype(np.uint8)))
+    d_off.copy_(torch.from_numpy(off2))
+    second = run(n)
+    np.testing.assert_array_equal(second, lbo[perm])
+    third = run(n - 100)  # different argument set -> new capture
+    np.testing.assert_array_equal(third[:n - 100], lbo[perm][:n - 100])
+    eng.close()
