@@ -42,7 +42,7 @@ I_K = {"MT": 5, "RAD2": 10, "FS1": 9, "CCM1": 12, "VB2": 15, "BJ1": 10}
 KINDS = ("MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1")
 # DRAM bytes (read + write) of one tab_kernel launch on the 10^4-node cfg2
 # batch, from the ncu --set full capture summarised in profiles/round1_tab_ncu.md
-TAB_TRAFFIC_BYTES = 6788608
+TAB_TRAFFIC_BYTES = 6819072
 
 
 def _dist():
