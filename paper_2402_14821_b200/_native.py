@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbplb.so")
+LIB_PATH = os.environ.get("BPLB_LIB") or os.path.join(_HERE, "libbplb.so")  # BPLB_LIB: A/B builds
 
 NKINDS = 6
 F_PHASED = 0x1

@@ -11,6 +11,7 @@ ap.add_argument("--cfg", default="cfg2")
 ap.add_argument("--nodes", type=int, default=10_000)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--notab", action="store_true")
+ap.add_argument("--kinds", default="0,1,2,3,4,5")
 a = ap.parse_args()
 c, k, flat, off = (W.cfg2_nodes if a.cfg == "cfg2" else W.cfg5_nodes)(a.nodes)
 wdt = np.uint8 if c <= 255 else (np.uint16 if c <= 65535 else np.int32)
@@ -28,7 +29,7 @@ for i in range(a.reps):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(st)
     eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, int(np.diff(off).max()), c, 2**62,
-                           list(range(6)), fl, d_lb.data_ptr(), d_ex.data_ptr(), wbytes=np.dtype(wdt).itemsize,
+                           [int(x) for x in a.kinds.split(",")], fl, d_lb.data_ptr(), d_ex.data_ptr(), wbytes=np.dtype(wdt).itemsize,
                            stream_ptr=st.cuda_stream)
     e.record(st)
     torch.cuda.synchronize()
