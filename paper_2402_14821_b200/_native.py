@@ -61,9 +61,9 @@ SIGNATURES = {
     "bplb_check_batch": (ctypes.c_int, [_vp, _i32p, _i64p, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_int64, _i32p, ctypes.c_int32, ctypes.c_int32,
                                         _i64p, _u8p, _i64p, _i64p]),
-    "bplb_check_batch_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _i64p, ctypes.c_int64,
-                                           ctypes.c_int64, ctypes.c_int64, _i32p, ctypes.c_int32,
-                                           ctypes.c_int32, _i64p, _u8p, _i64p, _i64p]),
+    "bplb_check_batch_ex": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
+                                           ctypes.c_int32, _vp, _vp, _vp, _vp]),
     "bplb_check_batch_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
                                                ctypes.c_int64, ctypes.c_int64, _i32p, ctypes.c_int32,
                                                ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
@@ -104,6 +104,19 @@ def load_library(path: str = LIB_PATH):
             fn.argtypes = args
         _lib = lib
         return lib
+
+
+_cbyte_from_buffer = ctypes.c_byte.from_buffer
+_addressof = ctypes.addressof
+
+
+def _addr(a: np.ndarray) -> int:
+    """Data pointer of a contiguous array as a plain int (about 2.5x cheaper
+    than a.ctypes.data for writable arrays; read-only ones fall back)."""
+    try:
+        return _addressof(_cbyte_from_buffer(a))
+    except (TypeError, ValueError, BufferError):
+        return a.ctypes.data
 
 
 def _raise(rc: int, what: str):
@@ -217,20 +230,25 @@ class Engine:
             wbytes = 4
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         n = len(off) - 1
-        ks = np.ascontiguousarray(kinds, dtype=np.int32)
+        key = tuple(kinds)
+        ks = self._kinds_cache.get(key)
+        if ks is None:
+            ks = self._kinds_cache[key] = (ctypes.c_int32 * len(key))(*key)
         if out is None:
             lb = np.empty(n, dtype=np.int64)
             ex = np.empty(n, dtype=np.uint8)
         else:
             lb, ex = out
+            if not (isinstance(lb, np.ndarray) and lb.dtype == np.int64 and lb.flags.c_contiguous and len(lb) >= n
+                    and isinstance(ex, np.ndarray) and ex.itemsize == 1 and ex.flags.c_contiguous and len(ex) >= n):
+                raise ValueError("out must be (int64[n], uint8[n]) contiguous arrays")
         best = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
         arg = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        # plain ints for every pointer (ctypes pointer objects cost ~1-2 us each)
         rc = self._lib.bplb_check_batch_ex(
-            self.handle, _vp(w.ctypes.data), wbytes, off.ctypes.data_as(_i64p), n, int(c), _clamp_k(k),
-            ks.ctypes.data_as(_i32p), len(ks), int(flags), lb.ctypes.data_as(_i64p),
-            ex.ctypes.data_as(_u8p),
-            best.ctypes.data_as(_i64p) if best is not None else None,
-            arg.ctypes.data_as(_i64p) if arg is not None else None)
+            self.handle, _addr(w) if w.size else None, wbytes, _addr(off), n, int(c), _clamp_k(k),
+            _addressof(ks), len(key), int(flags), _addr(lb), _addr(ex),
+            _addr(best) if best is not None else None, _addr(arg) if arg is not None else None)
         if rc != 0:
             _raise(rc, "bplb_check_batch")
         if want_best:

@@ -119,14 +119,15 @@ bool is_pinned(const void* ptr) {
 // captured once per key into a CUDA graph.
 struct GraphKey {
     const void *w, *off;
-    void *lb, *ex, *best, *arg;
+    void *lb, *ex, *best, *arg, *err;
     int64_t n, max_r, c, k;
     int flags, wbytes, kmask, gen;
     cudaStream_t s;
     int kinds[6];
     int nk;
     bool operator==(const GraphKey& o) const {
-        if (w != o.w || off != o.off || lb != o.lb || ex != o.ex || best != o.best || arg != o.arg || n != o.n ||
+        if (w != o.w || off != o.off || lb != o.lb || ex != o.ex || best != o.best || arg != o.arg || err != o.err ||
+            n != o.n ||
             max_r != o.max_r || c != o.c || k != o.k || flags != o.flags || wbytes != o.wbytes ||
             kmask != o.kmask || gen != o.gen || s != o.s || nk != o.nk)
             return false;
@@ -150,7 +151,7 @@ struct bplb_engine {
     DevBuf d_w, d_off, d_res, d_lb, d_ex, d_best, d_arg, d_err, d_lam, d_wide, d_multi;
     HostBuf h_stage, h_res;
     // batched small-c path: cached table of transformed values for (tab_c, tab_kmask)
-    DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist;
+    DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist, d_tabready;
     DevBuf d_inst, d_assign, d_redr;  // device-side reduction of node states
     DevBuf d_skeys;                   // single-check table path: keys[8] + CTA counter
     MappedBuf m_single;               // single-check table path: weights in, result out
@@ -158,13 +159,26 @@ struct bplb_engine {
     bool skeys_zeroed = false;
     size_t tab_attr_smem = 0;
     int tab_per_sm = 1;
+    int hist_per_sm = 3;          // persistent histogram CTAs per SM (BPLB_HIST_PER_SM)
+    bool hist_carveout = false;
+    // cross-stream ordering of calls that share the engine's scratch: the
+    // last asynchronous call's stream and an event recorded after its work
+    cudaEvent_t ev_tail = nullptr;
+    cudaStream_t tail_stream = nullptr;
+    bool tail_valid = false;
     int64_t tab_c = -1;
     int tab_kmask = -1, tab_KV = 0, tab_nsub = 0, tab_P = 0;
     int64_t tab_nodes = 0;  // capacity of d_tabkeys / d_tabhist (nodes)
     int64_t launches = 0;
     double last_ms = 0.0;
-    cudaGraphExec_t graph_exec = nullptr;  // device-batch table path, for graph_key
-    GraphKey graph_key{};
+    // table-path launches replayed from CUDA graphs, one per argument set
+    // (a search loop or the bench repeats them), least recently used evicted
+    struct GraphSlot {
+        GraphKey key{};
+        cudaGraphExec_t exec = nullptr;
+        uint64_t used = 0;
+    } graphs[4];
+    uint64_t graph_clock = 0;
     int tab_gen = 0;        // bumped whenever a table-path buffer is (re)allocated
     bool graphs_ok = true;  // capture failed once: launch directly
     int prof_kernel = 0;       // bracket the contraction kernel with ev_pk0 / ev_pk1
@@ -260,6 +274,19 @@ int tab_warps(const bplb_engine* e, int KV, int nb = 2) {
     return 0;
 }
 
+// Order this call's stream X after the previous asynchronous call's work
+// when that ran on another stream (engine scratch buffers are shared).
+int join_stream(bplb_engine* e, cudaStream_t X) {
+    if (e->tail_valid && e->tail_stream != X) CUDA_TRY(cudaStreamWaitEvent(X, e->ev_tail, 0));
+    return 0;
+}
+int mark_tail(bplb_engine* e, cudaStream_t X) {
+    CUDA_TRY(cudaEventRecord(e->ev_tail, X));
+    e->tail_stream = X;
+    e->tail_valid = true;
+    return 0;
+}
+
 // Tabulate f_k(w, lambda) for capacity c and the requested kinds (cached).
 int tab_ensure(bplb_engine* e, const bplb::KParams& p) {
     const int kmask = tab_kmask(p);
@@ -327,6 +354,8 @@ int tab_reserve(bplb_engine* e, int64_t n) {
     if ((rc = e->d_tabhist.grow((size_t)(n / bplb::TAB_TM + 1) * ((bplb::TAB_MAX_C + 3) / 4 * 4 + 1) * bplb::TAB_TM * 4)))
         return rc;
     CUDA_TRY(cudaMemsetAsync(e->d_tabkeys.p, 0, (size_t)n * bplb::TAB_KSLOT * 4, e->stream));
+    if ((rc = e->d_tabready.grow((size_t)(n / bplb::TAB_TM + 1) * 4))) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_tabready.p, 0, (size_t)(n / bplb::TAB_TM + 1) * 4, e->stream));
 
 
     e->tab_nodes = n;
@@ -377,6 +406,13 @@ bplb::TabDev tab_dev(bplb_engine* e, const bplb::KParams& p, int64_t n_nodes) {
     t.nsub = e->tab_nsub;
     t.P = e->tab_P;
     t.gkeys = (unsigned*)e->d_tabkeys.p;
+    t.trace = nullptr;
+#ifdef TAB_TRACE
+    static unsigned long long* tr = nullptr;
+    if (!tr) cudaMalloc(&tr, (size_t)4096 * 16 * 16 * 8 * 2);
+    t.trace = tr;
+#endif
+    t.ready = (unsigned*)e->d_tabready.p + p.node0 / bplb::TAB_TM;
     t.ntiles = (n_nodes + bplb::TAB_TM - 1) / bplb::TAB_TM;
     t.H = (float*)e->d_tabhist.p + (p.node0 / bplb::TAB_TM) * (t.KV + 1) * bplb::TAB_TM;
     return t;
@@ -386,10 +422,23 @@ int tab_hist(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     p.n_nodes = n_nodes;
     const bplb::TabDev t = tab_dev(e, p, n_nodes);
     const size_t hs = ((size_t)bplb::TAB_TM * (t.KV + 1) + 2 * bplb::TAB_HPAD) * 4;  // <= 20.5 KB (KV <= 288)
-    if (p.wbytes == 1 && !((uintptr_t)p.w & 15))
-        bplb::tab_hist_u8_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT8, hs, e->stream>>>(p, t);
+    // persistent: the CTAs walk the tiles in order next to the tab_kernel
+    // CTAs that consume them (e->hist_per_sm CTAs of 8 warps per SM).  An
+    // SM's smem carveout is fixed while CTAs are resident: the histogram
+    // kernels ask for the maximum so a tab_kernel CTA fits beside them.
+    if (!e->hist_carveout) {
+        CUDA_TRY(cudaFuncSetAttribute(bplb::tab_hist_u8_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));
+        CUDA_TRY(cudaFuncSetAttribute(bplb::tab_hist_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));
+        e->hist_carveout = true;
+    }
+    if (p.wbytes == 1 && !((uintptr_t)p.w & 15))  // packed counts: half the scratch
+        bplb::tab_hist_u8_kernel<<<(unsigned)std::min<int64_t>(t.ntiles, (int64_t)e->hist_per_sm * e->num_sms),
+                                   bplb::TAB_HNT8, (size_t)bplb::TAB_TM / 2 * (t.KV + 1) * 4, e->stream>>>(p, t);
     else
-        bplb::tab_hist_kernel<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(p, t);
+        bplb::tab_hist_kernel<<<(unsigned)std::min<int64_t>(t.ntiles, (int64_t)std::max(1, e->hist_per_sm / 2) * e->num_sms),
+                                bplb::TAB_HNT, hs, e->stream>>>(p, t);
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -418,6 +467,22 @@ int tab_contract(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
     if (e->prof_kernel) CUDA_TRY(cudaEventRecord(e->ev_pk0, e->stream));
     CUDA_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
+#ifdef TAB_TRACE
+    {  // dump: grid, nw, P, ntiles, hist ctas, then [cta][warp][16] stamps, then [tile] publish stamps
+        std::vector<unsigned long long> h((size_t)grid * nw * 16), hp((size_t)t.ntiles);
+        cudaStreamSynchronize(e->stream);
+        cudaMemcpy(h.data(), t.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(hp.data(), t.trace + 4096 * 16 * 16, hp.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemset(t.trace, 0, (size_t)4096 * 16 * 16 * 8 * 2);
+        if (FILE* f = fopen(getenv("BPLB_TAB_TRACE") ? getenv("BPLB_TAB_TRACE") : "tab_trace.bin", "ab")) {
+            long long hd[5] = {(long long)grid, (long long)nw, (long long)P, (long long)t.ntiles, 0};
+            fwrite(hd, 8, 5, f);
+            fwrite(h.data(), 8, h.size(), f);
+            fwrite(hp.data(), 8, hp.size(), f);
+            fclose(f);
+        }
+    }
+#endif
     if (e->prof_kernel) {
         CUDA_TRY(cudaEventRecord(e->ev_pk1, e->stream));
         e->prof_recorded = 1;
@@ -430,7 +495,7 @@ int tab_contract(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
 int tab_fin(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     p.n_nodes = n_nodes;
     CUDA_TRY(launch_pdl(bplb::tab_fin_kernel, dim3((unsigned)((n_nodes + 63) / 64)), dim3(64), 0, e->stream, p,
-                        (unsigned*)e->d_tabkeys.p));
+                        (unsigned*)e->d_tabkeys.p, (unsigned*)e->d_tabready.p + p.node0 / bplb::TAB_TM));
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -445,6 +510,49 @@ int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
     if ((rc = tab_hist(e, p, n_nodes))) return rc;
     if ((rc = tab_contract(e, p, n_nodes))) return rc;
     return tab_fin(e, p, n_nodes);
+}
+
+// launch_tab on e->stream replayed from a cached CUDA graph (captured on
+// first use of an argument set): one launch call instead of three.  w / off
+// are the device (or device-alias) inputs; the outputs and error flag come
+// from p.  Falls back to direct launches where capture is unavailable.
+int launch_tab_graph(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r, const int* ks, int nkinds,
+                     const void* w, const void* off) {
+    if (!e->graphs_ok || e->prof_kernel) return launch_tab(e, p, n_nodes, 0);
+    cudaStream_t s = e->stream;
+    GraphKey key{w, off, p.lb_out, p.ex_out, p.best_out, p.arg_out, p.err_out, n_nodes, max_r, p.c, p.k, p.flags,
+                 p.wbytes, tab_kmask(p), e->tab_gen, s, {ks[0], ks[1], ks[2], ks[3], ks[4], ks[5]}, nkinds};
+    bplb_engine::GraphSlot* slot = nullptr;
+    for (auto& g : e->graphs)
+        if (g.exec && g.key == key) slot = &g;
+    if (!slot) {
+        slot = &e->graphs[0];
+        for (auto& g : e->graphs)
+            if (!g.exec || g.used < slot->used) slot = &g;
+        if (slot->exec) cudaGraphExecDestroy(slot->exec);
+        slot->exec = nullptr;
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = e->launches;
+        int rc = launch_tab(e, p, n_nodes, 0);
+        cudaError_t ce = cudaStreamEndCapture(s, &g);
+        e->launches = l0;  // counted when the graph runs
+        if (!rc && ce == cudaSuccess) ce = cudaGraphInstantiate(&slot->exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (rc) return rc;
+        if (ce != cudaSuccess) {  // no graphs here: launch directly from now on
+            cudaGetLastError();
+            e->graphs_ok = false;
+            slot->exec = nullptr;
+            return launch_tab(e, p, n_nodes, 0);
+        }
+        slot->key = key;
+    }
+    slot->used = ++e->graph_clock;
+    cudaError_t ce = cudaGraphLaunch(slot->exec, s);
+    if (ce != cudaSuccess) return fail(BPLB_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce));
+    e->launches += 3;
+    return 0;
 }
 
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
@@ -572,10 +680,15 @@ int bplb_engine_create(int device, bplb_engine** out) {
     e->device = device;
     e->num_sms = prop.multiProcessorCount;
     e->smem_optin = prop.sharedMemPerBlockOptin;
+    if (const char* v = getenv("BPLB_HIST_PER_SM")) e->hist_per_sm = std::max(1, atoi(v));
+#ifdef TAB_TRACE
+    e->graphs_ok = false;  // stamps are read back per launch
+#endif
     bool ok = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) == cudaSuccess &&
 
               cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaEventCreate(&e->ev0) == cudaSuccess && cudaEventCreate(&e->ev1) == cudaSuccess;
+              cudaEventCreate(&e->ev0) == cudaSuccess && cudaEventCreate(&e->ev1) == cudaSuccess &&
+              cudaEventCreateWithFlags(&e->ev_tail, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < 4 && ok; ++i)
         ok = cudaStreamCreateWithFlags(&e->cstream[i], cudaStreamNonBlocking) == cudaSuccess &&
              cudaEventCreateWithFlags(&e->ev_up[i], cudaEventDisableTiming) == cudaSuccess &&
@@ -601,8 +714,10 @@ int bplb_engine_destroy(bplb_engine* e) {
     e->m_single.release();
     e->m_err.release();
     cudaEventDestroy(e->ev0);
+    if (e->ev_tail) cudaEventDestroy(e->ev_tail);
     cudaEventDestroy(e->ev1);
-    if (e->graph_exec) cudaGraphExecDestroy(e->graph_exec);
+    for (auto& g : e->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (e->ev_pk0) cudaEventDestroy(e->ev_pk0);
     if (e->ev_pk1) cudaEventDestroy(e->ev_pk1);
     for (int i = 0; i < 4; ++i) {
@@ -656,6 +771,7 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     if (k >= r) flags &= ~(BPLB_F_PHASED | BPLB_F_CANCEL);
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, e->stream)) return rc;
     const bool timing = flags & BPLB_F_TIMING;
     if (int rc = e->d_w.grow((size_t)std::max<int64_t>(r, 1) * 4 + 64)) return rc;
     if (int rc = e->d_res.grow(sizeof(bplb_result) + 16)) return rc;
@@ -756,6 +872,7 @@ int bplb_dff_bound_batch(bplb_engine* e, int32_t kind, const int32_t* w, int64_t
         return fail(BPLB_EINVAL, "lambda range outside the parameter domain of the kind");
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, e->stream)) return rc;
     const int64_t L = hi - lo + 1;
     int rc;
     if ((rc = e->d_w.grow((size_t)std::max<int64_t>(r, 1) * 4 + 64))) return rc;
@@ -825,6 +942,7 @@ int bplb_check_batch_device_ex(bplb_engine* e, const void* d_w, int32_t wbytes, 
     cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, s)) return rc;
     bplb::KParams p;
     fill_params(p, c, k, ks, nkinds, flags);
     p.w = (const int*)d_w;
@@ -845,40 +963,12 @@ int bplb_check_batch_device_ex(bplb_engine* e, const void* d_w, int32_t wbytes, 
         // instead of three, captured once per argument set
         rc = tab_ensure(e, p);
         if (!rc) rc = tab_reserve(e, n_nodes);
-        if (!rc) {
-            GraphKey key{d_w, d_off, d_lb, d_ex, d_best, d_arg, n_nodes, max_r, c, k, flags, wbytes,
-                         tab_kmask(p), e->tab_gen, s, {ks[0], ks[1], ks[2], ks[3], ks[4], ks[5]}, nkinds};
-            if (!(e->graph_exec && e->graph_key == key)) {
-                if (e->graph_exec) cudaGraphExecDestroy(e->graph_exec);
-                e->graph_exec = nullptr;
-                cudaGraph_t g = nullptr;
-                CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-                const int64_t l0 = e->launches;
-                rc = launch_tab(e, p, n_nodes, 0);
-                cudaError_t ce = cudaStreamEndCapture(s, &g);
-                e->launches = l0;  // counted when the graph runs
-                if (!rc && ce == cudaSuccess) ce = cudaGraphInstantiate(&e->graph_exec, g, 0);
-                if (g) cudaGraphDestroy(g);
-                if (!rc && ce != cudaSuccess) {  // no graphs here: launch directly from now on
-                    cudaGetLastError();
-                    e->graphs_ok = false;
-                    e->graph_exec = nullptr;
-                    rc = launch_tab(e, p, n_nodes, 0);
-                    e->stream = saved;
-                    return rc;
-                }
-                if (!rc) e->graph_key = key;
-            }
-            if (!rc) {
-                cudaError_t ce = cudaGraphLaunch(e->graph_exec, s);
-                if (ce != cudaSuccess) rc = fail(BPLB_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce));
-                e->launches += 3;
-            }
-        }
+        if (!rc) rc = launch_tab_graph(e, p, n_nodes, max_r, ks, nkinds, d_w, d_off);
     } else {
         rc = launch_node(e, p, n_nodes, max_r, 0);
     }
     e->stream = saved;
+    if (!rc) rc = mark_tail(e, s);  // asynchronous: later calls on other streams order after it
     return rc;
 }
 
@@ -895,18 +985,20 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
     if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
     if (n_nodes == 0) return 0;
     if (off[0] != 0) return fail(BPLB_EINVAL, "offsets[0] must be 0");
-    int64_t max_r = 0;
-    for (int64_t i = 0; i < n_nodes; ++i) {
-        int64_t d = off[i + 1] - off[i];
-        if (d < 0) return fail(BPLB_EINVAL, "offsets must be non-decreasing");
-        max_r = std::max(max_r, d);
+    int64_t max_r = 0, min_d = 0;
+    for (int64_t i = 0; i < n_nodes; ++i) {  // branch-free: vectorises
+        const int64_t d = off[i + 1] - off[i];
+        max_r = d > max_r ? d : max_r;
+        min_d = d < min_d ? d : min_d;
     }
+    if (min_d < 0) return fail(BPLB_EINVAL, "offsets must be non-decreasing");
     if (max_r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items in a node for the GPU envelope");
     if (k >= max_r) flags &= ~(BPLB_F_PHASED | BPLB_F_CANCEL);  // no node can exceed k
     const int64_t total = off[n_nodes];
     if (total > 0 && !w) return fail(BPLB_EINVAL, "null weights");
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, e->stream)) return rc;
     int rc;
     const bool timing = flags & BPLB_F_TIMING;
     if ((rc = e->d_w.grow((size_t)std::max<int64_t>(total, 1) * 4 + 64))) return rc;
@@ -958,7 +1050,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         q.w = (const int*)w_alias;
         q.off = (const int64_t*)off_alias;
         if (tab_path(e, q, n_nodes, max_r)) {
-            if ((rc = launch_tab(e, q, n_nodes, 0))) return rc;
+            if ((rc = launch_tab_graph(e, q, n_nodes, max_r, ks, nkinds, w_alias, off_alias))) return rc;
             goto outputs;
         }
     }
@@ -1052,6 +1144,7 @@ int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_ite
     if (n_nodes == 0) return 0;
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, e->stream)) return rc;
     const bool timing = flags & BPLB_F_TIMING;
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
     int obytes = 4, rc;
@@ -1175,6 +1268,7 @@ int bplb_reduce_batch(bplb_engine* e, const int32_t* inst_w, int64_t n_items, in
     if (int rc = check_c(c)) return rc;
     std::lock_guard<std::mutex> lock(e->mu);
     CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, e->stream)) return rc;
     off_out[0] = 0;
     if (n_nodes == 0) return 0;
     int obytes = 4, rc;

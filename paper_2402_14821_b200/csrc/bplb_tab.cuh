@@ -57,6 +57,9 @@ struct TabDev {
     int P;                        // = nsub: CTA b holds sub-chunk b % P
     unsigned* gkeys;              // [node * 8 + kind], zero between launches
     int64_t ntiles;
+    unsigned long long* trace;    // TAB_TRACE builds only: globaltimer stamps (see scripts/tab_trace_summary.py)
+    unsigned* ready;              // [tile] 1 once the tile's histogram is stored (release);
+                                  // zero between launches (tab_fin_kernel clears it)
     float* H;                     // [tile][KV + 1][16] fp32 counts of this launch's tiles; row KV
                                   // holds the tile's occupied row range {lo, hi} (int bits)
 };
@@ -195,38 +198,71 @@ __device__ __forceinline__ void tab_hist_node_u8(const KParams& p, int64_t b, in
     *bad |= bd;
 }
 
-constexpr int TAB_HNT = TAB_TM * 32;
-constexpr int TAB_HPAD = 0;
-__global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int KV = t.KV, ld = KV + 1, c = (int)p.c;
-    unsigned* Hs = (unsigned*)smem + TAB_HPAD;  // [16][KV + 1]
-    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
-    for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
-    const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
-    unsigned bad = 0;
-    if (node < p.node0 + p.n_nodes) {
-        const int64_t o = lane < 2 ? p.off[node + lane] : 0;
-        const int64_t b = __shfl_sync(0xffffffffu, o, 0), e = __shfl_sync(0xffffffffu, o, 1);
-        unsigned* row = Hs + j * ld;
-        if (p.wbytes == 1) tab_hist_node_u8(p, b, (int)(e - b), row, c, KV, &bad);
-        else if (p.wbytes == 2) tab_hist_node<2>(p, b, (int)(e - b), row, c, KV, &bad);
-        else tab_hist_node<4>(p, b, (int)(e - b), row, c, KV, &bad);
+// Phase A -> B hand-off per tile instead of per grid: the histogram kernels
+// let tab_kernel launch at once (PDL trigger at their start; every phase-A
+// CTA is resident by the time a tab_kernel CTA is) and publish each stored
+// tile with a release flag that tab_kernel acquires before its TMA copy, so
+// the contraction overlaps the histogram pass (over PCIe in e2e calls).
+__device__ __forceinline__ void tab_trigger_dependents() {
+#if __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void tab_publish(unsigned* flag) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // consumers read by TMA (async proxy)
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+}
+__device__ __forceinline__ bool tab_poll(const unsigned* flag) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v) asm volatile("fence.proxy.async.global;" ::: "memory");
+    return v != 0u;
+}
+__device__ __forceinline__ void tab_await(const unsigned* flag) {
+    unsigned v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v) break;
+        __nanosleep(128);
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+#ifdef TAB_TRACE
+__device__ __forceinline__ void tab_stamp(unsigned long long* slot) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    *slot = g;
+}
+#define TAB_STAMP(slot_) tab_stamp(slot_)
+#else
+#define TAB_STAMP(slot_) ((void)0)
+#endif
+
+// Store one tile's counts (Hs: [16][KV + 1] u32, stride ld; PACK: two
+// nodes per word, [8][KV + 1], node 2m + h in half h of row m) as fp32
+// [w][16] plus the occupied row range [lo, hi) (rounded to 4) in header row
+// KV, then publish it.  All NT threads of the CTA call it.
+template <int NT, bool PACK = false>
+__device__ __forceinline__ void tab_store_tile(const TabDev& t, const unsigned* Hs, int tile) {
+    const int KV = t.KV, ld = KV + 1;
     __shared__ int s_lo, s_hi;
     if (threadIdx.x == 0) { s_lo = KV; s_hi = 0; }
     __syncthreads();
-    // fp32 [w][16]: float4 i holds w = i / 4, nodes 4 (i & 3) .. + 3; plus the
-    // rows that hold any count, [lo, hi) rounded to 4, in header row KV
     float4* dst = (float4*)(t.H + (int64_t)tile * (KV + 1) * TAB_TM);
     int lo = KV, hi = 0;
-    for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT) {
-        const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
-        dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
-        if (a[0] | a[ld] | a[2 * ld] | a[3 * ld]) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
+    for (int i = threadIdx.x; i < KV * 4; i += NT) {
+        unsigned n0, n1, n2, n3;  // nodes 4 (i & 3) .. + 3 at w = i / 4 + 1
+        if (PACK) {
+            const unsigned* a = Hs + (i & 3) * 2 * ld + (i >> 2);
+            const unsigned x = a[0], y = a[ld];
+            n0 = x & 0xffffu; n1 = x >> 16; n2 = y & 0xffffu; n3 = y >> 16;
+        } else {
+            const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
+            n0 = a[0]; n1 = a[ld]; n2 = a[2 * ld]; n3 = a[3 * ld];
+        }
+        dst[i] = make_float4((float)n0, (float)n1, (float)n2, (float)n3);
+        if (n0 | n1 | n2 | n3) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
     }
     if (lo < hi) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
     __syncthreads();
@@ -234,8 +270,37 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) 
         const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
         dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
     }
-    // (read back by TMA in tab_kernel after the PDL grid-dependency wait,
-    // which orders this grid's completed writes before the copies)
+    __syncthreads();  // every store of the tile precedes the flag (cumulativity)
+    if (threadIdx.x == 0) {
+        tab_publish(t.ready + tile);
+        TAB_STAMP(t.trace + 4096 * 16 * 16 + tile);  // tile published
+    }
+}
+
+constexpr int TAB_HNT = TAB_TM * 32;
+constexpr int TAB_HPAD = 0;
+__global__ void __launch_bounds__(TAB_HNT) tab_hist_kernel(KParams p, TabDev t) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    tab_trigger_dependents();
+    const int KV = t.KV, ld = KV + 1, c = (int)p.c;
+    unsigned* Hs = (unsigned*)smem + TAB_HPAD;  // [16][KV + 1]
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+    for (int tile = blockIdx.x; tile < (int)t.ntiles; tile += gridDim.x) {  // tiles in order
+        for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
+        unsigned bad = 0;
+        if (node < p.node0 + p.n_nodes) {
+            const int64_t o = lane < 2 ? p.off[node + lane] : 0;
+            const int64_t b = __shfl_sync(0xffffffffu, o, 0), e = __shfl_sync(0xffffffffu, o, 1);
+            unsigned* row = Hs + j * ld;
+            if (p.wbytes == 1) tab_hist_node_u8(p, b, (int)(e - b), row, c, KV, &bad);
+            else if (p.wbytes == 2) tab_hist_node<2>(p, b, (int)(e - b), row, c, KV, &bad);
+            else tab_hist_node<4>(p, b, (int)(e - b), row, c, KV, &bad);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
+        tab_store_tile<TAB_HNT>(t, Hs, tile);
+    }
 }
 
 // Phase A from node states given as bin assignments (bplb_check_batch_assign
@@ -253,6 +318,7 @@ template <int AB>
 __global__ void __launch_bounds__(TAB_HNT) tab_hist_assign_kernel(KParams p, TabDev t, const int* inst_w, int n_items,
                                                                    int n_bins, const void* assign, int* err) {
     extern __shared__ __align__(16) unsigned char smem[];
+    tab_trigger_dependents();
     const int KV = t.KV, ld = KV + 1, c = (int)p.c;
     unsigned* Hs = (unsigned*)smem;                                  // [16][KV + 1]
     int* iw = (int*)(Hs + TAB_TM * ld);                              // [n_items]
@@ -309,95 +375,69 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_assign_kernel(KParams p, Tab
         if (s_bad) atomicExch(err, 1);
         if (s_rerr) atomicOr(err + 1, s_rerr);
     }
-    __shared__ int s_lo, s_hi;
-    if (threadIdx.x == 0) { s_lo = KV; s_hi = 0; }
-    __syncthreads();
-    float4* dst = (float4*)(t.H + (int64_t)tile * (KV + 1) * TAB_TM);
-    int lo = KV, hi = 0;
-    for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT) {
-        const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
-        dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
-        if (a[0] | a[ld] | a[2 * ld] | a[3 * ld]) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
-    }
-    if (lo < hi) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
-        dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
-    }
+    tab_store_tile<TAB_HNT>(t, Hs, tile);
 }
 
-// uint8 weights: one CTA of 8 warps per 16-node tile, a half-warp per node
-// (all of a lane's vector loads issued before any is counted), so a 10^4-node
-// batch's tiles are resident in one wave (same output as tab_hist_kernel).
+// uint8 weights: CTAs of 8 warps walk the 16-node tiles in order (two per
+// SM next to the tab_kernel CTA, which consumes each tile as it is
+// published), a half-warp per node (all of a lane's vector loads issued
+// before any is counted); same output as tab_hist_kernel.
 constexpr int TAB_HNT8 = 256;
 __global__ void __launch_bounds__(TAB_HNT8) tab_hist_u8_kernel(KParams p, TabDev t) {
     extern __shared__ __align__(16) unsigned char smem[];
+    tab_trigger_dependents();
     const int KV = t.KV, ld = KV + 1, c = (int)p.c;
-    unsigned* Hs = (unsigned*)smem;  // [16][KV + 1]
+    unsigned* Hs = (unsigned*)smem;  // [8][KV + 1]: nodes 2m, 2m + 1 in the halves of row m (counts <= r < 2^16)
     const int lane = threadIdx.x & 31, hl = lane & 15, j = threadIdx.x >> 4;  // node j of the tile
-    const int tile = blockIdx.x;
-    for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT8) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
-    const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
-    unsigned bad = 0;
-    const bool live = node < p.node0 + p.n_nodes;
-    const int64_t o = live && hl < 2 ? p.off[node + hl] : 0;
-    const int64_t b = __shfl_sync(0xffffffffu, o, lane & 16), e = __shfl_sync(0xffffffffu, o, (lane & 16) + 1);
-    if (live) {
-        const int r = (int)(e - b);
-        unsigned* row = Hs + j * ld;
-        const int64_t e0 = b & ~(int64_t)15;
-        const int lead = (int)(b - e0);
-        const int nv = (lead + r + 15) / 16;
-        const uint4* src = (const uint4*)((const unsigned char*)p.w + e0);
-        const unsigned cc = c >= 255 ? 0xffffffffu : (unsigned)c * 0x01010101u;
-        for (int v0 = 0; v0 < nv; v0 += 32) {
-            uint4 x[2];
+    for (int tile = blockIdx.x; tile < (int)t.ntiles; tile += gridDim.x) {  // tiles in order
+        for (int i = threadIdx.x; i < TAB_TM / 2 * ld; i += TAB_HNT8) Hs[i] = 0u;
+        __syncthreads();
+        const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
+        unsigned bad = 0;
+        const bool live = node < p.node0 + p.n_nodes;
+        const int64_t o = live && hl < 2 ? p.off[node + hl] : 0;
+        const int64_t b = __shfl_sync(0xffffffffu, o, lane & 16), e = __shfl_sync(0xffffffffu, o, (lane & 16) + 1);
+        if (live) {
+            const int r = (int)(e - b);
+            unsigned* row = Hs + (j >> 1) * ld;
+            const unsigned one = 1u << ((j & 1) * 16);
+            const int64_t e0 = b & ~(int64_t)15;
+            const int lead = (int)(b - e0);
+            const int nv = (lead + r + 15) / 16;
+            const uint4* src = (const uint4*)((const unsigned char*)p.w + e0);
+            const unsigned cc = c >= 255 ? 0xffffffffu : (unsigned)c * 0x01010101u;
+            for (int v0 = 0; v0 < nv; v0 += 32) {
+                uint4 x[2];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int v = v0 + hl + 16 * u;
-                x[u] = v < nv ? src[v] : make_uint4(0u, 0u, 0u, 0u);
-            }
+                for (int u = 0; u < 2; ++u) {
+                    const int v = v0 + hl + 16 * u;
+                    x[u] = v < nv ? src[v] : make_uint4(0u, 0u, 0u, 0u);
+                }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int v = v0 + hl + 16 * u;
-                if (v >= nv) continue;
-                const unsigned wds[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-                const int elo = v * 16 - lead;
-                const int a0 = max(0, -elo), a1 = min(16, r - elo);
-                const unsigned inm = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
+                for (int u = 0; u < 2; ++u) {
+                    const int v = v0 + hl + 16 * u;
+                    if (v >= nv) continue;
+                    const unsigned wds[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+                    const int elo = v * 16 - lead;
+                    const int a0 = max(0, -elo), a1 = min(16, r - elo);
+                    const unsigned inm = ((1u << a1) - 1u) & ~((1u << a0) - 1u);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const unsigned wd = wds[q];
-                    const unsigned badb = __vcmpeq4(wd, 0u) | __vcmpgtu4(wd, cc);
-                    const unsigned in4 = (inm >> (4 * q)) & 0xfu;
+                    for (int q = 0; q < 4; ++q) {
+                        const unsigned wd = wds[q];
+                        const unsigned badb = __vcmpeq4(wd, 0u) | __vcmpgtu4(wd, cc);
+                        const unsigned in4 = (inm >> (4 * q)) & 0xfu;
 #pragma unroll
-                    for (int e2 = 0; e2 < 4; ++e2) {
-                        const bool use = ((in4 >> e2) & 1u) && !((badb >> (8 * e2)) & 1u);
-                        bad |= ((in4 >> e2) & 1u) & ((badb >> (8 * e2)) & 1u);
-                        atomicAdd(row + (use ? (int)((wd >> (8 * e2)) & 0xffu) - 1 : KV), 1u);
+                        for (int e2 = 0; e2 < 4; ++e2) {
+                            const bool use = ((in4 >> e2) & 1u) && !((badb >> (8 * e2)) & 1u);
+                            bad |= ((in4 >> e2) & 1u) & ((badb >> (8 * e2)) & 1u);
+                            atomicAdd(row + (use ? (int)((wd >> (8 * e2)) & 0xffu) - 1 : KV), one);
+                        }
                     }
                 }
             }
         }
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
-    __shared__ int s_lo, s_hi;
-    if (threadIdx.x == 0) { s_lo = KV; s_hi = 0; }
-    __syncthreads();
-    float4* dst = (float4*)(t.H + (int64_t)tile * (KV + 1) * TAB_TM);
-    int lo = KV, hi = 0;
-    for (int i = threadIdx.x; i < KV * 4; i += TAB_HNT8) {
-        const unsigned* a = Hs + (i & 3) * 4 * ld + (i >> 2);
-        dst[i] = make_float4((float)a[0], (float)a[ld], (float)a[2 * ld], (float)a[3 * ld]);
-        if (a[0] | a[ld] | a[2 * ld] | a[3 * ld]) { lo = min(lo, i >> 2); hi = max(hi, (i >> 2) + 1); }
-    }
-    if (lo < hi) { atomicMin(&s_lo, lo); atomicMax(&s_hi, hi); }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        const int l4 = s_lo < s_hi ? s_lo & ~3 : 0, h4 = s_lo < s_hi ? (s_hi + 3) & ~3 : 0;
-        dst[KV * 4 + threadIdx.x] = make_float4(__int_as_float(l4), __int_as_float(h4), 0.f, 0.f);
+        if (__any_sync(0xffffffffu, bad) && lane == 0 && p.err_out) atomicExch(p.err_out, 1);
+        tab_store_tile<TAB_HNT8, true>(t, Hs, tile);
     }
 }
 
@@ -497,8 +537,11 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     if (warp == 0 && lane == 0)
         tab_bulk_load(Fs, t.T + (size_t)part * (KV + 2) * TAB_SUB, (unsigned)((KV + 2) * TAB_SUB * 4), tbar);
     if (threadIdx.x < TAB_SUB) Ms[threadIdx.x] = __ldg(t.meta + part * TAB_SUB + threadIdx.x);
-#if __CUDA_ARCH__ >= 900
-    cudaGridDependencySynchronize();  // the histogram pass is complete
+    // (no grid-dependency wait: each tile is acquired from its ready flag)
+#ifdef TAB_TRACE
+    unsigned long long* tr = t.trace + ((size_t)blockIdx.x * nw + warp) * 16;
+    int ntr = 2;
+    if (lane == 0) TAB_STAMP(tr);
 #endif
     // ---- contraction ----------------------------------------------------------
     // this CTA's tiles of its part: rank, rank + cpp, ... (strided)
@@ -507,13 +550,20 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
     const int ntl = (int)t.ntiles;  // < 2^31 (host-checked)
     const int it0 = 0, it1 = rank < ntl ? (ntl - rank + cpp - 1) / cpp : 0;  // local tile indices
     // lane 0: copy local tile k's histogram into buf by TMA
-    auto load_tile = [&](float* buf, int k, unsigned long long* bar) {
+    auto copy_tile = [&](float* buf, int k, unsigned long long* bar) {
         const int tl = rank + k * cpp;
         tab_bulk_load(buf, t.H + (int64_t)tl * (KV + 1) * TAB_TM, (unsigned)((KV + 1) * TAB_TM * 4), bar);
+    };
+    auto load_tile = [&](float* buf, int k, unsigned long long* bar) {  // waits for the tile
+        tab_await(t.ready + rank + k * cpp);
+        copy_tile(buf, k, bar);
     };
     if (threadIdx.x == 0) s_next = nw;
     __syncthreads();
     tab_bar_wait(tbar, 0);  // the table sub-chunk has landed
+#ifdef TAB_TRACE
+    if (lane == 0) TAB_STAMP(tr + 1);
+#endif
     const int ng = lane >> 4, lc = lane & 15;
     const int s = 0;
     int kt = it0 + warp;  // local tile index
@@ -530,7 +580,13 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
         int nx = 0;
         if (lane == 0) nx = atomicAdd(&s_next, 1);
         const int nxt = it0 + __shfl_sync(FULL, nx, 0);
-        if (NB == 2 && nxt < it1 && lane == 0) load_tile(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, nxt, bars + (b ^ 1));
+        // (not yet published: copied after this tile's sweep instead of
+        // holding the sweep up)
+        bool deferred = false;
+        if (NB == 2 && nxt < it1 && lane == 0) {
+            if (tab_poll(t.ready + rank + nxt * cpp)) copy_tile(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, nxt, bars + (b ^ 1));
+            else deferred = true;
+        }
         const float* H = Hbuf + b * (KV + 2) * TAB_TM;
         tab_bar_wait(bars + b, (phase >> b) & 1);
         phase ^= 1u << b;
@@ -568,6 +624,7 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
             }
 #undef TAB_FMA_BLOCK
         }
+        if (deferred) load_tile(Hbuf + (b ^ 1) * (KV + 2) * TAB_TM, nxt, bars + (b ^ 1));
         if (NB == 1) {
             __syncwarp();  // every lane is done with the buffer
             if (nxt < it1 && lane == 0) load_tile(Hbuf, nxt, bars);
@@ -618,18 +675,22 @@ __global__ void __launch_bounds__(512, 1) tab_kernel(KParams p, TabDev t) {
             }
         }
         __syncwarp();  // every lane is done with buffer b before it is refilled
+#ifdef TAB_TRACE
+        if (lane == 0 && ntr < 16) TAB_STAMP(tr + ntr++);
+#endif
         kt = nxt;
         if (NB == 2) b ^= 1;
     }
 }
 
 // Per-node results (PDL-chained after tab_kernel): one thread per node.
-__global__ void __launch_bounds__(64) tab_fin_kernel(KParams p, unsigned* gkeys) {
+__global__ void __launch_bounds__(64) tab_fin_kernel(KParams p, unsigned* gkeys, unsigned* ready) {
 #if __CUDA_ARCH__ >= 900
     cudaGridDependencySynchronize();  // every tab_kernel tile has landed
 #endif
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < p.n_nodes) tab_node_result(p, gkeys, p.node0 + i);
+    if (i * TAB_TM < p.n_nodes) ready[i] = 0u;  // tile i of this launch
 }
 
 // One small check on the cached table (the drop-in single-node call,

@@ -529,3 +529,33 @@ def test_device_batch_graph_replay(oracle):
     third = run(n - 100)  # different argument set -> new capture
     np.testing.assert_array_equal(third[:n - 100], lbo[perm][:n - 100])
     eng.close()
+
+
+def test_interleaved_streams_share_engine(oracle):
+    """An asynchronous device-resident call on a caller stream followed at
+    once (no synchronisation) by host-buffer calls on the engine's stream:
+    the engine orders the second after the first (shared scratch), so both
+    results stay exact, repeatedly."""
+    import torch
+
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.Engine(0)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream()
+    c, k, flat, off = W.cfg2_nodes(3000)
+    n = len(off) - 1
+    w8 = flat.astype(np.uint8)
+    d_w = torch.from_numpy(w8).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    d_lb = torch.zeros(n, dtype=torch.int64, device=dev)
+    d_ex = torch.zeros(n, dtype=torch.uint8, device=dev)
+    mr = int(np.diff(off).max())
+    lbo, _ = oracle.check_batch(flat, off, c, 2**62)
+    for _ in range(6):
+        eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, mr, c, 2**62, list(range(6)), 0,
+                               d_lb.data_ptr(), d_ex.data_ptr(), stream_ptr=st.cuda_stream, wbytes=1)
+        lb, _ = eng.check_batch(w8, off, c, 2**62, list(range(6)), 0)
+        np.testing.assert_array_equal(lb, lbo)
+        st.synchronize()
+        np.testing.assert_array_equal(d_lb.cpu().numpy(), lbo)
