@@ -41,8 +41,8 @@ UNIT = "checks/s"
 I_K = {"MT": 5, "RAD2": 10, "FS1": 9, "CCM1": 12, "VB2": 15, "BJ1": 10}
 KINDS = ("MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1")
 # DRAM bytes (read + write) of one tab_kernel launch on the 10^4-node cfg2
-# batch, from the ncu --set full capture summarised in profiles/round1_tab_ncu.md
-TAB_TRAFFIC_BYTES = 6819072
+# batch, from the ncu --set full capture summarised in profiles/round1_overlap_ncu.md
+TAB_TRAFFIC_BYTES = 6822912
 
 
 def _dist():
@@ -424,7 +424,7 @@ def run_ours(args):
                              "FMA/clk x 2 flop x max SM clock; no FP32 figure in MEASURED_PEAKS.json -- a "
                              "packed-FFMA2 microbenchmark, scripts/micro/ffma2_test.cu, reaches 89% of it); "
                              "traffic = DRAM bytes of one launch from the committed ncu capture "
-                             "(profiles/round1_tab_ncu.md); compute-bound, not HBM: the kernel reads its "
+                             "(profiles/round1_overlap_ncu.md); compute-bound, not HBM: the kernel reads its "
                              "L2-resident histograms once per table sub-chunk"},
         "canonical_int_ops": {"achieved_gops": ops / (kms / 1e3) / 1e9, "peak_gops": int_peak,
                               "frac": ops / (kms / 1e3) / 1e9 / int_peak,

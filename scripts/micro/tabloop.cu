@@ -9,13 +9,13 @@ __device__ __forceinline__ void ffma2(unsigned long long& acc, float h, unsigned
 }
 constexpr int KV = 152;
 template <int V>
-__global__ void __launch_bounds__(256, 1) k(float* out, int reps) {
+__global__ void __launch_bounds__(512, 1) k(float* out, int reps) {
     extern __shared__ __align__(16) float sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int SUB = V == 0 ? 64 : 128;
     float* F = sm;                                   // [KV+2][SUB]
     float* H = sm + (KV + 2) * SUB + warp * (KV + 2) * 16;
-    for (int i = threadIdx.x; i < (KV + 2) * SUB; i += 256) F[i] = (i % 7) * 0.5f;
+    for (int i = threadIdx.x; i < (KV + 2) * SUB; i += blockDim.x) F[i] = (i % 7) * 0.5f;
     for (int i = lane; i < (KV + 2) * 16; i += 32) H[i] = (i % 5);
     __syncthreads();
     constexpr int NA = V == 0 ? 8 : 16;
@@ -47,20 +47,20 @@ __global__ void __launch_bounds__(256, 1) k(float* out, int reps) {
     for (int a = 0; a < NA; ++a) s += __uint_as_float((unsigned)acc[a][0]) + __uint_as_float((unsigned)(acc[a][1] >> 32));
     if (s == 1.2345f) out[0] = s;
 }
-template <int V> void run(float* d) {
+template <int V> void run(float* d, int nw) {
     constexpr int SUB = V == 0 ? 64 : 128;
-    size_t smem = ((KV + 2) * SUB + 8 * (KV + 2) * 16) * 4;
+    size_t smem = ((KV + 2) * SUB + nw * (KV + 2) * 16) * 4;
     cudaFuncSetAttribute(k<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     int reps = 200;
-    k<V><<<148, 256, smem>>>(d, 2);
+    k<V><<<148, nw * 32, smem>>>(d, 2);
     cudaEventRecord(e0);
-    k<V><<<148, 256, smem>>>(d, reps);
+    k<V><<<148, nw * 32, smem>>>(d, reps);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     double nodes = V == 0 ? 8 * 2 : 16, cols = V == 0 ? 4 * 16 : 4 * 32;
-    double fma = 148.0 * 8 * nodes * cols * KV * reps;
-    printf("V=%d: %.1f FMA/clk/SM  (%s)\n", V, fma / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
+    double fma = 148.0 * nw * nodes * cols * KV * reps;
+    printf("V=%d warps=%d: %.1f FMA/clk/SM  (%s)\n", V, nw, fma / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
 }
-int main() { float* d; cudaMalloc(&d, 4); run<0>(d); run<1>(d); return 0; }
+int main() { float* d; cudaMalloc(&d, 4); for (int nw : {4, 8, 12, 16}) run<0>(d, nw); return 0; }
