@@ -559,3 +559,32 @@ def test_interleaved_streams_share_engine(oracle):
         np.testing.assert_array_equal(lb, lbo)
         st.synchronize()
         np.testing.assert_array_equal(d_lb.cpu().numpy(), lbo)
+
+
+def test_chunked_pageable_batch_matches_oracle(oracle):
+    """Pageable host buffers large enough for the chunked upload (4 chunks,
+    sub-ranges starting at node0 > 0 on 16-node tiles): per-tile ready flags
+    and keys are offset per chunk; every node matches the oracle, twice in a
+    row (flags cleared between calls), and again interleaved with a pinned
+    zero-copy call."""
+    import torch
+
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.Engine(0)
+    c, k, flat, off = W.cfg2_nodes(6000)
+    w8 = flat.astype(np.uint8)
+    lbo, _ = oracle.check_batch(flat, off, c, 2**62)
+    lbs, exs = oracle.check_batch(flat, off, c, k)  # lower_bound_seq early exit at k
+    for _ in range(2):
+        lb, _ = eng.check_batch(w8, off, c, 2**62, list(range(6)), 0)
+        np.testing.assert_array_equal(lb, lbo)
+        lb, ex = eng.check_batch(w8, off, c, k, list(range(6)), _native.F_PHASED)
+        np.testing.assert_array_equal(lb, lbs)
+        np.testing.assert_array_equal(ex, exs)
+    pw = torch.from_numpy(w8).pin_memory().numpy()
+    po = torch.from_numpy(off).pin_memory().numpy()
+    lb2, _ = eng.check_batch(pw, po, c, 2**62, list(range(6)), 0)
+    lb3, _ = eng.check_batch(w8, off, c, 2**62, list(range(6)), 0)
+    np.testing.assert_array_equal(lb2, lbo)
+    np.testing.assert_array_equal(lb3, lbo)
