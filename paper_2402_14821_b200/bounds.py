@@ -69,6 +69,7 @@ _KIND_ID = {"MT": 0, "RAD2": 1, "FS1": 2, "CCM1": 3, "VB2": 4, "BJ1": 5}
 _BY_ID = {v: DffKind[k] for k, v in _KIND_ID.items()}
 
 DEFAULT_DFF_ORDER: tuple[DffKind, ...] = tuple(DffKind)
+_DEFAULT_RESOLVED = (DEFAULT_DFF_ORDER, tuple(_KIND_ID[x.name] for x in DEFAULT_DFF_ORDER))
 
 
 def _kind(k) -> DffKind:
@@ -81,6 +82,27 @@ def _kind(k) -> DffKind:
 
 def kind_ids(kinds: Sequence) -> list[int]:
     return [_kind(k).id for k in kinds]
+
+
+_RESOLVED: dict = {}
+
+
+def resolve_kinds(kinds: Sequence) -> tuple[tuple, tuple]:
+    """(DffKind tuple, id tuple) for a kinds sequence, cached: the drop-in
+    single-check calls sit on a solver's per-node path."""
+    if kinds is DEFAULT_DFF_ORDER:
+        return _DEFAULT_RESOLVED
+    try:
+        key = tuple(kinds)
+        hit = _RESOLVED.get(key)
+    except TypeError:
+        key, hit = None, None
+    if hit is None:
+        ks = tuple(_kind(x) for x in kinds)
+        hit = (ks, tuple(_KIND_ID[x.name] for x in ks))
+        if key is not None and len(_RESOLVED) < 256:
+            _RESOLVED[key] = hit
+    return hit
 
 
 @dataclass(frozen=True)
@@ -290,18 +312,20 @@ def dff_bound(kind, red, lam: int) -> int:
     return int(dff_bound_batch(kind, red, lam, lam)[0])
 
 
-def _result_seq(res: _native.BplbResult, kinds: Sequence[DffKind], k: int) -> BoundResult:
+def _result_seq(res: _native.BplbResult, kinds: Sequence[DffKind], ids: Sequence[int], k: int) -> BoundResult:
+    best, ev, arg, nl = res.best[:], res.evaluated[:], res.arg_lambda[:], res.n_lambda[:]
     out = BoundResult(lb=0)
+    per, args = out.per_dff, out.arg
+    lb = evals = 0
     for i in range(res.n_done):
-        kind = kinds[i]
-        kid = kind.id
-        best = int(res.best[kid]) if res.evaluated[kid] else 0
-        out.per_dff[kind] = best
-        out.arg[kind] = int(res.arg_lambda[kid])
-        out.evals += int(res.n_lambda[kid])
-        if best > out.lb:
-            out.lb = best
-    out.exceeded_k = out.lb > k
+        kind, kid = kinds[i], ids[i]
+        b = best[kid] if ev[kid] else 0
+        per[kind] = b
+        args[kind] = arg[kid]
+        evals += nl[kid]
+        if b > lb:
+            lb = b
+    out.lb, out.evals, out.exceeded_k = lb, evals, lb > k
     return out
 
 
@@ -314,9 +338,9 @@ def lower_bound_seq(red, k: int, kinds: Sequence = DEFAULT_DFF_ORDER) -> BoundRe
     whose best exceeds ``k``; ``per_dff`` / ``evals`` / ``lb`` then match the
     reference's early-exit semantics exactly (0 for empty ranges, keys in
     evaluation order)."""
-    kinds = [_kind(x) for x in kinds]
+    kinds, ids = resolve_kinds(kinds)
     c, w = as_reduced(red)
     if not kinds:
         return BoundResult(lb=0, exceeded_k=0 > k)
-    res = _native.default_engine().check(w, c, k, [x.id for x in kinds], _native.F_PHASED)
-    return _result_seq(res, kinds, k)
+    res = _native.default_engine().check(w, c, k, ids, _native.F_PHASED)
+    return _result_seq(res, kinds, ids, k)

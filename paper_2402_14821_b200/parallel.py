@@ -20,7 +20,7 @@ import threading
 from typing import Sequence
 
 from . import _native
-from .bounds import DEFAULT_DFF_ORDER, BoundResult, DffKind, _kind, _result_seq
+from .bounds import DEFAULT_DFF_ORDER, BoundResult, DffKind, _kind, _result_seq, resolve_kinds
 from .instances import as_reduced
 
 __all__ = ["SharedMax", "lower_bound_par", "GpuBoundEngine", "ParallelBoundEngine",
@@ -54,29 +54,31 @@ class SharedMax:
             return self._value
 
 
-def _result_par(res: _native.BplbResult, kinds: Sequence[DffKind], k: int) -> BoundResult:
+def _result_par(res: _native.BplbResult, kinds: Sequence[DffKind], ids: Sequence[int], k: int) -> BoundResult:
     # parallel.py:105-119: kinds with at least one evaluated unit, in kinds
     # order; empty ranges never appear.
+    best, ev, arg = res.best[:], res.evaluated[:], res.arg_lambda[:]
     out = BoundResult(lb=0, evals=int(res.evals_total))
-    for kind in kinds:
-        kid = kind.id
-        if res.evaluated[kid]:
-            best = int(res.best[kid])
-            out.per_dff[kind] = best
-            out.arg[kind] = int(res.arg_lambda[kid])
-            if best > out.lb:
-                out.lb = best
-    out.exceeded_k = out.lb > k
+    per, args = out.per_dff, out.arg
+    lb = 0
+    for kind, kid in zip(kinds, ids):
+        if ev[kid]:
+            b = best[kid]
+            per[kind] = b
+            args[kind] = arg[kid]
+            if b > lb:
+                lb = b
+    out.lb, out.exceeded_k = lb, lb > k
     return out
 
 
 def _run_par(engine: _native.Engine, red, k: int, kinds, cancellation: bool) -> BoundResult:
-    kinds = [_kind(x) for x in kinds]
+    kinds, ids = resolve_kinds(kinds)
     c, w = as_reduced(red)
     if not kinds:
         return BoundResult(lb=0, exceeded_k=0 > k)
-    res = engine.check(w, c, k, [x.id for x in kinds], _native.F_CANCEL if cancellation else 0)
-    return _result_par(res, kinds, k)
+    res = engine.check(w, c, k, ids, _native.F_CANCEL if cancellation else 0)
+    return _result_par(res, kinds, ids, k)
 
 
 def lower_bound_par(red, k: int, kinds: Sequence = DEFAULT_DFF_ORDER, workers: int = 1,
@@ -116,12 +118,12 @@ class GpuBoundEngine:
     def __call__(self, red, k: int) -> BoundResult:
         eng = self._eng()
         if self.mode == "seq":
-            kinds = list(self.kinds)
+            kinds, ids = resolve_kinds(self.kinds)
             c, w = as_reduced(red)
             if not kinds:
                 return BoundResult(lb=0, exceeded_k=0 > k)
-            res = eng.check(w, c, k, [x.id for x in kinds], _native.F_PHASED)
-            return _result_seq(res, kinds, k)
+            res = eng.check(w, c, k, ids, _native.F_PHASED)
+            return _result_seq(res, kinds, ids, k)
         return _run_par(eng, red, k, self.kinds, self.cancellation)
 
     def close(self) -> None:
