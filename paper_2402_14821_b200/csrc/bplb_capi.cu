@@ -161,6 +161,8 @@ struct bplb_engine {
     int tab_per_sm = 1;
     int hist_per_sm = 3;          // persistent histogram CTAs per SM (BPLB_HIST_PER_SM)
     bool hist_carveout = false;
+    bool single_cluster_ok = true;    // drop-in checks as one thread-block cluster
+    bool single_cluster_attr = false;
     // cross-stream ordering of calls that share the engine's scratch: the
     // last asynchronous call's stream and an event recorded after its work
     cudaEvent_t ev_tail = nullptr;
@@ -681,6 +683,7 @@ int bplb_engine_create(int device, bplb_engine** out) {
     e->num_sms = prop.multiProcessorCount;
     e->smem_optin = prop.sharedMemPerBlockOptin;
     if (const char* v = getenv("BPLB_HIST_PER_SM")) e->hist_per_sm = std::max(1, atoi(v));
+    if (const char* v = getenv("BPLB_SINGLE_CLUSTER")) e->single_cluster_ok = atoi(v) != 0;  // A/B switch
 #ifdef TAB_TRACE
     e->graphs_ok = false;  // stamps are read back per launch
 #endif
@@ -794,6 +797,53 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
             e->skeys_zeroed = true;
         }
         const size_t woff = 256 + sizeof(bplb_result);  // [result][err] [weights]
+        if (e->single_cluster_ok && e->tab_nsub <= 16) {
+            // histogram built here (host-validated weights) and passed by
+            // value to one cluster of nsub CTAs; result in mapped memory
+            bplb::SingleHist hist;
+            std::memset(&hist, 0, sizeof(hist));
+            for (int64_t i = 0; i < r; ++i) {
+                const int32_t x = w[i];
+                if (x < 1 || x > c) return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+                ++hist.h[x - 1];  // r <= 65535
+            }
+            if ((rc = e->m_single.grow(woff))) return rc;
+            p.res_out = (bplb_result*)e->m_single.d;
+            p.err_out = nullptr;
+            const bplb::TabDev t = tab_dev(e, p, 1);
+            if (!e->single_cluster_attr) {
+                CUDA_TRY(cudaFuncSetAttribute(bplb::tab_single_cluster_kernel,
+                                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                e->single_cluster_attr = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)e->tab_nsub);
+            cfg.blockDim = dim3(bplb::TAB_SNT);
+            cfg.dynamicSmemBytes = (size_t)e->tab_KV * 4 + 16 * 64 * 4;
+            cfg.stream = e->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)e->tab_nsub;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaError_t ce = cudaLaunchKernelEx(&cfg, bplb::tab_single_cluster_kernel, p, t, hist);
+            if (ce == cudaSuccess) {
+                e->launches++;
+                if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+                CUDA_TRY(cudaStreamSynchronize(e->stream));
+                if (timing) {
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+                    e->last_ms = ms;
+                }
+                std::memcpy(out, e->m_single.h, sizeof(bplb_result));
+                return 0;
+            }
+            cudaGetLastError();  // no cluster of this size here: the counter-based kernel below
+            e->single_cluster_ok = false;
+        }
         if ((rc = e->m_single.grow(woff + (size_t)r * 4))) return rc;
         if (r > 0) std::memcpy((char*)e->m_single.h + woff, w, (size_t)r * 4);
         p.w = (const int*)((char*)e->m_single.d + woff);

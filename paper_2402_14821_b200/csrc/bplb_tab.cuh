@@ -446,20 +446,24 @@ __global__ void __launch_bounds__(TAB_HNT8) tab_hist_u8_kernel(KParams p, TabDev
 // them: full collection, PHASED (stop after the first kind whose running max
 // exceeds k, bounds.py:512-526) or CANCEL (later kinds skip once lb > k,
 // Alg. 4).  The node's keys are cleared for the next launch.
+__device__ __forceinline__ void tab_node_emit(const KParams& p, const unsigned (&key)[K_COUNT], int64_t node);
 __device__ __forceinline__ void tab_node_result(const KParams& p, unsigned* gkeys, int64_t node) {
-    const int c = (int)p.c;
-    const bool phased = p.flags & BPLB_F_PHASED;
-    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
     unsigned* g = gkeys + node * TAB_KSLOT;
     const uint4 k0 = __ldcg((const uint4*)g);  // written by atomics (L2) in phase B
     const uint2 k1 = __ldcg((const uint2*)(g + 4));
     *(uint4*)g = make_uint4(0u, 0u, 0u, 0u);
     *(uint2*)(g + 4) = make_uint2(0u, 0u);
+    const unsigned key[K_COUNT] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y};
+    tab_node_emit(p, key, node);
+}
+__device__ __forceinline__ void tab_node_emit(const KParams& p, const unsigned (&key)[K_COUNT], int64_t node) {
+    const int c = (int)p.c;
+    const bool phased = p.flags & BPLB_F_PHASED;
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
     // kind domains (bplb_domain, 32-bit: c <= 288); the VB2 cap
     // floor((2^64-1)/(r*max_w)) is >= 2^30 > c here, so VB2 is [2, c]
     const int lo[K_COUNT] = {0, c / 4 + 1, 1, 1, 2, 1};
     const int hi[K_COUNT] = {c == 1 ? 0 : (c + 1) / 2, c / 3, 100, c / 2, c, c};
-    const unsigned key[K_COUNT] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y};
     unsigned ev = 0;  // evaluated kinds (bit mask)
     int64_t lb = 0;
     int n_done = 0;
@@ -760,6 +764,71 @@ __global__ void __launch_bounds__(TAB_SNT) tab_single_kernel(KParams p, TabDev t
             __threadfence_system();  // result may live in mapped host memory
         }
     }
+}
+
+// The drop-in single check as one thread-block cluster (one CTA per 64-column
+// sub-chunk, nsub <= 16): the host validates the weights and passes the
+// node's histogram by value (no mapped-memory read in the kernel), every CTA
+// keeps its per-kind best keys in smem, and CTA 0 gathers them over DSMEM
+// after a cluster barrier and writes the result (no global atomics, no
+// counters, no fences: the host reads it after the stream completes).
+struct SingleHist {
+    unsigned short h[TAB_MAX_C + 4];  // counts of w = 1..c at w - 1, zero up to KV
+};
+__global__ void __launch_bounds__(TAB_SNT) tab_single_cluster_kernel(KParams p, TabDev t, SingleHist hist) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int KV = t.KV, sub = blockIdx.x, tid = threadIdx.x;
+    float* H = (float*)smem;                           // [KV]
+    float* part = (float*)(smem + (size_t)KV * 4);     // [16][64]
+    __shared__ unsigned skey[TAB_KSLOT];
+    for (int i = tid; i < KV; i += TAB_SNT) H[i] = (float)hist.h[i];
+    if (tid < TAB_KSLOT) skey[tid] = 0u;
+    const int col = tid & 63, q = tid >> 6, rq = (KV + 15) / 16;
+    const float* T = t.T + (size_t)sub * (KV + 2) * TAB_SUB + col;
+    float tv[18];
+    const int w0 = q * rq, w1 = min(KV, w0 + rq);
+#pragma unroll
+    for (int u = 0; u < 18; ++u) tv[u] = w0 + u < w1 ? __ldg(T + (size_t)(w0 + u) * TAB_SUB) : 0.0f;
+    __syncthreads();
+    float S = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 18; ++u) S = fmaf(w0 + u < w1 ? H[w0 + u] : 0.0f, tv[u], S);
+    part[q * 64 + col] = S;
+    __syncthreads();
+    if (tid < 64) {
+        float Sf = 0.0f;  // integers < 2^23: every partial sum is exact
+#pragma unroll
+        for (int g = 0; g < 16; ++g) Sf += part[g * 64 + col];
+        const int4 m = __ldg(t.meta + sub * TAB_SUB + col);
+        const int kind = m.w >> 16;
+        const unsigned bits = __float_as_uint(Sf + 8388608.0f);
+        const unsigned n2 = 2u * bits + (unsigned)m.y;
+        const unsigned qd = __umulhi(n2, (unsigned)m.x) >> m.z;
+        const unsigned key = (qd << 9) | (unsigned)(m.w & 0xffff);
+        if (kind < K_COUNT && (m.w & 0xffff)) atomicMax(&skey[kind], key);
+    }
+    // cluster barrier (arrive.release / wait.acquire): every CTA's keys are
+    // visible to CTA 0, and stay alive until the second barrier
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    if (rank == 0 && tid < 32) {
+        unsigned nct;
+        asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nct));
+        unsigned best = 0u;
+        const unsigned loc = (unsigned)__cvta_generic_to_shared(&skey[tid < K_COUNT ? tid : 0]);
+        for (unsigned j = 0; j < nct && tid < K_COUNT; ++j) {
+            unsigned ra, v;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(loc), "r"(j));
+            asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+            best = max(best, v);
+        }
+        unsigned key[K_COUNT];
+#pragma unroll
+        for (int kd = 0; kd < K_COUNT; ++kd) key[kd] = __shfl_sync(0xffffffffu, best, kd);
+        if (tid == 0) tab_node_emit(p, key, 0);
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace bplb
