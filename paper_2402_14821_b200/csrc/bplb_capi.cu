@@ -1244,8 +1244,12 @@ int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_ite
             const size_t hs = ((size_t)bplb::TAB_TM * (KV + 1) + ((n_items + 3) & ~3) + (size_t)bplb::TAB_TM * n_bins) * 4;
             auto hk = abytes == 1 ? bplb::tab_hist_assign_kernel<1> : bplb::tab_hist_assign_kernel<2>;
             if (hs > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
-            hk<<<(unsigned)t.ntiles, bplb::TAB_HNT, hs, e->stream>>>(q, t, (const int*)e->d_inst.p, (int)n_items,
-                                                                    (int)n_bins, a_dev, (int*)e->m_err.d);
+            // persistent, one CTA per SM beside the tab_kernel CTA that
+            // consumes its published tiles (max-shared carveout, as tab_hist)
+            CUDA_TRY(cudaFuncSetAttribute(hk, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+            hk<<<(unsigned)std::min<int64_t>(t.ntiles, e->num_sms), bplb::TAB_HNT, hs, e->stream>>>(
+                q, t, (const int*)e->d_inst.p, (int)n_items, (int)n_bins, a_dev, (int*)e->m_err.d);
             e->launches++;
             CUDA_TRY(cudaGetLastError());
             if ((rc = tab_contract(e, q, n_nodes))) return rc;

@@ -324,58 +324,60 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_assign_kernel(KParams p, Tab
     int* iw = (int*)(Hs + TAB_TM * ld);                              // [n_items]
     unsigned* loads = (unsigned*)(iw + ((n_items + 3) & ~3));        // [16][n_bins]
     const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
-    const int tile = blockIdx.x;
     const unsigned openv = AB == 1 ? 0xffu : 0xffffu;
     __shared__ int s_bad, s_rerr;
     if (threadIdx.x == 0) { s_bad = 0; s_rerr = 0; }
-    for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int i = threadIdx.x; i < TAB_TM * n_bins; i += TAB_HNT) loads[i] = 0u;
     for (int i = threadIdx.x; i < n_items; i += TAB_HNT) {
         const int x = __ldg(inst_w + i);
         if (x < 1 || x > c) s_bad = 1;
         iw[i] = x;
     }
-    __syncthreads();
-    const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
-    int rerr = 0;
-    if (node < p.node0 + p.n_nodes && !s_bad) {
-        unsigned* row = Hs + j * ld;
-        unsigned* ld_ = loads + j * n_bins;
-        constexpr int PER = 16 / AB;
-        const int64_t b0 = node * (int64_t)n_items;
-        const int64_t e0 = b0 & ~(int64_t)(PER - 1);
-        const int lead = (int)(b0 - e0);
-        const int nv = (lead + n_items + PER - 1) / PER;
-        const uint4* src = (const uint4*)((const unsigned char*)assign + e0 * AB);
-        for (int v = lane; v < nv; v += 32) {
-            const uint4 x = src[v];  // possibly mapped host memory (zero-copy)
-            const unsigned wds[4] = {x.x, x.y, x.z, x.w};
-            const int elo = v * PER - lead;  // item index of element 0
+    // persistent: tiles in order, published one by one (as tab_hist_u8_kernel)
+    for (int tile = blockIdx.x; tile < (int)t.ntiles; tile += gridDim.x) {
+        for (int i = threadIdx.x; i < TAB_TM * ld / 4; i += TAB_HNT) ((uint4*)Hs)[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = threadIdx.x; i < TAB_TM * n_bins; i += TAB_HNT) loads[i] = 0u;
+        __syncthreads();
+        const int64_t node = p.node0 + (int64_t)tile * TAB_TM + j;
+        int rerr = 0;
+        if (node < p.node0 + p.n_nodes && !s_bad) {
+            unsigned* row = Hs + j * ld;
+            unsigned* ld_ = loads + j * n_bins;
+            constexpr int PER = 16 / AB;
+            const int64_t b0 = node * (int64_t)n_items;
+            const int64_t e0 = b0 & ~(int64_t)(PER - 1);
+            const int lead = (int)(b0 - e0);
+            const int nv = (lead + n_items + PER - 1) / PER;
+            const uint4* src = (const uint4*)((const unsigned char*)assign + e0 * AB);
+            for (int v = lane; v < nv; v += 32) {
+                const uint4 x = src[v];  // possibly mapped host memory (zero-copy)
+                const unsigned wds[4] = {x.x, x.y, x.z, x.w};
+                const int elo = v * PER - lead;  // item index of element 0
 #pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                const int i = elo + e;
-                if ((unsigned)i >= (unsigned)n_items) continue;
-                const unsigned word = wds[(e * AB) >> 2];
-                const unsigned b = (word >> (((e * AB) & 3) * 8)) & openv;
-                if (b == openv) atomicAdd(row + iw[i] - 1, 1u);
-                else if (b < (unsigned)n_bins) atomicAdd(ld_ + b, (unsigned)iw[i]);
-                else rerr |= 2;
+                for (int e = 0; e < PER; ++e) {
+                    const int i = elo + e;
+                    if ((unsigned)i >= (unsigned)n_items) continue;
+                    const unsigned word = wds[(e * AB) >> 2];
+                    const unsigned b = (word >> (((e * AB) & 3) * 8)) & openv;
+                    if (b == openv) atomicAdd(row + iw[i] - 1, 1u);
+                    else if (b < (unsigned)n_bins) atomicAdd(ld_ + b, (unsigned)iw[i]);
+                    else rerr |= 2;
+                }
+            }
+            __syncwarp();
+            for (int b = lane; b < n_bins; b += 32) {
+                const unsigned L = ld_[b];
+                if (L > (unsigned)c) rerr |= 1;
+                else if (L > 0u) atomicAdd(row + L - 1, 1u);
             }
         }
-        __syncwarp();
-        for (int b = lane; b < n_bins; b += 32) {
-            const unsigned L = ld_[b];
-            if (L > (unsigned)c) rerr |= 1;
-            else if (L > 0u) atomicAdd(row + L - 1, 1u);
-        }
+        if (rerr) atomicOr(&s_rerr, rerr);
+        tab_store_tile<TAB_HNT>(t, Hs, tile);  // (its barriers order the counts before the stores)
     }
-    if (rerr) atomicOr(&s_rerr, rerr);
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_bad) atomicExch(err, 1);
         if (s_rerr) atomicOr(err + 1, s_rerr);
     }
-    tab_store_tile<TAB_HNT>(t, Hs, tile);
 }
 
 // uint8 weights: CTAs of 8 warps walk the 16-node tiles in order (two per
