@@ -588,3 +588,38 @@ def test_chunked_pageable_batch_matches_oracle(oracle):
     lb3, _ = eng.check_batch(w8, off, c, 2**62, list(range(6)), 0)
     np.testing.assert_array_equal(lb2, lbo)
     np.testing.assert_array_equal(lb3, lbo)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 100, 150, 255, 256, 280, 288])
+def test_single_check_cluster_kernel(oracle, c):
+    """Drop-in single checks on the cached table (one thread-block cluster of
+    up to 16 CTAs; c = 288 needs the full 16) equal the oracle's
+    lower_bound_seq and every field of the node kernel's result (full and
+    early-exit modes; the cancel mode's verdict); an invalid weight raises."""
+    from paper_2402_14821_b200 import _native
+
+    eng = _native.default_engine()
+    rng = np.random.default_rng(1000 + c)
+    for r in (0, 1, 17, 120, 400):
+        if r * 101 * c >= 1 << 23:
+            continue
+        w = rng.integers(1, c + 1, size=r).astype(np.int32)
+        red = ReducedInstance.from_array(c, w)
+        want = oracle.lower_bound_seq(w, c, 2**62)
+        got = G.lower_bound_seq(red, 2**62)
+        assert {k.name: v for k, v in got.per_dff.items()} == want.per_dff, (c, r)
+        assert {k.name: v for k, v in got.arg.items()} == want.arg, (c, r)
+        k = max(0, got.lb - 1)
+        a = eng.check(w, c, k, list(range(6)), _native.F_CANCEL)
+        b = eng.check(w, c, k, list(range(6)), _native.F_CANCEL | _native.F_NOTAB)
+        assert a.exceeded == b.exceeded  # which units a cancelled sweep skips is path-specific
+        for fl in (0, _native.F_PHASED):
+            a = eng.check(w, c, k, list(range(6)), fl)
+            b = eng.check(w, c, k, list(range(6)), fl | _native.F_NOTAB)
+            for f in ("lb", "exceeded", "n_done", "evals_total"):
+                assert getattr(a, f) == getattr(b, f), (c, r, fl, f)
+            for f in ("best", "arg_lambda", "n_lambda", "evals", "evaluated"):
+                assert list(getattr(a, f)) == list(getattr(b, f)), (c, r, fl, f)
+    bad = np.array([1, c + 1], dtype=np.int32)
+    with pytest.raises(ValueError):
+        eng.check(bad, c, 2**62, list(range(6)), 0)
