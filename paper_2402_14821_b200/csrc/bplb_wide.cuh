@@ -27,7 +27,14 @@ constexpr int ISLICE = 32 * GMOD_MAX * 8; // items per modular tile (4096)
 constexpr int LLW = 128;             // lambdas per lane-lookup unit (4 x 32)
 constexpr int WIDE_MAX_SEGS = 3 * K_COUNT;
 constexpr int64_t WIDE_MAX_C = (int64_t)1 << 27;
-constexpr int SCAN_TILE = 4096;      // entries per scan block
+constexpr int SCAN_TILE_MIN = 512;  // entries per scan block (at least)
+// Scan tile for n entries: >= 512 and a multiple of WT, with at most ~512
+// blocks, so every SM gets work and each block's prefix over the block
+// sums before it stays short.
+inline int64_t scan_tile(int64_t n) {
+    const int64_t t = ((n + 511) / 512 + WT - 1) / WT * WT;
+    return t < SCAN_TILE_MIN ? SCAN_TILE_MIN : t;
+}
 
 
 struct WSeg {
@@ -66,11 +73,12 @@ struct WideBufs {
     int* vb2;                   // [r]
     unsigned long long* acc;    // [c+1] VB2 per-lambda D (indexed by lambda)
     unsigned long long* pz;     // [2*101] FS1 P and Z (indexed by lambda)
+    int64_t tile;               // scan tile (scan_tile(c + 2))
 };
 
 inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
     int64_t n = c + 2;
-    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    int64_t nb = (n + scan_tile(n) - 1) / scan_tile(n);
     *nblocks_out = nb;
     size_t b = 0;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -84,10 +92,11 @@ inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
 }
 
 inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
-    int64_t n = c + 2, nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    int64_t n = c + 2, nb = (n + scan_tile(n) - 1) / scan_tile(n);
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     char* p = (char*)base;
     WideBufs w;
+    w.tile = scan_tile(n);
     w.state = (WideState*)p; p += al(sizeof(WideState));
     w.rec = (ulonglong2*)p; p += al((size_t)n * 16);
     w.bsum = (unsigned long long*)p; p += al((size_t)nb * 16);
@@ -148,11 +157,11 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
     }
 }
 
-// Block-level inclusive scan of (count, count*(i-1)) over one SCAN_TILE tile.
-__device__ __forceinline__ void tile_sums(const ulonglong2* rec, int64_t n, int64_t t0,
+// Block-level sums of (count, count*(i-1)) over one scan tile.
+__device__ __forceinline__ void tile_sums(const ulonglong2* rec, int64_t n, int64_t t0, int64_t tile,
                                           unsigned long long* sc, unsigned long long* sw) {
     unsigned long long a = 0, bw = 0;
-    for (int64_t i = t0 + threadIdx.x; i < min(n, t0 + SCAN_TILE); i += WT) {
+    for (int64_t i = t0 + threadIdx.x; i < min(n, t0 + tile); i += WT) {
         unsigned long long x = rec[i].y;
         a += x;
         bw += x * (unsigned long long)(i - 1);
@@ -178,7 +187,7 @@ __global__ void __launch_bounds__(WT) wide_scan_reduce(WideBufs b, int64_t c) {
     __shared__ unsigned long long red[WT / 32];
     const int64_t n = c + 2;
     unsigned long long sc, sw;
-    tile_sums(b.rec, n, (int64_t)blockIdx.x * SCAN_TILE, &sc, &sw);
+    tile_sums(b.rec, n, (int64_t)blockIdx.x * b.tile, b.tile, &sc, &sw);
     unsigned long long tc = block_sum_u64(sc, red);
     unsigned long long tw = block_sum_u64(sw, red);
     if (threadIdx.x == 0) {
@@ -187,24 +196,24 @@ __global__ void __launch_bounds__(WT) wide_scan_reduce(WideBufs b, int64_t c) {
     }
 }
 
-// Thread 0 of every block serially prefix-sums the block totals before it
-// (nblocks <= 65K at c = 2^27; cheap relative to the tile), then the block
+// Every block sums the block totals before it (<= ~512, in parallel), then
 // writes its tile with a warp-level scan.
 __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
     __shared__ unsigned long long carry_c[WT / 32 + 1], carry_w[WT / 32 + 1];
-    __shared__ unsigned long long base_c, base_w;
+    __shared__ unsigned long long base_c, base_w, red[WT / 32];
     const int64_t n = c + 2;
-    if (threadIdx.x == 0) {
+    {
         unsigned long long a = 0, bw = 0;
-        for (int j = 0; j < (int)blockIdx.x; ++j) { a += b.bsum[2 * j]; bw += b.bsum[2 * j + 1]; }
-        base_c = a;
-        base_w = bw;
+        for (int j = threadIdx.x; j < (int)blockIdx.x; j += WT) { a += b.bsum[2 * j]; bw += b.bsum[2 * j + 1]; }
+        a = block_sum_u64(a, red);
+        bw = block_sum_u64(bw, red);
+        if (threadIdx.x == 0) { base_c = a; base_w = bw; }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long rc = base_c, rw = base_w;
-    const int64_t t0 = (int64_t)blockIdx.x * SCAN_TILE;
-    const int64_t t1 = min(n, t0 + SCAN_TILE);
+    const int64_t t0 = (int64_t)blockIdx.x * b.tile;
+    const int64_t t1 = min(n, t0 + b.tile);
     for (int64_t s = t0; s < t1; s += WT) {
         const int64_t i = s + threadIdx.x;
         unsigned long long x = i < t1 ? b.rec[i].y : 0;

@@ -6,7 +6,8 @@ import numpy as np
 import paper_2402_14821_b200 as G
 from paper_2402_14821_b200 import _native, workloads as W
 
-c, w = W.cfg1()
+import os
+c, w = (W.cfg3 if os.environ.get("CFG") == "cfg3" else W.cfg1)()
 red = G.ReducedInstance.from_array(c, w)
 eng = _native.default_engine()
 wa = red.array()
