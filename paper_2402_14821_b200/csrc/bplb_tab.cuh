@@ -220,9 +220,12 @@ __device__ __forceinline__ bool tab_poll(const unsigned* flag) {
 }
 __device__ __forceinline__ void tab_await(const unsigned* flag) {
     unsigned v;
-    for (;;) {
+    for (unsigned spins = 0;; ++spins) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (v) break;
+        // a tile never published (a broken invariant) must fail the launch
+        // loudly instead of hanging the GPU: ~2^22 polls is seconds
+        if (spins > (1u << 22)) __trap();
         __nanosleep(128);
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
