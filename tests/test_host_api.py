@@ -156,3 +156,20 @@ def test_node_assignments_reduce_to_node_batch():
         asg = np.where(a[i] == openv, -1, a[i].astype(np.int64))
         red = reduce_packing_arrays(w, asg, k, c)
         np.testing.assert_array_equal(red, flat[off[i]:off[i + 1]])
+
+
+def test_addr_helper_matches_ctypes_data():
+    """_native._addr (the cheap pointer read on the batch-call path) returns
+    the array's data pointer for writable, read-only and empty arrays."""
+    import numpy as np
+
+    from paper_2402_14821_b200._native import _addr
+
+    a = np.arange(100, dtype=np.int64)
+    assert _addr(a) == a.ctypes.data
+    ro = np.frombuffer(b"\x01\x02\x03\x04", dtype=np.uint8)
+    assert not ro.flags.writeable and _addr(ro) == ro.ctypes.data
+    e = np.zeros(0, dtype=np.uint8)
+    assert _addr(e) == e.ctypes.data
+    v = a[10:]
+    assert _addr(v) == v.ctypes.data
