@@ -47,6 +47,62 @@ __global__ void __launch_bounds__(512, 1) k(float* out, int reps) {
     for (int a = 0; a < NA; ++a) s += __uint_as_float((unsigned)acc[a][0]) + __uint_as_float((unsigned)(acc[a][1] >> 32));
     if (s == 1.2345f) out[0] = s;
 }
+// V=2: 2 node groups x 16 column groups, 8 nodes x 8 columns per lane
+// (128-column sub-chunk): 4 LDS.128 per 32 FFMA2 instead of 3 per 16.
+__global__ void __launch_bounds__(512, 1) k2(float* out, int reps) {
+    extern __shared__ __align__(16) float sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int SUB = 128;
+    float* F = sm;
+    float* H = sm + (KV + 2) * SUB + warp * (KV + 2) * 16;
+    for (int i = threadIdx.x; i < (KV + 2) * SUB; i += blockDim.x) F[i] = (i % 7) * 0.5f;
+    for (int i = lane; i < (KV + 2) * 16; i += 32) H[i] = (i % 5);
+    __syncthreads();
+    unsigned long long acc[8][4];
+    for (int a = 0; a < 8; ++a) for (int q = 0; q < 4; ++q) acc[a][q] = 0;
+    const float* Fp = F + (lane & 15) * 8;
+    const float* Hp = H + (lane >> 4) * 8;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+        for (int kk = 0; kk < KV; kk += 2) {
+            ulonglong2 f[2][2];
+            float4 h[2][2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                f[u][0] = *(const ulonglong2*)(Fp + (kk + u) * SUB);
+                f[u][1] = *(const ulonglong2*)(Fp + (kk + u) * SUB + 4);
+                h[u][0] = *(const float4*)(Hp + (kk + u) * 16);
+                h[u][1] = *(const float4*)(Hp + (kk + u) * 16 + 4);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float hv[8] = {h[u][0].x, h[u][0].y, h[u][0].z, h[u][0].w, h[u][1].x, h[u][1].y, h[u][1].z, h[u][1].w};
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    ffma2(acc[a][0], hv[a], f[u][0].x); ffma2(acc[a][1], hv[a], f[u][0].y);
+                    ffma2(acc[a][2], hv[a], f[u][1].x); ffma2(acc[a][3], hv[a], f[u][1].y);
+                }
+            }
+        }
+    }
+    float s = 0;
+    for (int a = 0; a < 8; ++a) for (int q = 0; q < 4; ++q) s += __uint_as_float((unsigned)acc[a][q]);
+    if (s == 1.2345f) out[0] = s;
+}
+void run2(float* d, int nw) {
+    size_t smem = ((KV + 2) * 128 + nw * (KV + 2) * 16) * 4;
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    int reps = 200;
+    k2<<<148, nw * 32, smem>>>(d, 2);
+    cudaEventRecord(e0);
+    k2<<<148, nw * 32, smem>>>(d, reps);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double fma = 148.0 * nw * 16 * 128 * (double)KV * reps;
+    printf("V=2 warps=%d: %.1f FMA/clk/SM  (%s)\n", nw, fma / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
+}
 template <int V> void run(float* d, int nw) {
     constexpr int SUB = V == 0 ? 64 : 128;
     size_t smem = ((KV + 2) * SUB + nw * (KV + 2) * 16) * 4;
@@ -63,4 +119,9 @@ template <int V> void run(float* d, int nw) {
     double fma = 148.0 * nw * nodes * cols * KV * reps;
     printf("V=%d warps=%d: %.1f FMA/clk/SM  (%s)\n", V, nw, fma / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
 }
-int main() { float* d; cudaMalloc(&d, 4); for (int nw : {4, 8, 12, 16}) run<0>(d, nw); return 0; }
+int main() {
+    float* d; cudaMalloc(&d, 4);
+    for (int nw : {4, 8, 12, 16}) run<0>(d, nw);
+    for (int nw : {4, 8, 12}) run2(d, nw);
+    return 0;
+}
