@@ -153,6 +153,7 @@ struct bplb_engine {
     // batched small-c path: cached table of transformed values for (tab_c, tab_kmask)
     DevBuf d_tab, d_tabmeta, d_tabkeys, d_tabhist, d_tabready;
     DevBuf d_inst, d_assign, d_redr;  // device-side reduction of node states
+    std::vector<int32_t> inst_host;   // what d_inst holds
     DevBuf d_skeys;                   // single-check table path: keys[8] + CTA counter
     MappedBuf m_single;               // single-check table path: weights in, result out
     MappedBuf m_err;                  // batch calls: error flag written by the kernels
@@ -161,6 +162,7 @@ struct bplb_engine {
     int tab_per_sm = 1;
     int hist_per_sm = 3;          // persistent histogram CTAs per SM (BPLB_HIST_PER_SM)
     bool hist_carveout = false;
+    bool assign_carveout = false;
     bool single_cluster_ok = true;    // drop-in checks as one thread-block cluster
     bool single_cluster_attr = false;
     // cross-stream ordering of calls that share the engine's scratch: the
@@ -195,7 +197,23 @@ namespace {
 // Copy host -> device (direct DMA when the source is pinned, through the
 // engine's pinned staging buffer otherwise).
 int h2d(bplb_engine* e, void* dst, const void* src, size_t bytes, size_t stage_off = 0,
-        cudaStream_t s = nullptr, int pinned = -1) {
+        cudaStream_t s = nullptr, int pinned = -1);
+
+// The instance weights of an assignment batch on the device (a search
+// re-checks the same instance every call: re-uploaded only when they change).
+int upload_inst(bplb_engine* e, const int32_t* inst_w, int64_t n_items) {
+    void* before = e->d_inst.p;
+    if (int rc = e->d_inst.grow((size_t)std::max<int64_t>(n_items, 1) * 4)) return rc;
+    const size_t bytes = (size_t)n_items * 4;
+    if (e->d_inst.p == before && e->inst_host.size() == (size_t)n_items &&
+        (n_items == 0 || std::memcmp(e->inst_host.data(), inst_w, bytes) == 0))
+        return 0;
+    e->inst_host.assign(inst_w, inst_w + n_items);
+    // from the engine's copy: stays valid after the call returns
+    return h2d(e, e->d_inst.p, e->inst_host.data(), bytes, 0, e->stream, 1);
+}
+
+int h2d(bplb_engine* e, void* dst, const void* src, size_t bytes, size_t stage_off, cudaStream_t s, int pinned) {
     if (bytes == 0) return 0;
     if (!s) s = e->stream;
     if (pinned < 0) pinned = bytes > 65536 ? is_pinned(src) : 1;
@@ -623,7 +641,6 @@ int reduce_device(bplb_engine* e, const int32_t* inst_w, int64_t n_items, int64_
     *obytes = c <= 255 ? 1 : (c <= 65535 ? 2 : 4);
     int rc;
     const size_t asz = (size_t)n_nodes * (size_t)n_items * (size_t)abytes;
-    if ((rc = e->d_inst.grow((size_t)std::max<int64_t>(n_items, 1) * 4))) return rc;
     if ((rc = e->d_assign.grow(std::max<size_t>(asz, 16)))) return rc;
     if ((rc = e->d_w.grow((size_t)std::max<int64_t>(n_nodes * n_items, 1) * 4 + 64))) return rc;
     if ((rc = e->d_off.grow((size_t)(n_nodes + 1) * 8))) return rc;
@@ -632,7 +649,7 @@ int reduce_device(bplb_engine* e, const int32_t* inst_w, int64_t n_items, int64_
     CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 8, e->stream));
     CUDA_TRY(cudaMemsetAsync(e->d_redr.p, 0, 8, e->stream));
     if (asz > 65536 && !is_pinned(assign) && (rc = e->h_stage.grow(asz + 64))) return rc;
-    if ((rc = h2d(e, e->d_inst.p, inst_w, (size_t)n_items * 4, 0, e->stream, 1))) return rc;
+    if ((rc = upload_inst(e, inst_w, n_items))) return rc;
     if ((rc = h2d(e, e->d_assign.p, assign, asz))) return rc;
     bplb::ReduceArgs a;
     a.w = (const int*)e->d_inst.p;
@@ -1230,8 +1247,7 @@ int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_ite
                 if ((rc = h2d(e, e->d_assign.p, assign, asz))) return rc;
                 a_dev = e->d_assign.p;
             }
-            if ((rc = e->d_inst.grow((size_t)std::max<int64_t>(n_items, 1) * 4))) return rc;
-            if ((rc = h2d(e, e->d_inst.p, inst_w, (size_t)n_items * 4, 0, e->stream, 1))) return rc;
+            if ((rc = upload_inst(e, inst_w, n_items))) return rc;
             if ((rc = tab_ensure(e, q))) return rc;
             if ((rc = tab_reserve(e, n_nodes))) return rc;
             int64_t* lb_dev = (int64_t*)device_alias(lb_out);
@@ -1257,8 +1273,15 @@ int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_ite
             if (hs > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs));
             // persistent, one CTA per SM beside the tab_kernel CTA that
             // consumes its published tiles (max-shared carveout, as tab_hist)
-            CUDA_TRY(cudaFuncSetAttribute(hk, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          cudaSharedmemCarveoutMaxShared));
+            if (!e->assign_carveout) {
+                CUDA_TRY(cudaFuncSetAttribute(bplb::tab_hist_assign_kernel<1>,
+                                              cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              cudaSharedmemCarveoutMaxShared));
+                CUDA_TRY(cudaFuncSetAttribute(bplb::tab_hist_assign_kernel<2>,
+                                              cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              cudaSharedmemCarveoutMaxShared));
+                e->assign_carveout = true;
+            }
             hk<<<(unsigned)std::min<int64_t>(t.ntiles, e->num_sms), bplb::TAB_HNT, hs, e->stream>>>(
                 q, t, (const int*)e->d_inst.p, (int)n_items, (int)n_bins, a_dev, (int*)e->m_err.d);
             e->launches++;
