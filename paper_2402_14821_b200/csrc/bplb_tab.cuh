@@ -15,19 +15,21 @@
 // multiply-high division and the max over lambda (lowest lambda on ties) a
 // segmented warp REDUX, both fused into the epilogue.
 //
-// Three PDL-chained launches per batch:
-//   A  tab_hist_kernel: one CTA per 16-node tile, one warp per node, counts
-//      the CSR weights into a smem scratch and writes them as fp32
-//      [tile][w][16 nodes] (L2-resident)
-//   B  tab_kernel, one CTA per SM: each CTA holds one 64-column sub-chunk of the table
-//      ([w][64] fp32, loaded by TMA while phase A runs) and sweeps a static
-//      range of tiles; each warp double-buffers tile histograms in smem with
-//      TMA bulk copies and runs an 8-node x 4-column register tile per lane
-//      (lanes: 2 node groups x 16 column groups; histogram reads are
-//      broadcasts).  Per-(node, kind) best keys meet in a global u32
-//      atomicMax array.
-//   C  tab_fin_kernel: one thread per node replays the kinds in order (modes
-//      as in warp_node_kernel), writes the outputs and clears its keys.
+// Three launches per batch (one CUDA graph when the arguments repeat):
+//   A  tab_hist_u8_kernel / tab_hist_kernel: persistent CTAs walk the 16-node
+//      tiles in order, count the CSR weights into smem and store each tile
+//      as fp32 [tile][w][16 nodes] (L2-resident), publishing it with a
+//      release flag; they trigger B's launch at their start
+//   B  tab_kernel, one CTA per SM beside A's CTAs: each CTA holds one
+//      64-column sub-chunk of the table ([w][64] fp32, TMA) and sweeps a
+//      static range of tiles, acquiring each tile's flag before copying it;
+//      each warp double-buffers tile histograms in smem with TMA bulk copies
+//      and runs an 8-node x 4-column register tile per lane (lanes: 2 node
+//      groups x 16 column groups; histogram reads are broadcasts).
+//      Per-(node, kind) best keys meet in a global u32 atomicMax array.
+//   C  tab_fin_kernel (PDL after B): one thread per node replays the kinds in
+//      order (modes as in warp_node_kernel), writes the outputs and clears
+//      its keys and its tile's flag.
 #pragma once
 #include "bplb_node.cuh"
 
