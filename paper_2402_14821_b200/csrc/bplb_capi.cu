@@ -162,6 +162,7 @@ struct bplb_engine {
     int tab_per_sm = 1;
     int hist_per_sm = 3;          // persistent histogram CTAs per SM (BPLB_HIST_PER_SM)
     bool hist_carveout = false;
+    int64_t multi_grid = 0;  // BPLB_MULTI_GRID: override of the single-node multi-CTA grid (tuning)
     bool assign_carveout = false;
     bool single_cluster_ok = true;    // drop-in checks as one thread-block cluster
     bool single_cluster_attr = false;
@@ -614,9 +615,12 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
     if (per_sm < 1) per_sm = 1;
     int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
     if (multi) {  // co-resident grid (CTAs may wait on each other), sized by the work
+        // at most one CTA per SM: two per SM measured 7-10 % slower (cfg3
+        // 125 vs 113 us; every CTA repeats the node setup and meets the
+        // others at the phase barriers)
         const int64_t cells = std::max<int64_t>(max_r, 1) * (3 * std::min<int64_t>(p.c, 1 << 24) + 100);
-        grid = std::min<int64_t>((int64_t)std::min(per_sm, 2) * e->num_sms,
-                                 std::max<int64_t>(1, cells / 16384));
+        grid = std::min<int64_t>((int64_t)e->num_sms, std::max<int64_t>(1, cells / 16384));
+        if (e->multi_grid > 0) grid = std::min<int64_t>((int64_t)per_sm * e->num_sms, e->multi_grid);
     }
     if (grid_cap > 0) grid = std::min<int64_t>(grid, grid_cap);
     if (grid < 1) return 0;
@@ -711,6 +715,7 @@ int bplb_engine_create(int device, bplb_engine** out) {
     e->num_sms = prop.multiProcessorCount;
     e->smem_optin = prop.sharedMemPerBlockOptin;
     if (const char* v = getenv("BPLB_HIST_PER_SM")) e->hist_per_sm = std::max(1, atoi(v));
+    if (const char* v = getenv("BPLB_MULTI_GRID")) e->multi_grid = atoll(v);
     if (const char* v = getenv("BPLB_SINGLE_CLUSTER")) e->single_cluster_ok = atoi(v) != 0;  // A/B switch
 #ifdef TAB_TRACE
     e->graphs_ok = false;  // stamps are read back per launch
