@@ -623,3 +623,18 @@ def test_single_check_cluster_kernel(oracle, c):
     bad = np.array([1, c + 1], dtype=np.int32)
     with pytest.raises(ValueError):
         eng.check(bad, c, 2**62, list(range(6)), 0)
+
+
+@pytest.mark.parametrize("c", [510, 1022, 262_142, 262_143, 1_048_574, 1_048_577])
+def test_wide_scan_tiles_dff_vectors(oracle, c):
+    """The grid-wide path's cumulative table (adaptive scan tile: c + 2
+    entries split into <= ~512 blocks, boundaries exercised by c) gives the
+    oracle's per-lambda bounds: MT over its whole range, VB2 and BJ1 over a
+    window at both ends."""
+    rng = np.random.default_rng(c % 9973)
+    w = rng.integers(1, c + 1, size=300).astype(np.int32)
+    red = ReducedInstance.from_array(c, w)
+    for kind, lo, hi in (("MT", 0, min(4000, (c + 1) // 2)), ("VB2", 2, min(600, c)), ("BJ1", max(1, c - 500), c)):
+        got = G.dff_bound_batch(kind, red, lo, hi)
+        want = oracle.dff_bound_batch(kind, w, c, lo, hi)
+        np.testing.assert_array_equal(got, want, err_msg=f"{kind} c={c}")
