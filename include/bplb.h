@@ -53,6 +53,9 @@ extern "C" {
 #define BPLB_F_CANCEL 0x2   /* Alg. 4 guard "if lb <= k" per work unit
                                (parallel.py:76-77): units observing lb > k skip */
 #define BPLB_F_TIMING 0x4   /* record device time of the last call (bplb_last_device_ms) */
+#define BPLB_F_NOPRUNE 0x10 /* dense sweep: evaluate every lambda of the grid (the paper's
+                               Alg. 2-4 work) instead of skipping the lambdas whose integer
+                               upper bound cannot change the result (bplb_prune.cuh) */
 #define BPLB_F_NOTAB  0x8   /* batched calls: do not use the histogram x table kernel
                                (selects the warp-per-node kernel; parity testing) */
 
@@ -164,6 +167,20 @@ BPLB_API double bplb_last_device_ms(bplb_engine *eng);
  * one and returns its duration (0 if none was recorded). */
 BPLB_API int bplb_profile_kernel(bplb_engine *eng, int on);
 BPLB_API double bplb_last_kernel_ms(bplb_engine *eng);
+
+/* Which kernel family served the engine's last check / batch launch (test
+ * and measurement hook); *detail (optional) = table path: warps per
+ * contraction CTA; prune path: 1 in lb mode, 0 in per-kind key mode;
+ * node kernels: grid of a multi-CTA single check. */
+#define BPLB_PATH_NONE 0
+#define BPLB_PATH_TAB 1          /* histogram x table contraction (c <= 288 batches)   */
+#define BPLB_PATH_TAB_SINGLE 2   /* table path, one check (cluster / counter kernel)   */
+#define BPLB_PATH_WARP 3         /* warp-per-node kernel (dense sweep)                 */
+#define BPLB_PATH_NODE_TABLE 4   /* CTA-per-node kernel, cumulative tables             */
+#define BPLB_PATH_NODE_SORT 5    /* CTA-per-node kernel, sorted weights                */
+#define BPLB_PATH_WIDE 6         /* grid-wide kernels (one large instance)             */
+#define BPLB_PATH_PRUNE 7        /* CTA-per-node bound-pruned sweep (bplb_prune.cuh)   */
+BPLB_API int bplb_last_path(bplb_engine *eng, int32_t *detail);
 
 /* Thread-local message describing the last error on this thread. */
 BPLB_API const char *bplb_last_error(void);

@@ -22,6 +22,10 @@ F_PHASED = 0x1
 F_CANCEL = 0x2
 F_TIMING = 0x4
 F_NOTAB = 0x8  # batched: skip the histogram x table kernel (parity testing)
+F_NOPRUNE = 0x10  # dense sweep: every lambda evaluated (no bound pruning)
+
+# bplb_last_path ids (include/bplb.h)
+PATHS = {0: "none", 1: "tab", 2: "tab_single", 3: "warp", 4: "node_table", 5: "node_sort", 6: "wide", 7: "prune"}
 
 E_INVAL, E_RANGE, E_CUDA, E_NOMEM, E_NODEV = -1, -2, -3, -4, -5
 
@@ -79,6 +83,7 @@ SIGNATURES = {
     "bplb_last_device_ms": (ctypes.c_double, [_vp]),
     "bplb_profile_kernel": (ctypes.c_int, [_vp, ctypes.c_int]),
     "bplb_last_kernel_ms": (ctypes.c_double, [_vp]),
+    "bplb_last_path": (ctypes.c_int, [_vp, _i32p]),
     "bplb_last_error": (ctypes.c_char_p, []),
     "bplb_version": (ctypes.c_char_p, []),
 }
@@ -193,6 +198,13 @@ class Engine:
 
     def last_kernel_ms(self) -> float:
         return float(self._lib.bplb_last_kernel_ms(self.handle))
+
+    def last_path(self) -> tuple[str, int]:
+        """(kernel family, detail) of the last check / batch launch: which
+        kernel actually served it (tests assert the intended path ran)."""
+        d = ctypes.c_int32(0)
+        p = self._lib.bplb_last_path(self.handle, ctypes.byref(d))
+        return PATHS.get(int(p), str(p)), int(d.value)
 
     def check(self, w: np.ndarray, c: int, k: int, kinds, flags: int) -> BplbResult:
         w = as_i32(w)

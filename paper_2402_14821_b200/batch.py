@@ -29,7 +29,8 @@ def csr_from_lists(nodes: Sequence[Sequence[int]]) -> tuple[np.ndarray, np.ndarr
 
 def lower_bound_batch(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
                       kinds: Sequence = DEFAULT_DFF_ORDER, *, mode: str = "full",
-                      want_best: bool = False, engine: _native.Engine | None = None):
+                      want_best: bool = False, dense: bool = False,
+                      engine: _native.Engine | None = None):
     """Evaluate the LB collection for every node of a CSR batch on the GPU.
 
     ``weights`` may be int32, or -- to cut host->device bytes -- uint16
@@ -43,8 +44,14 @@ def lower_bound_batch(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
     Returns ``(lb int64[n], exceeded bool[n])`` and, with ``want_best``,
     also ``best int64[n, 6]`` and ``arg_lambda int64[n, 6]`` indexed by kind
     id (MT, RAD2, FS1, CCM1, VB2, BJ1).
+
+    ``dense=True`` evaluates every lambda of the grid (the paper's sweep)
+    instead of skipping the lambdas whose integer upper bound provably
+    cannot change the outputs (bplb_prune.cuh); both are bit-exact.
     """
     flags = {"full": 0, "seq": _native.F_PHASED, "cancel": _native.F_CANCEL}[mode]
+    if dense:
+        flags |= _native.F_NOPRUNE
     eng = engine or _native.default_engine()
     return eng.check_batch(weights, offsets, c, k, kind_ids(kinds), flags, want_best=want_best)
 

@@ -10,8 +10,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libbplb.so")
+GEN_OUT = os.path.join(HERE, "libbplb_gen.so")  # synthetic node generator (workload data, not the path)
 SOURCES = ["bplb_capi.cu"]
-HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh", "bplb_reduce.cuh"]
+HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_prune.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh", "bplb_reduce.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -31,7 +32,24 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_gen(force: bool = False) -> str:
+    src = os.path.join(CSRC, "bplb_gen.cu")
+    if not force and os.path.exists(GEN_OUT) and os.path.getmtime(GEN_OUT) > os.path.getmtime(src):
+        return GEN_OUT
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+           "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared", "-o", GEN_OUT + ".tmp", src,
+           "-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libbplb_gen.so")
+    os.replace(GEN_OUT + ".tmp", GEN_OUT)
+    return GEN_OUT
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_gen(force)
     if not force and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -13,6 +13,7 @@
 #include "../../include/bplb.h"
 #include "bplb_core.h"
 #include "bplb_node.cuh"
+#include "bplb_prune.cuh"
 #include "bplb_wide.cuh"
 #include "bplb_warp.cuh"
 #include "bplb_tab.cuh"
@@ -159,6 +160,9 @@ struct bplb_engine {
     MappedBuf m_err;                  // batch calls: error flag written by the kernels
     bool skeys_zeroed = false;
     size_t tab_attr_smem = 0;
+    size_t prune_attr_smem = 0;
+    int last_path = 0;    // BPLB_PATH_* of the last batch / check launch (bplb_last_path)
+    int last_detail = 0;  // path detail (table path: warps per contraction CTA)
     int tab_per_sm = 1;
     int hist_per_sm = 3;          // persistent histogram CTAs per SM (BPLB_HIST_PER_SM)
     bool hist_carveout = false;
@@ -272,6 +276,8 @@ int launch_warp(bplb_engine* e, bplb::KParams& p, int64_t n_nodes) {
     p.n_nodes = n_nodes;
     bplb::warp_node_kernel<<<(unsigned)grid, bplb::WNT, smem, e->stream>>>(p);
     e->launches++;
+    e->last_path = BPLB_PATH_WARP;
+    e->last_detail = 0;
     CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -490,6 +496,8 @@ int tab_contract(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     int64_t grid = std::max<int64_t>(std::min<int64_t>((int64_t)e->tab_per_sm * e->num_sms, cpp * P), P);
     if (e->prof_kernel) CUDA_TRY(cudaEventRecord(e->ev_pk0, e->stream));
     CUDA_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, e->stream, p, t));
+    e->last_path = BPLB_PATH_TAB;
+    e->last_detail = nw;
 #ifdef TAB_TRACE
     {  // dump: grid, nw, P, ntiles, hist ctas, then [cta][warp][16] stamps, then [tile] publish stamps
         std::vector<unsigned long long> h((size_t)grid * nw * 16), hp((size_t)t.ntiles);
@@ -564,7 +572,13 @@ int launch_tab_graph(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t 
         if (slot->exec) cudaGraphExecDestroy(slot->exec);
         slot->exec = nullptr;
         cudaGraph_t g = nullptr;
-        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            // e.g. the legacy default stream (cudaStreamLegacy) cannot be
+            // captured: clear the error and launch directly from now on
+            cudaGetLastError();
+            e->graphs_ok = false;
+            return launch_tab(e, p, n_nodes, 0);
+        }
         const int64_t l0 = e->launches;
         int rc = launch_tab(e, p, n_nodes, 0);
         cudaError_t ce = cudaStreamEndCapture(s, &g);
@@ -584,12 +598,44 @@ int launch_tab_graph(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t 
     cudaError_t ce = cudaGraphLaunch(slot->exec, s);
     if (ce != cudaSuccess) return fail(BPLB_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce));
     e->launches += 3;
+    e->last_path = BPLB_PATH_TAB;
+    e->last_detail = tab_warps(e, e->tab_KV, 2);
     return 0;
 }
 
 // Launch the node-resident kernel over n nodes.  max_r bounds every node.
 // multi: one node, every CTA of a co-resident grid sweeps part of it
 // (single-check latency path); p.ms must point at a zeroed MultiState.
+// Bound-pruned node kernel (bplb_prune.cuh) for batches of nodes with
+// 2 <= c <= 2^18 whose largest node fits its shared-memory layout.
+bool prune_path(const bplb_engine* e, const bplb::KParams& p, int64_t max_r) {
+    if ((p.flags & BPLB_F_NOPRUNE) || p.lam_out || p.ms || p.c < 2 || p.c > bplb::PR_MAX_C || max_r > (1 << 14))
+        return false;
+    return bplb::prune_smem_bytes(bplb::prune_rcap(max_r), p.c) <= e->smem_optin;
+}
+
+int launch_prune(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r) {
+    const int rcap = bplb::prune_rcap(max_r);
+    const size_t smem = bplb::prune_smem_bytes(rcap, p.c);
+    if (smem > e->prune_attr_smem) {
+        CUDA_TRY(cudaFuncSetAttribute(bplb::prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        e->prune_attr_smem = smem;
+    }
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::prune_kernel, bplb::PNT, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
+    if (grid < 1) return 0;
+    p.n_nodes = n_nodes;
+    const int lbmode = !p.best_out && !p.arg_out && !p.res_out;
+    bplb::prune_kernel<<<(unsigned)grid, bplb::PNT, smem, e->stream>>>(p, rcap, lbmode);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    e->last_path = BPLB_PATH_PRUNE;
+    e->last_detail = lbmode;
+    return 0;
+}
+
 bool node_fits(int64_t r, int64_t c) {
     return r <= (c <= bplb::TABLE_MAX_C ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT);
 }
@@ -598,6 +644,7 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
                 bool multi = false, int slot = 0) {
     if (!multi && grid_cap == 0 && !(p.flags & BPLB_F_NOTAB) && tab_path(e, p, n_nodes, max_r))
         return launch_tab(e, p, n_nodes, slot);
+    if (!multi && grid_cap == 0 && prune_path(e, p, max_r)) return launch_prune(e, p, n_nodes, max_r);
     if (!multi && grid_cap == 0 && warp_path(p, n_nodes)) return launch_warp(e, p, n_nodes);
     const bool table = p.c <= bplb::TABLE_MAX_C;
     if (max_r > (table ? NODE_R_MAX_TABLE : NODE_R_MAX_SORT))
@@ -627,6 +674,8 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
     p.n_nodes = n_nodes;
     kern<<<(unsigned)grid, bplb::NT, smem, e->stream>>>(p, rcap);
     e->launches++;
+    e->last_path = table ? BPLB_PATH_NODE_TABLE : BPLB_PATH_NODE_SORT;
+    e->last_detail = multi ? (int)grid : 0;
     CUDA_TRY(cudaGetLastError());
     return 0;
 }
@@ -743,7 +792,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
                       &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
-                      &e->d_tabkeys, &e->d_tabhist, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys})
+                      &e->d_tabkeys, &e->d_tabhist, &e->d_tabready, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -781,6 +830,12 @@ int bplb_profile_kernel(bplb_engine* e, int on) {
     e->prof_kernel = on != 0;
     e->prof_recorded = 0;
     return 0;
+}
+
+int bplb_last_path(bplb_engine* e, int32_t* detail) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (detail) *detail = e->last_detail;
+    return e->last_path;
 }
 
 double bplb_last_kernel_ms(bplb_engine* e) {
@@ -864,6 +919,8 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
             cudaError_t ce = cudaLaunchKernelEx(&cfg, bplb::tab_single_cluster_kernel, p, t, hist);
             if (ce == cudaSuccess) {
                 e->launches++;
+                e->last_path = BPLB_PATH_TAB_SINGLE;
+                e->last_detail = e->tab_nsub;
                 if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
                 CUDA_TRY(cudaStreamSynchronize(e->stream));
                 if (timing) {
@@ -887,6 +944,8 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
         bplb::tab_single_kernel<<<(unsigned)e->tab_nsub, bplb::TAB_SNT, (size_t)KV * 4 + 16 * 64 * 4, e->stream>>>(
             p, t, (int)r, (unsigned*)e->d_skeys.p, (int*)e->d_skeys.p + 8);
         e->launches++;
+        e->last_path = BPLB_PATH_TAB_SINGLE;
+        e->last_detail = 0;
         CUDA_TRY(cudaGetLastError());
         if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
         CUDA_TRY(cudaStreamSynchronize(e->stream));
@@ -911,6 +970,7 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     p.err_out = (int*)((char*)e->d_res.p + sizeof(bplb_result));  // copied back with the result
     CUDA_TRY(cudaMemsetAsync(p.err_out, 0, 4, e->stream));
     if (!node_fits(r, c)) {
+        e->last_path = BPLB_PATH_WIDE;
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);
         if (rc) return fail(rc, bplb::wide_error());
@@ -982,6 +1042,7 @@ int bplb_dff_bound_batch(bplb_engine* e, int32_t kind, const int32_t* w, int64_t
     if (r == 0) {  // bounds.py:478-479
         CUDA_TRY(cudaMemsetAsync(e->d_lam.p, 0, (size_t)L * 8, e->stream));
     } else if (!node_fits(r, c)) {
+        e->last_path = BPLB_PATH_WIDE;
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);
         if (rc) return fail(rc, bplb::wide_error());
@@ -1190,6 +1251,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             q.ex_out = p.ex_out + i;
             q.best_out = p.best_out ? p.best_out + i * K_COUNT : nullptr;
             q.arg_out = p.arg_out ? p.arg_out + i * K_COUNT : nullptr;
+            e->last_path = BPLB_PATH_WIDE;
             rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap,
                                   &e->launches, q, off[i + 1] - off[i], nullptr);
             if (rc) return fail(rc, bplb::wide_error());
@@ -1242,7 +1304,10 @@ int bplb_check_batch_assign(bplb_engine* e, const int32_t* inst_w, int64_t n_ite
         const bool tab = !(flags & BPLB_F_NOTAB) && (abytes == 1 || abytes == 2) && c <= bplb::TAB_MAX_C &&
                          n_items <= 65535 && std::max<int64_t>(n_items, 1) * maxf < (1ll << 23) &&
                          n_bins <= bplb::TAB_ASSIGN_MAX_BINS && n_bins < (abytes == 1 ? 255 : 65535) &&
-                         n_nodes >= 256 && n_nodes <= ((int64_t)1 << 30) && tab_warps(e, ((int)c + 3) / 4 * 4) >= 2;
+                         n_nodes >= 256 && n_nodes <= ((int64_t)1 << 30) && tab_warps(e, ((int)c + 3) / 4 * 4) >= 2 &&
+                         // the histogram kernel's shared memory (16 node rows, the instance, 16 x bins)
+                         ((size_t)bplb::TAB_TM * (((c + 3) / 4 * 4) + 1) + ((n_items + 3) & ~3) +
+                          (size_t)bplb::TAB_TM * n_bins) * 4 + 64 <= e->smem_optin;
         if (tab) {
             const void* a_dev = device_alias(assign);
             const size_t asz = (size_t)n_nodes * (size_t)n_items * (size_t)abytes;

@@ -206,7 +206,7 @@ __device__ __forceinline__ void mod_group(const int* __restrict__ items, int g, 
 
 // Walk items [i_begin, i_end) in groups of 32 x G items (G = 16 or 8;
 // 4 for weighted distinct-value lists).  ofs / vb2 select FS1 or VB2.
-template <bool WIDE, bool WEIGHTED = false>
+template <bool WIDE, bool WEIGHTED = false, int GMAX = 16>
 __device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_begin, int i_end,
                                          uint32_t c, u64 cinv, int64_t lam_a, int L, u64* tot,
                                          uint32_t one, bool vb2,
@@ -218,7 +218,7 @@ __device__ __forceinline__ void mod_walk(const int* __restrict__ items, int i_be
         if (WEIGHTED) {
             mod_group<WIDE, WEIGHTED, 4>(items, g, i_end, c, cinv, lam_a, L, tot, one, counts, ofs, vb2);
             g += 4 * kWarp;
-        } else if (rem > 8 * kWarp) {
+        } else if (GMAX >= 16 && rem > 8 * kWarp) {
             mod_group<WIDE, WEIGHTED, 16>(items, g, i_end, c, cinv, lam_a, L, tot, one, counts, ofs, vb2);
             g += 16 * kWarp;
         } else {

@@ -310,10 +310,14 @@ __device__ void sweep_multi(const KParams& p, NodeCtl& ctl, const LK& lk, const 
             if (phased) {
                 // Alg. 2: a kind runs to completion; stop at the first kind
                 // boundary where the earlier kinds' max exceeds k
+                // (the first kind in the order always runs: no earlier kind)
                 int prev = 0;
-                for (int i = 0; i < p.nk && p.kinds[i] != kd; ++i)
+                bool has_prev = false;
+                for (int i = 0; i < p.nk && p.kinds[i] != kd; ++i) {
                     prev = max(prev, *(volatile int*)&ms->kmax[p.kinds[i]]);
-                skip = (int64_t)prev > p.k;
+                    has_prev = true;
+                }
+                skip = has_prev && (int64_t)prev > p.k;
             } else {
                 skip = (int64_t)(*(volatile int*)&ms->lb) > p.k;  // Alg. 4 guard
             }

@@ -1,0 +1,659 @@
+// bplb_prune.cuh -- bound-pruned lambda sweep: one CTA per reduced instance
+// (persistent over a batch of search-node states), for 2 <= c <= PR_MAX_C.
+//
+// The reference evaluates every grid point (kind, lambda) of the collection
+// (bounds.py:463-527).  Most of them cannot matter for the answer, and that
+// can be proven per lambda from O(1) node statistics, exactly:
+//
+//   VB2  (bounds.py:189-197, 410-438): piece(v) = floor((v l - 1)/c) lies in
+//        [(v l - c)/c, (v l - 1)/c], so the per-lambda sum S(l) is at most
+//        S_hi(l) = 2 floor((l Vs - ns)/c) - 2 max(0, ceil(l Vm/c) - nm)
+//                  + (n_eq + 2 n_big)(l - 1)
+//        (Vs / Vm: sums of small / mirrored values), and its relaxation
+//        without the floors is LINEAR in l.
+//   CCM1 (bounds.py:181-186, 390-407): floor(v/l) in [(v-l+1)/l, v/l] gives
+//        S_hi(l) = 2 floor(Vs/l) + (n_eq + 2 n_big) q
+//                  - 2 max(0, ceil((Vm - n_big (l-1))/l)),  q = floor(c/l).
+//   BJ1  (bounds.py:200-206, 441-460): with cm = c mod l, every transformed
+//        item obeys f(w) <= w (l - cm)/l, so the bound is at most
+//        ceil(W / (c - cm)).
+//   (all three checked against the oracle on 1e8 (instance, kind, l) points)
+//
+// A lambda is skipped when its upper bound cannot beat what the sweep
+// already holds:
+//   lb mode  (only lb / exceeded requested): UB(l) <= best bound of ANY kind;
+//   key mode (per-kind best + lowest arg lambda requested): (UB(l), l) cannot
+//            beat the kind's (best, lowest lambda) key -- UB < best, or
+//            UB == best at a higher lambda.
+// Skipped lambdas provably cannot change the outputs, so lb, exceeded,
+// per-kind best and arg lambda are bit-exact with the full sweep.
+//
+// MT and RAD2 (bounds.py:155-170, 373-387) are piecewise constant in lambda:
+// their lookups N(l-1), N(c-l), N(c-2l), N(2l-1), W(.) change only at
+// l = w+1, c-w+1, floor((c-w)/2)+1, floor((w+2)/2).  The maximum and its
+// lowest lambda are therefore attained at the range start or at one of
+// those candidates, which are the only lambdas evaluated when they are
+// fewer than the range (the reference's own l2 sweep uses the same fact,
+// bounds.py:139-152).
+//
+// Lookups: a presence bitmask over the values [0, c] with per-word rank
+// prefixes (one LDS.64 + POPC) indexes cumulative count / weight tables over
+// the distinct values, so N(x) and W(x) cost two shared loads for any x.
+#pragma once
+#include "bplb_node.cuh"
+
+namespace bplb {
+
+constexpr int PNT = 256;
+constexpr int PNW = PNT / 32;
+constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in smem
+constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
+constexpr int PR_MAX_SEGS = 20;
+
+enum { PU_CAND = 0, PU_LOOK = 1, PU_WALK = 2, PU_PRUNE = 3 };
+
+struct LkRank {
+    const uint2* rk;        // [c/32 + 1]: {presence mask of 32i..32i+31, #distinct values < 32i}
+    const int* cn;          // [d + 1]: cn[j] = #{w <= j-th smallest distinct value}, cn[0] = 0
+    const long long* cw;    // [d + 1]: the matching weight sums
+    int r, d;
+    int64_t c;
+    __device__ __forceinline__ int rank(int64_t x) const {  // #distinct values <= x, clamped
+        if (x < 0) return 0;
+        if (x >= c) return d;
+        const uint2 e = rk[x >> 5];
+        return (int)e.y + __popc(e.x & (0xFFFFFFFFu >> (31 - ((int)x & 31))));
+    }
+    __device__ __forceinline__ int64_t n_le(int64_t x) const { return cn[rank(x)]; }
+    __device__ __forceinline__ void both(int64_t x, int64_t* n, int64_t* w) const {
+        const int j = rank(x);
+        *n = cn[j];
+        *w = cw[j];
+    }
+};
+
+struct PSeg {
+    int kind, type;
+    int64_t lo, hi;   // inclusive lambda range
+    int chunk;        // lambdas (or items, PU_CAND) per unit
+    int first, count; // unit index range
+};
+
+struct PruneCtl {
+    NodeStats st;
+    int64_t lo[K_COUNT], hi[K_COUNT];
+    PSeg segs[PR_MAX_SEGS];
+    int nseg, nunits;
+    int kseg_first[K_COUNT], kseg_count[K_COUNT];
+    u64 key[K_COUNT];
+    unsigned long long evals[K_COUNT];
+    int evaluated[K_COUNT];
+    int lb;
+    int unit_next, unit_end;
+    int n_vb2, d;
+    int n_done, bad, skip;
+    long long wsum[PNW], wsum2[PNW];
+};
+
+struct PruneMem {
+    int* sw;          // raw weights [r]
+    int* vb2;         // VB2 walk items (2w != c, w < c)
+    uint2* rk;        // presence words
+    int* cn;          // cumulative counts by distinct rank
+    long long* cw;    // cumulative weights by distinct rank
+    u64* tot;         // per-warp walk accumulators [PNW][32]
+};
+
+__host__ __device__ inline int prune_rcap(int64_t max_r) { return (int)((max_r + 3) & ~3ll) + 4; }
+
+__host__ __device__ inline size_t prune_smem_bytes(int rcap, int64_t c) {
+    size_t s = (size_t)PNW * 32 * 8;            // tot
+    s += (size_t)(rcap + 2) * 8;                // cw
+    s += (size_t)((c >> 5) + 2) * 8;            // rk
+    s += (size_t)(rcap + 2) * 4;                // cn
+    s += (size_t)rcap * 4 * 2;                  // sw, vb2
+    return s + 64;
+}
+
+// ---- upper-bound tests (true => bound(l) <= B is guaranteed) ----------------
+// Integer envelope: c <= 2^18, r <= 2^14 (PR envelope) keeps every product
+// below 2^63 (l Vs <= 2^18 * 2^14 * 2^17).
+__device__ __forceinline__ bool ub_le_vb2(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
+    const int64_t ns = st.n_small, nm = st.n_big - st.n_full, K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
+    // c * S_hi without the floors (linear in lambda)
+    const int64_t env = 2 * (lam * st.Vs - ns) - 2 * (lam * st.Vm - c * nm) + c * K * (lam - 1);
+    if (env <= 2 * c * B * (lam - 1)) return true;
+    const int64_t fs = (int64_t)((uint64_t)(lam * st.Vs - ns) / (uint64_t)c);  // l Vs >= 2 ns > ns
+    int64_t y = (int64_t)(((uint64_t)(lam * st.Vm) + (uint64_t)c - 1) / (uint64_t)c) - nm;
+    y = y > 0 ? y : 0;
+    return 2 * fs - 2 * y + K * (lam - 1) <= 2 * B * (lam - 1);
+}
+
+__device__ __forceinline__ bool ub_le_ccm1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
+    const int64_t q = (int64_t)((uint32_t)c / (uint32_t)lam);
+    const int64_t K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
+    const int64_t lhs = 2 * st.Vs - 2 * st.Vm + 2 * (int64_t)st.n_big * (lam - 1);
+    if (lhs <= (2 * B - K) * q * lam) return true;
+    const int64_t z = st.Vm - (int64_t)st.n_big * (lam - 1);
+    const int64_t y = z > 0 ? (z + lam - 1) / lam : 0;
+    return 2 * (st.Vs / lam) + K * q - 2 * y <= 2 * B * q;
+}
+
+__device__ __forceinline__ bool ub_le_bj1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
+    const int64_t cm = (int64_t)((uint32_t)c % (uint32_t)lam);
+    return st.W <= B * (c - cm);
+}
+
+__device__ __forceinline__ bool ub_le(int kind, const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
+    if (B < 0) return false;
+    if (kind == K_VB2) return ub_le_vb2(st, c, lam, B);
+    if (kind == K_CCM1) return ub_le_ccm1(st, c, lam, B);
+    return ub_le_bj1(st, c, lam, B);
+}
+
+// Every lambda of [l1, l2] has bound <= B (relaxations monotone over ranges).
+__device__ __forceinline__ bool ub_le_range(int kind, const NodeStats& st, int64_t c, int64_t l1, int64_t l2,
+                                            int64_t B) {
+    if (B < 0) return false;
+    if (kind == K_VB2) {
+        const int64_t ns = st.n_small, nm = st.n_big - st.n_full, K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
+        auto g = [&](int64_t l) {
+            return 2 * (l * st.Vs - ns) - 2 * (l * st.Vm - c * nm) + c * K * (l - 1) - 2 * c * B * (l - 1);
+        };
+        return g(l1) <= 0 && g(l2) <= 0;
+    }
+    if (kind == K_CCM1) {
+        const int64_t K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
+        const int64_t lhs = 2 * st.Vs - 2 * st.Vm + 2 * (int64_t)st.n_big * (l2 - 1);
+        const int64_t coef = 2 * B - K;
+        return coef >= 0 ? lhs <= coef * (c - l2 + 1) : lhs <= coef * c;
+    }
+    return c - l2 + 1 > 0 && st.W <= B * (c - l2 + 1);
+}
+
+// Pruning threshold snapshot (the shared best only grows, so a stale one is safe).
+struct Thr {
+    int64_t B, a_rel;
+    bool has, lbmode;
+};
+
+__device__ __forceinline__ Thr read_thr(const PruneCtl& ctl, int kind, bool lbmode) {
+    Thr t;
+    t.lbmode = lbmode;
+    if (lbmode) {
+        t.B = *(volatile const int*)&ctl.lb;
+        t.has = true;
+        t.a_rel = 0;
+    } else {
+        const u64 key = *(volatile const u64*)&ctl.key[kind];
+        t.has = key != 0;
+        t.B = (int64_t)(key >> 32);
+        t.a_rel = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu));
+    }
+    return t;
+}
+
+__device__ __forceinline__ bool lam_skip(const Thr& t, int kind, const NodeStats& st, int64_t c, int64_t lo,
+                                         int64_t lam) {
+    if (!t.has) return false;
+    if (t.lbmode) return ub_le(kind, st, c, lam, t.B);
+    const int64_t rel = lam - lo;
+    if (rel == t.a_rel) return true;  // the current arg itself: already evaluated
+    if (rel > t.a_rel) return ub_le(kind, st, c, lam, t.B);
+    return t.B >= 1 && ub_le(kind, st, c, lam, t.B - 1);
+}
+
+__device__ __forceinline__ bool range_skip(const Thr& t, int kind, const NodeStats& st, int64_t c, int64_t lo,
+                                           int64_t l1, int64_t l2) {
+    if (!t.has) return false;
+    if (t.lbmode) return ub_le_range(kind, st, c, l1, l2, t.B);
+    if (l1 - lo > t.a_rel) return ub_le_range(kind, st, c, l1, l2, t.B);
+    return t.B >= 1 && ub_le_range(kind, st, c, l1, l2, t.B - 1);
+}
+
+// ---- segments ------------------------------------------------------------------
+// phase 0: exact seeds (MT / RAD2 candidates, FS1, the first VB2 window, a
+// CCM1 / BJ1 window at c/4+1 where their maxima sit on typical nodes);
+// phase 1: the pruned remainder of VB2, CCM1, BJ1.
+__device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, int r) {
+    const int64_t lo = ctl.lo[kind], hi = ctl.hi[kind];
+    if (hi < lo) return;
+    auto push = [&](int type, int64_t a, int64_t b, int chunk, int count) {
+        if (b < a || count <= 0) return;
+        PSeg& s = ctl.segs[ctl.nseg++];
+        s.kind = kind;
+        s.type = type;
+        s.lo = a;
+        s.hi = b;
+        s.chunk = chunk;
+        s.first = ctl.nunits;
+        s.count = count;
+        ctl.nunits += count;
+        ctl.kseg_count[kind]++;
+    };
+    auto pushr = [&](int type, int64_t a, int64_t b, int chunk) {
+        if (b >= a) push(type, a, b, chunk, (int)((b - a + chunk) / chunk));
+    };
+    const int64_t n = hi - lo + 1;
+    switch (kind) {
+    case K_MT: case K_RAD2:
+        if (phase == 0) {
+            const int64_t ncand = (kind == K_MT ? 2 : 4) * (int64_t)r + 1;
+            if (n > ncand) push(PU_CAND, lo, hi, 32, (r + 31) / 32 > 0 ? (r + 31) / 32 : 1);
+            else pushr(PU_LOOK, lo, hi, 32);
+        }
+        break;
+    case K_FS1:
+        if (phase == 0) pushr(PU_WALK, lo, hi, 32);
+        break;
+    case K_VB2:
+        if (phase == 0) pushr(PU_WALK, lo, min(hi, lo + 31), 32);
+        else pushr(PU_PRUNE, lo + 32, hi, PR_SUPER);
+        break;
+    default: {  // CCM1, BJ1
+        int64_t s0 = c / 4 + 1;
+        s0 = s0 < lo ? lo : (s0 > hi ? hi : s0);
+        const int64_t s1 = min(hi, s0 + 31);
+        if (phase == 0) pushr(PU_LOOK, s0, s1, 32);
+        else {
+            pushr(PU_PRUNE, s1 + 1, hi, PR_SUPER);
+            pushr(PU_PRUNE, lo, s0 - 1, PR_SUPER);
+        }
+    }
+    }
+}
+
+// ---- one unit ----------------------------------------------------------------------
+template <class LK>
+__device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, int u,
+                           bool lbmode) {
+    const int lane = threadIdx.x & 31;
+    int si = 0;
+    while (si + 1 < ctl.nseg && ctl.segs[si + 1].first <= u) ++si;
+    const PSeg sg = ctl.segs[si];
+    const int kind = sg.kind;
+    const int64_t c = p.c;
+    const int64_t lo_k = ctl.lo[kind];
+    const NodeStats& st = ctl.st;
+    u64* key = &ctl.key[kind];
+    int64_t wmax = -1;
+    int64_t nev = 0;
+    if (sg.type == PU_CAND) {
+        const int i = (u - sg.first) * 32 + lane;
+        const bool vi = i < st.r;
+        const int64_t w = vi ? m.sw[i] : 0;
+        if (u == sg.first) {  // the range start (first segment of the staircase)
+            const int64_t lam = sg.lo;
+            int64_t b = 0;
+            if (lane == 0) {
+                const int64_t S = kind == K_MT ? bplb_mt_sum(lk, c, st.r, lam) : bplb_rad2_sum(lk, c, st.r, lam);
+                b = bplb_bound(S, c);
+            }
+            wmax = max(wmax, emit_warp(lane == 0, lam, b, lo_k, key, nullptr, 0, 0));
+            nev = sg.hi - sg.lo + 1;
+        }
+        const int nc = kind == K_MT ? 2 : 4;
+#pragma unroll 1
+        for (int j = 0; j < nc; ++j) {
+            int64_t lam;
+            if (kind == K_MT) lam = j == 0 ? w + 1 : c - w + 1;
+            else lam = j == 0 ? w + 1 : (j == 1 ? (c - w) / 2 + 1 : (j == 2 ? (w + 2) / 2 : c - w + 1));
+            const bool v = vi && lam >= sg.lo && lam <= sg.hi;
+            int64_t b = 0;
+            if (v) {
+                const int64_t S = kind == K_MT ? bplb_mt_sum(lk, c, st.r, lam) : bplb_rad2_sum(lk, c, st.r, lam);
+                b = bplb_bound(S, c);
+            }
+            wmax = max(wmax, emit_warp(v, lam, b, lo_k, key, nullptr, 0, 0));
+        }
+    } else if (sg.type == PU_LOOK) {
+        const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        const int64_t lam = lam_a + lane;
+        const bool valid = lam <= lam_b;
+        int64_t S = 0;
+        if (valid) {
+            switch (kind) {
+            case K_MT: S = bplb_mt_sum(lk, c, st.r, lam); break;
+            case K_RAD2: S = bplb_rad2_sum(lk, c, st.r, lam); break;
+            case K_CCM1: S = bplb_ccm1_sum(lk, st, c, lam); break;
+            default: S = bplb_bj1_sum(lk, st, c, lam); break;
+            }
+        }
+        const int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+        wmax = emit_warp(valid, lam, b, lo_k, key, nullptr, 0, 0);
+        nev = lam_b - lam_a + 1;
+    } else if (sg.type == PU_WALK) {
+        const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        const int L = (int)(lam_b - lam_a + 1);
+        u64* t = m.tot + (threadIdx.x >> 5) * 32;
+        t[lane] = 0;
+        __syncwarp();
+        const uint32_t c32 = (uint32_t)c;
+        const u64 cinv = bplb_cinv(c32);
+        if (kind == K_VB2) mod_walk<false, false, 8>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, p.one, true);
+        else mod_walk<false, false, 8>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, p.one, false);
+        __syncwarp();
+        const int64_t lam = lam_a + lane;
+        const bool valid = lane < L;
+        int64_t S = 0;
+        if (valid)
+            S = kind == K_VB2 ? bplb_vb2_sum(st, c, lam, t[lane])
+                              : bplb_fs1_sum(st, lam, t[lane], (uint64_t)bplb_fs1_zero(lk, c, st.maxw, lam));
+        const int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+        wmax = emit_warp(valid, lam, b, lo_k, key, nullptr, 0, 0);
+        nev = L;
+    } else {  // PU_PRUNE
+        const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        nev = lam_b - lam_a + 1;
+        const Thr t0 = read_thr(ctl, kind, lbmode);
+        if (!range_skip(t0, kind, st, c, lo_k, lam_a, lam_b)) {
+            const uint32_t c32 = (uint32_t)c;
+            const u64 cinv = bplb_cinv(c32);
+            for (int64_t sub = lam_a; sub <= lam_b; sub += 32) {
+                const int64_t sub_b = min(lam_b, sub + 31);
+                const int64_t lam = sub + lane;
+                const bool in = lam <= sub_b;
+                const Thr th = read_thr(ctl, kind, lbmode);
+                const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                if (!mask) continue;
+                const int n = __popc(mask);
+                bool have = false;
+                int64_t b = 0;
+                if (kind == K_VB2) {
+                    if (n >= 6) {  // dense cluster: walk the 32-lambda window
+                        u64* tt = m.tot + (threadIdx.x >> 5) * 32;
+                        tt[lane] = 0;
+                        __syncwarp();
+                        mod_walk<false, false, 8>(m.vb2, 0, ctl.n_vb2, c32, cinv, sub, (int)(sub_b - sub + 1), tt,
+                                                  p.one, true);
+                        __syncwarp();
+                        if (in) {
+                            have = true;
+                            b = bplb_bound(bplb_vb2_sum(st, c, lam, tt[lane]), 2 * (lam - 1));
+                        }
+                    } else {  // a few lambdas: one warp pass over the items each
+                        unsigned mm = mask;
+                        while (mm) {
+                            const int j = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const int64_t lj = sub + j;
+                            u64 D = 0;
+                            for (int i = lane; i < ctl.n_vb2; i += 32) {
+                                const uint32_t x = (uint32_t)m.vb2[i];
+                                D += bplb_mulmod(x, (uint32_t)lj, 2 * x < c32 ? 1u : 0u, c32, cinv);
+                            }
+                            D = warp_sum_u64(D);
+                            if (lane == j) {
+                                have = true;
+                                b = bplb_bound(bplb_vb2_sum(st, c, lj, D), 2 * (lj - 1));
+                            }
+                        }
+                    }
+                } else {  // CCM1 / BJ1: harmonic lookups or a dense item pass
+                    const int64_t span = kind == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
+                    const int64_t tmax = span / sub;
+                    const int64_t T = kind == K_CCM1 ? 26 : 40;
+                    const int64_t cost_lane = T * (tmax + 1);
+                    const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + 24);
+                    const int64_t cost_dense = n * (10 * (((int64_t)st.r + 31) / 32) + 24);
+                    if (cost_lane <= cost_coop && cost_lane <= cost_dense) {
+                        if (in) {
+                            have = true;
+                            const int64_t S = kind == K_CCM1 ? bplb_ccm1_sum(lk, st, c, lam) : bplb_bj1_sum(lk, st, c, lam);
+                            b = bplb_bound(S, bplb_fc(kind, c, lam));
+                        }
+                    } else {
+                        const bool dense = cost_dense < cost_coop;
+                        unsigned mm = mask;
+                        while (mm) {
+                            const int j = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const int64_t lj = sub + j;
+                            int64_t S;
+                            if (kind == K_CCM1) {
+                                if (dense) S = ccm1_dense_raw(m.sw, st.r, st, c, lj);
+                                else {
+                                    int64_t part = bplb_ccm1_part(lk, st, c, lj, 1 + lane, 32);
+                                    part = (int64_t)warp_sum_u64((u64)part);
+                                    S = bplb_ccm1_from_part(st, c, lj, part);
+                                }
+                            } else {
+                                if (dense) S = bj1_dense(m.sw, st.r, c, lj);
+                                else {
+                                    int64_t fl, rem;
+                                    bplb_bj1_part(lk, st, c, lj, lane, 32, &fl, &rem);
+                                    fl = (int64_t)warp_sum_u64((u64)fl);
+                                    rem = (int64_t)warp_sum_u64((u64)rem);
+                                    S = bplb_bj1_from_parts(c, lj, fl, rem);
+                                }
+                            }
+                            if (lane == j) {
+                                have = true;
+                                b = bplb_bound(S, bplb_fc(kind, c, lj));
+                            }
+                        }
+                    }
+                }
+                wmax = max(wmax, emit_warp(have, lam, b, lo_k, key, nullptr, 0, 0));
+            }
+        }
+    }
+    if (lane == 0) {
+        if (nev) atomicAdd(&ctl.evals[kind], (unsigned long long)nev);
+        ctl.evaluated[kind] = 1;
+        if (wmax >= 0) atomicMax(&ctl.lb, (int)wmax);
+    }
+}
+
+template <class LK>
+__device__ void prune_run(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, bool lbmode,
+                          bool cancel) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&ctl.unit_next, 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= ctl.unit_end) break;
+        if (cancel && (int64_t)(*(volatile int*)&ctl.lb) > p.k) continue;  // Alg. 4 guard
+        prune_unit(p, ctl, lk, m, u, lbmode);
+    }
+}
+
+// lbmode: only lb / exceeded are produced (cross-kind pruning).
+__global__ void __launch_bounds__(PNT, 3) prune_kernel(KParams p, int rcap, int lbmode) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ PruneCtl ctl;
+    const int64_t c = p.c;
+    const int nwords = (int)(c >> 5) + 1;
+    PruneMem m;
+    {
+        unsigned char* q = smem;
+        m.tot = (u64*)q; q += PNW * 32 * 8;
+        m.cw = (long long*)q; q += (size_t)(rcap + 2) * 8;
+        m.rk = (uint2*)q; q += (size_t)(nwords + 1) * 8;
+        m.cn = (int*)q; q += (size_t)(rcap + 2) * 4;
+        m.sw = (int*)q; q += (size_t)rcap * 4;
+        m.vb2 = (int*)q;
+    }
+    const bool phased = p.flags & BPLB_F_PHASED;
+    const bool cancel = (p.flags & BPLB_F_CANCEL) && !phased;
+    const bool lbm = lbmode && !phased;
+    for (int64_t node = p.node0 + blockIdx.x; node < p.node0 + p.n_nodes; node += gridDim.x) {
+        const int64_t base = p.off[node];
+        const int r = (int)(p.off[node + 1] - base);
+        if (threadIdx.x == 0) {
+            NodeStats& st = ctl.st;
+            st.r = r; st.maxw = 0; st.n_small = st.n_eq = st.n_big = st.n_full = 0;
+            st.W = st.Vs = st.Vm = 0;
+            for (int i = 0; i < K_COUNT; ++i) {
+                ctl.key[i] = 0; ctl.evals[i] = 0; ctl.evaluated[i] = 0;
+                ctl.kseg_count[i] = 0; ctl.kseg_first[i] = 0;
+            }
+            ctl.lb = 0; ctl.n_vb2 = 0; ctl.nseg = 0; ctl.nunits = 0; ctl.n_done = 0; ctl.bad = 0;
+        }
+        for (int i = threadIdx.x; i <= nwords; i += PNT) m.rk[i] = make_uint2(0u, 0u);
+        for (int i = threadIdx.x; i < r + 2; i += PNT) { m.cn[i] = 0; m.cw[i] = 0; }
+        for (int i = threadIdx.x; i < r; i += PNT) m.sw[i] = load_w(p, base + i);
+        __syncthreads();
+        // ---- statistics, presence bits, VB2 item list --------------------------
+        {
+            int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
+            long long l_W = 0, l_Vs = 0, l_Vm = 0;
+            for (int i = threadIdx.x; i < r; i += PNT) {
+                const int x = m.sw[i];
+                if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
+                l_max = max(l_max, x);
+                l_W += x;
+                if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
+                else if (2 * (int64_t)x == c) l_e++;
+                else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
+                atomicOr(&m.rk[x >> 5].x, 1u << (x & 31));
+                if (2 * (int64_t)x != c && (int64_t)x < c) m.vb2[atomicAdd(&ctl.n_vb2, 1)] = x;
+            }
+            l_max = __reduce_max_sync(0xffffffffu, (unsigned)l_max);
+            l_bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)l_bad);
+            l_s = __reduce_add_sync(0xffffffffu, l_s);
+            l_e = __reduce_add_sync(0xffffffffu, l_e);
+            l_b = __reduce_add_sync(0xffffffffu, l_b);
+            l_f = __reduce_add_sync(0xffffffffu, l_f);
+            l_W = (long long)warp_sum_u64((u64)l_W);
+            l_Vs = (long long)warp_sum_u64((u64)l_Vs);
+            l_Vm = (long long)warp_sum_u64((u64)l_Vm);
+            if ((threadIdx.x & 31) == 0) {
+                atomicMax(&ctl.st.maxw, l_max);
+                if (l_bad) ctl.bad = 1;
+                atomicAdd(&ctl.st.n_small, l_s);
+                atomicAdd(&ctl.st.n_eq, l_e);
+                atomicAdd(&ctl.st.n_big, l_b);
+                atomicAdd(&ctl.st.n_full, l_f);
+                atomicAdd((unsigned long long*)&ctl.st.W, (unsigned long long)l_W);
+                atomicAdd((unsigned long long*)&ctl.st.Vs, (unsigned long long)l_Vs);
+                atomicAdd((unsigned long long*)&ctl.st.Vm, (unsigned long long)l_Vm);
+            }
+        }
+        __syncthreads();
+        const bool bad = ctl.bad;
+        if (!bad) {
+            // rank prefixes over the presence words (contiguous range per thread)
+            const int per = (nwords + PNT - 1) / PNT;
+            const int b0 = threadIdx.x * per, b1 = min(nwords, b0 + per);
+            long long s = 0;
+            for (int i = b0; i < b1; ++i) s += __popc(m.rk[i].x);
+            long long run = block_excl_scan(s, ctl.wsum);
+            for (int i = b0; i < b1; ++i) {
+                m.rk[i].y = (unsigned)run;
+                run += __popc(m.rk[i].x);
+            }
+            if (threadIdx.x == PNT - 1) ctl.d = (int)run;
+            __syncthreads();
+            // counts / weights per distinct value (index = its 1-based rank)
+            for (int i = threadIdx.x; i < r; i += PNT) {
+                const int x = m.sw[i];
+                const uint2 e = m.rk[x >> 5];
+                const int j = (int)e.y + __popc(e.x & (0xFFFFFFFFu >> (31 - (x & 31))));
+                atomicAdd(&m.cn[j], 1);
+                atomicAdd((unsigned long long*)&m.cw[j], (unsigned long long)x);
+            }
+            __syncthreads();
+            // inclusive scan of cn / cw over [0, d]
+            const int nd = ctl.d + 1;
+            const int pe = (nd + PNT - 1) / PNT;
+            const int e0 = threadIdx.x * pe, e1 = min(nd, e0 + pe);
+            long long sc = 0, sw = 0;
+            for (int i = e0; i < e1; ++i) { sc += m.cn[i]; sw += m.cw[i]; }
+            long long rc = block_excl_scan(sc, ctl.wsum);
+            long long rw = block_excl_scan(sw, ctl.wsum2);
+            for (int i = e0; i < e1; ++i) {
+                rc += m.cn[i];
+                rw += m.cw[i];
+                m.cn[i] = (int)rc;
+                m.cw[i] = rw;
+            }
+        }
+        if (threadIdx.x == 0) {
+            bplb_stats_finish(&ctl.st, c);
+            for (int kd = 0; kd < K_COUNT; ++kd) {
+                int64_t lo, hi;
+                bplb_domain(kd, c, &lo, &hi);
+                if (kd == K_VB2) hi = bplb_vb2_hi(c, r, ctl.st.maxw);
+                if (!kind_in(p, kd)) hi = lo - 1;
+                ctl.lo[kd] = lo; ctl.hi[kd] = hi;
+            }
+            if (!bad) {
+                if (phased) {
+                    for (int i = 0; i < p.nk; ++i) {
+                        const int kd = p.kinds[i];
+                        ctl.kseg_first[kd] = ctl.nunits;
+                        prune_add_kind(ctl, kd, 0, c, r);
+                        prune_add_kind(ctl, kd, 1, c, r);
+                        ctl.kseg_count[kd] = ctl.nunits - ctl.kseg_first[kd];  // units of the kind
+                    }
+                } else {
+                    for (int ph = 0; ph < 2; ++ph)
+                        for (int i = 0; i < p.nk; ++i) prune_add_kind(ctl, p.kinds[i], ph, c, r);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- sweep ---------------------------------------------------------------------
+        LkRank lk{m.rk, m.cn, m.cw, r, ctl.d, c};
+        if (!bad) {
+            if (phased) {
+                for (int i = 0; i < p.nk; ++i) {
+                    const int kd = p.kinds[i];
+                    if (threadIdx.x == 0) {
+                        ctl.unit_next = ctl.kseg_first[kd];
+                        ctl.unit_end = ctl.kseg_first[kd] + ctl.kseg_count[kd];
+                        ctl.n_done = i + 1;
+                    }
+                    __syncthreads();
+                    prune_run(p, ctl, lk, m, false, false);
+                    __syncthreads();
+                    if ((int64_t)ctl.lb > p.k) break;
+                }
+            } else {
+                if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
+                __syncthreads();
+                prune_run(p, ctl, lk, m, lbm, cancel);
+            }
+        }
+        __syncthreads();
+        // ---- outputs (as node_kernel) ----------------------------------------------
+        if (threadIdx.x == 0) {
+            if (bad && p.err_out) atomicExch(p.err_out, 1);
+            int64_t lb = lbm ? (int64_t)ctl.lb : 0;
+            bplb_result res;
+            for (int kd = 0; kd < K_COUNT; ++kd) {
+                const u64 key = ctl.key[kd];
+                const bool ev = ctl.evaluated[kd] && kind_in(p, kd);
+                res.best[kd] = ev ? (int64_t)(key >> 32) : 0;
+                res.arg_lambda[kd] = ev && key ? ctl.lo[kd] + (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu))
+                                               : ctl.lo[kd];
+                res.n_lambda[kd] = ctl.hi[kd] >= ctl.lo[kd] ? ctl.hi[kd] - ctl.lo[kd] + 1 : 0;
+                res.evals[kd] = (int64_t)ctl.evals[kd];
+                res.evaluated[kd] = ev;
+                if (!lbm && ev && res.best[kd] > lb) lb = res.best[kd];
+            }
+            res.lb = lb;
+            res.exceeded = lb > p.k;
+            res.n_done = ctl.n_done;
+            int64_t et = 0;
+            for (int kd = 0; kd < K_COUNT; ++kd) et += res.evals[kd];
+            res.evals_total = et;
+            if (p.res_out) p.res_out[node] = res;
+            if (p.lb_out) p.lb_out[node] = lb;
+            if (p.ex_out) p.ex_out[node] = (uint8_t)(lb > p.k);
+            if (p.best_out)
+                for (int kd = 0; kd < K_COUNT; ++kd) p.best_out[node * K_COUNT + kd] = res.best[kd];
+            if (p.arg_out)
+                for (int kd = 0; kd < K_COUNT; ++kd) p.arg_out[node * K_COUNT + kd] = res.arg_lambda[kd];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace bplb

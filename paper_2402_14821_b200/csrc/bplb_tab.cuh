@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(TAB_HNT) tab_hist_assign_kernel(KParams p, Tab
     const unsigned openv = AB == 1 ? 0xffu : 0xffffu;
     __shared__ int s_bad, s_rerr;
     if (threadIdx.x == 0) { s_bad = 0; s_rerr = 0; }
+    __syncthreads();  // the flags are cleared before any thread may set s_bad
     for (int i = threadIdx.x; i < n_items; i += TAB_HNT) {
         const int x = __ldg(inst_w + i);
         if (x < 1 || x > c) s_bad = 1;

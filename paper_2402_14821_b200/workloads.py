@@ -21,6 +21,8 @@ All workload code is data generation, not the bound path.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 __all__ = ["cfg1", "cfg2_instance", "cfg3", "cfg3u", "cfg4", "node_batch", "l2_host", "CONFIGS"]
@@ -174,3 +176,95 @@ CONFIGS = {
     "cfg4": "large instance: 1e5 items, capacity 1e6, single check",
     "cfg5": "batched search-node sweep of the 1000-item cfg3 instance",
 }
+
+
+# ---------------------------------------------------------------------------
+# Native node generator (csrc/bplb_gen.cu -> libbplb_gen.so): the same
+# search-node definition as above with a splitmix64 stream per node keyed by
+# (seed, node), identical on the host and on the device, fast enough for the
+# 10^6-node batches of cfg5 (the numpy generator above needs minutes).
+# ---------------------------------------------------------------------------
+
+GEN_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbplb_gen.so")
+CFG5_SEED = 5  # node stream of the cfg5 headline batch (native generator)
+_gen = None
+
+
+def _gen_lib():
+    global _gen
+    if _gen is None:
+        import ctypes
+
+        if not os.path.exists(GEN_LIB_PATH):
+            raise RuntimeError(f"{GEN_LIB_PATH} missing: build with paper_2402_14821_b200/build_native.py")
+        lib = ctypes.CDLL(GEN_LIB_PATH)
+        vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        lib.bplbgen_nodes_host.argtypes = [vp, i32, vp, i64, i32, u64, i64, i64, vp, vp, vp, i32]
+        lib.bplbgen_sizes_device.argtypes = [vp, i32, vp, i64, i32, u64, i64, i64, vp, vp]
+        lib.bplbgen_fill_device.argtypes = [vp, i32, vp, i64, i32, u64, i64, i64, vp, vp, vp, vp]
+        for f in (lib.bplbgen_nodes_host, lib.bplbgen_sizes_device, lib.bplbgen_fill_device):
+            f.restype = ctypes.c_int
+        _gen = lib
+    return _gen
+
+
+def heavy_order(w: np.ndarray) -> np.ndarray:
+    """Item indices by weight descending, stable by index (the commit order)."""
+    return np.argsort(-np.asarray(w, dtype=np.int64), kind="stable").astype(np.int32)
+
+
+def gen_nodes_host(w: np.ndarray, c: int, k: int, seed: int, n_nodes: int, first_node: int = 0,
+                   want_assign: bool = False, threads: int | None = None):
+    """CSR (int32 weights, int64 offsets) of native-generator nodes
+    [first_node, first_node + n_nodes); with ``want_assign`` also the bin
+    assignments (uint16, 0xFFFF = open) of the same nodes."""
+    w = np.ascontiguousarray(w, dtype=np.int32)
+    order = heavy_order(w)
+    off = np.zeros(n_nodes + 1, dtype=np.int64)
+    nt = threads or max(1, min(32, os.cpu_count() or 1))
+    lib = _gen_lib()
+    rc = lib.bplbgen_nodes_host(w.ctypes.data, w.size, order.ctypes.data, c, k, seed, first_node, n_nodes,
+                                off.ctypes.data, None, None, nt)
+    if rc:
+        raise ValueError("bad generator arguments")
+    flat = np.empty(max(1, int(off[-1])), dtype=np.int32)
+    asg = np.empty((n_nodes, w.size), dtype=np.uint16) if want_assign else None
+    rc = lib.bplbgen_nodes_host(w.ctypes.data, w.size, order.ctypes.data, c, k, seed, first_node, n_nodes,
+                                off.ctypes.data, flat.ctypes.data, asg.ctypes.data if want_assign else None, nt)
+    if rc:
+        raise ValueError("bad generator arguments")
+    flat = flat[:off[-1]]
+    return (flat, off, asg) if want_assign else (flat, off)
+
+
+def gen_nodes_device(w: np.ndarray, c: int, k: int, seed: int, n_nodes: int, first_node: int = 0,
+                     device=None, want_assign: bool = False):
+    """The same nodes generated on the GPU: torch tensors (weights int32,
+    offsets int64[, assignments uint16 as int16 storage]) on ``device``."""
+    import torch
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    wt = torch.as_tensor(np.ascontiguousarray(w, dtype=np.int32), device=dev)
+    order = torch.as_tensor(heavy_order(w), device=dev)
+    off = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    lib = _gen_lib()
+    with torch.cuda.device(dev):
+        rc = lib.bplbgen_sizes_device(wt.data_ptr(), wt.numel(), order.data_ptr(), c, k, seed, first_node, n_nodes,
+                                      off.data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"bplbgen_sizes_device failed ({rc})")
+        total = int(off[-1].item())
+        flat = torch.empty(max(1, total), dtype=torch.int32, device=dev)
+        asg = torch.empty((n_nodes, wt.numel()), dtype=torch.int16, device=dev) if want_assign else None
+        rc = lib.bplbgen_fill_device(wt.data_ptr(), wt.numel(), order.data_ptr(), c, k, seed, first_node, n_nodes,
+                                     off.data_ptr(), flat.data_ptr(), asg.data_ptr() if want_assign else None, s)
+        if rc:
+            raise RuntimeError(f"bplbgen_fill_device failed ({rc})")
+    return (flat, off, asg) if want_assign else (flat, off)
+
+
+def cfg5_instance():
+    """cfg5: the cfg3 instance (1000 items, c = 1e5) and k = 334 bins."""
+    c, w = cfg3()
+    return c, 334, w

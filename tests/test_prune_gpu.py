@@ -1,0 +1,158 @@
+"""GPU parity of the bound-pruned sweep (csrc/bplb_prune.cuh).
+
+The pruned kernel skips lambdas whose integer upper bound cannot change the
+outputs; every output must still be bit-exact with the reference's full
+sweep.  Checked against the pinned C oracle (oracle/, restating bounds.py) on
+fresh seeded nodes -- including >= 1000 nodes of the cfg5 headline batch --
+and against the dense (every-lambda) GPU kernels for the arg lambdas, in all
+three modes, and the tests assert that the pruned kernel actually served the
+call (bplb_last_path)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2402_14821_b200 import _native, workloads as W
+from paper_2402_14821_b200.batch import lower_bound_batch
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+ALL = list(range(6))
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = _native.Engine(0)
+    yield e
+    e.close()
+
+
+def _oracle_best(flat, off, c, k=2**62):
+    lbo, exo, besto = O.check_batch(flat, off, c, k, want_best=True)
+    return lbo, exo, besto
+
+
+def _rand_batch(rng, c, n, rmax, special=True):
+    nodes = []
+    for _ in range(n):
+        r = int(rng.integers(0, rmax + 1))
+        w = rng.integers(1, c + 1, r)
+        if special and r and rng.random() < 0.3:
+            pick = rng.integers(0, r, max(1, r // 4))
+            w[pick] = rng.choice([c, max(1, c // 2), max(1, (c + 1) // 2), 1], pick.size)
+        nodes.append(w.astype(np.int32))
+    off = np.zeros(n + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(x) for x in nodes])
+    flat = np.concatenate(nodes) if off[-1] else np.zeros(0, np.int32)
+    return flat.astype(np.int32), off
+
+
+def test_cfg5_1000_nodes_lb_mode(eng):
+    """cfg5 (1000-item c=1e5 instance, native generator): 1200 nodes, lb mode."""
+    c, k, w = W.cfg5_instance()
+    flat, off = W.gen_nodes_host(w, c, k, W.CFG5_SEED, 1200)
+    lb, ex = eng.check_batch(flat, off, c, 2**62, ALL, 0)
+    assert eng.last_path() == ("prune", 1)
+    O.set_threads(O.max_threads())
+    lbo, exo = O.check_batch(flat, off, c, 2**62)
+    np.testing.assert_array_equal(lb, lbo)
+    # decision mode k = 334 (lower_bound_seq early exit)
+    lb2, ex2 = eng.check_batch(flat, off, c, k, ALL, _native.F_PHASED)
+    lbo2, exo2 = O.check_batch(flat, off, c, k)
+    np.testing.assert_array_equal(lb2, lbo2)
+    np.testing.assert_array_equal(ex2, exo2)
+
+
+def test_cfg5_key_mode_best_and_arg(eng):
+    """Per-kind best (oracle) and lowest arg lambda (dense GPU sweep) on 200 cfg5 nodes."""
+    c, k, w = W.cfg5_instance()
+    flat, off = W.gen_nodes_host(w, c, k, W.CFG5_SEED, 200, first_node=5000)
+    lb, ex, best, arg = eng.check_batch(flat, off, c, 2**62, ALL, 0, want_best=True)
+    assert eng.last_path() == ("prune", 0)
+    lbo, exo, besto = _oracle_best(flat, off, c)
+    np.testing.assert_array_equal(lb, lbo)
+    np.testing.assert_array_equal(best, besto)
+    lbd, exd, bestd, argd = eng.check_batch(flat, off, c, 2**62, ALL, _native.F_NOPRUNE, want_best=True)
+    assert eng.last_path()[0] != "prune"
+    np.testing.assert_array_equal(bestd, besto)
+    np.testing.assert_array_equal(arg, argd)
+
+
+@pytest.mark.parametrize("c", [2, 3, 4, 5, 7, 8, 31, 150, 151, 289, 500, 1000, 1001, 4095, 65536, 99991,
+                               100000, 262144])
+def test_random_nodes_vs_oracle(eng, c):
+    rng = np.random.default_rng(c)
+    rmax = 300 if c >= 65536 else 600
+    flat, off = _rand_batch(rng, c, 96, rmax)
+    flags_list = [0, _native.F_PHASED, _native.F_CANCEL]
+    lbo, exo, besto = _oracle_best(flat, off, c)
+    # lb mode (full)
+    lb, ex = eng.check_batch(flat, off, c, 2**62, ALL, _native.F_NOTAB)
+    assert eng.last_path()[0] == "prune"
+    np.testing.assert_array_equal(lb, lbo)
+    # key mode (full) vs oracle best and dense arg
+    lb, ex, best, arg = eng.check_batch(flat, off, c, 2**62, ALL, _native.F_NOTAB, want_best=True)
+    np.testing.assert_array_equal(best, besto)
+    _, _, bestd, argd = eng.check_batch(flat, off, c, 2**62, ALL, _native.F_NOTAB | _native.F_NOPRUNE,
+                                        want_best=True)
+    np.testing.assert_array_equal(bestd, besto)
+    np.testing.assert_array_equal(arg, argd)
+    # decision modes at a k inside the bound range
+    kk = int(np.median(lbo)) if len(lbo) else 0
+    lbs, exs = O.check_batch(flat, off, c, kk)
+    for fl in flags_list[1:]:
+        lb, ex = eng.check_batch(flat, off, c, kk, ALL, fl | _native.F_NOTAB)
+        np.testing.assert_array_equal(ex, exs)
+        if fl == _native.F_PHASED:
+            np.testing.assert_array_equal(lb, lbs)
+        else:  # cancel: exact when not exceeded, any computed value > k otherwise
+            np.testing.assert_array_equal(lb[~exs], lbs[~exs])
+            assert np.all(lb[exs] > kk) and np.all(lb[exs] <= lbo[exs])
+
+
+@pytest.mark.parametrize("kinds", [[4], [5, 3], [0, 1], [2], [3, 4, 5], [5, 4, 3, 2, 1, 0]])
+def test_kind_subsets_and_orders(eng, kinds):
+    rng = np.random.default_rng(len(kinds) * 7 + kinds[0])
+    c = 99991
+    flat, off = _rand_batch(rng, c, 64, 400)
+    names = [O.KIND_NAMES[i] for i in kinds]
+    lbo, exo, besto = O.check_batch(flat, off, c, 2**62, kinds=names, want_best=True)
+    lb, ex = eng.check_batch(flat, off, c, 2**62, kinds, 0)
+    np.testing.assert_array_equal(lb, lbo)
+    lb, ex, best, arg = eng.check_batch(flat, off, c, 2**62, kinds, 0, want_best=True)
+    np.testing.assert_array_equal(best[:, kinds], besto)
+    kk = int(np.median(lbo))
+    lbs, exs = O.check_batch(flat, off, c, kk, kinds=names)
+    lb, ex = eng.check_batch(flat, off, c, kk, kinds, _native.F_PHASED)
+    np.testing.assert_array_equal(lb, lbs)
+    np.testing.assert_array_equal(ex, exs)
+
+
+def test_bad_weight_raises(eng):
+    flat = np.array([5, 7, 0, 3], dtype=np.int32)
+    off = np.array([0, 2, 4], dtype=np.int64)
+    with pytest.raises(ValueError):
+        eng.check_batch(flat, off, 1000, 2**62, ALL, 0)
+    flat = np.array([5, 1001], dtype=np.int32)
+    with pytest.raises(ValueError):
+        eng.check_batch(flat, np.array([0, 2], dtype=np.int64), 1000, 2**62, ALL, 0)
+
+
+def test_device_generator_matches_host():
+    import torch
+
+    c, k, w = W.cfg5_instance()
+    flat, off = W.gen_nodes_host(w, c, k, W.CFG5_SEED, 3000, first_node=12345)
+    df, do = W.gen_nodes_device(w, c, k, W.CFG5_SEED, 3000, first_node=12345, device="cuda:0")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(do.cpu().numpy(), off)
+    np.testing.assert_array_equal(df.cpu().numpy()[:off[-1]], flat)
+
+
+def test_lower_bound_batch_dense_flag():
+    c, k, w = W.cfg5_instance()
+    flat, off = W.gen_nodes_host(w, c, k, W.CFG5_SEED, 64, first_node=777)
+    a = lower_bound_batch(c, flat, off, 2**62)
+    b = lower_bound_batch(c, flat, off, 2**62, dense=True)
+    np.testing.assert_array_equal(a[0], b[0])
