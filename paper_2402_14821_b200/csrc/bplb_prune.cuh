@@ -211,6 +211,24 @@ __device__ __forceinline__ bool range_skip(const Thr& t, int kind, const NodeSta
     return t.B >= 1 && ub_le_range(kind, st, c, l1, l2, t.B - 1);
 }
 
+// CCM1 dense sum over an unsorted item array in shared memory (the
+// global-memory ccm1_dense_raw reads through __ldg).
+__device__ __forceinline__ int64_t ccm1_dense_smem(const int* w, int n, const NodeStats& st, int64_t c,
+                                                   int64_t lam) {
+    const int lane = threadIdx.x & 31;
+    const Div31 dv = bplb_div31((uint32_t)lam);
+    const uint32_t c32 = (uint32_t)c;
+    long long a = 0;
+    for (int i = lane; i < n; i += kWarp) {
+        const uint32_t x = (uint32_t)w[i];
+        if (2ull * x < c32) a += bplb_udiv31(x, dv);
+        else if (2ull * x > c32) a -= bplb_udiv31(c32 - x, dv);
+    }
+    const int64_t A = (int64_t)warp_sum_u64((u64)a);
+    const int64_t cq = c / lam;
+    return 2 * A + (int64_t)st.n_eq * cq + 2 * (int64_t)st.n_big * cq;
+}
+
 // ---- segments ------------------------------------------------------------------
 // phase 0: exact seeds (MT / RAD2 candidates, FS1, the first VB2 window, a
 // CCM1 / BJ1 window at c/4+1 where their maxima sit on typical nodes);
@@ -415,7 +433,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
                             const int64_t lj = sub + j;
                             int64_t S;
                             if (kind == K_CCM1) {
-                                if (dense) S = ccm1_dense_raw(m.sw, st.r, st, c, lj);
+                                if (dense) S = ccm1_dense_smem(m.sw, st.r, st, c, lj);
                                 else {
                                     int64_t part = bplb_ccm1_part(lk, st, c, lj, 1 + lane, 32);
                                     part = (int64_t)warp_sum_u64((u64)part);

@@ -18,7 +18,9 @@ lb = torch.empty(n, dtype=torch.int64, device="cuda:0")
 ex = torch.empty(n, dtype=torch.uint8, device="cuda:0")
 best = torch.empty(n * 6, dtype=torch.int64, device="cuda:0")
 arg = torch.empty(n * 6, dtype=torch.int64, device="cuda:0")
-s = torch.cuda.current_stream().cuda_stream
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)  # a real stream handle (the legacy default stream's 0 means "engine stream")
+s = stream.cuda_stream
 
 def run(nn, flags, kk=2**62, want=False):
     eng.check_batch_device(flat.data_ptr(), off.data_ptr(), nn, max_r, c, kk, list(range(6)), flags,
@@ -30,7 +32,7 @@ def timeit(nn, flags, reps=3, **kw):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     for _ in range(reps):
-        e0.record(); run(nn, flags, **kw); e1.record(); torch.cuda.synchronize()
+        e0.record(stream); run(nn, flags, **kw); e1.record(stream); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     return min(ts)
 
