@@ -11,6 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libbplb.so")
 GEN_OUT = os.path.join(HERE, "libbplb_gen.so")  # synthetic node generator (workload data, not the path)
+PEAKS_OUT = os.path.join(HERE, "libbplb_peaks.so")  # measured issue-rate denominators (bench.py only)
 SOURCES = ["bplb_capi.cu"]
 HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_prune.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh", "bplb_reduce.cuh"]
 
@@ -32,8 +33,9 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_gen(force: bool = False) -> str:
-    src = os.path.join(CSRC, "bplb_gen.cu")
+def build_gen(force: bool = False, src_name: str = "bplb_gen.cu", out: str = GEN_OUT) -> str:
+    src = os.path.join(CSRC, src_name)
+    GEN_OUT = out  # noqa: N806
     if not force and os.path.exists(GEN_OUT) and os.path.getmtime(GEN_OUT) > os.path.getmtime(src):
         return GEN_OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -43,13 +45,14 @@ def build_gen(force: bool = False) -> str:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libbplb_gen.so")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(GEN_OUT)}")
     os.replace(GEN_OUT + ".tmp", GEN_OUT)
     return GEN_OUT
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     build_gen(force)
+    build_gen(force, "bplb_peaks.cu", PEAKS_OUT)
     if not force and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,0 +1,121 @@
+// bplb_peaks.cu -- measured issue-rate denominators for the roofline of the
+// integer bound kernels (measurement infrastructure, not the product path;
+// built as libbplb_peaks.so and called by bench.py on the GPU box).
+//
+// The LB-collection kernels are integer-issue bound: their
+// roofline is the rate at which an SM can issue the instruction mix they
+// execute.  MEASURED_PEAKS.json carries HBM and bf16 tensor figures only, so
+// this library measures, on the box, with every SM busy:
+//   alu   : independent integer adds (ptxas splits them between IADD3 on the
+//           ALU pipe and IMAD.IADD on the FMA pipe: an issue-rate probe)
+//   imad  : IMAD integer multiply-adds (FMA pipe on sm_100)
+//   mix   : IADD3 and IMAD interleaved 1:1 -- both pipes, i.e. the warp
+//           scheduler's issue ceiling (1 warp-instruction / clk / SMSP)
+//   ffma  : FP32 FMA (FMA pipe), reported in flop/s
+//   clock : the SM clock during the runs (clock64 cycles / globaltimer ns)
+// Rates are warp-instructions/s (x32 for thread ops) over 148 SMs.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+namespace {
+
+constexpr int kNT = 256;   // 8 warps per CTA
+constexpr int kAcc = 8;    // independent chains per thread
+constexpr int kUnroll = 8; // inner unroll
+
+template <int MODE>
+__global__ void __launch_bounds__(kNT) issue_kernel(uint32_t* sink, int iters, uint32_t seed,
+                                                    unsigned long long* cyc, unsigned long long* ns) {
+    uint32_t a[kAcc];
+    float f[kAcc];
+#pragma unroll
+    for (int i = 0; i < kAcc; ++i) {
+        a[i] = seed * (threadIdx.x + 1) + i;
+        f[i] = (float)(a[i] & 0xff) * 1e-3f;
+    }
+    const uint32_t s1 = seed | 1u, s2 = seed ^ 0x9e3779b9u;
+    const float fm = 1.0000001f, fa = 1e-7f;
+    unsigned long long c0 = clock64(), t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+            for (int i = 0; i < kAcc; ++i) {
+                if (MODE == 0) {  // IADD3 (a variable operand: no constant folding of the chain)
+                    asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(a[(i + 1) % kAcc]));
+                } else if (MODE == 1) {  // IMAD
+                    asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(s1), "r"(s2));
+                } else if (MODE == 2) {  // interleaved ALU / FMA pipe
+                    if (i & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(a[i - 1]), "r"(s2));
+                    else asm volatile("add.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(a[i + 1]));
+                } else {  // FFMA
+                    asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(fm), "f"(fa));
+                }
+            }
+        }
+    }
+    unsigned long long c1 = clock64(), t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < kAcc; ++i) x ^= a[i] ^ __float_as_uint(f[i]);
+    if (x == 0x12345678u) sink[0] = x;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        *cyc = c1 - c0;
+        *ns = t1 - t0;
+    }
+}
+
+template <int MODE>
+int run_one(int sms, int per_sm, int iters, double* rate, double* mhz) {
+    uint32_t* sink;
+    unsigned long long* d;
+    if (cudaMalloc(&sink, 4) != cudaSuccess) return -1;
+    if (cudaMalloc(&d, 16) != cudaSuccess) return -1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = sms * per_sm;
+    issue_kernel<MODE><<<grid, kNT>>>(sink, 16, 7u, d, d + 1);  // warm-up
+    cudaEventRecord(e0);
+    issue_kernel<MODE><<<grid, kNT>>>(sink, iters, 7u, d, d + 1);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long h[2] = {0, 0};
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    const double warp_inst = (double)grid * (kNT / 32) * (double)iters * kUnroll * kAcc;
+    *rate = warp_inst / (ms * 1e-3);
+    *mhz = h[1] ? (double)h[0] / (double)h[1] * 1e3 : 0.0;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    cudaFree(d);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace
+
+extern "C" {
+
+// out[0..3]: warp-instructions/s for alu, imad, mix, ffma; out[4..7]: the SM
+// MHz seen by each run; out[8]: SM count.  Returns 0 on success.
+__attribute__((visibility("default"))) int bplb_measure_issue_peaks(int device, double* out) {
+    if (cudaSetDevice(device) != cudaSuccess) return -1;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int per_sm = 4;  // 32 warps per SM: 8 per scheduler
+    const int iters = 4096;
+    int rc = 0;
+    rc |= run_one<0>(sms, per_sm, iters, &out[0], &out[4]);
+    rc |= run_one<1>(sms, per_sm, iters, &out[1], &out[5]);
+    rc |= run_one<2>(sms, per_sm, iters, &out[2], &out[6]);
+    rc |= run_one<3>(sms, per_sm, iters, &out[3], &out[7]);
+    out[8] = sms;
+    return rc;
+}
+
+}  // extern "C"

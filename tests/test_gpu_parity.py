@@ -251,35 +251,64 @@ def _tab_batch(rng, c, n, max_r):
     return G.csr_from_lists(nodes)
 
 
-@pytest.mark.parametrize("c", [1, 2, 3, 7, 8, 100, 150, 151, 255, 280])
-def test_tab_batch_vs_oracle(oracle, c):
-    """The table kernel (>= 256 nodes, small c) against the oracle in all
-    three modes, with ragged node sizes (r = 0 included) and a partial tile."""
+TAB_ENVELOPE = 1 << 23  # max_r * max f < 2^23 (csrc/bplb_capi.cu tab_path)
+
+
+def _tab_case(oracle, c, max_r, kinds, n=517, seed=None):
+    """One table-path batch against the oracle (all outputs, three modes) and
+    against the warp-per-node kernel (arg lambdas, per-kind best); asserts the
+    table kernel actually served every call (bplb_last_path)."""
     from paper_2402_14821_b200 import _native
 
-    rng = np.random.default_rng(c)
-    max_r = min(500, (1 << 24) // (101 * c))
-    w, off = _tab_batch(rng, c, 517, max_r)
-    lb, ex, best, arg = G.lower_bound_batch(c, w, off, 2**62, want_best=True)
-    lbo, exo, besto = oracle.check_batch(w, off, c, 2**62, want_best=True)
-    np.testing.assert_array_equal(best, besto, err_msg=f"c={c}")
-    np.testing.assert_array_equal(lb, lbo)
-    # same arg-lambdas as the warp-per-node kernel
+    rng = np.random.default_rng(c if seed is None else seed)
+    w, off = _tab_batch(rng, c, n, max_r)
     eng = _native.default_engine()
-    lbw, exw, bestw, argw = eng.check_batch(w, off, c, 2**62, list(range(6)), _native.F_NOTAB, want_best=True)
+    lb, ex, best, arg = eng.check_batch(w, off, c, 2**62, kinds, 0, want_best=True)
+    path = eng.last_path()
+    assert path[0] == "tab" and path[1] >= 2, path
+    lbo, exo, besto = oracle.check_batch(w, off, c, 2**62, want_best=True, kinds=kinds)
+    np.testing.assert_array_equal(best[:, kinds], besto, err_msg=f"c={c}")
+    np.testing.assert_array_equal(lb, lbo)
+    # same arg-lambdas as the dense warp-per-node kernel
+    lbw, exw, bestw, argw = eng.check_batch(w, off, c, 2**62, kinds, _native.F_NOTAB | _native.F_NOPRUNE,
+                                            want_best=True)
+    assert eng.last_path()[0] == "warp"
     np.testing.assert_array_equal(arg, argw)
     np.testing.assert_array_equal(best, bestw)
     kk = int(np.median(lbo))
     for mode, fl in (("seq", _native.F_PHASED), ("cancel", _native.F_CANCEL)):
-        lb2, ex2 = G.lower_bound_batch(c, w, off, kk, mode=mode)
-        lbo2, exo2 = oracle.check_batch(w, off, c, kk)
-        np.testing.assert_array_equal(ex2, exo2)
+        got = eng.check_batch(w, off, c, kk, kinds, fl, want_best=True)
+        assert eng.last_path()[0] == "tab"
+        lbo2, exo2 = oracle.check_batch(w, off, c, kk, kinds=kinds)
+        np.testing.assert_array_equal(got[1], exo2)
         if mode == "seq":
-            np.testing.assert_array_equal(lb2, lbo2)
-        got = eng.check_batch(w, off, c, kk, list(range(6)), fl, want_best=True)
-        ref = eng.check_batch(w, off, c, kk, list(range(6)), fl | _native.F_NOTAB, want_best=True)
+            np.testing.assert_array_equal(got[0], lbo2)
+        # kinds in order with the same guard as the warp kernel: identical outputs
+        ref = eng.check_batch(w, off, c, kk, kinds, fl | _native.F_NOTAB | _native.F_NOPRUNE, want_best=True)
         for a, b in zip(got, ref):
             np.testing.assert_array_equal(a, b)
+    return path
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 7, 8, 100, 150, 151, 200, 255, 280, 288])
+def test_tab_batch_vs_oracle(oracle, c):
+    """The table kernel (>= 256 nodes, small c) against the oracle in all
+    three modes, with ragged node sizes (r = 0 included) and a partial tile,
+    at the fp32 envelope edge (max_r * 101c just below 2^23)."""
+    max_r = min(500, (TAB_ENVELOPE - 1) // (101 * c))
+    _tab_case(oracle, c, max_r, list(range(6)))
+
+
+@pytest.mark.parametrize("c", [200, 255, 288])
+def test_tab_batch_large_c_without_fs1(oracle, c):
+    """Without FS1 (max f = 2c) nodes of 500 items stay inside the envelope:
+    the 4-6-warp contraction CTAs of the largest capacities, with max_r = 500
+    and at the envelope edge."""
+    kinds = [0, 1, 3, 4, 5]
+    widths = set()
+    for max_r in (500, min(65535, (TAB_ENVELOPE - 1) // (2 * c))):
+        widths.add(_tab_case(oracle, c, max_r, kinds, n=300, seed=c + max_r)[1])
+    assert all(2 <= nw <= 6 for nw in widths), widths
 
 
 def test_tab_kind_subsets_and_orders():
@@ -293,7 +322,8 @@ def test_tab_kind_subsets_and_orders():
     for kinds in ([4], [2, 0], [5, 3, 1], [1], [3, 4, 5, 0, 1, 2]):
         for fl in (0, _native.F_PHASED, _native.F_CANCEL):
             got = eng.check_batch(w, off, 150, 190, kinds, fl, want_best=True)
-            ref = eng.check_batch(w, off, 150, 190, kinds, fl | _native.F_NOTAB, want_best=True)
+            ref = eng.check_batch(w, off, 150, 190, kinds, fl | _native.F_NOTAB | _native.F_NOPRUNE,
+                                  want_best=True)
             for a, b in zip(got, ref):
                 np.testing.assert_array_equal(a, b, err_msg=f"{kinds} {fl}")
 

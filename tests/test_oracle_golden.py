@@ -142,3 +142,29 @@ def test_oracle_pins_dffstats_golden(oracle):
         w = np.asarray(x["weights"], dtype=np.int64)
         _, _, best = oracle.check_batch(w, np.array([0, len(w)]), x["c"], 2**62, want_best=True)
         assert {k: int(best[0, i]) for i, k in enumerate(kinds)} == roots, x["name"]
+
+
+def test_oracle_pins_cfg5_reference_golden(oracle):
+    """96 nodes of the cfg5 headline batch (native generator, spread over all
+    10^6 nodes) with the reference's lower_bound_seq outputs
+    (tests/golden/make_golden_cfg5.py): full-mode per-kind maxima and
+    decision-mode (k = 334) lb / exceeded; the committed node weights are the
+    generator's output (regenerated here)."""
+    import os
+
+    from paper_2402_14821_b200 import workloads as W
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_ref.npz"))
+    c, k, w = W.cfg5_instance()
+    assert int(g["c"]) == c and int(g["k"]) == k
+    off = g["offsets"]
+    for j, i in enumerate(g["node_ids"][::8]):
+        f, o = W.gen_nodes_host(w, c, k, W.CFG5_SEED, 1, first_node=int(i))
+        np.testing.assert_array_equal(f, g["weights"][off[8 * j]:off[8 * j + 1]])
+    oracle.set_threads(oracle.max_threads())
+    lb, ex, best = oracle.check_batch(g["weights"], off, c, 2**62, want_best=True)
+    np.testing.assert_array_equal(best, g["best"])
+    np.testing.assert_array_equal(lb, g["lb"])
+    lb, ex = oracle.check_batch(g["weights"], off, c, k)
+    np.testing.assert_array_equal(lb, g["dec_lb"])
+    np.testing.assert_array_equal(ex, g["dec_exceeded"].astype(bool))

@@ -156,3 +156,50 @@ def test_lower_bound_batch_dense_flag():
     a = lower_bound_batch(c, flat, off, 2**62)
     b = lower_bound_batch(c, flat, off, 2**62, dense=True)
     np.testing.assert_array_equal(a[0], b[0])
+
+
+def test_cfg5_reference_golden(eng):
+    """The headline batch's reference outputs (96 nodes across the 10^6-node
+    stream, tests/golden/cfg5_ref.npz, made by the reference itself): the
+    pruned kernel in lb mode, key mode and decision mode (k = 334, the
+    lower_bound_seq early exit), and the dense sweep."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_ref.npz"))
+    c, k = int(g["c"]), int(g["k"])
+    w, off = g["weights"], g["offsets"]
+    lb, ex = eng.check_batch(w, off, c, 2**62, ALL, 0)
+    assert eng.last_path() == ("prune", 1)
+    np.testing.assert_array_equal(lb, g["lb"])
+    lb, ex, best, arg = eng.check_batch(w, off, c, 2**62, ALL, 0, want_best=True)
+    assert eng.last_path() == ("prune", 0)
+    np.testing.assert_array_equal(best, g["best"])
+    lb, ex = eng.check_batch(w, off, c, k, ALL, _native.F_PHASED)
+    assert eng.last_path()[0] == "prune"
+    np.testing.assert_array_equal(lb, g["dec_lb"])
+    np.testing.assert_array_equal(ex, g["dec_exceeded"].astype(bool))
+    lb, ex, best, arg = eng.check_batch(w, off, c, 2**62, ALL, _native.F_NOPRUNE, want_best=True)
+    np.testing.assert_array_equal(best, g["best"])
+
+
+def test_cfg5_device_batch_matches_golden_nodes(eng):
+    """The bench's device-resident path: nodes generated on the GPU at the
+    golden node ids, checked by bplb_check_batch_device, equal the
+    reference's outputs."""
+    import os
+
+    import torch
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg5_ref.npz"))
+    c, k, w = W.cfg5_instance()
+    ids = g["node_ids"]
+    s = torch.cuda.Stream()
+    for j in (0, 50, 95):
+        df, do = W.gen_nodes_device(w, c, k, W.CFG5_SEED, 1, first_node=int(ids[j]), device="cuda:0")
+        lb = torch.empty(1, dtype=torch.int64, device="cuda:0")
+        ex = torch.empty(1, dtype=torch.uint8, device="cuda:0")
+        torch.cuda.synchronize()
+        eng.check_batch_device(df.data_ptr(), do.data_ptr(), 1, int(do[1] - do[0]), c, 2**62, ALL, 0,
+                               lb.data_ptr(), ex.data_ptr(), stream_ptr=s.cuda_stream)
+        s.synchronize()
+        assert int(lb[0]) == int(g["lb"][j])
