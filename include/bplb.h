@@ -156,6 +156,28 @@ BPLB_API int bplb_reduce_batch(bplb_engine *eng, const int32_t *inst_w, int64_t 
                       int64_t n_bins, const void *assign, int32_t abytes, int64_t n_nodes,
                       int64_t c, int64_t *offsets_out, int32_t *weights_out);
 
+/* Multi-GPU batched checks in one call.
+ * bplb_multi_create makes one engine per entry of devices[ndev] (an id may
+ * repeat: several engines on one GPU).  bplb_check_batch_multi shards the
+ * nodes of a host CSR batch into contiguous ranges balanced by item count,
+ * checks each range on its own engine / device from its own host thread
+ * (upload, kernel and verdicts per shard, concurrently), and writes every
+ * shard's outputs into the caller's arrays at the shard's node offset (the
+ * gather).  Arguments, outputs and errors as bplb_check_batch_ex; the first
+ * failing shard's error is returned.  bplb_multi_last_bounds writes the last
+ * call's node boundaries (ndev + 1 values); bplb_multi_engine exposes an
+ * engine (measurement hooks).  No reference counterpart: the reference runs
+ * one node per call on one host (propagator.py:274-276, parallel.py:84-119). */
+typedef struct bplb_multi bplb_multi;
+BPLB_API int bplb_multi_create(const int32_t *devices, int32_t ndev, bplb_multi **out);
+BPLB_API int bplb_multi_destroy(bplb_multi *m);
+BPLB_API int bplb_multi_engine(bplb_multi *m, int32_t i, bplb_engine **out);
+BPLB_API int bplb_multi_last_bounds(bplb_multi *m, int64_t *bounds_out);
+BPLB_API int bplb_check_batch_multi(bplb_multi *m, const void *w_concat, int32_t wbytes,
+                           const int64_t *offsets, int64_t n_nodes, int64_t c, int64_t k,
+                           const int32_t *kinds, int32_t nkinds, int32_t flags, int64_t *lb_out,
+                           uint8_t *exceeded_out, int64_t *best_out, int64_t *arg_out);
+
 /* Number of kernel launches issued by the engine since creation (for the
  * bench's gpu_launches claim), and device time of the last TIMING call. */
 BPLB_API int64_t bplb_launch_count(bplb_engine *eng);

@@ -22,7 +22,7 @@ from .bounds import (
 )
 from .instances import ArrayReducedInstance, ReducedInstance, reduce_packing_arrays
 from .parallel import GpuBoundEngine, ParallelBoundEngine, SharedMax, default_workers, lower_bound_par
-from .batch import (csr_from_lists, lower_bound_batch, lower_bound_batch_assign, open_marker,
+from .batch import (csr_from_lists, lower_bound_batch, lower_bound_batch_assign, lower_bound_batch_multi, open_marker,
                     reduce_packing_batch)
 
 __version__ = "0.1.0"
@@ -51,6 +51,7 @@ __all__ = [
     "lambda_range",
     "lower_bound_batch",
     "lower_bound_batch_assign",
+    "lower_bound_batch_multi",
     "open_marker",
     "reduce_packing_batch",
     "lower_bound_par",

@@ -79,6 +79,13 @@ SIGNATURES = {
                                                ctypes.c_int32, ctypes.c_int32, _i64p, _u8p, _i64p, _i64p]),
     "bplb_reduce_batch": (ctypes.c_int, [_vp, _i32p, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
                                          ctypes.c_int64, ctypes.c_int64, _i64p, _i32p]),
+    "bplb_multi_create": (ctypes.c_int, [_i32p, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    "bplb_multi_destroy": (ctypes.c_int, [_vp]),
+    "bplb_multi_engine": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    "bplb_multi_last_bounds": (ctypes.c_int, [_vp, _i64p]),
+    "bplb_check_batch_multi": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
+                                              ctypes.c_int32, _vp, _vp, _vp, _vp]),
     "bplb_launch_count": (ctypes.c_int64, [_vp]),
     "bplb_last_device_ms": (ctypes.c_double, [_vp]),
     "bplb_profile_kernel": (ctypes.c_int, [_vp, ctypes.c_int]),
@@ -325,6 +332,76 @@ class Engine:
             flags, lb_ptr, ex_ptr, best_ptr or None, arg_ptr or None, stream_ptr or None)
         if rc != 0:
             _raise(rc, "bplb_check_batch_device")
+
+
+class MultiEngine:
+    """Several engines behind one call (``bplb_multi``): a host CSR batch is
+    sharded over ``devices`` (contiguous node ranges balanced by item count,
+    one host thread per shard) and the verdicts land in one output array."""
+
+    def __init__(self, devices):
+        self._lib = load_library()
+        self.devices = [int(d) for d in devices]
+        arr = (ctypes.c_int32 * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        rc = self._lib.bplb_multi_create(arr, len(self.devices), ctypes.byref(h))
+        if rc != 0:
+            _raise(rc, "bplb_multi_create")
+        self._h = h
+        self._kinds_cache: dict = {}
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.bplb_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_bounds(self) -> np.ndarray:
+        b = np.empty(len(self.devices) + 1, dtype=np.int64)
+        rc = self._lib.bplb_multi_last_bounds(self._h, b.ctypes.data_as(_i64p))
+        if rc != 0:
+            _raise(rc, "bplb_multi_last_bounds")
+        return b
+
+    def launch_count(self) -> int:
+        total = 0
+        for i in range(len(self.devices)):
+            e = ctypes.c_void_p()
+            if self._lib.bplb_multi_engine(self._h, i, ctypes.byref(e)) == 0:
+                total += int(self._lib.bplb_launch_count(e))
+        return total
+
+    def check_batch(self, w: np.ndarray, offsets: np.ndarray, c: int, k: int, kinds, flags: int,
+                    want_best: bool = False):
+        if isinstance(w, np.ndarray) and w.dtype in (np.uint16, np.uint8) and w.flags.c_contiguous:
+            wbytes = w.itemsize
+        else:
+            w = as_i32(w)
+            wbytes = 4
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        n = len(off) - 1
+        key = tuple(kinds)
+        ks = self._kinds_cache.get(key)
+        if ks is None:
+            ks = self._kinds_cache[key] = (ctypes.c_int32 * len(key))(*key)
+        lb = np.empty(n, dtype=np.int64)
+        ex = np.empty(n, dtype=np.uint8)
+        best = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        arg = np.empty((n, NKINDS), dtype=np.int64) if want_best else None
+        rc = self._lib.bplb_check_batch_multi(
+            self._h, _addr(w) if w.size else None, wbytes, _addr(off), n, int(c), _clamp_k(k),
+            _addressof(ks), len(key), int(flags), _addr(lb), _addr(ex),
+            _addr(best) if best is not None else None, _addr(arg) if arg is not None else None)
+        if rc != 0:
+            _raise(rc, "bplb_check_batch_multi")
+        if want_best:
+            return lb, ex.view(bool), best, arg
+        return lb, ex.view(bool)
 
 
 _engines: dict[int, Engine] = {}

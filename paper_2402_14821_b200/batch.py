@@ -16,7 +16,7 @@ import numpy as np
 from . import _native
 from .bounds import DEFAULT_DFF_ORDER, kind_ids
 
-__all__ = ["lower_bound_batch", "csr_from_lists"]
+__all__ = ["lower_bound_batch", "lower_bound_batch_multi", "csr_from_lists"]
 
 
 def csr_from_lists(nodes: Sequence[Sequence[int]]) -> tuple[np.ndarray, np.ndarray]:
@@ -54,6 +54,30 @@ def lower_bound_batch(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
         flags |= _native.F_NOPRUNE
     eng = engine or _native.default_engine()
     return eng.check_batch(weights, offsets, c, k, kind_ids(kinds), flags, want_best=want_best)
+
+
+def lower_bound_batch_multi(c: int, weights: np.ndarray, offsets: np.ndarray, k: int,
+                            kinds: Sequence = DEFAULT_DFF_ORDER, *, devices: Sequence[int] | None = None,
+                            mode: str = "full", want_best: bool = False, dense: bool = False,
+                            engine: "_native.MultiEngine | None" = None):
+    """:func:`lower_bound_batch` over several GPUs in ONE call from one
+    process (``bplb_check_batch_multi``): the nodes are sharded over
+    ``devices`` (default: every visible GPU) in contiguous ranges balanced by
+    item count, checked concurrently, and returned in node order."""
+    flags = {"full": 0, "seq": _native.F_PHASED, "cancel": _native.F_CANCEL}[mode]
+    if dense:
+        flags |= _native.F_NOPRUNE
+    if engine is None:
+        if devices is None:
+            import torch
+
+            devices = list(range(max(1, torch.cuda.device_count())))
+        engine = _native.MultiEngine(devices)
+        try:
+            return engine.check_batch(weights, offsets, c, k, kind_ids(kinds), flags, want_best=want_best)
+        finally:
+            engine.close()
+    return engine.check_batch(weights, offsets, c, k, kind_ids(kinds), flags, want_best=want_best)
 
 
 def open_marker(dtype) -> int:

@@ -18,6 +18,7 @@
 #include "bplb_warp.cuh"
 #include "bplb_tab.cuh"
 #include "bplb_reduce.cuh"
+#include <thread>
 #include <vector>
 
 namespace {
@@ -1452,6 +1453,104 @@ int bplb_check_batch(bplb_engine* e, const int32_t* w, const int64_t* off, int64
                      int64_t* lb_out, uint8_t* ex_out, int64_t* best_out, int64_t* arg_out) {
     return bplb_check_batch_ex(e, w, 4, off, n_nodes, c, k, kinds, nkinds, flags, lb_out, ex_out,
                                best_out, arg_out);
+}
+
+
+// ---- multi-GPU batched checks (one call, several devices) ------------------
+// the batched path shards over the GPUs of one box.
+// The nodes of a host CSR batch are split into contiguous ranges balanced
+// by item count, each range checked by its own engine on its own host
+// thread (bplb_check_batch_ex: upload, kernel, verdicts); the gather is the
+// per-shard write of lb / exceeded / best / arg into the caller's arrays.
+struct bplb_multi {
+    std::vector<bplb_engine*> engines;
+    std::vector<int64_t> bounds;  // node boundaries of the last call (size engines + 1)
+    std::mutex mu;
+};
+
+int bplb_multi_create(const int32_t* devices, int32_t ndev, bplb_multi** out) {
+    if (!out || !devices || ndev < 1 || ndev > 64) return fail(BPLB_EINVAL, "bad device list");
+    *out = nullptr;
+    bplb_multi* m = new bplb_multi();
+    for (int32_t i = 0; i < ndev; ++i) {
+        bplb_engine* e = nullptr;
+        int rc = bplb_engine_create(devices[i], &e);
+        if (rc) {
+            std::string msg = g_err;
+            bplb_multi_destroy(m);
+            return fail(rc, msg);
+        }
+        m->engines.push_back(e);
+    }
+    m->bounds.assign((size_t)ndev + 1, 0);
+    *out = m;
+    return 0;
+}
+
+int bplb_multi_destroy(bplb_multi* m) {
+    if (!m) return 0;
+    for (bplb_engine* e : m->engines) bplb_engine_destroy(e);
+    delete m;
+    return 0;
+}
+
+int bplb_multi_engine(bplb_multi* m, int32_t i, bplb_engine** out) {
+    if (!m || !out || i < 0 || i >= (int32_t)m->engines.size()) return fail(BPLB_EINVAL, "bad engine index");
+    *out = m->engines[(size_t)i];
+    return 0;
+}
+
+int bplb_multi_last_bounds(bplb_multi* m, int64_t* bounds_out) {
+    if (!m || !bounds_out) return fail(BPLB_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lock(m->mu);
+    std::memcpy(bounds_out, m->bounds.data(), m->bounds.size() * 8);
+    return 0;
+}
+
+int bplb_check_batch_multi(bplb_multi* m, const void* w, int32_t wbytes, const int64_t* off,
+                           int64_t n_nodes, int64_t c, int64_t k, const int32_t* kinds, int32_t nkinds,
+                           int32_t flags, int64_t* lb_out, uint8_t* ex_out, int64_t* best_out,
+                           int64_t* arg_out) {
+    if (!m) return fail(BPLB_EINVAL, "null multi-engine");
+    if (wbytes != 4 && wbytes != 2 && wbytes != 1) return fail(BPLB_EINVAL, "wbytes must be 4, 2 or 1");
+    if (n_nodes < 0 || (n_nodes > 0 && (!off || !lb_out || !ex_out))) return fail(BPLB_EINVAL, "bad batch arguments");
+    if (n_nodes == 0) return 0;
+    if (off[0] != 0) return fail(BPLB_EINVAL, "offsets[0] must be 0");
+    std::lock_guard<std::mutex> lock(m->mu);
+    const int G = (int)m->engines.size();
+    const int64_t total = off[n_nodes];
+    // contiguous node ranges with ~total/G items each (at least one node each
+    // while nodes last): boundary g = first node whose offset reaches g*total/G
+    std::vector<int64_t>& b = m->bounds;
+    b.assign((size_t)G + 1, 0);
+    b[(size_t)G] = n_nodes;
+    for (int g = 1; g < G; ++g) {
+        const int64_t target = total / G * g + std::min<int64_t>(g, total % G);
+        int64_t x = std::lower_bound(off, off + n_nodes + 1, target) - off;
+        if (total == 0) x = n_nodes * g / G;
+        x = std::max(x, b[(size_t)g - 1]);
+        b[(size_t)g] = std::min(x, n_nodes);
+    }
+    std::vector<int> rcs((size_t)G, 0);
+    std::vector<std::string> errs((size_t)G);
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g) {
+        const int64_t lo = b[(size_t)g], hi = b[(size_t)g + 1];
+        if (hi <= lo) continue;
+        th.emplace_back([&, g, lo, hi]() {
+            std::vector<int64_t> so((size_t)(hi - lo + 1));
+            for (int64_t i = lo; i <= hi; ++i) so[(size_t)(i - lo)] = off[i] - off[lo];
+            rcs[(size_t)g] = bplb_check_batch_ex(
+                m->engines[(size_t)g], (const char*)w + off[lo] * wbytes, wbytes, so.data(), hi - lo, c, k, kinds,
+                nkinds, flags, lb_out + lo, ex_out + lo, best_out ? best_out + lo * K_COUNT : nullptr,
+                arg_out ? arg_out + lo * K_COUNT : nullptr);
+            if (rcs[(size_t)g]) errs[(size_t)g] = g_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G; ++g)
+        if (rcs[(size_t)g]) return fail(rcs[(size_t)g], "shard " + std::to_string(g) + ": " + errs[(size_t)g]);
+    return 0;
 }
 
 }  // extern "C"

@@ -14,8 +14,10 @@
 
 from __future__ import annotations
 
+import dataclasses
+import enum
 from collections import defaultdict
-from typing import Sequence
+from typing import Callable, Sequence
 
 import numpy as np
 
@@ -37,6 +39,64 @@ def make_gpu_bound_engine(cfg=None, *, kinds: Sequence = DEFAULT_DFF_ORDER, devi
         kinds = cfg.dff_order
     eng = GpuBoundEngine(kinds=kinds, device=device, mode=mode)
     return eng, eng.close
+
+
+class BoundModeGPU(enum.Enum):
+    """The reference's ``BoundMode`` (search.py:44-55) plus ``DFFS_GPU``;
+    ``from_name`` parses like the reference's (case-insensitive value)."""
+
+    L2 = "l2"
+    DFFS_SEQ = "dffs-seq"
+    DFFS_PAR = "dffs-par"
+    DFFS_GPU = DFFS_GPU
+
+    @classmethod
+    def from_name(cls, name: str) -> "BoundModeGPU":
+        for mode in cls:
+            if mode.value == name.strip().lower():
+                return mode
+        valid = ", ".join(m.value for m in cls)
+        raise ValueError(f"unknown bound mode {name!r} (expected one of {valid})")
+
+
+def install_dffs_gpu(search, cli=None, *, device: int | None = None,
+                     factory: Callable | None = None) -> Callable[[], None]:
+    """Plug ``dffs-gpu`` into the reference solver without editing it.
+
+    ``search`` / ``cli`` are the reference's ``binpack.search`` /
+    ``binpack.cli`` modules.  ``search.make_bound_engine`` (search.py:127-141)
+    is wrapped: a config whose ``bound_mode`` value is ``"dffs-gpu"`` gets
+    ``make_gpu_bound_engine(cfg)`` (``lower_bound_seq`` semantics, so the
+    search explores exactly the nodes of ``dffs-seq``); every other mode is
+    mapped back to the reference's own enum member and served by the
+    original factory.  With ``cli``, its ``BoundMode`` becomes
+    :class:`BoundModeGPU` so ``--bound dffs-gpu`` parses (cli.py:127-134,
+    143-155).  ``factory`` replaces the GPU factory (tests inject the
+    oracle).  Returns a callable that undoes the patch.
+    """
+    orig = search.make_bound_engine
+    ref_mode = search.BoundMode
+    make = factory or (lambda cfg: make_gpu_bound_engine(cfg, device=device))
+
+    def make_bound_engine(cfg):
+        value = getattr(cfg.bound_mode, "value", cfg.bound_mode)
+        if value == DFFS_GPU:
+            return make(cfg)
+        if not isinstance(cfg.bound_mode, ref_mode):
+            cfg = dataclasses.replace(cfg, bound_mode=ref_mode(value))
+        return orig(cfg)
+
+    search.make_bound_engine = make_bound_engine
+    cli_mode = getattr(cli, "BoundMode", None) if cli is not None else None
+    if cli is not None:
+        cli.BoundMode = BoundModeGPU
+
+    def uninstall() -> None:
+        search.make_bound_engine = orig
+        if cli is not None:
+            cli.BoundMode = cli_mode
+
+    return uninstall
 
 
 def _instance_parts(inst):

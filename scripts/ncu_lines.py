@@ -4,7 +4,7 @@ ncu's CSV source export carries no per-line metrics here, so this joins the
 per-instruction SASS page (exec counts, warp-state samples) with nvdisasm's
 line table of the SAME build (-lineinfo):
 
-    python scripts/ncu_lines.py gpurun_out/prof.ncu-rep <kernel-regex> [libbplb.so] [mangled-substring]
+    python scripts/ncu_lines.py gpurun_out/prof.ncu-rep <kernel-regex> [libbplb.so] [mangled-substring] [frame-file]
 
 Only valid when the report was captured from the library passed in.
 """
@@ -30,35 +30,48 @@ def sass_rows(rep, kernel_sub=""):
     return [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr) and r != hdr]
 
 
-def line_table(lib, kernel_sub):
+def line_table(lib, kernel_sub, frame_file=None):
+    """SASS offset -> (file, line).  nvdisasm prints an instruction's inline
+    chain innermost first; by default the OUTERMOST frame is used (the line in
+    the kernel body), with ``frame_file`` the innermost frame in that file
+    (e.g. bplb_prune.cuh: lines inside the inlined device functions)."""
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
     cub = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")][0]
     dis = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
     table = {}
     func = None
-    cur = None
+    chain, cur, fresh = [], None, True
     for line in dis.splitlines():
         m = re.match(r"\s*\.text\.(\S+):", line)
         if m:
             func = m.group(1)
             continue
-        m = re.search(r'//## File "([^"]+)", line (\d+)(?:.*inlined at "([^"]+)", line (\d+))?', line)
+        m = re.search(r'//## File "([^"]+)", line (\d+)', line)
         if m:
-            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            if fresh:
+                chain, fresh = [], False
+            chain.append((os.path.basename(m.group(1)), int(m.group(2))))
+            cur = chain[-1]
+            if frame_file:
+                inner = [fr for fr in chain if fr[0] == frame_file]
+                if inner:
+                    cur = inner[0]
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", line)
-        if m and func and kernel_sub in func:
-            table[int(m.group(1), 16)] = cur
+        if m:
+            fresh = True
+            if func and kernel_sub in func:
+                table[int(m.group(1), 16)] = cur
     return table
 
 
-def main(rep, kernel_sub, lib="paper_2402_14821_b200/libbplb.so", mangled=None):
+def main(rep, kernel_sub, lib="paper_2402_14821_b200/libbplb.so", mangled=None, frame_file=None):
     """kernel_sub filters the ncu report (demangled name regex); mangled (or
     kernel_sub) selects the function in the library's line table."""
     rows = sass_rows(rep, kernel_sub)
     base = int(rows[0]["Address"], 16)
-    table = line_table(lib, mangled or kernel_sub)
+    table = line_table(lib, mangled or kernel_sub, frame_file)
     S, I = "Warp Stall Sampling (All Samples)", "Instructions Executed"
     agg_s, agg_i = collections.Counter(), collections.Counter()
     reasons = collections.defaultdict(collections.Counter)
