@@ -48,9 +48,11 @@ constexpr int PNT = 256;
 constexpr int PNW = PNT / 32;
 constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in smem
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
+constexpr int PR_QMAX = 32;            // block bounds for CCM1 / BJ1 where floor(c / lambda) <= PR_QMAX
+constexpr int PR_BLK_UNIT = 32 * 256;  // lambdas per block unit: 32 blocks of 256, one per lane
 constexpr int PR_MAX_SEGS = 20;
 
-enum { PU_CAND = 0, PU_LOOK = 1, PU_WALK = 2, PU_PRUNE = 3 };
+enum { PU_CAND = 0, PU_LOOK = 1, PU_WALK = 2, PU_PRUNE = 3, PU_BLK = 4 };
 
 struct LkRank {
     const uint2* rk;        // [c/32 + 1]: {presence mask of 32i..32i+31, #distinct values < 32i}
@@ -171,6 +173,92 @@ __device__ __forceinline__ bool ub_le_range(int kind, const NodeStats& st, int64
     return c - l2 + 1 > 0 && st.W <= B * (c - l2 + 1);
 }
 
+// ---- block upper bounds (true => bound(l) <= B for EVERY l in [l1, l2]) -------
+// The per-lambda relaxations above drop each floor separately; over a block of
+// lambdas the exact step functions can be bounded by evaluating them at the
+// block ends instead (the same O(1)-lookup sums as the exact sweep), which is
+// tight wherever no item crosses a step inside the block.
+//
+// CCM1 (bounds.py:181-186, 390-407): S(l) = 2 Sm(l) + K floor(c/l) - 2 Bg(l),
+// Sm(l) = sum over small w of floor(w/l) and Bg(l) = sum over mirrored
+// v = c - w of floor(v/l) are non-increasing in l, F(l) = 2 floor(c/l) > 0, so
+// on [l1, l2]:  S(l) <= 2 Sm(l1) + K floor(c/l1) - 2 Bg(l2),  F(l) >= 2 floor(c/l2).
+__device__ __forceinline__ bool ccm1_blk_le(const LkRank& lk, const NodeStats& st, int64_t c, int64_t l1,
+                                            int64_t l2, int64_t B) {
+    const int hs = (int)((c - 1) / 2);
+    const int L1 = (int)l1, L2 = (int)l2;
+    int sm = 0, bg = 0;
+    const int nbase = st.r - st.n_big;  // #{w : 2w <= c}
+    for (int x = L1; x <= hs; x += L1) sm += st.n_small - (int)lk.n_le(x - 1);
+    for (int x = L2; x <= hs; x += L2) bg += (int)lk.n_le(c - x) - nbase;
+    const int64_t K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
+    const int64_t q1 = (int64_t)((uint32_t)c / (uint32_t)L1), q2 = (int64_t)((uint32_t)c / (uint32_t)L2);
+    return 2 * (int64_t)sm + K * q1 - 2 * (int64_t)bg <= B * 2 * q2;
+}
+
+// sum over items w in [lo, hi] with w > T of (w - T)
+__device__ __forceinline__ int64_t lk_excess(const LkRank& lk, int64_t lo, int64_t hi, int64_t T) {
+    if (lo < T + 1) lo = T + 1;
+    if (hi < lo) return 0;
+    int64_t n1, w1, n0, w0;
+    lk.both(hi, &n1, &w1);
+    lk.both(lo - 1, &n0, &w0);
+    return (w1 - w0) - T * (n1 - n0);
+}
+
+// BJ1 (bounds.py:200-206, 441-460) on [l1, l2] inside one q-interval
+// (floor(c/l) = q for every l): with cm = c - q l and P(l) = l - cm =
+// (q+1) l - c > 0, f(c) = q P and every item contributes
+//   f(w)/f(c) = (a + theta)/q,  a = floor(w/l),
+//   theta = max(0, w - a l - cm) / P = max(0, w - c + (q - a) l) / ((q+1) l - c) in [0, 1).
+// An item whose a is constant on the block (w in [t l2, (t+1) l1 - 1]) has a
+// linear-fractional theta, monotone in l: increasing iff w < c (t+1)/(q+1),
+// so its maximum sits at l2 (below the pivot) or l1 (above).  An item that
+// crosses a step (w in [t l1, t l2 - 1]) contributes < t + 1.  Summing
+// (W / N lookups per bucket):  sum f(w)/f(c) <= (I + X2/P(l2) + X1/P(l1)) / q.
+// Integer envelope (c <= 2^18, r <= 2^14, q <= PR_QMAX): every product < 2^60.
+__device__ __forceinline__ bool bj1_blk_q_le(const LkRank& lk, const NodeStats& st, int64_t c, int64_t q,
+                                             int64_t l1, int64_t l2, int64_t B) {
+    const int64_t P1 = (q + 1) * l1 - c, P2 = (q + 1) * l2 - c;
+    int64_t I = 0, X1 = 0, X2 = 0;
+    const int tmax = (int)((uint32_t)st.maxw / (uint32_t)l1);
+    for (int t = 0; t <= tmax; ++t) {
+        const int64_t lo = (int64_t)t * l2, hi = (int64_t)(t + 1) * l1 - 1;
+        if (hi >= lo) {
+            int64_t nh, wh, nl, wl;
+            lk.both(hi, &nh, &wh);
+            lk.both(lo - 1, &nl, &wl);
+            I += (int64_t)t * (nh - nl);
+            if (t < q) {
+                const int64_t pv = (int64_t)(((uint32_t)c * (uint32_t)(t + 1) + (uint32_t)q) / (uint32_t)(q + 1));
+                X2 += lk_excess(lk, lo, min(hi, pv - 1), c - (q - t) * l2);
+                X1 += lk_excess(lk, max(lo, pv), hi, c - (q - t) * l1);
+            }
+        }
+        if (t >= 1 && l2 > l1) I += (int64_t)(t + 1) * (lk.n_le((int64_t)t * l2 - 1) - lk.n_le((int64_t)t * l1 - 1));
+    }
+    return I * P1 * P2 + X2 * P1 + X1 * P2 <= B * q * P1 * P2;
+}
+
+// BJ1 on any [l1, l2]: split at the q-interval ends (at most 8 pieces).
+__device__ __forceinline__ bool bj1_blk_le(const LkRank& lk, const NodeStats& st, int64_t c, int64_t l1,
+                                           int64_t l2, int64_t B) {
+    int64_t a = l1;
+    for (int piece = 0; piece < 8 && a <= l2; ++piece) {
+        const int64_t q = (int64_t)((uint32_t)c / (uint32_t)a);
+        const int64_t e = min(l2, (int64_t)((uint32_t)c / (uint32_t)q));
+        if (!bj1_blk_q_le(lk, st, c, q, a, e, B)) return false;
+        a = e + 1;
+    }
+    return a > l2;
+}
+
+__device__ __forceinline__ bool blk_ub_le(int kind, const LkRank& lk, const NodeStats& st, int64_t c, int64_t l1,
+                                          int64_t l2, int64_t B) {
+    if (B < 0) return false;
+    return kind == K_CCM1 ? ccm1_blk_le(lk, st, c, l1, l2, B) : bj1_blk_le(lk, st, c, l1, l2, B);
+}
+
 // Pruning threshold snapshot (the shared best only grows, so a stale one is safe).
 struct Thr {
     int64_t B, a_rel;
@@ -209,6 +297,14 @@ __device__ __forceinline__ bool range_skip(const Thr& t, int kind, const NodeSta
     if (t.lbmode) return ub_le_range(kind, st, c, l1, l2, t.B);
     if (l1 - lo > t.a_rel) return ub_le_range(kind, st, c, l1, l2, t.B);
     return t.B >= 1 && ub_le_range(kind, st, c, l1, l2, t.B - 1);
+}
+
+__device__ __forceinline__ bool blk_skip(const Thr& t, int kind, const LkRank& lk, const NodeStats& st, int64_t c,
+                                         int64_t lo, int64_t l1, int64_t l2) {
+    if (!t.has) return false;
+    if (t.lbmode) return blk_ub_le(kind, lk, st, c, l1, l2, t.B);
+    if (l1 - lo > t.a_rel) return blk_ub_le(kind, lk, st, c, l1, l2, t.B);
+    return t.B >= 1 && blk_ub_le(kind, lk, st, c, l1, l2, t.B - 1);
 }
 
 // CCM1 dense sum over an unsorted item array in shared memory (the
@@ -274,11 +370,70 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
         const int64_t s1 = min(hi, s0 + 31);
         if (phase == 0) pushr(PU_LOOK, s0, s1, 32);
         else {
-            pushr(PU_PRUNE, s1 + 1, hi, PR_SUPER);
-            pushr(PU_PRUNE, lo, s0 - 1, PR_SUPER);
+            // block bounds where floor(c / l) <= PR_QMAX (l >= bl), per-lambda
+            // relaxations below (tight there: the dropped floors are small
+            // against c / l)
+            const int64_t bl = max(lo, c / (PR_QMAX + 1) + 1);
+            auto region = [&](int64_t a, int64_t b) {  // [a, b] outside the seed window
+                if (b < a) return;
+                if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), PR_SUPER);
+                if (b >= bl) pushr(PU_BLK, max(a, bl), b, PR_BLK_UNIT);
+            };
+            region(s1 + 1, hi);
+            region(lo, s0 - 1);
         }
     }
     }
+}
+
+// ---- block unit: CCM1 / BJ1 over up to 32 x 256 lambdas --------------------------
+// level 1: lane j bounds the 256-lambda block j; level 2: every surviving
+// block is re-bounded as 32 sub-blocks of 8 lambdas (one per lane); level 3:
+// the lambdas of surviving sub-blocks (4 sub-blocks per warp pass) get the
+// per-lambda relaxation and, if still live, the exact sum (harmonic lookups,
+// bounds.py:390-407 / 441-460).  Returns the best bound the warp evaluated.
+template <class LK>
+__device__ int64_t blk_unit(const KParams& p, PruneCtl& ctl, const LK& lk, int kind, int64_t lam_a, int64_t lam_b,
+                            bool lbmode, u64* key) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = p.c, lo_k = ctl.lo[kind];
+    const NodeStats& st = ctl.st;
+    int64_t wmax = -1;
+    const int64_t s1 = lam_a + 256 * (int64_t)lane;
+    bool live = s1 <= lam_b;
+    if (live) live = !blk_skip(read_thr(ctl, kind, lbmode), kind, lk, st, c, lo_k, s1, min(lam_b, s1 + 255));
+    unsigned m1 = __ballot_sync(0xffffffffu, live);
+    while (m1) {
+        const int j = __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        const int64_t base = lam_a + 256 * (int64_t)j;
+        const int64_t top = min(lam_b, base + 255);
+        const int64_t s2 = base + 8 * (int64_t)lane;
+        bool live2 = s2 <= top;
+        if (live2) live2 = !blk_skip(read_thr(ctl, kind, lbmode), kind, lk, st, c, lo_k, s2, min(top, s2 + 7));
+        unsigned m2 = __ballot_sync(0xffffffffu, live2);
+        while (m2) {
+            unsigned mm = m2;
+            for (int g = 0; g < (lane >> 3); ++g) mm &= mm - 1;  // this lane's sub-block: the (lane/8)-th set bit
+            const bool hb = mm != 0;
+            const int64_t lam = hb ? base + 8 * (int64_t)(__ffs(mm) - 1) + (lane & 7) : 0;
+            for (int g = 0; g < 4; ++g) m2 &= m2 - 1;
+            const bool in = hb && lam <= top;
+            const Thr th = read_thr(ctl, kind, lbmode);
+            const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
+            int64_t b = 0;
+            if (keep) {
+                const int64_t S = kind == K_CCM1 ? bplb_ccm1_sum(lk, st, c, lam) : bplb_bj1_sum(lk, st, c, lam);
+                b = bplb_bound(S, bplb_fc(kind, c, lam));
+            }
+            const int64_t mx = emit_warp(keep, lam, b, lo_k, key, nullptr, 0, 0);
+            if (mx > wmax) {
+                wmax = mx;
+                if (lbmode && lane == 0) atomicMax(&ctl.lb, (int)mx);  // tighten the threshold now
+            }
+        }
+    }
+    return wmax;
 }
 
 // ---- one unit ----------------------------------------------------------------------
@@ -362,6 +517,11 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         const int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
         wmax = emit_warp(valid, lam, b, lo_k, key, nullptr, 0, 0);
         nev = L;
+    } else if (sg.type == PU_BLK) {
+        const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
+        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+        nev = lam_b - lam_a + 1;
+        wmax = blk_unit(p, ctl, lk, kind, lam_a, lam_b, lbmode, key);
     } else {  // PU_PRUNE
         const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
