@@ -50,6 +50,7 @@ constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
 constexpr int PR_QMAX = 32;            // block bounds for CCM1 / BJ1 where floor(c / lambda) <= PR_QMAX
 constexpr int PR_BLK_UNIT = 32 * 256;  // lambdas per block unit: 32 blocks of 256, one per lane
+constexpr int PR_QCAP = 256;           // CTA queue of 256-lambda blocks that survived their block bound
 constexpr int PR_MAX_SEGS = 20;
 
 enum { PU_CAND = 0, PU_LOOK = 1, PU_WALK = 2, PU_PRUNE = 3, PU_BLK = 4 };
@@ -61,10 +62,10 @@ struct LkRank {
     int r, d;
     int64_t c;
     __device__ __forceinline__ int rank(int64_t x) const {  // #distinct values <= x, clamped
-        if (x < 0) return 0;
-        if (x >= c) return d;
-        const uint2 e = rk[x >> 5];
-        return (int)e.y + __popc(e.x & (0xFFFFFFFFu >> (31 - ((int)x & 31))));
+        // branch-free: no weight is 0, so rank(x <= 0) = 0, and rank(x >= c) = d
+        const int xi = (int)(x < 0 ? 0 : (x > c ? c : x));
+        const uint2 e = rk[xi >> 5];
+        return (int)e.y + __popc(e.x & (0xFFFFFFFFu >> (31 - (xi & 31))));
     }
     __device__ __forceinline__ int64_t n_le(int64_t x) const { return cn[rank(x)]; }
     __device__ __forceinline__ void both(int64_t x, int64_t* n, int64_t* w) const {
@@ -94,6 +95,8 @@ struct PruneCtl {
     int unit_next, unit_end;
     int n_vb2, d;
     int n_done, bad, skip;
+    int q_n, q_next;           // block queue: entries pushed / taken
+    unsigned blkq[PR_QCAP];    // kind << 28 | first lambda of the block
     long long wsum[PNW], wsum2[PNW];
 };
 
@@ -392,56 +395,104 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
 // the lambdas of surviving sub-blocks (4 sub-blocks per warp pass) get the
 // per-lambda relaxation and, if still live, the exact sum (harmonic lookups,
 // bounds.py:390-407 / 441-460).  Returns the best bound the warp evaluated.
+// Level 2 + 3 of one 256-lambda block [base, top] of CCM1 / BJ1: 32 sub-blocks
+// of 8 lambdas (one per lane) re-bounded, then the lambdas of the surviving
+// sub-blocks (4 sub-blocks per warp pass) get the per-lambda relaxation and,
+// if still live, the exact sum (harmonic lookups, bounds.py:390-407 /
+// 441-460).  Returns the best bound the warp evaluated (-1: none).
 template <class LK>
-__device__ int64_t blk_unit(const KParams& p, PruneCtl& ctl, const LK& lk, int kind, int64_t lam_a, int64_t lam_b,
-                            bool lbmode, u64* key) {
+__device__ int64_t blk_block(const KParams& p, PruneCtl& ctl, const LK& lk, int kind, int64_t base, int64_t top,
+                             bool lbmode) {
     const int lane = threadIdx.x & 31;
     const int64_t c = p.c, lo_k = ctl.lo[kind];
     const NodeStats& st = ctl.st;
+    u64* key = &ctl.key[kind];
     int64_t wmax = -1;
-    const int64_t s1 = lam_a + 256 * (int64_t)lane;
-    bool live = s1 <= lam_b;
-    if (live) live = !blk_skip(read_thr(ctl, kind, lbmode), kind, lk, st, c, lo_k, s1, min(lam_b, s1 + 255));
-    unsigned m1 = __ballot_sync(0xffffffffu, live);
-    while (m1) {
-        const int j = __ffs(m1) - 1;
-        m1 &= m1 - 1;
-        const int64_t base = lam_a + 256 * (int64_t)j;
-        const int64_t top = min(lam_b, base + 255);
-        const int64_t s2 = base + 8 * (int64_t)lane;
-        bool live2 = s2 <= top;
-        if (live2) live2 = !blk_skip(read_thr(ctl, kind, lbmode), kind, lk, st, c, lo_k, s2, min(top, s2 + 7));
-        unsigned m2 = __ballot_sync(0xffffffffu, live2);
-        while (m2) {
-            unsigned mm = m2;
-            for (int g = 0; g < (lane >> 3); ++g) mm &= mm - 1;  // this lane's sub-block: the (lane/8)-th set bit
-            const bool hb = mm != 0;
-            const int64_t lam = hb ? base + 8 * (int64_t)(__ffs(mm) - 1) + (lane & 7) : 0;
-            for (int g = 0; g < 4; ++g) m2 &= m2 - 1;
-            const bool in = hb && lam <= top;
-            const Thr th = read_thr(ctl, kind, lbmode);
-            const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
-            int64_t b = 0;
-            if (keep) {
-                const int64_t S = kind == K_CCM1 ? bplb_ccm1_sum(lk, st, c, lam) : bplb_bj1_sum(lk, st, c, lam);
-                b = bplb_bound(S, bplb_fc(kind, c, lam));
-            }
-            const int64_t mx = emit_warp(keep, lam, b, lo_k, key, nullptr, 0, 0);
-            if (mx > wmax) {
-                wmax = mx;
-                if (lbmode && lane == 0) atomicMax(&ctl.lb, (int)mx);  // tighten the threshold now
-            }
+    const int64_t s2 = base + 8 * (int64_t)lane;
+    bool live2 = s2 <= top;
+    if (live2) live2 = !blk_skip(read_thr(ctl, kind, lbmode), kind, lk, st, c, lo_k, s2, min(top, s2 + 7));
+    unsigned m2 = __ballot_sync(0xffffffffu, live2);
+    while (m2) {
+        unsigned mm = m2;
+        for (int g = 0; g < (lane >> 3); ++g) mm &= mm - 1;  // this lane's sub-block: the (lane/8)-th set bit
+        const bool hb = mm != 0;
+        const int64_t lam = hb ? base + 8 * (int64_t)(__ffs(mm) - 1) + (lane & 7) : 0;
+        for (int g = 0; g < 4; ++g) m2 &= m2 - 1;
+        const bool in = hb && lam <= top;
+        const Thr th = read_thr(ctl, kind, lbmode);
+        const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
+        int64_t b = 0;
+        if (keep) {
+            const int64_t S = kind == K_CCM1 ? bplb_ccm1_sum(lk, st, c, lam) : bplb_bj1_sum(lk, st, c, lam);
+            b = bplb_bound(S, bplb_fc(kind, c, lam));
+        }
+        const int64_t mx = emit_warp(keep, lam, b, lo_k, key, nullptr, 0, 0);
+        if (mx > wmax) {
+            wmax = mx;
+            if (lane == 0) atomicMax(&ctl.lb, (int)mx);  // tighten the threshold now
         }
     }
     return wmax;
 }
 
+// Level 1 of a block unit (CCM1 / BJ1, up to 32 x 256 lambdas): lane j bounds
+// the 256-lambda block j; the surviving blocks go to the CTA queue, drained by
+// every warp after the unit sweep (so one unit's survivors do not serialise on
+// one warp); blocks that do not fit in the queue are processed here.
+template <class LK>
+__device__ int64_t blk_unit(const KParams& p, PruneCtl& ctl, const LK& lk, int kind, int64_t lam_a, int64_t lam_b,
+                            bool lbmode) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = p.c, lo_k = ctl.lo[kind];
+    const NodeStats& st = ctl.st;
+    const int64_t s1 = lam_a + 256 * (int64_t)lane;
+    bool live = s1 <= lam_b;
+    if (live) live = !blk_skip(read_thr(ctl, kind, lbmode), kind, lk, st, c, lo_k, s1, min(lam_b, s1 + 255));
+    unsigned m1 = __ballot_sync(0xffffffffu, live);
+    if (!m1) return -1;
+    int q0 = 0;
+    if (lane == 0) q0 = atomicAdd(&ctl.q_n, __popc(m1));
+    q0 = __shfl_sync(0xffffffffu, q0, 0);
+    const int pos = q0 + __popc(m1 & ((1u << lane) - 1u));
+    if (live && pos < PR_QCAP) ctl.blkq[pos] = ((unsigned)kind << 28) | (unsigned)s1;
+    int64_t wmax = -1;
+    if (q0 + __popc(m1) > PR_QCAP) {  // overflow: the blocks past the queue's end, inline
+        unsigned mo = __ballot_sync(0xffffffffu, live && pos >= PR_QCAP);
+        while (mo) {
+            const int j = __ffs(mo) - 1;
+            mo &= mo - 1;
+            const int64_t base = lam_a + 256 * (int64_t)j;
+            wmax = max(wmax, blk_block(p, ctl, lk, kind, base, min(lam_b, base + 255), lbmode));
+        }
+    }
+    return wmax;
+}
+
+// Drain the block queue (all warps; after a barrier that ends the unit sweep).
+template <class LK>
+__device__ void blk_drain(const KParams& p, PruneCtl& ctl, const LK& lk, bool lbmode, bool cancel) {
+    const int lane = threadIdx.x & 31;
+    const int n = min(*(volatile int*)&ctl.q_n, PR_QCAP);
+    for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&ctl.q_next, 1);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= n) break;
+        if (cancel && (int64_t)(*(volatile int*)&ctl.lb) > p.k) continue;  // Alg. 4 guard
+        const unsigned e = ctl.blkq[i];
+        const int kind = (int)(e >> 28);
+        const int64_t base = (int64_t)(e & 0x0FFFFFFFu);
+        const int64_t wm = blk_block(p, ctl, lk, kind, base, min(ctl.hi[kind], base + 255), lbmode);
+        if (lane == 0 && wm >= 0) atomicMax(&ctl.lb, (int)wm);
+    }
+}
+
 // ---- one unit ----------------------------------------------------------------------
 template <class LK>
 __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, int u,
-                           bool lbmode) {
+                           bool lbmode, int& si) {
     const int lane = threadIdx.x & 31;
-    int si = 0;
+    // a warp claims increasing unit ids: its segment index only moves forward
     while (si + 1 < ctl.nseg && ctl.segs[si + 1].first <= u) ++si;
     const PSeg sg = ctl.segs[si];
     const int kind = sg.kind;
@@ -521,7 +572,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
         nev = lam_b - lam_a + 1;
-        wmax = blk_unit(p, ctl, lk, kind, lam_a, lam_b, lbmode, key);
+        wmax = blk_unit(p, ctl, lk, kind, lam_a, lam_b, lbmode);
     } else {  // PU_PRUNE
         const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
@@ -631,14 +682,17 @@ template <class LK>
 __device__ void prune_run(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, bool lbmode,
                           bool cancel) {
     const int lane = threadIdx.x & 31;
+    int si = 0;
     for (;;) {
         int u = 0;
         if (lane == 0) u = atomicAdd(&ctl.unit_next, 1);
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= ctl.unit_end) break;
         if (cancel && (int64_t)(*(volatile int*)&ctl.lb) > p.k) continue;  // Alg. 4 guard
-        prune_unit(p, ctl, lk, m, u, lbmode);
+        prune_unit(p, ctl, lk, m, u, lbmode, si);
     }
+    __syncthreads();  // every unit done: the block queue is complete
+    blk_drain(p, ctl, lk, lbmode, cancel);
 }
 
 // lbmode: only lb / exceeded are produced (cross-kind pruning).
@@ -785,6 +839,8 @@ __global__ void __launch_bounds__(PNT, 3) prune_kernel(KParams p, int rcap, int 
                     const int kd = p.kinds[i];
                     if (threadIdx.x == 0) {
                         ctl.unit_next = ctl.kseg_first[kd];
+                        ctl.q_n = 0;
+                        ctl.q_next = 0;
                         ctl.unit_end = ctl.kseg_first[kd] + ctl.kseg_count[kd];
                         ctl.n_done = i + 1;
                     }
@@ -794,7 +850,10 @@ __global__ void __launch_bounds__(PNT, 3) prune_kernel(KParams p, int rcap, int 
                     if ((int64_t)ctl.lb > p.k) break;
                 }
             } else {
-                if (threadIdx.x == 0) { ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk; }
+                if (threadIdx.x == 0) {
+                    ctl.unit_next = 0; ctl.unit_end = ctl.nunits; ctl.n_done = p.nk;
+                    ctl.q_n = 0; ctl.q_next = 0;
+                }
                 __syncthreads();
                 prune_run(p, ctl, lk, m, lbm, cancel);
             }
