@@ -106,12 +106,14 @@ struct NodeStats {
     int64_t W;         // sum of weights
     int64_t Vs, Vm;    // sum of smalls, sum of mirrored values
     int64_t dq, dr;    // (Vs - Vm) = c*dq + dr   (VB2 closed form)
+    uint64_t cinv;     // floor((2^64 - 1) / c): division-free floor(x / c)
 };
 
 BPLB_HD void bplb_stats_finish(NodeStats* st, int64_t c) {
     int64_t dv = st->Vs - st->Vm;
     st->dq = dv / c;
     st->dr = dv - st->dq * c;
+    st->cinv = 0xFFFFFFFFFFFFFFFFull / (uint64_t)c;
 }
 
 // VB2 per-lambda transformed sum from D(lambda) = sum over VB2 items of the

@@ -123,25 +123,48 @@ __host__ __device__ inline size_t prune_smem_bytes(int rcap, int64_t c) {
 // ---- upper-bound tests (true => bound(l) <= B is guaranteed) ----------------
 // Integer envelope: c <= 2^18, r <= 2^14 (PR envelope) keeps every product
 // below 2^63 (l Vs <= 2^18 * 2^14 * 2^17).
+// f(c, lambda) per kind (bplb_core.h bplb_fc) with 32-bit divisions (c < 2^31).
+__device__ __forceinline__ int64_t pr_fc(int kind, int64_t c, int64_t lam) {
+    switch (kind) {
+    case K_MT: case K_RAD2: return c;
+    case K_FS1: return c * lam;
+    case K_CCM1: return 2 * (int64_t)((uint32_t)c / (uint32_t)lam);
+    case K_VB2: return 2 * (lam - 1);
+    default: {
+        const int64_t q = (int64_t)((uint32_t)c / (uint32_t)lam);
+        return q * (lam - (c - q * lam));
+    }
+    }
+}
+
+// floor(x / c) for x < 2^64 with cinv = floor((2^64 - 1) / c): the estimate is
+// low by at most one (no 64-bit division in the per-lambda tests).
+__device__ __forceinline__ uint64_t pr_udiv_c(uint64_t x, uint32_t c, uint64_t cinv) {
+    const uint64_t q = __umul64hi(x, cinv);
+    return x - q * c >= c ? q + 1 : q;
+}
+
 __device__ __forceinline__ bool ub_le_vb2(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
     const int64_t ns = st.n_small, nm = st.n_big - st.n_full, K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
     // c * S_hi without the floors (linear in lambda)
     const int64_t env = 2 * (lam * st.Vs - ns) - 2 * (lam * st.Vm - c * nm) + c * K * (lam - 1);
     if (env <= 2 * c * B * (lam - 1)) return true;
-    const int64_t fs = (int64_t)((uint64_t)(lam * st.Vs - ns) / (uint64_t)c);  // l Vs >= 2 ns > ns
-    int64_t y = (int64_t)(((uint64_t)(lam * st.Vm) + (uint64_t)c - 1) / (uint64_t)c) - nm;
+    const int64_t fs = (int64_t)pr_udiv_c((uint64_t)(lam * st.Vs - ns), (uint32_t)c, st.cinv);  // l Vs >= 2 ns > ns
+    int64_t y = (int64_t)pr_udiv_c((uint64_t)(lam * st.Vm) + (uint64_t)c - 1, (uint32_t)c, st.cinv) - nm;
     y = y > 0 ? y : 0;
     return 2 * fs - 2 * y + K * (lam - 1) <= 2 * B * (lam - 1);
 }
 
+// (PR envelope: Vs, Vm < 2^31, so the divisions are 32-bit)
 __device__ __forceinline__ bool ub_le_ccm1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
-    const int64_t q = (int64_t)((uint32_t)c / (uint32_t)lam);
+    const uint32_t L = (uint32_t)lam;
+    const int64_t q = (int64_t)((uint32_t)c / L);
     const int64_t K = (int64_t)st.n_eq + 2 * (int64_t)st.n_big;
     const int64_t lhs = 2 * st.Vs - 2 * st.Vm + 2 * (int64_t)st.n_big * (lam - 1);
     if (lhs <= (2 * B - K) * q * lam) return true;
     const int64_t z = st.Vm - (int64_t)st.n_big * (lam - 1);
-    const int64_t y = z > 0 ? (z + lam - 1) / lam : 0;
-    return 2 * (st.Vs / lam) + K * q - 2 * y <= 2 * B * q;
+    const int64_t y = z > 0 ? (int64_t)(((uint32_t)z + L - 1) / L) : 0;
+    return 2 * (int64_t)((uint32_t)st.Vs / L) + K * q - 2 * y <= 2 * B * q;
 }
 
 __device__ __forceinline__ bool ub_le_bj1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
@@ -256,10 +279,50 @@ __device__ __forceinline__ bool bj1_blk_le(const LkRank& lk, const NodeStats& st
     return a > l2;
 }
 
-__device__ __forceinline__ bool blk_ub_le(int kind, const LkRank& lk, const NodeStats& st, int64_t c, int64_t l1,
-                                          int64_t l2, int64_t B) {
+// Out of line (like the other heavy helpers below): prune_kernel inlined
+// everything into ~640 KB of SASS, and instruction-fetch stalls led its
+// warp-state samples; one copy of each loop keeps the hot code in cache.
+__device__ __noinline__ bool blk_ub_le(int kind, const LkRank lk, const NodeStats& st, int64_t c, int64_t l1,
+                                       int64_t l2, int64_t B) {
     if (B < 0) return false;
     return kind == K_CCM1 ? ccm1_blk_le(lk, st, c, l1, l2, B) : bj1_blk_le(lk, st, c, l1, l2, B);
+}
+
+// Exact per-lambda sums through the lookup structure, one out-of-line copy.
+__device__ __noinline__ int64_t pr_lookup_sum(int kind, const LkRank lk, const NodeStats& st, int64_t c,
+                                              int64_t lam) {
+    switch (kind) {
+    case K_MT: return bplb_mt_sum(lk, c, st.r, lam);
+    case K_RAD2: return bplb_rad2_sum(lk, c, st.r, lam);
+    case K_CCM1: return bplb_ccm1_sum(lk, st, c, lam);
+    default: return bplb_bj1_sum(lk, st, c, lam);
+    }
+}
+
+// The modular walk (FS1 / VB2 states over a 32-lambda window), one copy.
+__device__ __noinline__ void pr_walk(const int* items, int n, uint32_t c32, u64 cinv, int64_t lam_a, int L,
+                                     u64* t, uint32_t one, bool vb2) {
+    mod_walk<false, false, 8>(items, 0, n, c32, cinv, lam_a, L, t, one, vb2);
+}
+
+// One lambda of CCM1 / BJ1 by the whole warp: a dense pass over the items
+// (small lambda) or the harmonic lookups split over the lanes; one copy.
+__device__ int64_t ccm1_dense_smem(const int* w, int n, const NodeStats& st, int64_t c, int64_t lam);
+__device__ __noinline__ int64_t pr_warp_sum(int kind, bool dense, const LkRank lk, const NodeStats& st,
+                                            const int* sw, int64_t c, int64_t lj) {
+    const int lane = threadIdx.x & 31;
+    if (kind == K_CCM1) {
+        if (dense) return ccm1_dense_smem(sw, st.r, st, c, lj);
+        int64_t part = bplb_ccm1_part(lk, st, c, lj, 1 + lane, 32);
+        part = (int64_t)warp_sum_u64((u64)part);
+        return bplb_ccm1_from_part(st, c, lj, part);
+    }
+    if (dense) return bj1_dense(sw, st.r, c, lj);
+    int64_t fl, rem;
+    bplb_bj1_part(lk, st, c, lj, lane, 32, &fl, &rem);
+    fl = (int64_t)warp_sum_u64((u64)fl);
+    rem = (int64_t)warp_sum_u64((u64)rem);
+    return bplb_bj1_from_parts(c, lj, fl, rem);
 }
 
 // Pruning threshold snapshot (the shared best only grows, so a stale one is safe).
@@ -312,8 +375,7 @@ __device__ __forceinline__ bool blk_skip(const Thr& t, int kind, const LkRank& l
 
 // CCM1 dense sum over an unsorted item array in shared memory (the
 // global-memory ccm1_dense_raw reads through __ldg).
-__device__ __forceinline__ int64_t ccm1_dense_smem(const int* w, int n, const NodeStats& st, int64_t c,
-                                                   int64_t lam) {
+__device__ int64_t ccm1_dense_smem(const int* w, int n, const NodeStats& st, int64_t c, int64_t lam) {
     const int lane = threadIdx.x & 31;
     const Div31 dv = bplb_div31((uint32_t)lam);
     const uint32_t c32 = (uint32_t)c;
@@ -423,8 +485,8 @@ __device__ int64_t blk_block(const KParams& p, PruneCtl& ctl, const LK& lk, int 
         const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
         int64_t b = 0;
         if (keep) {
-            const int64_t S = kind == K_CCM1 ? bplb_ccm1_sum(lk, st, c, lam) : bplb_bj1_sum(lk, st, c, lam);
-            b = bplb_bound(S, bplb_fc(kind, c, lam));
+            const int64_t S = pr_lookup_sum(kind, lk, st, c, lam);
+            b = bplb_bound(S, pr_fc(kind, c, lam));
         }
         const int64_t mx = emit_warp(keep, lam, b, lo_k, key, nullptr, 0, 0);
         if (mx > wmax) {
@@ -510,7 +572,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
             const int64_t lam = sg.lo;
             int64_t b = 0;
             if (lane == 0) {
-                const int64_t S = kind == K_MT ? bplb_mt_sum(lk, c, st.r, lam) : bplb_rad2_sum(lk, c, st.r, lam);
+                const int64_t S = pr_lookup_sum(kind, lk, st, c, lam);
                 b = bplb_bound(S, c);
             }
             wmax = max(wmax, emit_warp(lane == 0, lam, b, lo_k, key, nullptr, 0, 0));
@@ -525,7 +587,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
             const bool v = vi && lam >= sg.lo && lam <= sg.hi;
             int64_t b = 0;
             if (v) {
-                const int64_t S = kind == K_MT ? bplb_mt_sum(lk, c, st.r, lam) : bplb_rad2_sum(lk, c, st.r, lam);
+                const int64_t S = pr_lookup_sum(kind, lk, st, c, lam);
                 b = bplb_bound(S, c);
             }
             wmax = max(wmax, emit_warp(v, lam, b, lo_k, key, nullptr, 0, 0));
@@ -537,14 +599,9 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         const bool valid = lam <= lam_b;
         int64_t S = 0;
         if (valid) {
-            switch (kind) {
-            case K_MT: S = bplb_mt_sum(lk, c, st.r, lam); break;
-            case K_RAD2: S = bplb_rad2_sum(lk, c, st.r, lam); break;
-            case K_CCM1: S = bplb_ccm1_sum(lk, st, c, lam); break;
-            default: S = bplb_bj1_sum(lk, st, c, lam); break;
-            }
+            S = pr_lookup_sum(kind, lk, st, c, lam);
         }
-        const int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+        const int64_t b = valid ? bplb_bound(S, pr_fc(kind, c, lam)) : 0;
         wmax = emit_warp(valid, lam, b, lo_k, key, nullptr, 0, 0);
         nev = lam_b - lam_a + 1;
     } else if (sg.type == PU_WALK) {
@@ -556,8 +613,8 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         __syncwarp();
         const uint32_t c32 = (uint32_t)c;
         const u64 cinv = bplb_cinv(c32);
-        if (kind == K_VB2) mod_walk<false, false, 8>(m.vb2, 0, ctl.n_vb2, c32, cinv, lam_a, L, t, p.one, true);
-        else mod_walk<false, false, 8>(m.sw, 0, st.r, c32, cinv, lam_a, L, t, p.one, false);
+        if (kind == K_VB2) pr_walk(m.vb2, ctl.n_vb2, c32, cinv, lam_a, L, t, p.one, true);
+        else pr_walk(m.sw, st.r, c32, cinv, lam_a, L, t, p.one, false);
         __syncwarp();
         const int64_t lam = lam_a + lane;
         const bool valid = lane < L;
@@ -565,7 +622,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         if (valid)
             S = kind == K_VB2 ? bplb_vb2_sum(st, c, lam, t[lane])
                               : bplb_fs1_sum(st, lam, t[lane], (uint64_t)bplb_fs1_zero(lk, c, st.maxw, lam));
-        const int64_t b = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+        const int64_t b = valid ? bplb_bound(S, pr_fc(kind, c, lam)) : 0;
         wmax = emit_warp(valid, lam, b, lo_k, key, nullptr, 0, 0);
         nev = L;
     } else if (sg.type == PU_BLK) {
@@ -597,7 +654,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
                         u64* tt = m.tot + (threadIdx.x >> 5) * 32;
                         tt[lane] = 0;
                         __syncwarp();
-                        mod_walk<false, false, 8>(m.vb2, 0, ctl.n_vb2, c32, cinv, sub, (int)(sub_b - sub + 1), tt,
+                        pr_walk(m.vb2, ctl.n_vb2, c32, cinv, sub, (int)(sub_b - sub + 1), tt,
                                                   p.one, true);
                         __syncwarp();
                         if (in) {
@@ -624,7 +681,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
                     }
                 } else {  // CCM1 / BJ1: harmonic lookups or a dense item pass
                     const int64_t span = kind == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
-                    const int64_t tmax = span / sub;
+                    const int64_t tmax = (int64_t)((uint32_t)span / (uint32_t)sub);
                     const int64_t T = kind == K_CCM1 ? 26 : 40;
                     const int64_t cost_lane = T * (tmax + 1);
                     const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + 24);
@@ -632,8 +689,8 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
                     if (cost_lane <= cost_coop && cost_lane <= cost_dense) {
                         if (in) {
                             have = true;
-                            const int64_t S = kind == K_CCM1 ? bplb_ccm1_sum(lk, st, c, lam) : bplb_bj1_sum(lk, st, c, lam);
-                            b = bplb_bound(S, bplb_fc(kind, c, lam));
+                            const int64_t S = pr_lookup_sum(kind, lk, st, c, lam);
+                            b = bplb_bound(S, pr_fc(kind, c, lam));
                         }
                     } else {
                         const bool dense = cost_dense < cost_coop;
@@ -642,27 +699,10 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
                             const int j = __ffs(mm) - 1;
                             mm &= mm - 1;
                             const int64_t lj = sub + j;
-                            int64_t S;
-                            if (kind == K_CCM1) {
-                                if (dense) S = ccm1_dense_smem(m.sw, st.r, st, c, lj);
-                                else {
-                                    int64_t part = bplb_ccm1_part(lk, st, c, lj, 1 + lane, 32);
-                                    part = (int64_t)warp_sum_u64((u64)part);
-                                    S = bplb_ccm1_from_part(st, c, lj, part);
-                                }
-                            } else {
-                                if (dense) S = bj1_dense(m.sw, st.r, c, lj);
-                                else {
-                                    int64_t fl, rem;
-                                    bplb_bj1_part(lk, st, c, lj, lane, 32, &fl, &rem);
-                                    fl = (int64_t)warp_sum_u64((u64)fl);
-                                    rem = (int64_t)warp_sum_u64((u64)rem);
-                                    S = bplb_bj1_from_parts(c, lj, fl, rem);
-                                }
-                            }
+                            const int64_t S = pr_warp_sum(kind, dense, lk, st, m.sw, c, lj);
                             if (lane == j) {
                                 have = true;
-                                b = bplb_bound(S, bplb_fc(kind, c, lj));
+                                b = bplb_bound(S, pr_fc(kind, c, lj));
                             }
                         }
                     }
