@@ -1553,4 +1553,17 @@ int bplb_check_batch_multi(bplb_multi* m, const void* w, int32_t wbytes, const i
     return 0;
 }
 
+#ifdef PRUNE_TRACE
+// development builds: copy the prune-kernel unit trace (longlong4 records)
+BPLB_API int bplb_prune_trace(long long* out, int cap) {
+    int n = 0;
+    cudaMemcpyFromSymbol(&n, bplb::g_prune_trace_n, sizeof(int));
+    n = std::min(n, std::min(cap, bplb::PRUNE_TRACE_CAP));
+    if (n > 0) cudaMemcpyFromSymbol(out, bplb::g_prune_trace, (size_t)n * sizeof(longlong4));
+    int z = 0;
+    cudaMemcpyToSymbol(bplb::g_prune_trace_n, &z, sizeof(int));
+    return n;
+}
+#endif
+
 }  // extern "C"

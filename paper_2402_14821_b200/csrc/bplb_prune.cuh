@@ -48,9 +48,11 @@ constexpr int PNT = 256;
 constexpr int PNW = PNT / 32;
 constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in smem
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
-constexpr int PR_QMAX = 32;            // block bounds for CCM1 / BJ1 where floor(c / lambda) <= PR_QMAX
+constexpr int PR_QMAX = 32;            // block bounds for CCM1 where floor(c / lambda) <= PR_QMAX
+constexpr int PR_QMAX_BJ1 = 32;        // ... and for BJ1 (its block bound costs O(q) lookups per q-piece)
 constexpr int PR_BLK_UNIT = 32 * 256;  // lambdas per block unit: 32 blocks of 256, one per lane
-constexpr int PR_QCAP = 256;           // CTA queue of 256-lambda blocks that survived their block bound
+constexpr int PR_QCAP = 2048;
+constexpr unsigned PR_QEMPTY = 0x7FFFFFFFu;  // a reserved queue slot with nothing to do          // CTA queue: CCM1/BJ1 256-lambda blocks and 32-lambda sub-ranges left to evaluate
 constexpr int PR_MAX_SEGS = 20;
 
 enum { PU_CAND = 0, PU_LOOK = 1, PU_WALK = 2, PU_PRUNE = 3, PU_BLK = 4 };
@@ -108,6 +110,23 @@ struct PruneMem {
     long long* cw;    // cumulative weights by distinct rank
     u64* tot;         // per-warp walk accumulators [PNW][32]
 };
+
+#ifdef PRUNE_TRACE
+// Per-unit cycle trace of the first CTAs (development builds only:
+// scripts/prune_trace.py builds libbplb_trace.so with -DPRUNE_TRACE).
+constexpr int PRUNE_TRACE_CTAS = 8;
+constexpr int PRUNE_TRACE_CAP = 1 << 16;
+__device__ longlong4 g_prune_trace[PRUNE_TRACE_CAP];
+__device__ int g_prune_trace_n;
+__device__ __forceinline__ void prune_trace_rec(const PruneCtl& ctl, int cta, int u, int si, long long t0) {
+    if ((threadIdx.x & 31) || cta >= PRUNE_TRACE_CTAS) return;
+    const int i = atomicAdd(&g_prune_trace_n, 1);
+    if (i >= PRUNE_TRACE_CAP) return;
+    const PSeg& sg = ctl.segs[si];
+    g_prune_trace[i] = make_longlong4(((long long)cta << 32) | ((long long)u << 8) | (threadIdx.x >> 5),
+                                      ((long long)sg.kind << 8) | sg.type, t0, clock64());
+}
+#endif
 
 __host__ __device__ inline int prune_rcap(int64_t max_r) { return (int)((max_r + 3) & ~3ll) + 4; }
 
@@ -427,7 +446,7 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
         break;
     case K_VB2:
         if (phase == 0) pushr(PU_WALK, lo, min(hi, lo + 31), 32);
-        else pushr(PU_PRUNE, lo + 32, hi, PR_SUPER);
+        else pushr(PU_PRUNE, lo + 32, hi, PR_BLK_UNIT);
         break;
     default: {  // CCM1, BJ1
         int64_t s0 = c / 4 + 1;
@@ -438,10 +457,10 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
             // block bounds where floor(c / l) <= PR_QMAX (l >= bl), per-lambda
             // relaxations below (tight there: the dropped floors are small
             // against c / l)
-            const int64_t bl = max(lo, c / (PR_QMAX + 1) + 1);
+            const int64_t bl = max(lo, c / ((kind == K_BJ1 ? PR_QMAX_BJ1 : PR_QMAX) + 1) + 1);
             auto region = [&](int64_t a, int64_t b) {  // [a, b] outside the seed window
                 if (b < a) return;
-                if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), PR_SUPER);
+                if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), PR_BLK_UNIT);
                 if (b >= bl) pushr(PU_BLK, max(a, bl), b, PR_BLK_UNIT);
             };
             region(s1 + 1, hi);
@@ -530,9 +549,112 @@ __device__ int64_t blk_unit(const KParams& p, PruneCtl& ctl, const LK& lk, int k
     return wmax;
 }
 
-// Drain the block queue (all warps; after a barrier that ends the unit sweep).
+// One 32-lambda sub-range [sub, sub_b] of a PU_PRUNE segment (VB2, or CCM1 /
+// BJ1 below the block-bound region): the per-lambda relaxation, then the
+// exact sums of the lambdas it keeps -- the VB2 walk over the window (or one
+// warp pass per lambda when only a few survive), CCM1 / BJ1 by harmonic
+// lookups per lane, split over the warp, or a dense pass over the items,
+// whichever is cheapest.  Returns the best bound evaluated (-1: none).
 template <class LK>
-__device__ void blk_drain(const KParams& p, PruneCtl& ctl, const LK& lk, bool lbmode, bool cancel) {
+__device__ int64_t prune_sub(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, int kind,
+                             int64_t sub, int64_t sub_b, bool lbmode) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = p.c, lo_k = ctl.lo[kind];
+    const NodeStats& st = ctl.st;
+    u64* key = &ctl.key[kind];
+    const uint32_t c32 = (uint32_t)c;
+    const u64 cinv = st.cinv;
+                const int64_t lam = sub + lane;
+                const bool in = lam <= sub_b;
+                const Thr th = read_thr(ctl, kind, lbmode);
+                const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                if (!mask) return -1;
+                const int n = __popc(mask);
+                bool have = false;
+                int64_t b = 0;
+                if (kind == K_VB2) {
+                    if (n >= 6) {  // dense cluster: walk the 32-lambda window
+                        u64* tt = m.tot + (threadIdx.x >> 5) * 32;
+                        tt[lane] = 0;
+                        __syncwarp();
+                        pr_walk(m.vb2, ctl.n_vb2, c32, cinv, sub, (int)(sub_b - sub + 1), tt,
+                                                  p.one, true);
+                        __syncwarp();
+                        if (in) {
+                            have = true;
+                            b = bplb_bound(bplb_vb2_sum(st, c, lam, tt[lane]), 2 * (lam - 1));
+                        }
+                    } else {  // a few lambdas: one warp pass over the items each
+                        unsigned mm = mask;
+                        while (mm) {
+                            const int j = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const int64_t lj = sub + j;
+                            u64 D = 0;
+                            for (int i = lane; i < ctl.n_vb2; i += 32) {
+                                const uint32_t x = (uint32_t)m.vb2[i];
+                                D += bplb_mulmod(x, (uint32_t)lj, 2 * x < c32 ? 1u : 0u, c32, cinv);
+                            }
+                            D = warp_sum_u64(D);
+                            if (lane == j) {
+                                have = true;
+                                b = bplb_bound(bplb_vb2_sum(st, c, lj, D), 2 * (lj - 1));
+                            }
+                        }
+                    }
+                } else {  // CCM1 / BJ1: harmonic lookups or a dense item pass
+                    const int64_t span = kind == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
+                    const int64_t tmax = (int64_t)((uint32_t)span / (uint32_t)sub);
+                    const int64_t T = kind == K_CCM1 ? 26 : 40;
+                    const int64_t cost_lane = T * (tmax + 1);
+                    const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + 24);
+                    const int64_t cost_dense = n * (10 * (((int64_t)st.r + 31) / 32) + 24);
+                    if (cost_lane <= cost_coop && cost_lane <= cost_dense) {
+                        if (in) {
+                            have = true;
+                            const int64_t S = pr_lookup_sum(kind, lk, st, c, lam);
+                            b = bplb_bound(S, pr_fc(kind, c, lam));
+                        }
+                    } else {
+                        const bool dense = cost_dense < cost_coop;
+                        unsigned mm = mask;
+                        while (mm) {
+                            const int j = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            const int64_t lj = sub + j;
+                            const int64_t S = pr_warp_sum(kind, dense, lk, st, m.sw, c, lj);
+                            if (lane == j) {
+                                have = true;
+                                b = bplb_bound(S, pr_fc(kind, c, lj));
+                            }
+                        }
+                    }
+                }
+                return emit_warp(have, lam, b, lo_k, key, nullptr, 0, 0);
+}
+
+// One 256-lambda block of a PU_PRUNE segment: its 32-lambda sub-ranges.
+template <class LK>
+__device__ int64_t prune_block(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, int kind,
+                               int64_t base, int64_t top, bool lbmode) {
+    int64_t wmax = -1;
+    for (int64_t sub = base; sub <= top; sub += 32) {
+        const int64_t mx = prune_sub(p, ctl, lk, m, kind, sub, min(top, sub + 31), lbmode);
+        if (mx > wmax) {
+            wmax = mx;
+            if ((threadIdx.x & 31) == 0) atomicMax(&ctl.lb, (int)mx);  // tighten the threshold now
+        }
+    }
+    return wmax;
+}
+
+// Drain the CTA queue (all warps; after the barrier that ends the unit sweep):
+// 256-lambda blocks of CCM1 / BJ1 (levels 2 + 3) and 32-lambda sub-ranges of
+// PU_PRUNE segments.
+template <class LK>
+__device__ void blk_drain(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, bool lbmode,
+                          bool cancel) {
     const int lane = threadIdx.x & 31;
     const int n = min(*(volatile int*)&ctl.q_n, PR_QCAP);
     for (;;) {
@@ -542,10 +664,25 @@ __device__ void blk_drain(const KParams& p, PruneCtl& ctl, const LK& lk, bool lb
         if (i >= n) break;
         if (cancel && (int64_t)(*(volatile int*)&ctl.lb) > p.k) continue;  // Alg. 4 guard
         const unsigned e = ctl.blkq[i];
-        const int kind = (int)(e >> 28);
+        if (e == PR_QEMPTY) continue;
+        const int kind = (int)((e >> 28) & 7u);
         const int64_t base = (int64_t)(e & 0x0FFFFFFFu);
-        const int64_t wm = blk_block(p, ctl, lk, kind, base, min(ctl.hi[kind], base + 255), lbmode);
+#ifdef PRUNE_TRACE
+        const long long t0 = clock64();
+#endif
+        const int64_t wm = (e & 0x80000000u)
+                               ? prune_sub(p, ctl, lk, m, kind, base, min(ctl.hi[kind], base + 31), lbmode)
+                               : blk_block(p, ctl, lk, kind, base, min(ctl.hi[kind], base + 255), lbmode);
         if (lane == 0 && wm >= 0) atomicMax(&ctl.lb, (int)wm);
+#ifdef PRUNE_TRACE
+        if (lane == 0 && blockIdx.x < PRUNE_TRACE_CTAS) {
+            const int ti = atomicAdd(&g_prune_trace_n, 1);
+            if (ti < PRUNE_TRACE_CAP)
+                g_prune_trace[ti] = make_longlong4(((long long)blockIdx.x << 32) | 0xFFFE0000ll | (threadIdx.x >> 5),
+                                                   ((long long)kind << 8) | ((e & 0x80000000u) ? 3 : 4) |
+                                                       ((long long)base << 16), t0, clock64());
+        }
+#endif
     }
 }
 
@@ -630,84 +767,66 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
         nev = lam_b - lam_a + 1;
         wmax = blk_unit(p, ctl, lk, kind, lam_a, lam_b, lbmode);
-    } else {  // PU_PRUNE
+    } else {  // PU_PRUNE: up to 32 x 256 lambdas; the surviving 32-lambda sub-ranges go to the CTA queue
         const int64_t lam_a = sg.lo + (int64_t)(u - sg.first) * sg.chunk;
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
         nev = lam_b - lam_a + 1;
-        const Thr t0 = read_thr(ctl, kind, lbmode);
-        if (!range_skip(t0, kind, st, c, lo_k, lam_a, lam_b)) {
-            const uint32_t c32 = (uint32_t)c;
-            const u64 cinv = bplb_cinv(c32);
-            for (int64_t sub = lam_a; sub <= lam_b; sub += 32) {
-                const int64_t sub_b = min(lam_b, sub + 31);
-                const int64_t lam = sub + lane;
-                const bool in = lam <= sub_b;
-                const Thr th = read_thr(ctl, kind, lbmode);
-                const bool keep = in && !lam_skip(th, kind, st, c, lo_k, lam);
-                const unsigned mask = __ballot_sync(0xffffffffu, keep);
-                if (!mask) continue;
-                const int n = __popc(mask);
-                bool have = false;
-                int64_t b = 0;
-                if (kind == K_VB2) {
-                    if (n >= 6) {  // dense cluster: walk the 32-lambda window
-                        u64* tt = m.tot + (threadIdx.x >> 5) * 32;
-                        tt[lane] = 0;
-                        __syncwarp();
-                        pr_walk(m.vb2, ctl.n_vb2, c32, cinv, sub, (int)(sub_b - sub + 1), tt,
-                                                  p.one, true);
-                        __syncwarp();
-                        if (in) {
-                            have = true;
-                            b = bplb_bound(bplb_vb2_sum(st, c, lam, tt[lane]), 2 * (lam - 1));
-                        }
-                    } else {  // a few lambdas: one warp pass over the items each
-                        unsigned mm = mask;
-                        while (mm) {
-                            const int j = __ffs(mm) - 1;
-                            mm &= mm - 1;
-                            const int64_t lj = sub + j;
-                            u64 D = 0;
-                            for (int i = lane; i < ctl.n_vb2; i += 32) {
-                                const uint32_t x = (uint32_t)m.vb2[i];
-                                D += bplb_mulmod(x, (uint32_t)lj, 2 * x < c32 ? 1u : 0u, c32, cinv);
-                            }
-                            D = warp_sum_u64(D);
-                            if (lane == j) {
-                                have = true;
-                                b = bplb_bound(bplb_vb2_sum(st, c, lj, D), 2 * (lj - 1));
-                            }
-                        }
-                    }
-                } else {  // CCM1 / BJ1: harmonic lookups or a dense item pass
-                    const int64_t span = kind == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
-                    const int64_t tmax = (int64_t)((uint32_t)span / (uint32_t)sub);
-                    const int64_t T = kind == K_CCM1 ? 26 : 40;
-                    const int64_t cost_lane = T * (tmax + 1);
-                    const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + 24);
-                    const int64_t cost_dense = n * (10 * (((int64_t)st.r + 31) / 32) + 24);
-                    if (cost_lane <= cost_coop && cost_lane <= cost_dense) {
-                        if (in) {
-                            have = true;
-                            const int64_t S = pr_lookup_sum(kind, lk, st, c, lam);
-                            b = bplb_bound(S, pr_fc(kind, c, lam));
-                        }
-                    } else {
-                        const bool dense = cost_dense < cost_coop;
-                        unsigned mm = mask;
-                        while (mm) {
-                            const int j = __ffs(mm) - 1;
-                            mm &= mm - 1;
-                            const int64_t lj = sub + j;
-                            const int64_t S = pr_warp_sum(kind, dense, lk, st, m.sw, c, lj);
-                            if (lane == j) {
-                                have = true;
-                                b = bplb_bound(S, pr_fc(kind, c, lj));
-                            }
-                        }
-                    }
+        // level 1: lane j tests the 256-lambda block j with the range relaxation
+        const int64_t s1 = lam_a + 256 * (int64_t)lane;
+        const bool l1 = s1 <= lam_b &&
+                        !range_skip(read_thr(ctl, kind, lbmode), kind, st, c, lo_k, s1, min(lam_b, s1 + 255));
+        unsigned m1 = __ballot_sync(0xffffffffu, l1);
+        if (lbmode) {
+            // lb mode: every sub-range of a surviving block goes to the CTA queue; its
+            // per-lambda tests run in the drain, balanced over the warps and against
+            // the threshold the seeds and the units have raised by then
+            if (m1) {
+                int q0 = 0;
+                if (lane == 0) q0 = atomicAdd(&ctl.q_n, 8 * __popc(m1));
+                q0 = __shfl_sync(0xffffffffu, q0, 0);
+                const int pos = q0 + 8 * __popc(m1 & ((1u << lane) - 1u));
+                if (l1 && pos < PR_QCAP)  // a block straddling the end: its slots become empty entries
+                    for (int j = 0; j < 8 && pos + j < PR_QCAP; ++j)
+                        ctl.blkq[pos + j] = pos + 8 <= PR_QCAP
+                                                ? 0x80000000u | ((unsigned)kind << 28) | (unsigned)(s1 + 32 * j)
+                                                : PR_QEMPTY;
+                unsigned mo = __ballot_sync(0xffffffffu, l1 && pos + 8 > PR_QCAP);
+                while (mo) {  // queue overflow: inline
+                    const int j = __ffs(mo) - 1;
+                    mo &= mo - 1;
+                    const int64_t base = lam_a + 256 * (int64_t)j;
+                    wmax = max(wmax, prune_block(p, ctl, lk, m, kind, base, min(lam_b, base + 255), lbmode));
                 }
-                wmax = max(wmax, emit_warp(have, lam, b, lo_k, key, nullptr, 0, 0));
+            }
+            m1 = 0;
+        }
+        while (m1) {  // surviving 256-lambda blocks: per-lambda tests here (cheap), the
+                      // 32-lambda sub-ranges that keep a lambda go to the CTA queue
+            const int j1 = __ffs(m1) - 1;
+            m1 &= m1 - 1;
+            const int64_t base = lam_a + 256 * (int64_t)j1, top = min(lam_b, base + 255);
+            const Thr t0 = read_thr(ctl, kind, lbmode);
+            unsigned live = 0;  // bit j: sub-range j keeps a lambda
+            for (int64_t sub = base, j = 0; sub <= top; sub += 32, ++j) {
+                const int64_t lam = sub + lane;
+                const bool keep = lam <= top && !lam_skip(t0, kind, st, c, lo_k, lam);
+                if (__ballot_sync(0xffffffffu, keep)) live |= 1u << j;
+            }
+            const bool mine = lane < 8 && (live >> lane & 1u);
+            const unsigned mm = __ballot_sync(0xffffffffu, mine);
+            if (!mm) continue;
+            int q0 = 0;
+            if (lane == 0) q0 = atomicAdd(&ctl.q_n, __popc(mm));
+            q0 = __shfl_sync(0xffffffffu, q0, 0);
+            const int pos = q0 + __popc(mm & ((1u << lane) - 1u));
+            if (mine && pos < PR_QCAP)
+                ctl.blkq[pos] = 0x80000000u | ((unsigned)kind << 28) | (unsigned)(base + 32 * lane);
+            unsigned mo = __ballot_sync(0xffffffffu, mine && pos >= PR_QCAP);
+            while (mo) {  // queue overflow: inline
+                const int j = __ffs(mo) - 1;
+                mo &= mo - 1;
+                const int64_t sub = base + 32 * (int64_t)j;
+                wmax = max(wmax, prune_sub(p, ctl, lk, m, kind, sub, min(top, sub + 31), lbmode));
             }
         }
     }
@@ -717,6 +836,7 @@ __device__ void prune_unit(const KParams& p, PruneCtl& ctl, const LK& lk, const 
         if (wmax >= 0) atomicMax(&ctl.lb, (int)wmax);
     }
 }
+
 
 template <class LK>
 __device__ void prune_run(const KParams& p, PruneCtl& ctl, const LK& lk, const PruneMem& m, bool lbmode,
@@ -729,10 +849,28 @@ __device__ void prune_run(const KParams& p, PruneCtl& ctl, const LK& lk, const P
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= ctl.unit_end) break;
         if (cancel && (int64_t)(*(volatile int*)&ctl.lb) > p.k) continue;  // Alg. 4 guard
+#ifdef PRUNE_TRACE
+        const long long t0 = clock64();
+#endif
         prune_unit(p, ctl, lk, m, u, lbmode, si);
+#ifdef PRUNE_TRACE
+        prune_trace_rec(ctl, blockIdx.x, u, si, t0);
+#endif
     }
     __syncthreads();  // every unit done: the block queue is complete
-    blk_drain(p, ctl, lk, lbmode, cancel);
+#ifdef PRUNE_TRACE
+    const long long td = clock64();
+#endif
+    blk_drain(p, ctl, lk, m, lbmode, cancel);
+#ifdef PRUNE_TRACE
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < PRUNE_TRACE_CTAS) {
+        const int i = atomicAdd(&g_prune_trace_n, 1);
+        if (i < PRUNE_TRACE_CAP) {
+            g_prune_trace[i] = make_longlong4(((long long)blockIdx.x << 32) | 0xFFFF0000ll | (threadIdx.x >> 5),
+                                              ctl.q_n, td, clock64());
+        }
+    }
+#endif
 }
 
 // lbmode: only lb / exceeded are produced (cross-kind pruning).
