@@ -168,6 +168,10 @@ struct bplb_engine {
     int hist_per_sm = 3;          // persistent histogram CTAs per SM (BPLB_HIST_PER_SM)
     bool hist_carveout = false;
     int64_t multi_grid = 0;  // BPLB_MULTI_GRID: override of the single-node multi-CTA grid (tuning)
+    // r * c above which node-resident single checks take the pruned wide path
+    // instead (BPLB_WIDE_PRUNE_MIN_CELLS): off by default -- cfg3 (r * c = 1e8)
+    // measured 172 us there vs 104 us on the multi-CTA node kernel
+    int64_t wide_prune_min_cells = (int64_t)1 << 62;
     bool assign_carveout = false;
     bool single_cluster_ok = true;    // drop-in checks as one thread-block cluster
     bool single_cluster_attr = false;
@@ -766,6 +770,7 @@ int bplb_engine_create(int device, bplb_engine** out) {
     e->smem_optin = prop.sharedMemPerBlockOptin;
     if (const char* v = getenv("BPLB_HIST_PER_SM")) e->hist_per_sm = std::max(1, atoi(v));
     if (const char* v = getenv("BPLB_MULTI_GRID")) e->multi_grid = atoll(v);
+    if (const char* v = getenv("BPLB_WIDE_PRUNE_MIN_CELLS")) e->wide_prune_min_cells = atoll(v);
     if (const char* v = getenv("BPLB_SINGLE_CLUSTER")) e->single_cluster_ok = atoi(v) != 0;  // A/B switch
 #ifdef TAB_TRACE
     e->graphs_ok = false;  // stamps are read back per launch
@@ -970,7 +975,14 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     p.res_out = (bplb_result*)e->d_res.p;
     p.err_out = (int*)((char*)e->d_res.p + sizeof(bplb_result));  // copied back with the result
     CUDA_TRY(cudaMemsetAsync(p.err_out, 0, 4, e->stream));
-    if (!node_fits(r, c)) {
+    // the grid-wide path for nodes beyond the node-resident kernels, and for
+    // full-collection checks it can prune (seeded keys + bound tests): one
+    // launch sequence over all SMs beats the multi-CTA node kernel's phase
+    // hand-offs there (cfg3: r = 1e3, c = 1e5)
+    const bool wide_prunes = !(flags & (BPLB_F_PHASED | BPLB_F_CANCEL | BPLB_F_NOPRUNE)) &&
+                             c <= bplb::WIDE_PRUNE_MAX_C && r <= bplb::WIDE_PRUNE_MAX_R &&
+                             r * c >= e->wide_prune_min_cells;
+    if (!node_fits(r, c) || wide_prunes) {
         e->last_path = BPLB_PATH_WIDE;
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);

@@ -174,7 +174,7 @@ __device__ __forceinline__ bool ub_le_vb2(const NodeStats& st, int64_t c, int64_
     return 2 * fs - 2 * y + K * (lam - 1) <= 2 * B * (lam - 1);
 }
 
-// (PR envelope: Vs, Vm < 2^31, so the divisions are 32-bit)
+// (32-bit divisions while Vs, Vm < 2^32: always in the node-kernel envelope)
 __device__ __forceinline__ bool ub_le_ccm1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
     const uint32_t L = (uint32_t)lam;
     const int64_t q = (int64_t)((uint32_t)c / L);
@@ -182,8 +182,15 @@ __device__ __forceinline__ bool ub_le_ccm1(const NodeStats& st, int64_t c, int64
     const int64_t lhs = 2 * st.Vs - 2 * st.Vm + 2 * (int64_t)st.n_big * (lam - 1);
     if (lhs <= (2 * B - K) * q * lam) return true;
     const int64_t z = st.Vm - (int64_t)st.n_big * (lam - 1);
-    const int64_t y = z > 0 ? (int64_t)(((uint32_t)z + L - 1) / L) : 0;
-    return 2 * (int64_t)((uint32_t)st.Vs / L) + K * q - 2 * y <= 2 * B * q;
+    int64_t y, fs;
+    if (((uint64_t)st.Vs | (uint64_t)(z > 0 ? z : 0)) >> 32) {  // grid-wide sizes
+        y = z > 0 ? (z + lam - 1) / lam : 0;
+        fs = st.Vs / lam;
+    } else {
+        y = z > 0 ? (int64_t)(((uint32_t)z + L - 1) / L) : 0;
+        fs = (int64_t)((uint32_t)st.Vs / L);
+    }
+    return 2 * fs + K * q - 2 * y <= 2 * B * q;
 }
 
 __device__ __forceinline__ bool ub_le_bj1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
@@ -228,7 +235,8 @@ __device__ __forceinline__ bool ub_le_range(int kind, const NodeStats& st, int64
 // Sm(l) = sum over small w of floor(w/l) and Bg(l) = sum over mirrored
 // v = c - w of floor(v/l) are non-increasing in l, F(l) = 2 floor(c/l) > 0, so
 // on [l1, l2]:  S(l) <= 2 Sm(l1) + K floor(c/l1) - 2 Bg(l2),  F(l) >= 2 floor(c/l2).
-__device__ __forceinline__ bool ccm1_blk_le(const LkRank& lk, const NodeStats& st, int64_t c, int64_t l1,
+template <class LK>
+__device__ __forceinline__ bool ccm1_blk_le(const LK& lk, const NodeStats& st, int64_t c, int64_t l1,
                                             int64_t l2, int64_t B) {
     const int hs = (int)((c - 1) / 2);
     const int L1 = (int)l1, L2 = (int)l2;
@@ -242,7 +250,8 @@ __device__ __forceinline__ bool ccm1_blk_le(const LkRank& lk, const NodeStats& s
 }
 
 // sum over items w in [lo, hi] with w > T of (w - T)
-__device__ __forceinline__ int64_t lk_excess(const LkRank& lk, int64_t lo, int64_t hi, int64_t T) {
+template <class LK>
+__device__ __forceinline__ int64_t lk_excess(const LK& lk, int64_t lo, int64_t hi, int64_t T) {
     if (lo < T + 1) lo = T + 1;
     if (hi < lo) return 0;
     int64_t n1, w1, n0, w0;
@@ -261,8 +270,9 @@ __device__ __forceinline__ int64_t lk_excess(const LkRank& lk, int64_t lo, int64
 // so its maximum sits at l2 (below the pivot) or l1 (above).  An item that
 // crosses a step (w in [t l1, t l2 - 1]) contributes < t + 1.  Summing
 // (W / N lookups per bucket):  sum f(w)/f(c) <= (I + X2/P(l2) + X1/P(l1)) / q.
-// Integer envelope (c <= 2^18, r <= 2^14, q <= PR_QMAX): every product < 2^60.
-__device__ __forceinline__ bool bj1_blk_q_le(const LkRank& lk, const NodeStats& st, int64_t c, int64_t q,
+// Integer envelope: c <= 2^20, r <= 2^17, q <= PR_QMAX (the final comparison in 128 bits).
+template <class LK>
+__device__ __forceinline__ bool bj1_blk_q_le(const LK& lk, const NodeStats& st, int64_t c, int64_t q,
                                              int64_t l1, int64_t l2, int64_t B) {
     const int64_t P1 = (q + 1) * l1 - c, P2 = (q + 1) * l2 - c;
     int64_t I = 0, X1 = 0, X2 = 0;
@@ -282,11 +292,14 @@ __device__ __forceinline__ bool bj1_blk_q_le(const LkRank& lk, const NodeStats& 
         }
         if (t >= 1 && l2 > l1) I += (int64_t)(t + 1) * (lk.n_le((int64_t)t * l2 - 1) - lk.n_le((int64_t)t * l1 - 1));
     }
-    return I * P1 * P2 + X2 * P1 + X1 * P2 <= B * q * P1 * P2;
+    // 128-bit: the grid-wide path (c <= 2^20, r <= 2^17) exceeds 2^63 here
+    const __int128 P12 = (__int128)P1 * P2;
+    return (__int128)I * P12 + (__int128)X2 * P1 + (__int128)X1 * P2 <= (__int128)B * q * P12;
 }
 
 // BJ1 on any [l1, l2]: split at the q-interval ends (at most 8 pieces).
-__device__ __forceinline__ bool bj1_blk_le(const LkRank& lk, const NodeStats& st, int64_t c, int64_t l1,
+template <class LK>
+__device__ __forceinline__ bool bj1_blk_le(const LK& lk, const NodeStats& st, int64_t c, int64_t l1,
                                            int64_t l2, int64_t B) {
     int64_t a = l1;
     for (int piece = 0; piece < 8 && a <= l2; ++piece) {
@@ -301,7 +314,8 @@ __device__ __forceinline__ bool bj1_blk_le(const LkRank& lk, const NodeStats& st
 // Out of line (like the other heavy helpers below): prune_kernel inlined
 // everything into ~640 KB of SASS, and instruction-fetch stalls led its
 // warp-state samples; one copy of each loop keeps the hot code in cache.
-__device__ __noinline__ bool blk_ub_le(int kind, const LkRank lk, const NodeStats& st, int64_t c, int64_t l1,
+template <class LK>
+__device__ __noinline__ bool blk_ub_le(int kind, const LK lk, const NodeStats& st, int64_t c, int64_t l1,
                                        int64_t l2, int64_t B) {
     if (B < 0) return false;
     return kind == K_CCM1 ? ccm1_blk_le(lk, st, c, l1, l2, B) : bj1_blk_le(lk, st, c, l1, l2, B);
@@ -366,6 +380,16 @@ __device__ __forceinline__ Thr read_thr(const PruneCtl& ctl, int kind, bool lbmo
     return t;
 }
 
+// Key-mode threshold from a packed per-kind key (the grid-wide path).
+__device__ __forceinline__ Thr thr_from_key(u64 key) {
+    Thr t;
+    t.lbmode = false;
+    t.has = key != 0;
+    t.B = (int64_t)(key >> 32);
+    t.a_rel = (int64_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu));
+    return t;
+}
+
 __device__ __forceinline__ bool lam_skip(const Thr& t, int kind, const NodeStats& st, int64_t c, int64_t lo,
                                          int64_t lam) {
     if (!t.has) return false;
@@ -384,7 +408,8 @@ __device__ __forceinline__ bool range_skip(const Thr& t, int kind, const NodeSta
     return t.B >= 1 && ub_le_range(kind, st, c, l1, l2, t.B - 1);
 }
 
-__device__ __forceinline__ bool blk_skip(const Thr& t, int kind, const LkRank& lk, const NodeStats& st, int64_t c,
+template <class LK>
+__device__ __forceinline__ bool blk_skip(const Thr& t, int kind, const LK& lk, const NodeStats& st, int64_t c,
                                          int64_t lo, int64_t l1, int64_t l2) {
     if (!t.has) return false;
     if (t.lbmode) return blk_ub_le(kind, lk, st, c, l1, l2, t.B);

@@ -19,13 +19,18 @@
 #include <algorithm>
 #include <string>
 #include "bplb_node.cuh"
+#include "bplb_prune.cuh"
 
 namespace bplb {
 
 constexpr int WT = 256;              // threads per CTA (wide kernels)
 constexpr int ISLICE = 32 * GMOD_MAX * 8; // items per modular tile (4096)
 constexpr int LLW = 128;             // lambdas per lane-lookup unit (4 x 32)
-constexpr int WIDE_MAX_SEGS = 3 * K_COUNT;
+constexpr int WIDE_MAX_SEGS = 4 * K_COUNT;
+// Bound pruning on the grid-wide path (full-collection checks only): the
+// integer envelope of the bplb_prune.cuh upper bounds.
+constexpr int64_t WIDE_PRUNE_MAX_C = (int64_t)1 << 20;
+constexpr int64_t WIDE_PRUNE_MAX_R = (int64_t)1 << 17;
 constexpr int64_t WIDE_MAX_C = (int64_t)1 << 27;
 constexpr int SCAN_TILE_MIN = 512;  // entries per scan block (at least)
 // Scan tile for n entries: >= 512 and a multiple of WT, with at most ~512
@@ -64,6 +69,9 @@ struct WideState {
     long long unit_end;
     int need_final;        // VB2/FS1 were item-sliced
     int scan_blocks_done;
+    int prune;             // bound pruning: seeds (units [0, nA)) then the pruned rest
+    long long nA;
+    u64 thr[K_COUNT];      // per-kind keys after the seeds (the VB2 walk-chunk decisions)
 };
 
 struct WideBufs {
@@ -73,6 +81,7 @@ struct WideBufs {
     int* vb2;                   // [r]
     unsigned long long* acc;    // [c+1] VB2 per-lambda D (indexed by lambda)
     unsigned long long* pz;     // [2*101] FS1 P and Z (indexed by lambda)
+    unsigned char* chunk_ok;    // [c/LMOD + 2] VB2 walk chunk evaluated (pruning)
     int64_t tile;               // scan tile (scan_tile(c + 2))
 };
 
@@ -88,6 +97,7 @@ inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
     b += al((size_t)std::max<int64_t>(r, 1) * 4);
     b += al((size_t)(c + 1) * 8);
     b += al((size_t)2 * 101 * 8);
+    b += al((size_t)(c / LMOD + 2));
     return b;
 }
 
@@ -102,7 +112,8 @@ inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
     w.bsum = (unsigned long long*)p; p += al((size_t)nb * 16);
     w.vb2 = (int*)p; p += al((size_t)std::max<int64_t>(r, 1) * 4);
     w.acc = (unsigned long long*)p; p += al((size_t)(c + 1) * 8);
-    w.pz = (unsigned long long*)p;
+    w.pz = (unsigned long long*)p; p += al((size_t)2 * 101 * 8);
+    w.chunk_ok = (unsigned char*)p;
     return w;
 }
 
@@ -114,6 +125,7 @@ __global__ void wide_init(WideBufs b, int64_t c) {
     for (int64_t i = i0; i < n; i += stride) b.rec[i] = make_ulonglong2(0ull, 0ull);
     for (int64_t i = i0; i < c + 1; i += stride) b.acc[i] = 0;
     for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
+    for (int64_t i = i0; i < c / LMOD + 2; i += stride) b.chunk_ok[i] = 0;
     unsigned int* st = (unsigned int*)b.state;  // zero the state word by word
     for (int64_t i = i0; i < (int64_t)(sizeof(WideState) / 4); i += stride) st[i] = 0u;
 }
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
 // Lambda ranges and the unit plan (one thread).
 __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int use_range,
                           int64_t lo0, int64_t hi0, int kinds0, int kinds1, int kinds2, int kinds3,
-                          int kinds4, int kinds5, int phased) {
+                          int kinds4, int kinds5, int phased, int prune) {
     WideState* s = b.state;
     const int kinds[K_COUNT] = {kinds0, kinds1, kinds2, kinds3, kinds4, kinds5};
     bplb_stats_finish(&s->st, c);
@@ -274,6 +286,68 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
         s->nunits += g.count;
         s->kind_seg_count[kind]++;
     };
+    s->prune = prune;
+    s->nA = 0;
+    // CCM1 / BJ1 segments over [a, z]: a dense pass over the items at small
+    // lambda (the harmonic loop would be ~span/lambda L2 lookups), one warp per
+    // lambda while the loop is still long, one lane per lambda after.
+    auto push_div_look = [&](int kd, int64_t a, int64_t z) {
+        if (z < a) return;
+        const int64_t span = kd == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
+        const int64_t n = st.r > 0 ? st.r : 1;
+        int64_t sd = kd == K_CCM1 ? (64 * span) / (3 * n + 30) + 1 : (16 * span) / n + 1;
+        if (sd < a) sd = a;
+        if (sd > z + 1) sd = z + 1;
+        int64_t sp = span / 64 + 1;
+        if (sp < sd) sp = sd;
+        if (sp > z + 1) sp = z + 1;
+        push(kd, T_DIV, a, sd - 1, st.r > 8192 ? 1 : 8, 1);
+        push(kd, T_WLOOK, sd, sp - 1, 1, 1);
+        push(kd, T_LOOKUP, sp, z, LLW, 1);
+    };
+    auto push_mod = [&](int kd, int64_t a, int64_t z) {
+        const int64_t items = kd == K_VB2 ? s->n_vb2 : st.r;
+        int nsl = (int)((items + ISLICE - 1) / ISLICE);
+        if (nsl < 1) nsl = 1;
+        if (nsl > 1) s->need_final = 1;
+        push(kd, T_MOD, a, z, LMOD, nsl);
+    };
+    if (prune) {
+        // seeds (units [0, nA)): MT, RAD2 and FS1 complete, VB2's first walk
+        // chunk, a CCM1 / BJ1 window at c/4 + 1; then every other lambda,
+        // tested against the seeds' keys (bplb_prune.cuh bounds)
+        int64_t w0[K_COUNT], w1[K_COUNT];
+        for (int i = 0; i < nk; ++i) {
+            const int kd = kinds[i];
+            const int64_t lo = s->lo[kd], hi = s->hi[kd];
+            s->kind_seg_first[kd] = s->nseg;
+            w0[kd] = hi + 1; w1[kd] = hi;
+            if (hi < lo) continue;
+            switch (kd) {
+            case K_MT: case K_RAD2: push(kd, T_LOOKUP, lo, hi, LLW, 1); break;
+            case K_FS1: push_mod(kd, lo, hi); break;
+            case K_VB2: push_mod(kd, lo, min(hi, lo + LMOD - 1)); break;
+            default: {
+                int64_t a = c / 4 + 1;
+                a = a < lo ? lo : (a > hi ? hi : a);
+                w0[kd] = a; w1[kd] = min(hi, a + 31);
+                push(kd, T_LOOKUP, w0[kd], w1[kd], LLW, 1);
+            }
+            }
+        }
+        s->nA = s->nunits;
+        for (int i = 0; i < nk; ++i) {
+            const int kd = kinds[i];
+            const int64_t lo = s->lo[kd], hi = s->hi[kd];
+            if (hi < lo) continue;
+            if (kd == K_VB2) push_mod(kd, lo + LMOD, hi);
+            if (kd == K_CCM1 || kd == K_BJ1) {
+                push_div_look(kd, lo, w0[kd] - 1);
+                push_div_look(kd, w1[kd] + 1, hi);
+            }
+        }
+        return;
+    }
     // Heavy modular units first in concurrent mode (longest-processing-time
     // order); kind order in PHASED / CANCEL mode so cheap early kinds can
     // raise lb before later units start.
@@ -292,30 +366,8 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
         if (hi < lo) continue;
         switch (kd) {
         case K_MT: case K_RAD2: push(kd, T_LOOKUP, lo, hi, LLW, 1); break;
-        case K_FS1: case K_VB2: {
-            const int64_t items = kd == K_VB2 ? s->n_vb2 : st.r;
-            int nsl = (int)((items + ISLICE - 1) / ISLICE);
-            if (nsl < 1) nsl = 1;
-            if (nsl > 1) s->need_final = 1;
-            push(kd, T_MOD, lo, hi, LMOD, nsl);
-            break;
-        }
-        default: {
-            // CCM1 / BJ1: a dense pass over the items at small lambda (the
-            // harmonic loop would be ~span/lambda L2 lookups), one warp per
-            // lambda while the loop is still long, one lane per lambda after.
-            const int64_t span = kd == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
-            const int64_t n = st.r > 0 ? st.r : 1;
-            int64_t sd = kd == K_CCM1 ? (64 * span) / (3 * n + 30) + 1 : (16 * span) / n + 1;
-            if (sd < lo) sd = lo;
-            if (sd > hi + 1) sd = hi + 1;
-            int64_t sp = span / 64 + 1;
-            if (sp < sd) sp = sd;
-            if (sp > hi + 1) sp = hi + 1;
-            push(kd, T_DIV, lo, sd - 1, st.r > 8192 ? 1 : 8, 1);
-            push(kd, T_WLOOK, sd, sp - 1, 1, 1);
-            push(kd, T_LOOKUP, sp, hi, LLW, 1);
-        }
+        case K_FS1: case K_VB2: push_mod(kd, lo, hi); break;
+        default: push_div_look(kd, lo, hi);
         }
     }
 }
@@ -339,13 +391,26 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
     int64_t* lam_out = p.lam_out;
     int64_t wmax = -1;
     int64_t n_eval = 0;
+    // pruned group (bplb_prune.cuh bounds against the live per-kind keys):
+    // skipped lambdas still count as evaluated (they provably cannot change
+    // the outputs)
+    const bool pruned = s->prune && u >= s->nA;
+    const int64_t lo_k = s->lo[kind];
     if (sg.type == T_LOOKUP) {
         const int64_t lam_a = sg.lo + rel * sg.chunk;
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
         n_eval = lam_b - lam_a + 1;
-        for (int64_t l0 = lam_a; l0 <= lam_b; l0 += 32) {
+        bool skip_unit = false;
+        if (pruned) {
+            const Thr th = thr_from_key(*(volatile u64*)&s->key[kind]);
+            skip_unit = (c / lam_a <= PR_QMAX) ? blk_skip(th, kind, lk, st, c, lo_k, lam_a, lam_b)
+                                               : range_skip(th, kind, st, c, lo_k, lam_a, lam_b);
+        }
+        for (int64_t l0 = lam_a; l0 <= lam_b && !skip_unit; l0 += 32) {
             const int64_t lam = l0 + lane;
-            const bool valid = lam <= lam_b;
+            bool valid = lam <= lam_b;
+            if (pruned && valid) valid = !lam_skip(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam);
+            if (pruned && !__ballot_sync(0xffffffffu, valid)) continue;
             int64_t S = 0;
             if (valid) {
                 switch (kind) {
@@ -364,18 +429,22 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
         const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
         n_eval = lam_b - lam_a + 1;
         int64_t mine = 0;
+        unsigned done = 0;  // lanes whose lambda was evaluated
         for (int64_t lam = lam_a; lam <= lam_b; ++lam) {
+            if (pruned && lam_skip(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) continue;
             const int64_t S = kind == K_CCM1 ? ccm1_dense_raw(p.w, st.r, st, c, lam)
                                              : bj1_dense(p.w, st.r, c, lam);
             if (lam - lam_a == lane) mine = S;
+            done |= 1u << (lam - lam_a);
         }
         const int64_t lam = lam_a + lane;
-        const bool valid = lam <= lam_b;
+        const bool valid = lam <= lam_b && (done >> lane & 1u);
         int64_t bd = valid ? bplb_bound(mine, bplb_fc(kind, c, lam)) : 0;
         wmax = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
     } else if (sg.type == T_WLOOK) {
         const int64_t lam = sg.lo + rel;
         n_eval = 1;
+        if (pruned && lam_skip(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) goto tail;
         int64_t S;
         if (kind == K_CCM1) {
             int64_t part = bplb_ccm1_part(lk, st, c, lam, 1 + lane, 32);
@@ -388,8 +457,10 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
             rem = (int64_t)warp_sum_u64((u64)rem);
             S = bplb_bj1_from_parts(c, lam, fl, rem);
         }
-        int64_t bd = bplb_bound(S, bplb_fc(kind, c, lam));
-        wmax = emit_warp(lane == 0, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
+        {
+            int64_t bd = bplb_bound(S, bplb_fc(kind, c, lam));
+            wmax = emit_warp(lane == 0, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
+        }
     } else {  // T_MOD
         const long long chunk = rel / sg.nslice;
         const int slice = (int)(rel % sg.nslice);
@@ -399,6 +470,15 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
         const int n_items = kind == K_VB2 ? s->n_vb2 : st.r;
         const int* items = kind == K_VB2 ? b.vb2 : p.w;
         const int i0 = slice * ISLICE, i1 = min(n_items, i0 + ISLICE);
+        if (s->prune && kind == K_VB2) {
+            // one decision per walk chunk, identical in every slice: the keys
+            // snapshotted after the seeds (chunk_ok gates wide_final)
+            if (pruned && range_skip(thr_from_key(s->thr[K_VB2]), kind, st, c, lo_k, lam_a, lam_b)) {
+                n_eval = slice == 0 ? L : 0;
+                goto tail;
+            }
+            if (slice == 0 && lane == 0) b.chunk_ok[(lam_a - lo_k) / LMOD] = 1;
+        }
         const int warp = threadIdx.x >> 5;
         u64* t = tot + warp * LMOD;
         for (int j = lane; j < LMOD; j += kWarp) t[j] = 0;
@@ -429,6 +509,7 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
             }
         }
     }
+tail:
     if (lane == 0) {
         if (n_eval) atomicAdd(&s->evals[kind], (unsigned long long)n_eval);
         s->evaluated[kind] = 1;
@@ -439,7 +520,7 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
 // Persistent warp-unit kernel.  phase_kind >= 0 restricts to that kind's
 // segments (PHASED mode) and applies the Alg. 4 entry guard lb <= k.
 template <bool WIDE>
-__global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phase_kind) {
+__global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phase_kind, int part) {
     __shared__ u64 tot[(WT / 32) * LMOD];
     __shared__ long long u_begin, u_end;
     __shared__ int skip;
@@ -452,6 +533,12 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
             const int f = s->kind_seg_first[phase_kind], n = s->kind_seg_count[phase_kind];
             u_begin = n ? s->segs[f].first : 0;
             u_end = n ? s->segs[f + n - 1].first + s->segs[f + n - 1].count : 0;
+        } else if (part == 1) {  // pruning: the seeds
+            u_begin = 0;
+            u_end = s->nA;
+        } else if (part == 2) {  // pruning: the rest
+            u_begin = s->nA;
+            u_end = s->nunits;
         } else {
             u_begin = 0;
             u_end = s->nunits;
@@ -470,6 +557,13 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
         if (cancel && (int64_t)(*(volatile int*)&s->lb) > p.k) continue;
         wide_unit<WIDE>(p, b, s, lk, u, tot);
     }
+}
+
+// Pruning: snapshot the per-kind keys after the seeds, reset the unit counter.
+__global__ void wide_snapshot(WideBufs b) {
+    WideState* s = b.state;
+    for (int kd = 0; kd < K_COUNT; ++kd) s->thr[kd] = s->key[kd];
+    s->unit_next = 0;
 }
 
 // Reset the unit counter between phased launches and record the kind.
@@ -497,7 +591,8 @@ __global__ void __launch_bounds__(WT) wide_final(KParams p, WideBufs b, int only
         for (int64_t l0 = lo + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); l0 <= hi;
              l0 += stride) {
             const int64_t lam = l0 + (threadIdx.x & 31);
-            const bool valid = lam <= hi;
+            bool valid = lam <= hi;
+            if (valid && s->prune && kd == K_VB2) valid = b.chunk_ok[(lam - lo) / LMOD] != 0;
             int64_t S = 0;
             if (valid)
                 S = kd == K_VB2 ? bplb_vb2_sum(s->st, p.c, lam, b.acc[lam])
@@ -597,8 +692,12 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     wide_stats<<<g_stats, WT, 0, st>>>(b, p.w, r, c);
     wide_scan_reduce<<<(unsigned)nb, WT, 0, st>>>(b, c);
     wide_scan_apply<<<(unsigned)nb, WT, 0, st>>>(b, c);
+    // bound pruning: full-collection checks (no per-lambda output) inside the
+    // integer envelope of the bplb_prune.cuh bounds
+    const bool prune = !phased && !(p.flags & (BPLB_F_CANCEL | BPLB_F_NOPRUNE)) && !p.lam_out && !p.use_range &&
+                       c <= WIDE_PRUNE_MAX_C && r <= WIDE_PRUNE_MAX_R;
     wide_plan<<<1, 1, 0, st>>>(b, c, p.nk, nullptr, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3],
-                               ks[4], ks[5], (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0);
+                               ks[4], ks[5], (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0, prune ? 1 : 0);
     *launches += 5;
     int per_sm = 0;
     const bool wide = c >= (1 << 23);
@@ -607,16 +706,23 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     if (per_sm < 1) per_sm = 1;
     const int grid = per_sm * num_sms;
     const int g_fin = num_sms * 2;
-    if (phased) {
+    if (prune) {
+        units<<<grid, WT, 0, st>>>(p, b, -1, 1);
+        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
+        wide_snapshot<<<1, 1, 0, st>>>(b);
+        units<<<grid, WT, 0, st>>>(p, b, -1, 2);
+        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
+        *launches += 5;
+    } else if (phased) {
         for (int i = 0; i < p.nk; ++i) {
             wide_phase_begin<<<1, 1, 0, st>>>(b, i);
-            units<<<grid, WT, 0, st>>>(p, b, p.kinds[i]);
+            units<<<grid, WT, 0, st>>>(p, b, p.kinds[i], 0);
             wide_final<<<g_fin, WT, 0, st>>>(p, b, p.kinds[i]);
             wide_phase_end<<<1, 1, 0, st>>>(b, p.k);
             *launches += 4;
         }
     } else {
-        units<<<grid, WT, 0, st>>>(p, b, -1);
+        units<<<grid, WT, 0, st>>>(p, b, -1, 0);
         wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
         *launches += 2;
     }

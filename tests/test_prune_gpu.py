@@ -203,3 +203,37 @@ def test_cfg5_device_batch_matches_golden_nodes(eng):
                                lb.data_ptr(), ex.data_ptr(), stream_ptr=s.cuda_stream)
         s.synchronize()
         assert int(lb[0]) == int(g["lb"][j])
+
+
+@pytest.mark.parametrize("shape", [("cfg4", 0, 0), ("u", 30_000, 1_000_000), ("u", 20_000, 262_147),
+                                   ("tri", 9_000, 99_991), ("small", 40_000, 700_001)])
+def test_wide_path_pruned_equals_dense(eng, shape):
+    """Single checks on the grid-wide path (r > 16384 or c large): the pruned
+    full collection (seed launch, keys snapshot, pruned launch) returns the
+    same per-kind best, arg lambda, lb and evals as the dense sweep; cfg4
+    also against the reference goldens (VB2: 50011 at lambda 3)."""
+    kind, r, c = shape
+    rng = np.random.default_rng(r + c)
+    if kind == "cfg4":
+        c, w = W.cfg4()
+    elif kind == "u":
+        w = rng.integers(1, c + 1, r)
+    elif kind == "tri":
+        w = rng.integers(c // 4 + 1, c // 2, r)
+    else:
+        w = rng.integers(1, c // 50, r)
+    w = w.astype(np.int32)
+    a = eng.check(w, c, 2**62, ALL, 0)
+    assert eng.last_path()[0] == "wide"
+    b = eng.check(w, c, 2**62, ALL, _native.F_NOPRUNE)
+    for f in ("best", "arg_lambda", "evals", "evaluated"):
+        assert list(getattr(a, f)) == list(getattr(b, f)), f
+    assert a.lb == b.lb
+    if kind == "cfg4":
+        import os
+
+        g = np.load(os.path.join(os.path.dirname(__file__), "golden", "configs.npz"))
+        want = g["cfg4_best_nonvb2"].tolist()
+        got = list(a.best)
+        assert [x for i, x in enumerate(got) if i != 4] == [x for i, x in enumerate(want) if i != 4]
+        assert got[4] == 50011 and a.arg_lambda[4] == 3
