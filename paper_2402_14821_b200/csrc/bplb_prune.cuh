@@ -174,7 +174,9 @@ __device__ __forceinline__ bool ub_le_vb2(const NodeStats& st, int64_t c, int64_
     return 2 * fs - 2 * y + K * (lam - 1) <= 2 * B * (lam - 1);
 }
 
-// (32-bit divisions while Vs, Vm < 2^32: always in the node-kernel envelope)
+// (32-bit divisions in the node-kernel envelope, Vs, Vm < 2^32; WENV: the
+// grid-wide path's envelope, c <= 2^20, r <= 2^17, 64-bit divisions)
+template <bool WENV = false>
 __device__ __forceinline__ bool ub_le_ccm1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
     const uint32_t L = (uint32_t)lam;
     const int64_t q = (int64_t)((uint32_t)c / L);
@@ -182,15 +184,12 @@ __device__ __forceinline__ bool ub_le_ccm1(const NodeStats& st, int64_t c, int64
     const int64_t lhs = 2 * st.Vs - 2 * st.Vm + 2 * (int64_t)st.n_big * (lam - 1);
     if (lhs <= (2 * B - K) * q * lam) return true;
     const int64_t z = st.Vm - (int64_t)st.n_big * (lam - 1);
-    int64_t y, fs;
-    if (((uint64_t)st.Vs | (uint64_t)(z > 0 ? z : 0)) >> 32) {  // grid-wide sizes
-        y = z > 0 ? (z + lam - 1) / lam : 0;
-        fs = st.Vs / lam;
-    } else {
-        y = z > 0 ? (int64_t)(((uint32_t)z + L - 1) / L) : 0;
-        fs = (int64_t)((uint32_t)st.Vs / L);
+    if (WENV) {
+        const int64_t y = z > 0 ? (z + lam - 1) / lam : 0;
+        return 2 * (st.Vs / lam) + K * q - 2 * y <= 2 * B * q;
     }
-    return 2 * fs + K * q - 2 * y <= 2 * B * q;
+    const int64_t y = z > 0 ? (int64_t)(((uint32_t)z + L - 1) / L) : 0;
+    return 2 * (int64_t)((uint32_t)st.Vs / L) + K * q - 2 * y <= 2 * B * q;
 }
 
 __device__ __forceinline__ bool ub_le_bj1(const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
@@ -198,10 +197,11 @@ __device__ __forceinline__ bool ub_le_bj1(const NodeStats& st, int64_t c, int64_
     return st.W <= B * (c - cm);
 }
 
+template <bool WENV = false>
 __device__ __forceinline__ bool ub_le(int kind, const NodeStats& st, int64_t c, int64_t lam, int64_t B) {
     if (B < 0) return false;
     if (kind == K_VB2) return ub_le_vb2(st, c, lam, B);
-    if (kind == K_CCM1) return ub_le_ccm1(st, c, lam, B);
+    if (kind == K_CCM1) return ub_le_ccm1<WENV>(st, c, lam, B);
     return ub_le_bj1(st, c, lam, B);
 }
 
@@ -271,7 +271,7 @@ __device__ __forceinline__ int64_t lk_excess(const LK& lk, int64_t lo, int64_t h
 // crosses a step (w in [t l1, t l2 - 1]) contributes < t + 1.  Summing
 // (W / N lookups per bucket):  sum f(w)/f(c) <= (I + X2/P(l2) + X1/P(l1)) / q.
 // Integer envelope: c <= 2^20, r <= 2^17, q <= PR_QMAX (the final comparison in 128 bits).
-template <class LK>
+template <class LK, bool WENV>
 __device__ __forceinline__ bool bj1_blk_q_le(const LK& lk, const NodeStats& st, int64_t c, int64_t q,
                                              int64_t l1, int64_t l2, int64_t B) {
     const int64_t P1 = (q + 1) * l1 - c, P2 = (q + 1) * l2 - c;
@@ -292,20 +292,22 @@ __device__ __forceinline__ bool bj1_blk_q_le(const LK& lk, const NodeStats& st, 
         }
         if (t >= 1 && l2 > l1) I += (int64_t)(t + 1) * (lk.n_le((int64_t)t * l2 - 1) - lk.n_le((int64_t)t * l1 - 1));
     }
-    // 128-bit: the grid-wide path (c <= 2^20, r <= 2^17) exceeds 2^63 here
+    // node kernel envelope (c <= 2^18, r <= 2^14): every product < 2^60; the
+    // grid-wide path (c <= 2^20, r <= 2^17) compares in 128 bits
+    if (!WENV) return I * P1 * P2 + X2 * P1 + X1 * P2 <= B * q * P1 * P2;
     const __int128 P12 = (__int128)P1 * P2;
     return (__int128)I * P12 + (__int128)X2 * P1 + (__int128)X1 * P2 <= (__int128)B * q * P12;
 }
 
 // BJ1 on any [l1, l2]: split at the q-interval ends (at most 8 pieces).
-template <class LK>
+template <class LK, bool WENV>
 __device__ __forceinline__ bool bj1_blk_le(const LK& lk, const NodeStats& st, int64_t c, int64_t l1,
                                            int64_t l2, int64_t B) {
     int64_t a = l1;
     for (int piece = 0; piece < 8 && a <= l2; ++piece) {
         const int64_t q = (int64_t)((uint32_t)c / (uint32_t)a);
         const int64_t e = min(l2, (int64_t)((uint32_t)c / (uint32_t)q));
-        if (!bj1_blk_q_le(lk, st, c, q, a, e, B)) return false;
+        if (!bj1_blk_q_le<LK, WENV>(lk, st, c, q, a, e, B)) return false;
         a = e + 1;
     }
     return a > l2;
@@ -314,11 +316,11 @@ __device__ __forceinline__ bool bj1_blk_le(const LK& lk, const NodeStats& st, in
 // Out of line (like the other heavy helpers below): prune_kernel inlined
 // everything into ~640 KB of SASS, and instruction-fetch stalls led its
 // warp-state samples; one copy of each loop keeps the hot code in cache.
-template <class LK>
+template <class LK, bool WENV>
 __device__ __noinline__ bool blk_ub_le(int kind, const LK lk, const NodeStats& st, int64_t c, int64_t l1,
                                        int64_t l2, int64_t B) {
     if (B < 0) return false;
-    return kind == K_CCM1 ? ccm1_blk_le(lk, st, c, l1, l2, B) : bj1_blk_le(lk, st, c, l1, l2, B);
+    return kind == K_CCM1 ? ccm1_blk_le(lk, st, c, l1, l2, B) : bj1_blk_le<LK, WENV>(lk, st, c, l1, l2, B);
 }
 
 // Exact per-lambda sums through the lookup structure, one out-of-line copy.
@@ -390,14 +392,15 @@ __device__ __forceinline__ Thr thr_from_key(u64 key) {
     return t;
 }
 
+template <bool WENV = false>
 __device__ __forceinline__ bool lam_skip(const Thr& t, int kind, const NodeStats& st, int64_t c, int64_t lo,
                                          int64_t lam) {
     if (!t.has) return false;
-    if (t.lbmode) return ub_le(kind, st, c, lam, t.B);
+    if (t.lbmode) return ub_le<WENV>(kind, st, c, lam, t.B);
     const int64_t rel = lam - lo;
     if (rel == t.a_rel) return true;  // the current arg itself: already evaluated
-    if (rel > t.a_rel) return ub_le(kind, st, c, lam, t.B);
-    return t.B >= 1 && ub_le(kind, st, c, lam, t.B - 1);
+    if (rel > t.a_rel) return ub_le<WENV>(kind, st, c, lam, t.B);
+    return t.B >= 1 && ub_le<WENV>(kind, st, c, lam, t.B - 1);
 }
 
 __device__ __forceinline__ bool range_skip(const Thr& t, int kind, const NodeStats& st, int64_t c, int64_t lo,
@@ -408,13 +411,13 @@ __device__ __forceinline__ bool range_skip(const Thr& t, int kind, const NodeSta
     return t.B >= 1 && ub_le_range(kind, st, c, l1, l2, t.B - 1);
 }
 
-template <class LK>
+template <class LK, bool WENV = false>
 __device__ __forceinline__ bool blk_skip(const Thr& t, int kind, const LK& lk, const NodeStats& st, int64_t c,
                                          int64_t lo, int64_t l1, int64_t l2) {
     if (!t.has) return false;
-    if (t.lbmode) return blk_ub_le(kind, lk, st, c, l1, l2, t.B);
-    if (l1 - lo > t.a_rel) return blk_ub_le(kind, lk, st, c, l1, l2, t.B);
-    return t.B >= 1 && blk_ub_le(kind, lk, st, c, l1, l2, t.B - 1);
+    if (t.lbmode) return blk_ub_le<LK, WENV>(kind, lk, st, c, l1, l2, t.B);
+    if (l1 - lo > t.a_rel) return blk_ub_le<LK, WENV>(kind, lk, st, c, l1, l2, t.B);
+    return t.B >= 1 && blk_ub_le<LK, WENV>(kind, lk, st, c, l1, l2, t.B - 1);
 }
 
 // CCM1 dense sum over an unsorted item array in shared memory (the

@@ -403,13 +403,13 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
         bool skip_unit = false;
         if (pruned) {
             const Thr th = thr_from_key(*(volatile u64*)&s->key[kind]);
-            skip_unit = (c / lam_a <= PR_QMAX) ? blk_skip(th, kind, lk, st, c, lo_k, lam_a, lam_b)
+            skip_unit = (c / lam_a <= PR_QMAX) ? blk_skip<LkTableG, true>(th, kind, lk, st, c, lo_k, lam_a, lam_b)
                                                : range_skip(th, kind, st, c, lo_k, lam_a, lam_b);
         }
         for (int64_t l0 = lam_a; l0 <= lam_b && !skip_unit; l0 += 32) {
             const int64_t lam = l0 + lane;
             bool valid = lam <= lam_b;
-            if (pruned && valid) valid = !lam_skip(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam);
+            if (pruned && valid) valid = !lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam);
             if (pruned && !__ballot_sync(0xffffffffu, valid)) continue;
             int64_t S = 0;
             if (valid) {
@@ -431,7 +431,7 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
         int64_t mine = 0;
         unsigned done = 0;  // lanes whose lambda was evaluated
         for (int64_t lam = lam_a; lam <= lam_b; ++lam) {
-            if (pruned && lam_skip(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) continue;
+            if (pruned && lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) continue;
             const int64_t S = kind == K_CCM1 ? ccm1_dense_raw(p.w, st.r, st, c, lam)
                                              : bj1_dense(p.w, st.r, c, lam);
             if (lam - lam_a == lane) mine = S;
@@ -444,7 +444,7 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkT
     } else if (sg.type == T_WLOOK) {
         const int64_t lam = sg.lo + rel;
         n_eval = 1;
-        if (pruned && lam_skip(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) goto tail;
+        if (pruned && lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) goto tail;
         int64_t S;
         if (kind == K_CCM1) {
             int64_t part = bplb_ccm1_part(lk, st, c, lam, 1 + lane, 32);
