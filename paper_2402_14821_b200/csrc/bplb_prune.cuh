@@ -51,8 +51,14 @@ constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks o
 constexpr int PR_QMAX = 32;            // block bounds for CCM1 where floor(c / lambda) <= PR_QMAX
 constexpr int PR_QMAX_BJ1 = 32;        // ... and for BJ1 (its block bound costs O(q) lookups per q-piece)
 constexpr int PR_BLK_UNIT = 32 * 256;  // lambdas per block unit: 32 blocks of 256, one per lane
-constexpr int PR_QCAP = 2048;
-constexpr unsigned PR_QEMPTY = 0x7FFFFFFFu;  // a reserved queue slot with nothing to do          // CTA queue: CCM1/BJ1 256-lambda blocks and 32-lambda sub-ranges left to evaluate
+#ifndef PR_MINB
+#define PR_MINB 3  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef PR_QCAP_N
+#define PR_QCAP_N 2048
+#endif
+constexpr int PR_QCAP = PR_QCAP_N;  // CTA queue: CCM1/BJ1 256-lambda blocks and 32-lambda sub-ranges left to evaluate
+constexpr unsigned PR_QEMPTY = 0x7FFFFFFFu;  // a reserved queue slot with nothing to do
 constexpr int PR_MAX_SEGS = 20;
 
 enum { PU_CAND = 0, PU_LOOK = 1, PU_WALK = 2, PU_PRUNE = 3, PU_BLK = 4 };
@@ -902,7 +908,7 @@ __device__ void prune_run(const KParams& p, PruneCtl& ctl, const LK& lk, const P
 }
 
 // lbmode: only lb / exceeded are produced (cross-kind pruning).
-__global__ void __launch_bounds__(PNT, 3) prune_kernel(KParams p, int rcap, int lbmode) {
+__global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap, int lbmode) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PruneCtl ctl;
     const int64_t c = p.c;
