@@ -44,7 +44,10 @@
 
 namespace bplb {
 
-constexpr int PNT = 256;
+#ifndef PR_PNT
+#define PR_PNT 256  // threads per CTA (one node per CTA at a time)
+#endif
+constexpr int PNT = PR_PNT;
 constexpr int PNW = PNT / 32;
 constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in smem
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
