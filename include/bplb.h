@@ -56,6 +56,7 @@ extern "C" {
 #define BPLB_F_NOPRUNE 0x10 /* dense sweep: evaluate every lambda of the grid (the paper's
                                Alg. 2-4 work) instead of skipping the lambdas whose integer
                                upper bound cannot change the result (bplb_prune.cuh) */
+#define BPLB_F_NOTC   0x20  /* batched calls: the table path on the FP32 pipe, not tcgen05 (parity testing) */
 #define BPLB_F_NOTAB  0x8   /* batched calls: do not use the histogram x table kernel
                                (selects the warp-per-node kernel; parity testing) */
 
@@ -202,6 +203,7 @@ BPLB_API double bplb_last_kernel_ms(bplb_engine *eng);
 #define BPLB_PATH_NODE_SORT 5    /* CTA-per-node kernel, sorted weights                */
 #define BPLB_PATH_WIDE 6         /* grid-wide kernels (one large instance)             */
 #define BPLB_PATH_PRUNE 7        /* CTA-per-node bound-pruned sweep (bplb_prune.cuh)   */
+#define BPLB_PATH_TC 8           /* histogram x table contraction on tcgen05 (bplb_tc.cuh) */
 BPLB_API int bplb_last_path(bplb_engine *eng, int32_t *detail);
 
 /* Thread-local message describing the last error on this thread. */

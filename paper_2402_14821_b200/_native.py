@@ -23,9 +23,11 @@ F_CANCEL = 0x2
 F_TIMING = 0x4
 F_NOTAB = 0x8  # batched: skip the histogram x table kernel (parity testing)
 F_NOPRUNE = 0x10  # dense sweep: every lambda evaluated (no bound pruning)
+F_NOTC = 0x20  # batched table path on the FP32 pipe instead of the tensor cores (parity testing)
 
 # bplb_last_path ids (include/bplb.h)
-PATHS = {0: "none", 1: "tab", 2: "tab_single", 3: "warp", 4: "node_table", 5: "node_sort", 6: "wide", 7: "prune"}
+PATHS = {0: "none", 1: "tab", 2: "tab_single", 3: "warp", 4: "node_table", 5: "node_sort", 6: "wide", 7: "prune",
+         8: "tc"}
 
 E_INVAL, E_RANGE, E_CUDA, E_NOMEM, E_NODEV = -1, -2, -3, -4, -5
 

@@ -17,6 +17,7 @@
 #include "bplb_wide.cuh"
 #include "bplb_warp.cuh"
 #include "bplb_tab.cuh"
+#include "bplb_tc.cuh"
 #include "bplb_reduce.cuh"
 #include <thread>
 #include <vector>
@@ -172,6 +173,11 @@ struct bplb_engine {
     // instead (BPLB_WIDE_PRUNE_MIN_CELLS): off by default -- cfg3 (r * c = 1e8)
     // measured 172 us there vs 104 us on the multi-CTA node kernel
     int64_t wide_prune_min_cells = (int64_t)1 << 62;
+    bool tc_on = true;          // BPLB_TC=0: the table path on the FP32 pipe instead of tcgen05
+    DevBuf d_tcB, d_tcmeta;     // tensor-core table planes / column constants
+    int64_t tc_c = -1;
+    int tc_kmask = -1, tc_KT = 0, tc_nnt = 0;
+    size_t tc_attr_smem = 0;
     bool assign_carveout = false;
     bool single_cluster_ok = true;    // drop-in checks as one thread-block cluster
     bool single_cluster_attr = false;
@@ -537,10 +543,67 @@ int tab_fin(bplb_engine* e, bplb::KParams p, int64_t n_nodes) {
     return 0;
 }
 
+// Tensor-core planes of the cached table (bplb_tc.cuh), rebuilt with it.
+int tc_ensure(bplb_engine* e) {
+    if (e->tc_c == e->tab_c && e->tc_kmask == e->tab_kmask) return 0;
+    const int c = (int)e->tab_c;
+    const int KT = (c + 31) / 32 * 32;
+    const int ncols = e->tab_nsub * bplb::TAB_SUB;
+    const int nnt = (ncols + bplb::TC_NT - 1) / bplb::TC_NT;
+    int rc;
+    if ((rc = e->d_tcB.grow((size_t)nnt * bplb::tc_b_bytes(KT)))) return rc;
+    if ((rc = e->d_tcmeta.grow((size_t)nnt * bplb::TC_NT * sizeof(int4)))) return rc;
+    const int64_t n = (int64_t)nnt * bplb::TC_NT * KT;
+    bplb::tc_build_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4 * e->num_sms), 256, 0, e->stream>>>(
+        (uint8_t*)e->d_tcB.p, (int4*)e->d_tcmeta.p, (const float*)e->d_tab.p, (const int4*)e->d_tabmeta.p, e->tab_KV,
+        e->tab_nsub, KT, nnt, c);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    e->tc_c = e->tab_c;
+    e->tc_kmask = e->tab_kmask;
+    e->tc_KT = KT;
+    e->tc_nnt = nnt;
+    return 0;
+}
+
+bool tc_fits(const bplb_engine* e, int64_t c) {
+    const int KT = (int)(c + 31) / 32 * 32;
+    return e->tc_on && bplb::tc_smem_bytes(KT) + 256 <= e->smem_optin;
+}
+
+// The batch on the tensor cores: one 128-node CTA per tile, one launch.
+int launch_tc(bplb_engine* e, bplb::KParams& p, int64_t n_nodes) {
+    int rc;
+    if ((rc = tc_ensure(e))) return rc;
+    const size_t smem = bplb::tc_smem_bytes(e->tc_KT);
+    auto kern = p.wbytes == 1 ? bplb::tc_kernel<1> : (p.wbytes == 2 ? bplb::tc_kernel<2> : bplb::tc_kernel<4>);
+    if (smem > e->tc_attr_smem) {
+        for (auto k : {bplb::tc_kernel<1>, bplb::tc_kernel<2>, bplb::tc_kernel<4>})
+            CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        e->tc_attr_smem = smem;
+    }
+    bplb::TcDev t{(const uint8_t*)e->d_tcB.p, (const int4*)e->d_tcmeta.p, e->tc_KT, e->tc_nnt};
+    p.n_nodes = n_nodes;
+    const int64_t grid = (n_nodes + bplb::TC_M - 1) / bplb::TC_M;
+    if (grid < 1) return 0;
+    if (e->prof_kernel) CUDA_TRY(cudaEventRecord(e->ev_pk0, e->stream));
+    kern<<<(unsigned)grid, bplb::TC_THREADS, smem, e->stream>>>(p, t);
+    e->launches++;
+    CUDA_TRY(cudaGetLastError());
+    if (e->prof_kernel) {
+        CUDA_TRY(cudaEventRecord(e->ev_pk1, e->stream));
+        e->prof_recorded = 1;
+    }
+    e->last_path = BPLB_PATH_TC;
+    e->last_detail = (int)e->tc_nnt;
+    return 0;
+}
+
 int launch_tab(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int slot) {
     (void)slot;
     int rc;
     if ((rc = tab_ensure(e, p))) return rc;
+    if (!(p.flags & BPLB_F_NOTC) && tc_fits(e, p.c)) return launch_tc(e, p, n_nodes);
     if ((rc = tab_reserve(e, p.node0 + n_nodes))) return rc;
     if (p.node0 % bplb::TAB_TM) return fail(BPLB_EINVAL, "table path sub-range must start on a 16-node tile");
     if ((rc = tab_hist(e, p, n_nodes))) return rc;
@@ -602,9 +665,10 @@ int launch_tab_graph(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t 
     slot->used = ++e->graph_clock;
     cudaError_t ce = cudaGraphLaunch(slot->exec, s);
     if (ce != cudaSuccess) return fail(BPLB_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce));
-    e->launches += 3;
-    e->last_path = BPLB_PATH_TAB;
-    e->last_detail = tab_warps(e, e->tab_KV, 2);
+    const bool tc = !(p.flags & BPLB_F_NOTC) && tc_fits(e, p.c);  // what the captured launch_tab ran
+    e->launches += tc ? 1 : 3;
+    e->last_path = tc ? BPLB_PATH_TC : BPLB_PATH_TAB;
+    e->last_detail = tc ? e->tc_nnt : tab_warps(e, e->tab_KV, 2);
     return 0;
 }
 
@@ -771,6 +835,7 @@ int bplb_engine_create(int device, bplb_engine** out) {
     if (const char* v = getenv("BPLB_HIST_PER_SM")) e->hist_per_sm = std::max(1, atoi(v));
     if (const char* v = getenv("BPLB_MULTI_GRID")) e->multi_grid = atoll(v);
     if (const char* v = getenv("BPLB_WIDE_PRUNE_MIN_CELLS")) e->wide_prune_min_cells = atoll(v);
+    if (const char* v = getenv("BPLB_TC")) e->tc_on = atoi(v) != 0;
     if (const char* v = getenv("BPLB_SINGLE_CLUSTER")) e->single_cluster_ok = atoi(v) != 0;  // A/B switch
 #ifdef TAB_TRACE
     e->graphs_ok = false;  // stamps are read back per launch
@@ -798,7 +863,8 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
                       &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
-                      &e->d_tabkeys, &e->d_tabhist, &e->d_tabready, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys})
+                      &e->d_tabkeys, &e->d_tabhist, &e->d_tabready, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys,
+                      &e->d_tcB, &e->d_tcmeta})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -1575,6 +1641,13 @@ BPLB_API int bplb_prune_trace(long long* out, int cap) {
     int z = 0;
     cudaMemcpyToSymbol(bplb::g_prune_trace_n, &z, sizeof(int));
     return n;
+}
+#endif
+
+#ifdef TC_TRACE
+BPLB_API int bplb_tc_trace(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, bplb::g_tc_trace, 64 * 8);
+    return 0;
 }
 #endif
 
