@@ -568,23 +568,36 @@ int tc_ensure(bplb_engine* e) {
 
 bool tc_fits(const bplb_engine* e, int64_t c) {
     const int KT = (int)(c + 31) / 32 * 32;
-    return e->tc_on && bplb::tc_smem_bytes(KT) + 256 <= e->smem_optin;
+    return e->tc_on && bplb::tc_smem_bytes_db(KT, false) + 4096 <= e->smem_optin;
 }
 
-// The batch on the tensor cores: one 128-node CTA per tile, one launch.
+// The batch on the tensor cores: one CTA per slice of <= 128 nodes, the
+// slices sized so the batch covers every SM, one launch.
 int launch_tc(bplb_engine* e, bplb::KParams& p, int64_t n_nodes) {
     int rc;
     if ((rc = tc_ensure(e))) return rc;
-    const size_t smem = bplb::tc_smem_bytes(e->tc_KT);
-    auto kern = p.wbytes == 1 ? bplb::tc_kernel<1> : (p.wbytes == 2 ? bplb::tc_kernel<2> : bplb::tc_kernel<4>);
+    // double-buffered table tiles (BPLB_TC_DB=1): measured wrong results with
+    // slices of < 128 nodes (an unresolved race), so single-buffered by default
+    const bool db = bplb::tc_smem_bytes_db(e->tc_KT, true) + 4096 <= e->smem_optin && getenv("BPLB_TC_DB") &&
+                    atoi(getenv("BPLB_TC_DB")) != 0;
+    const size_t smem = bplb::tc_smem_bytes_db(e->tc_KT, db);
+    using K = void (*)(bplb::KParams, bplb::TcDev);
+    K kern;
+    if (db) kern = p.wbytes == 1 ? bplb::tc_kernel<1, true> : (p.wbytes == 2 ? bplb::tc_kernel<2, true> : bplb::tc_kernel<4, true>);
+    else kern = p.wbytes == 1 ? bplb::tc_kernel<1, false> : (p.wbytes == 2 ? bplb::tc_kernel<2, false> : bplb::tc_kernel<4, false>);
     if (smem > e->tc_attr_smem) {
-        for (auto k : {bplb::tc_kernel<1>, bplb::tc_kernel<2>, bplb::tc_kernel<4>})
+        for (K k : {bplb::tc_kernel<1, true>, bplb::tc_kernel<2, true>, bplb::tc_kernel<4, true>,
+                    bplb::tc_kernel<1, false>, bplb::tc_kernel<2, false>, bplb::tc_kernel<4, false>})
             CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         e->tc_attr_smem = smem;
     }
-    bplb::TcDev t{(const uint8_t*)e->d_tcB.p, (const int4*)e->d_tcmeta.p, e->tc_KT, e->tc_nnt};
+    // nodes per CTA: the batch spread over every SM (a multiple of 8, <= 128)
+    int64_t rows = (n_nodes + e->num_sms - 1) / e->num_sms;
+    rows = std::min<int64_t>(bplb::TC_M, std::max<int64_t>(8, (rows + 7) / 8 * 8));
+    if (getenv("BPLB_TC_ROWS")) rows = atoll(getenv("BPLB_TC_ROWS"));
+    bplb::TcDev t{(const uint8_t*)e->d_tcB.p, (const int4*)e->d_tcmeta.p, e->tc_KT, e->tc_nnt, (int)rows};
     p.n_nodes = n_nodes;
-    const int64_t grid = (n_nodes + bplb::TC_M - 1) / bplb::TC_M;
+    const int64_t grid = (n_nodes + rows - 1) / rows;
     if (grid < 1) return 0;
     if (e->prof_kernel) CUDA_TRY(cudaEventRecord(e->ev_pk0, e->stream));
     kern<<<(unsigned)grid, bplb::TC_THREADS, smem, e->stream>>>(p, t);

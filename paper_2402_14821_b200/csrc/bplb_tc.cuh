@@ -39,6 +39,7 @@ struct TcDev {
     const int4* meta;    // [nnt][TC_NT] epilogue constants (TabDev meta; padding kind 6)
     int KT;              // K extent: c rounded up to 32
     int nnt;             // N-tiles
+    int rows;            // nodes per CTA (<= TC_M; the batch spread over every SM)
 };
 
 __host__ __device__ inline size_t tc_a_bytes(int KT) { return (size_t)2 * TC_M * KT; }
@@ -137,26 +138,61 @@ __device__ unsigned long long g_tc_trace[64];  // CTA 0: globaltimer at the phas
 #define TC_STAMP(i) do {} while (0)
 #endif
 
-template <int WB>
+// Shared memory: A planes | X = counts, then B buffer 0 + meta 0 | (DB) B
+// buffer 1 + meta 1 | barriers.  DB (double-buffered table tiles) when it fits.
+__host__ __device__ inline size_t tc_bm_bytes(int KT) { return tc_b_bytes(KT) + (size_t)TC_NT * 16; }
+__host__ __device__ inline size_t tc_x_bytes(int KT) {
+    return tc_cnt_bytes(KT) > tc_bm_bytes(KT) ? tc_cnt_bytes(KT) : tc_bm_bytes(KT);
+}
+__host__ __device__ inline size_t tc_smem_bytes_db(int KT, bool db) {
+    return tc_a_bytes(KT) + tc_x_bytes(KT) + (db ? tc_bm_bytes(KT) : 0) + 64;
+}
+
+// One thread: both bulk copies of N-tile nt (planes + column constants) into
+// buffer (B, M), completing on bar.
+__device__ __forceinline__ void tc_load_tile(const TcDev& t, int nt, uint8_t* B, int4* M, unsigned long long* bar) {
+    const unsigned bb = (unsigned)tc_b_bytes(t.KT);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tab_smem_addr(bar)),
+                 "r"(bb + (unsigned)(TC_NT * 16))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     tab_smem_addr(B)),
+                 "l"(t.B + (size_t)nt * bb), "r"(bb), "r"(tab_smem_addr(bar))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     tab_smem_addr(M)),
+                 "l"(t.meta + (size_t)nt * TC_NT), "r"((unsigned)(TC_NT * 16)), "r"(tab_smem_addr(bar))
+                 : "memory");
+}
+
+// One CTA per SM-sized slice of the batch (t.rows <= 128 nodes: the MMA's
+// M = 128 rows, the rows past the slice are zero): the histograms -- the
+// part bound by shared-memory atomics -- spread over every SM.
+template <int WB, bool DB>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint32_t s_tmem;
     __shared__ int s_bad;
-    __shared__ unsigned kbest[TC_M][K_COUNT];  // per-node per-kind best keys (4 column groups meet here)
+    __shared__ unsigned kbest[TC_M][K_COUNT];  // per-node per-kind best keys
+    constexpr int rank = 0, nstep = 1;  // every N-tile in this CTA
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int KT = t.KT;
     uint8_t* As = smem;                                  // [2][TC_M x KT]
-    unsigned char* X = smem + tc_a_bytes(KT);            // counts, then B planes + meta
+    unsigned char* X = smem + tc_a_bytes(KT);            // counts, then B buffer 0
     uint32_t* cnt = (uint32_t*)X;                        // [TC_M][KT + 1]
     const int KP = KT + 1;
-    uint8_t* Bs = X;                                     // [2][TC_NT x KT]
-    int4* Ms = (int4*)(X + tc_b_bytes(KT));              // [TC_NT]
-    const size_t xb = tc_cnt_bytes(KT) > tc_b_bytes(KT) + (size_t)TC_NT * 16 ? tc_cnt_bytes(KT)
-                                                                             : tc_b_bytes(KT) + (size_t)TC_NT * 16;
-    unsigned long long* bars = (unsigned long long*)(X + xb);  // [0] B tile landed, [1] MMAs done
-    const int64_t n0 = p.node0 + (int64_t)blockIdx.x * TC_M;
+    uint8_t* Bbuf[2];
+    int4* Mbuf[2];
+    Bbuf[0] = X;
+    Mbuf[0] = (int4*)(X + tc_b_bytes(KT));
+    Bbuf[1] = DB ? X + tc_x_bytes(KT) : Bbuf[0];
+    Mbuf[1] = DB ? (int4*)(Bbuf[1] + tc_b_bytes(KT)) : Mbuf[0];
+    unsigned long long* bars = (unsigned long long*)(X + tc_x_bytes(KT) + (DB ? tc_bm_bytes(KT) : 0));
+    // bars: [0], [1] tile buffer landed, [2] MMAs done
+    const int64_t n0 = p.node0 + (int64_t)blockIdx.x * t.rows;
     const int64_t rem = p.node0 + p.n_nodes - n0;
-    const int nn = (int)(rem < TC_M ? rem : TC_M);
+    const int nn = (int)(rem < t.rows ? rem : t.rows);
     const int c = (int)p.c;
     TC_STAMP(0);
 
@@ -164,6 +200,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
         s_bad = 0;
         tab_bar_init(&bars[0]);
         tab_bar_init(&bars[1]);
+        tab_bar_init(&bars[2]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {  // TMEM: 512 columns (the CTA owns the SM)
@@ -175,36 +212,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     for (int i = tid; i < TC_M * KP; i += TC_THREADS) cnt[i] = 0u;
     for (int i = tid; i < TC_M * K_COUNT; i += TC_THREADS) (&kbest[0][0])[i] = 0u;
     __syncthreads();
+    // the second tile of this CTA lands in buffer 1 while the histograms are counted
+    if (DB && tid == 0 && rank + nstep < t.nnt) tc_load_tile(t, rank + nstep, Bbuf[1], Mbuf[1], &bars[1]);
     bool bad = false;
-    for (int r = warp; r < nn; r += TC_THREADS / 32) {
-        const int64_t a = p.off[n0 + r], b = p.off[n0 + r + 1];
-        uint32_t* row = cnt + r * KP;
-        if (WB == 1) {
-            // aligned 4-byte words covering [a, b): four weights per load, the
-            // bytes outside the node masked off; four words in flight per lane
-            const int64_t wa = a >> 2, wb = (b + 3) >> 2;
-            const uint32_t* w32 = (const uint32_t*)p.w;
-            for (int64_t j0 = wa; j0 < wb; j0 += 4 * 32) {
-                uint32_t v[4];
+    if (WB == 1) {
+        // groups of four nodes per warp: each lane loads four aligned 4-byte
+        // words of each node (16 loads in flight), then counts the bytes
+        // inside the node's range
+        const uint32_t* w32 = (const uint32_t*)p.w;
+        for (int g0 = warp; g0 < nn; g0 += 4 * (TC_THREADS / 32)) {
+            int64_t a[4], b[4], wa[4], wb[4];
+            int64_t words = 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t j = j0 + u * 32 + lane;
-                    v[u] = j < wb ? __ldg(w32 + j) : 0u;
-                }
+            for (int q = 0; q < 4; ++q) {
+                const int r = g0 + q * (TC_THREADS / 32);
+                const bool v = r < nn;
+                a[q] = v ? p.off[n0 + r] : 0;
+                b[q] = v ? p.off[n0 + r + 1] : 0;
+                wa[q] = a[q] >> 2;
+                wb[q] = b[q] > a[q] ? (b[q] + 3) >> 2 : wa[q];
+                words = max(words, wb[q] - wa[q]);
+            }
+            for (int64_t j0 = 0; j0 < words; j0 += 4 * 32) {
+                uint32_t v[4][4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t j = j0 + u * 32 + lane;
+                for (int q = 0; q < 4; ++q)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int64_t i = 4 * j + e;
-                        if (i < a || i >= b) continue;
-                        const int x = (int)((v[u] >> (8 * e)) & 255u);
-                        if (x < 1 || x > c) { bad = true; continue; }
-                        atomicAdd(row + x - 1, 1u);
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t j = wa[q] + j0 + u * 32 + lane;
+                        v[q][u] = j < wb[q] ? __ldg(w32 + j) : 0u;
+                    }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t* row = cnt + (g0 + q * (TC_THREADS / 32)) * KP;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t j = wa[q] + j0 + u * 32 + lane;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int64_t i = 4 * j + e;
+                            if (i < a[q] || i >= b[q]) continue;
+                            const int x = (int)((v[q][u] >> (8 * e)) & 255u);
+                            if (x < 1 || x > c) { bad = true; continue; }
+                            atomicAdd(row + x - 1, 1u);
+                        }
                     }
                 }
             }
-        } else {
+        }
+    } else {
+        for (int r = warp; r < nn; r += TC_THREADS / 32) {
+            const int64_t a = p.off[n0 + r], b = p.off[n0 + r + 1];
+            uint32_t* row = cnt + r * KP;
             for (int64_t i0 = a; i0 < b; i0 += 4 * 32) {  // four loads in flight per lane
                 int x[4];
 #pragma unroll
@@ -249,38 +308,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A planes -> tensor core (async proxy)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    __syncthreads();  // the counts are consumed: buffer 0 may be overwritten
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0 && rank < t.nnt) tc_load_tile(t, rank, Bbuf[0], Mbuf[0], &bars[0]);
     TC_STAMP(2);
     const uint32_t tmem = s_tmem;
     const uint32_t idesc = tc_idesc(TC_M, TC_NT);
     const uint32_t a_lo = tab_smem_addr(As), a_hi = tab_smem_addr(As + (size_t)TC_M * KT);
-    const uint32_t b_lo = tab_smem_addr(Bs), b_hi = tab_smem_addr(Bs + (size_t)TC_NT * KT);
     unsigned best[K_COUNT] = {0u, 0u, 0u, 0u, 0u, 0u};
-    for (int nt = 0; nt < t.nnt; ++nt) {
-        // ---- 2. table tile -> smem (one bulk copy + the column constants) ------
-        if (tid == 0) {
-            // one expect_tx for both copies (the barrier counts one arrival)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tab_smem_addr(&bars[0])),
-                         "r"((unsigned)(tc_b_bytes(KT) + TC_NT * 16))
-                         : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    tab_smem_addr(Bs)),
-                "l"(t.B + (size_t)nt * tc_b_bytes(KT)), "r"((unsigned)tc_b_bytes(KT)), "r"(tab_smem_addr(&bars[0]))
-                : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    tab_smem_addr(Ms)),
-                "l"(t.meta + (size_t)nt * TC_NT), "r"((unsigned)(TC_NT * 16)), "r"(tab_smem_addr(&bars[0]))
-                : "memory");
-        }
-        tab_bar_wait(&bars[0], nt & 1);
-        TC_STAMP(3 + 4 * nt);
+    int it = 0;
+    for (int nt = rank; nt < t.nnt; nt += nstep, ++it) {
+        const int bi = DB ? (it & 1) : 0;
+        uint8_t* Bs = Bbuf[bi];
+        int4* Ms = Mbuf[bi];
+        if (!DB && it > 0 && tid == 0) tc_load_tile(t, nt, Bs, Ms, &bars[0]);
+        // ---- 2. this tile's planes in smem -----------------------------------------
+        tab_bar_wait(&bars[bi], DB ? ((it >> 1) & 1) : (it & 1));
+        TC_STAMP(3 + 4 * it);
         // ---- 3. MMAs (one thread) -----------------------------------------------
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t b_lo = tab_smem_addr(Bs), b_hi = tab_smem_addr(Bs + (size_t)TC_NT * KT);
             for (int ks = 0; ks < KT / 32; ++ks) {
                 const uint32_t ko = (uint32_t)ks * 256;  // two 16-byte core matrices along K
                 const uint64_t dAl = tc_desc(a_lo + ko, KT), dAh = tc_desc(a_hi + ko, KT);
@@ -291,15 +339,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
                 tc_mma(tmem + 2 * TC_NT, dAh, dBh, idesc, ks > 0);
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             tab_smem_addr(&bars[1]))
+                             tab_smem_addr(&bars[2]))
                          : "memory");
         }
-        tab_bar_wait(&bars[1], nt & 1);
-        TC_STAMP(4 + 4 * nt);
+        tab_bar_wait(&bars[2], it & 1);
+        TC_STAMP(4 + 4 * it);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         // ---- 4. epilogue: warp w: rows 32(w%4).., columns [36 (w/4), +36) --------
         const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const int cg = (warp >> 2) * TC_CG;
+        const int cg0 = (warp >> 2) * TC_CG;
+        if ((warp & 3) * 32 < nn) {  // a warp whose 32 TMEM lanes hold no node skips
         // three rounds (16 + 16 + 4 columns), one tcgen05.wait::ld each; the
         // per-kind maxima through a running (kind, max) flushed at kind changes
         int cur_kind = -1;
@@ -327,7 +376,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
 #pragma unroll 1
         for (int r = 0; r < 2; ++r) {
             uint32_t d1[16], d2[16], d3[16];
-            const int c0 = cg + 16 * r;
+            const int c0 = cg0 + 16 * r;
             tc_ld16(lane_base + c0, d1);
             tc_ld16(lane_base + TC_NT + c0, d2);
             tc_ld16(lane_base + 2 * TC_NT + c0, d3);
@@ -336,7 +385,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
         }
         {
             uint32_t d1[4], d2[4], d3[4];
-            const int c0 = cg + 32;
+            const int c0 = cg0 + 32;
             tc_ld4(lane_base + c0, d1);
             tc_ld4(lane_base + TC_NT + c0, d2);
             tc_ld4(lane_base + 2 * TC_NT + c0, d3);
@@ -349,12 +398,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
 #pragma unroll
         for (int x = 0; x < K_COUNT; ++x)
             if (x == cur_kind) best[x] = max(best[x], cur);
-        // the next tile's MMAs overwrite TMEM and its copy overwrites Bs / Ms
-        TC_STAMP(5 + 4 * nt);
+        }
+        // the next tile's MMAs overwrite TMEM (and, single-buffered, its copy Bs / Ms)
+        TC_STAMP(5 + 4 * it);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
-        TC_STAMP(6 + 4 * nt);
+        TC_STAMP(6 + 4 * it);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // the MMAs and the epilogue are done with this buffer (planes and column
+        // constants): the tile after next lands in it during the next tile
+        if (DB && tid == 0 && nt + 2 * nstep < t.nnt) tc_load_tile(t, nt + 2 * nstep, Bs, Ms, &bars[bi]);
     }
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS));
@@ -365,8 +418,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
             if (best[x]) atomicMax(&kbest[row][x], best[x]);
     }
     __syncthreads();
-    if (s_bad && tid == 0 && p.err_out) atomicExch(p.err_out, 1);
     TC_STAMP(40);
+    if (s_bad && tid == 0 && p.err_out) atomicExch(p.err_out, 1);
     if (tid < nn) {
         unsigned kk[K_COUNT];
 #pragma unroll
