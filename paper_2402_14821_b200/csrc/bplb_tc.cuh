@@ -17,6 +17,8 @@
 //      u8 -> s32) into three TMEM accumulators: D1 = A_lo T_lo,
 //      D2 = A_lo T_hi + A_hi T_lo, D3 = A_hi T_hi, so
 //      S = D1 + 256 D2 + 65536 D3 exactly (integer MMA: no rounding at all);
+//      a slice whose counts are all < 256 (A_hi = 0) issues only the two
+//      A_lo products;
 //   4. every thread reads its node's row of D1..D3 (tcgen05.ld, TMEM lane =
 //      node), applies the exact ceil-div / key epilogue of the table path
 //      (key = bound << 9 | 511 - lambda) and keeps the per-kind maxima in
@@ -173,7 +175,7 @@ template <int WB, bool DB>
 __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint32_t s_tmem;
-    __shared__ int s_bad;
+    __shared__ int s_bad, s_hi;
     __shared__ unsigned kbest[TC_M][K_COUNT];  // per-node per-kind best keys
     constexpr int rank = 0, nstep = 1;  // every N-tile in this CTA
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
 
     if (tid == 0) {
         s_bad = 0;
+        s_hi = 0;
         tab_bar_init(&bars[0]);
         tab_bar_init(&bars[1]);
         tab_bar_init(&bars[2]);
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
             const uint32_t off = tc_core_off(arow, kc * 16, KT);
             *(uint4*)(As + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             *(uint4*)(As + (size_t)TC_M * KT + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            if (hi[0] | hi[1] | hi[2] | hi[3]) s_hi = 1;  // a count >= 256 somewhere
         }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // A planes -> tensor core (async proxy)
@@ -315,6 +319,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     const uint32_t tmem = s_tmem;
     const uint32_t idesc = tc_idesc(TC_M, TC_NT);
     const uint32_t a_lo = tab_smem_addr(As), a_hi = tab_smem_addr(As + (size_t)TC_M * KT);
+    const bool hiA = s_hi != 0;  // uniform: read after the barrier that follows the conversion
     unsigned best[K_COUNT] = {0u, 0u, 0u, 0u, 0u, 0u};
     int it = 0;
     for (int nt = rank; nt < t.nnt; nt += nstep, ++it) {
@@ -335,8 +340,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
                 const uint64_t dBl = tc_desc(b_lo + ko, KT), dBh = tc_desc(b_hi + ko, KT);
                 tc_mma(tmem, dAl, dBl, idesc, ks > 0);
                 tc_mma(tmem + TC_NT, dAl, dBh, idesc, ks > 0);
-                tc_mma(tmem + TC_NT, dAh, dBl, idesc, 1);
-                tc_mma(tmem + 2 * TC_NT, dAh, dBh, idesc, ks > 0);
+                if (hiA) {  // counts >= 256 in this slice: the A_hi plane's two products
+                    tc_mma(tmem + TC_NT, dAh, dBl, idesc, 1);
+                    tc_mma(tmem + 2 * TC_NT, dAh, dBh, idesc, ks > 0);
+                }
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              tab_smem_addr(&bars[2]))
@@ -379,7 +386,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
             const int c0 = cg0 + 16 * r;
             tc_ld16(lane_base + c0, d1);
             tc_ld16(lane_base + TC_NT + c0, d2);
-            tc_ld16(lane_base + 2 * TC_NT + c0, d3);
+            if (hiA) tc_ld16(lane_base + 2 * TC_NT + c0, d3);
+            else
+#pragma unroll
+                for (int j = 0; j < 16; ++j) d3[j] = 0u;
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             fold(d1, d2, d3, c0, 16);
         }
@@ -388,7 +398,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
             const int c0 = cg0 + 32;
             tc_ld4(lane_base + c0, d1);
             tc_ld4(lane_base + TC_NT + c0, d2);
-            tc_ld4(lane_base + 2 * TC_NT + c0, d3);
+            if (hiA) tc_ld4(lane_base + 2 * TC_NT + c0, d3);
+            else
+#pragma unroll
+                for (int j = 0; j < 4; ++j) d3[j] = 0u;
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             uint32_t e1[16], e2[16], e3[16];
 #pragma unroll
