@@ -1285,6 +1285,11 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
         bplb::KParams q = p;
         q.w = (const int*)w_alias;
         q.off = (const int64_t*)off_alias;
+        // weights read across PCIe: the FP32-pipe pipeline, whose persistent
+        // histogram pass streams the tiles while the contraction consumes
+        // them, is PCIe-bound; the tensor-core kernel's per-slice histograms
+        // would wait on PCIe latency (measured 266 vs 132 us on cfg2)
+        q.flags |= BPLB_F_NOTC;
         if (tab_path(e, q, n_nodes, max_r)) {
             if ((rc = launch_tab_graph(e, q, n_nodes, max_r, ks, nkinds, w_alias, off_alias))) return rc;
             goto outputs;
