@@ -1662,6 +1662,19 @@ BPLB_API int bplb_prune_trace(long long* out, int cap) {
 }
 #endif
 
+#ifdef WIDE_TRACE
+// development builds: copy the grid-wide unit trace and the segment table
+BPLB_API int bplb_wide_trace(long long* out, int cap) {
+    int n = 0;
+    cudaMemcpyFromSymbol(&n, bplb::g_wide_trace_n, sizeof(int));
+    n = std::min(n, std::min(cap, bplb::WIDE_TRACE_CAP));
+    if (n > 0) cudaMemcpyFromSymbol(out, bplb::g_wide_trace, (size_t)n * sizeof(longlong4));
+    int z = 0;
+    cudaMemcpyToSymbol(bplb::g_wide_trace_n, &z, sizeof(int));
+    return n;
+}
+#endif
+
 #ifdef TC_TRACE
 BPLB_API int bplb_tc_trace(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, bplb::g_tc_trace, 64 * 8);

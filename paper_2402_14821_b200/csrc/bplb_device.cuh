@@ -305,4 +305,26 @@ __device__ __forceinline__ int64_t emit_warp(bool valid, int64_t lam, int64_t bo
     return (int64_t)(mx - 1u);
 }
 
+// emit_warp with a per-warp cache of the key (lane 0's view, kc): the
+// atomicMax is sent only when the warp's candidate beats what it last saw, so
+// losing candidates do not queue on the key's L2 line.
+__device__ __forceinline__ int64_t emit_warp_cached(bool valid, int64_t lam, int64_t bound, int64_t kind_lo,
+                                                    u64* key, u64* kc, int64_t* lam_out, int64_t out_lo,
+                                                    int64_t out_hi) {
+    if (lam_out && valid && lam >= out_lo && lam <= out_hi) lam_out[lam - out_lo] = bound;
+    uint32_t bv = valid ? (uint32_t)bound + 1u : 0u;
+    uint32_t mx = __reduce_max_sync(0xffffffffu, bv);
+    if (mx == 0) return -1;
+    uint32_t rel = (valid && bv == mx) ? (uint32_t)(lam - kind_lo) : 0xFFFFFFFFu;
+    uint32_t mn = __reduce_min_sync(0xffffffffu, rel);
+    if ((threadIdx.x & 31) == 0) {
+        u64 k = ((u64)(mx - 1u) << 32) | (u64)(0xFFFFFFFFu - mn);
+        if (k > *kc) {
+            atomicMax(key, k);
+            *kc = k;
+        }
+    }
+    return (int64_t)(mx - 1u);
+}
+
 }  // namespace bplb

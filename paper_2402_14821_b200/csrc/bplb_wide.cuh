@@ -13,8 +13,16 @@
 //                 last block computes lambda ranges and the unit plan
 //   wide_units    all warp units (one launch per kind in PHASED mode:
 //                 the Alg. 3/4 "one launch per DFF, guard lb <= k" shape)
-//   wide_final    per-lambda bounds of item-sliced VB2/FS1 accumulators
+//   wide_final    per-lambda bounds of the sliced accumulators (item-sliced
+//                 VB2/FS1 walks, term-sliced CCM1/BJ1 harmonic sums)
 //   wide_finish   one warp writes the bplb_result / batch outputs
+// With bound pruning (full-collection checks) the units run in two launches:
+// the exact seeds, then wide_prefilter (threshold snapshot, VB2 walk chunks
+// tested once and compacted into a list) and the pruned rest.
+//
+// The lookups into the {W, N} records are L2 reads (16 MB at c = 1e6); every
+// harmonic loop issues HB iterations' loads before consuming any, so a lane
+// keeps 2 HB independent requests in flight instead of one dependent chain.
 #pragma once
 #include <algorithm>
 #include <string>
@@ -24,9 +32,11 @@
 namespace bplb {
 
 constexpr int WT = 256;              // threads per CTA (wide kernels)
-constexpr int ISLICE = 32 * GMOD_MAX * 8; // items per modular tile (4096)
+constexpr int ISLICE = 1024;         // items per modular tile (2 x 16 per lane)
 constexpr int LLW = 128;             // lambdas per lane-lookup unit (4 x 32)
-constexpr int WIDE_MAX_SEGS = 4 * K_COUNT;
+constexpr int HSL_TS = 2048;         // harmonic terms per sliced CCM1 / BJ1 unit (64 per lane)
+constexpr int WIDE_MAX_SEGS = 64;
+enum { T_HSL = 4 };                  // CCM1 / BJ1 lambda with more than HSL_TS terms: term slices
 // Bound pruning on the grid-wide path (full-collection checks only): the
 // integer envelope of the bplb_prune.cuh upper bounds.
 constexpr int64_t WIDE_PRUNE_MAX_C = (int64_t)1 << 20;
@@ -59,19 +69,23 @@ struct WideState {
     int nseg;
     long long nunits;
     int kind_seg_first[K_COUNT], kind_seg_count[K_COUNT];
-    u64 key[K_COUNT];
-    unsigned long long evals[K_COUNT];
+    // the fields every warp updates live on their own L2 lines (one line
+    // taking every unit's atomics queued the table lookups behind it)
+    alignas(256) u64 key[K_COUNT];
+    alignas(256) unsigned long long evals[K_COUNT];
     int evaluated[K_COUNT];
-    int lb;
+    alignas(256) int lb;
     int stop;              // PHASED: set when a completed kind exceeded k
     int n_done;
-    long long unit_next;
-    long long unit_end;
-    int need_final;        // VB2/FS1 were item-sliced
+    alignas(256) long long unit_next;
+    alignas(256) long long unit_end;
     int scan_blocks_done;
     int prune;             // bound pruning: seeds (units [0, nA)) then the pruned rest
     long long nA;
-    u64 thr[K_COUNT];      // per-kind keys after the seeds (the VB2 walk-chunk decisions)
+    u64 thr[K_COUNT];      // per-kind keys after the seeds (VB2 chunk / sliced-lambda decisions)
+    int vb2_seg;           // pruning: the VB2 rest segment, enumerated through vlist (-1: none)
+    int nvlist;            // surviving VB2 walk chunks
+    int64_t hsl_hi[K_COUNT];  // CCM1 / BJ1: lambdas [lo, hsl_hi] are term-sliced (T_HSL)
 };
 
 struct WideBufs {
@@ -81,7 +95,9 @@ struct WideBufs {
     int* vb2;                   // [r]
     unsigned long long* acc;    // [c+1] VB2 per-lambda D (indexed by lambda)
     unsigned long long* pz;     // [2*101] FS1 P and Z (indexed by lambda)
-    unsigned char* chunk_ok;    // [c/LMOD + 2] VB2 walk chunk evaluated (pruning)
+    int* vlist;                 // [c/LMOD + 2] pruning: surviving VB2 walk chunks (index from lo)
+    unsigned long long* hacc;   // [3 * hn] T_HSL partial sums: CCM1 part, BJ1 floor, BJ1 rem (by lambda)
+    int64_t hn;                 // c / HSL_TS + 2
     int64_t tile;               // scan tile (scan_tile(c + 2))
 };
 
@@ -97,7 +113,8 @@ inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
     b += al((size_t)std::max<int64_t>(r, 1) * 4);
     b += al((size_t)(c + 1) * 8);
     b += al((size_t)2 * 101 * 8);
-    b += al((size_t)(c / LMOD + 2));
+    b += al((size_t)(c / LMOD + 2) * 4);
+    b += al((size_t)3 * (c / HSL_TS + 2) * 8);
     return b;
 }
 
@@ -113,7 +130,9 @@ inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
     w.vb2 = (int*)p; p += al((size_t)std::max<int64_t>(r, 1) * 4);
     w.acc = (unsigned long long*)p; p += al((size_t)(c + 1) * 8);
     w.pz = (unsigned long long*)p; p += al((size_t)2 * 101 * 8);
-    w.chunk_ok = (unsigned char*)p;
+    w.vlist = (int*)p; p += al((size_t)(c / LMOD + 2) * 4);
+    w.hn = c / HSL_TS + 2;
+    w.hacc = (unsigned long long*)p;
     return w;
 }
 
@@ -125,7 +144,7 @@ __global__ void wide_init(WideBufs b, int64_t c) {
     for (int64_t i = i0; i < n; i += stride) b.rec[i] = make_ulonglong2(0ull, 0ull);
     for (int64_t i = i0; i < c + 1; i += stride) b.acc[i] = 0;
     for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
-    for (int64_t i = i0; i < c / LMOD + 2; i += stride) b.chunk_ok[i] = 0;
+    for (int64_t i = i0; i < 3 * b.hn; i += stride) b.hacc[i] = 0;
     unsigned int* st = (unsigned int*)b.state;  // zero the state word by word
     for (int64_t i = i0; i < (int64_t)(sizeof(WideState) / 4); i += stride) st[i] = 0u;
 }
@@ -135,16 +154,29 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
     int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
     long long l_W = 0, l_Vs = 0, l_Vm = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < r; i += stride) {
-        const int x = w[i];
-        if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
-        l_max = max(l_max, x);
-        l_W += x;
-        if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
-        else if (2 * (int64_t)x == c) l_e++;
-        else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
-        atomicAdd(&b.rec[x + 1].y, 1ull);
-        if (2 * (int64_t)x != c && x < c) b.vb2[atomicAdd(&b.state->n_vb2, 1)] = x;
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count: the VB2 item list is appended one warp
+    // allocation at a time (one counter atomic per warp, not per item)
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < r; i0 += stride) {
+        const int64_t i = i0 + lane;
+        const int x = i < r ? w[i] : 1;
+        const bool ok = i < r && x >= 1 && (int64_t)x <= c;
+        if (i < r && !ok) l_bad = 1;
+        bool isv = false;
+        if (ok) {
+            l_max = max(l_max, x);
+            l_W += x;
+            if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
+            else if (2 * (int64_t)x == c) l_e++;
+            else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
+            atomicAdd(&b.rec[x + 1].y, 1ull);
+            isv = 2 * (int64_t)x != c && x < c;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, isv);
+        int pos0 = 0;
+        if (lane == 0 && m) pos0 = atomicAdd(&b.state->n_vb2, __popc(m));
+        pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+        if (isv) b.vb2[pos0 + __popc(m & ((1u << lane) - 1u))] = x;
     }
     l_max = __reduce_max_sync(0xffffffffu, (unsigned)l_max);
     l_bad = (int)__reduce_or_sync(0xffffffffu, (unsigned)l_bad);
@@ -271,10 +303,12 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
         s->hi[kd] = hi;
         s->kind_seg_count[kd] = 0;
         s->kind_seg_first[kd] = 0;
+        s->hsl_hi[kd] = lo - 1;
     }
     s->nseg = 0;
     s->nunits = 0;
-    s->need_final = 0;
+    s->vb2_seg = -1;
+    s->nvlist = 0;
     if (s->bad) return;
     const NodeStats& st = s->st;
     auto push = [&](int kind, int type, int64_t a, int64_t z, int chunk, int nslice) {
@@ -288,28 +322,35 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
     };
     s->prune = prune;
     s->nA = 0;
-    // CCM1 / BJ1 segments over [a, z]: a dense pass over the items at small
-    // lambda (the harmonic loop would be ~span/lambda L2 lookups), one warp per
-    // lambda while the loop is still long, one lane per lambda after.
+    // CCM1 / BJ1 segments over [a, z] by the length of the harmonic loop
+    // (span / lambda terms, one or two L2 lookups each): term slices of
+    // HSL_TS spread over many warps where it is longer than HSL_TS (partial
+    // sums per lambda, finished in wide_final), one warp per lambda while it
+    // is longer than 64, one lane per lambda after.  The sliced lambdas come
+    // in doubling groups so every lambda of a group needs about the group's
+    // slice count (the surplus slices of its upper lambdas are empty).
     auto push_div_look = [&](int kd, int64_t a, int64_t z) {
         if (z < a) return;
         const int64_t span = kd == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
-        const int64_t n = st.r > 0 ? st.r : 1;
-        int64_t sd = kd == K_CCM1 ? (64 * span) / (3 * n + 30) + 1 : (16 * span) / n + 1;
-        if (sd < a) sd = a;
-        if (sd > z + 1) sd = z + 1;
+        int64_t sh = span / HSL_TS + 1;
+        if (sh < a) sh = a;
+        if (sh > z + 1) sh = z + 1;
         int64_t sp = span / 64 + 1;
-        if (sp < sd) sp = sd;
+        if (sp < sh) sp = sh;
         if (sp > z + 1) sp = z + 1;
-        push(kd, T_DIV, a, sd - 1, st.r > 8192 ? 1 : 8, 1);
-        push(kd, T_WLOOK, sd, sp - 1, 1, 1);
+        for (int64_t x = a; x < sh;) {
+            const int64_t y = min(sh - 1, 2 * x - 1);
+            push(kd, T_HSL, x, y, 1, (int)(span / x / HSL_TS + 1));
+            x = y + 1;
+        }
+        if (sh > a) s->hsl_hi[kd] = sh - 1;
+        push(kd, T_WLOOK, sh, sp - 1, 1, 1);
         push(kd, T_LOOKUP, sp, z, LLW, 1);
     };
     auto push_mod = [&](int kd, int64_t a, int64_t z) {
         const int64_t items = kd == K_VB2 ? s->n_vb2 : st.r;
         int nsl = (int)((items + ISLICE - 1) / ISLICE);
         if (nsl < 1) nsl = 1;
-        if (nsl > 1) s->need_final = 1;
         push(kd, T_MOD, a, z, LMOD, nsl);
     };
     if (prune) {
@@ -340,7 +381,10 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
             const int kd = kinds[i];
             const int64_t lo = s->lo[kd], hi = s->hi[kd];
             if (hi < lo) continue;
-            if (kd == K_VB2) push_mod(kd, lo + LMOD, hi);
+            if (kd == K_VB2 && hi >= lo + LMOD) {
+                s->vb2_seg = s->nseg;  // enumerated through the prefilter's chunk list
+                push_mod(kd, lo + LMOD, hi);
+            }
             if (kd == K_CCM1 || kd == K_BJ1) {
                 push_div_look(kd, lo, w0[kd] - 1);
                 push_div_look(kd, w1[kd] + 1, hi);
@@ -372,161 +416,292 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
     }
 }
 
-__device__ __forceinline__ int find_wseg(const WideState* s, long long u) {
-    int si = 0;
-    while (si + 1 < s->nseg && s->segs[si + 1].first <= u) ++si;
-    return si;
+// ---- batched harmonic loops over the global records (LkTableG layout) -------
+// rec[x + 1] = {W<=(x), N<=(x)}, rec[0] = {0, 0}; 32-bit value indices
+// (c <= WIDE_MAX_C = 2^27, every t * lambda below 2c).  HB iterations' loads
+// are issued before any is consumed; lanes past t_end load rec[0].
+constexpr int HB_CCM1 = 8;
+constexpr int HB_BJ1 = 4;
+
+// CCM1 (bounds.py:390-407): sum over t = t0, t0 + dt, ... <= t_end of
+//   base - N(t lam - 1) - N(c - t lam),  base = n_small + r - n_big
+// (bplb_ccm1_part with the loads batched).
+__device__ __forceinline__ int64_t ccm1_part_g(const ulonglong2* __restrict__ rec, int c, int lam, int t0,
+                                               int dt, int t_end, int64_t base) {
+    int64_t acc = 0;
+    for (int t = t0; t <= t_end; t += HB_CCM1 * dt) {
+        unsigned long long a[HB_CCM1], b[HB_CCM1];
+#pragma unroll
+        for (int j = 0; j < HB_CCM1; ++j) {
+            const int tt = t + j * dt;
+            const int x = tt <= t_end ? tt * lam : 0;
+            a[j] = __ldg(&rec[x].y);                      // N(t lam - 1)
+            b[j] = __ldg(&rec[x ? c - x + 1 : 0].y);      // N(c - t lam)
+        }
+#pragma unroll
+        for (int j = 0; j < HB_CCM1; ++j)
+            if (t + j * dt <= t_end) acc += base - (int64_t)a[j] - (int64_t)b[j];
+    }
+    return acc;
 }
 
-// One warp unit of the wide path.
+// BJ1 (bounds.py:441-460): buckets t = t0, t0 + dt, ... <= t_end of
+//   rem += W(hi) - W(lo) - lo (N(hi) - N(lo)),  lo = t lam + cm, hi = (t+1) lam - 1
+//   fl  += r - N(hi)  for t < tmax
+// (bplb_bj1_part with the loads batched; values clamped to c).
+__device__ __forceinline__ void bj1_part_g(const ulonglong2* __restrict__ rec, int c, int lam, int cm, int r,
+                                           int t0, int dt, int t_end, int tmax, int64_t* fl_out,
+                                           int64_t* rem_out) {
+    int64_t fl = 0, rem = 0;
+    for (int t = t0; t <= t_end; t += HB_BJ1 * dt) {
+        ulonglong2 L[HB_BJ1], H[HB_BJ1];
+#pragma unroll
+        for (int j = 0; j < HB_BJ1; ++j) {
+            const int tt = t + j * dt;
+            const bool ok = tt <= t_end;
+            const int tc = ok ? tt : 0;
+            const int lo = tc * lam + cm, hi = (tc + 1) * lam - 1;
+            L[j] = __ldg(&rec[ok ? min(lo, c) + 1 : 0]);
+            H[j] = __ldg(&rec[ok ? min(hi, c) + 1 : 0]);
+        }
+#pragma unroll
+        for (int j = 0; j < HB_BJ1; ++j) {
+            const int tt = t + j * dt;
+            if (tt <= t_end) {
+                const int64_t lo = (int64_t)tt * lam + cm;
+                rem += (int64_t)(H[j].x - L[j].x) - lo * (int64_t)(H[j].y - L[j].y);
+                if (tt < tmax) fl += (int64_t)r - (int64_t)H[j].y;
+            }
+        }
+    }
+    *fl_out = fl;
+    *rem_out = rem;
+}
+
+__device__ __forceinline__ int64_t ccm1_sum_g(const ulonglong2* rec, const NodeStats& st, int64_t c, int64_t lam) {
+    const int64_t base = (int64_t)st.n_small + st.r - st.n_big;
+    const int tmax = (int)(((c - 1) / 2) / lam);
+    return bplb_ccm1_from_part(st, c, lam, ccm1_part_g(rec, (int)c, (int)lam, 1, 1, tmax, base));
+}
+
+__device__ __forceinline__ int64_t bj1_sum_g(const ulonglong2* rec, const NodeStats& st, int64_t c, int64_t lam) {
+    const int L = (int)lam, tmax = st.maxw / L;
+    int64_t fl, rem;
+    bj1_part_g(rec, (int)c, L, (int)(c % lam), st.r, 0, 1, tmax, tmax, &fl, &rem);
+    return bplb_bj1_from_parts(c, lam, fl, rem);
+}
+
+// Read-only state of a wide_units launch, copied to shared memory once per
+// CTA (the per-unit reads of the global WideState were L2 round trips).
+struct WideRO {
+    NodeStats st;
+    int64_t lo[K_COUNT], hi[K_COUNT], hsl_hi[K_COUNT];
+    u64 thr[K_COUNT];
+    long long nA;
+    int prune, vb2_seg, n_vb2;
+};
+
+// One warp unit of the wide path.  segs / si: the block's shared copy of the
+// segment table and the warp's forward-only cursor (a warp claims increasing
+// unit ids).  cancel_now: the Alg. 4 guard has fired -- unsliced units are
+// skipped, sliced ones (partial sums per lambda) still run so no lambda is
+// finished from an incomplete sum.
+// WarpAcc: the warp's own evals / evaluated / lb / key views (lane 0),
+// flushed to the state at the end of the launch.
+struct WarpAcc {
+    unsigned long long ev[K_COUNT];
+    u64 kc[K_COUNT];
+    int evd, lb_sent;
+};
+
 template <bool WIDE>
-__device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const LkTableG& lk,
-                          long long u, u64* tot) {
+__device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const WideRO& ro, const LkTableG& lk,
+                          const WSeg* segs, int nseg, int& si, long long u, u64* tot, bool cancel_now,
+                          WarpAcc& wa) {
     const int lane = threadIdx.x & 31;
-    const WSeg sg = s->segs[find_wseg(s, u)];
+    while (si + 1 < nseg && segs[si + 1].first <= u) ++si;
+    const WSeg& sg = segs[si];
+    if (cancel_now && !(sg.type == T_HSL || (sg.type == T_MOD && sg.nslice > 1))) return;
     const int kind = sg.kind;
     const int64_t c = p.c;
-    const NodeStats& st = s->st;
+    const NodeStats& st = ro.st;
     const long long rel = u - sg.first;
     int64_t* lam_out = p.lam_out;
     int64_t wmax = -1;
     int64_t n_eval = 0;
-    // pruned group (bplb_prune.cuh bounds against the live per-kind keys):
-    // skipped lambdas still count as evaluated (they provably cannot change
-    // the outputs)
-    const bool pruned = s->prune && u >= s->nA;
-    const int64_t lo_k = s->lo[kind];
-    if (sg.type == T_LOOKUP) {
-        const int64_t lam_a = sg.lo + rel * sg.chunk;
-        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
-        n_eval = lam_b - lam_a + 1;
-        bool skip_unit = false;
-        if (pruned) {
-            const Thr th = thr_from_key(*(volatile u64*)&s->key[kind]);
-            skip_unit = (c / lam_a <= PR_QMAX) ? blk_skip<LkTableG, true>(th, kind, lk, st, c, lo_k, lam_a, lam_b)
-                                               : range_skip(th, kind, st, c, lo_k, lam_a, lam_b);
-        }
-        for (int64_t l0 = lam_a; l0 <= lam_b && !skip_unit; l0 += 32) {
-            const int64_t lam = l0 + lane;
-            bool valid = lam <= lam_b;
-            if (pruned && valid) valid = !lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam);
-            if (pruned && !__ballot_sync(0xffffffffu, valid)) continue;
-            int64_t S = 0;
-            if (valid) {
-                switch (kind) {
-                case K_MT: S = bplb_mt_sum(lk, c, st.r, lam); break;
-                case K_RAD2: S = bplb_rad2_sum(lk, c, st.r, lam); break;
-                case K_CCM1: S = bplb_ccm1_sum(lk, st, c, lam); break;
-                default: S = bplb_bj1_sum(lk, st, c, lam); break;
-                }
+    // pruned group (bplb_prune.cuh bounds against the live per-kind keys, read
+    // once per unit): skipped lambdas still count as evaluated (they provably
+    // cannot change the outputs)
+    const bool pruned = ro.prune && u >= ro.nA;
+    const int64_t lo_k = ro.lo[kind];
+    do {
+        if (sg.type == T_LOOKUP) {
+            const int64_t lam_a = sg.lo + rel * sg.chunk;
+            const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+            n_eval = lam_b - lam_a + 1;
+            bool skip_unit = false;
+            Thr th{};
+            if (pruned) {
+                const u64 kv = *(volatile u64*)&s->key[kind];
+                if (lane == 0 && kv > wa.kc[kind]) wa.kc[kind] = kv;
+                th = thr_from_key(kv);
+                skip_unit = (c / lam_a <= PR_QMAX) ? blk_skip<LkTableG, true>(th, kind, lk, st, c, lo_k, lam_a, lam_b)
+                                                   : range_skip(th, kind, st, c, lo_k, lam_a, lam_b);
             }
-            int64_t bd = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
-            int64_t m = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
-            wmax = m > wmax ? m : wmax;
-        }
-    } else if (sg.type == T_DIV) {
-        const int64_t lam_a = sg.lo + rel * sg.chunk;
-        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
-        n_eval = lam_b - lam_a + 1;
-        int64_t mine = 0;
-        unsigned done = 0;  // lanes whose lambda was evaluated
-        for (int64_t lam = lam_a; lam <= lam_b; ++lam) {
-            if (pruned && lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) continue;
-            const int64_t S = kind == K_CCM1 ? ccm1_dense_raw(p.w, st.r, st, c, lam)
-                                             : bj1_dense(p.w, st.r, c, lam);
-            if (lam - lam_a == lane) mine = S;
-            done |= 1u << (lam - lam_a);
-        }
-        const int64_t lam = lam_a + lane;
-        const bool valid = lam <= lam_b && (done >> lane & 1u);
-        int64_t bd = valid ? bplb_bound(mine, bplb_fc(kind, c, lam)) : 0;
-        wmax = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
-    } else if (sg.type == T_WLOOK) {
-        const int64_t lam = sg.lo + rel;
-        n_eval = 1;
-        if (pruned && lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) goto tail;
-        int64_t S;
-        if (kind == K_CCM1) {
-            int64_t part = bplb_ccm1_part(lk, st, c, lam, 1 + lane, 32);
-            part = (int64_t)warp_sum_u64((u64)part);
-            S = bplb_ccm1_from_part(st, c, lam, part);
-        } else {
-            int64_t fl, rem;
-            bplb_bj1_part(lk, st, c, lam, lane, 32, &fl, &rem);
-            fl = (int64_t)warp_sum_u64((u64)fl);
-            rem = (int64_t)warp_sum_u64((u64)rem);
-            S = bplb_bj1_from_parts(c, lam, fl, rem);
-        }
-        {
-            int64_t bd = bplb_bound(S, bplb_fc(kind, c, lam));
-            wmax = emit_warp(lane == 0, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
-        }
-    } else {  // T_MOD
-        const long long chunk = rel / sg.nslice;
-        const int slice = (int)(rel % sg.nslice);
-        const int64_t lam_a = sg.lo + chunk * sg.chunk;
-        const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
-        const int L = (int)(lam_b - lam_a + 1);
-        const int n_items = kind == K_VB2 ? s->n_vb2 : st.r;
-        const int* items = kind == K_VB2 ? b.vb2 : p.w;
-        const int i0 = slice * ISLICE, i1 = min(n_items, i0 + ISLICE);
-        if (s->prune && kind == K_VB2) {
-            // one decision per walk chunk, identical in every slice: the keys
-            // snapshotted after the seeds (chunk_ok gates wide_final)
-            if (pruned && range_skip(thr_from_key(s->thr[K_VB2]), kind, st, c, lo_k, lam_a, lam_b)) {
-                n_eval = slice == 0 ? L : 0;
-                goto tail;
-            }
-            if (slice == 0 && lane == 0) b.chunk_ok[(lam_a - lo_k) / LMOD] = 1;
-        }
-        const int warp = threadIdx.x >> 5;
-        u64* t = tot + warp * LMOD;
-        for (int j = lane; j < LMOD; j += kWarp) t[j] = 0;
-        __syncwarp();
-        const uint32_t c32 = (uint32_t)c;
-        const u64 cinv = bplb_cinv(c32);
-        mod_walk<WIDE>(items, i0, i1, c32, cinv, lam_a, L, t, p.one, kind == K_VB2);
-        __syncwarp();
-        if (sg.nslice > 1) {
-            for (int j = lane; j < L; j += kWarp) {
-                if (kind == K_VB2) atomicAdd(&b.acc[lam_a + j], t[j]);
-                else atomicAdd(&b.pz[lam_a + j], t[j]);
-            }
-            n_eval = slice == 0 ? L : 0;  // count each lambda once
-        } else {
-            n_eval = L;
-            for (int j0 = 0; j0 < L; j0 += kWarp) {
-                const int j = j0 + lane;
-                const bool valid = j < L;
-                const int64_t lam = lam_a + j;
+            for (int64_t l0 = lam_a; l0 <= lam_b && !skip_unit; l0 += 32) {
+                const int64_t lam = l0 + lane;
+                bool valid = lam <= lam_b;
+                if (pruned && valid) valid = !lam_skip<true>(th, kind, st, c, lo_k, lam);
+                if (pruned && !__ballot_sync(0xffffffffu, valid)) continue;
                 int64_t S = 0;
-                if (valid)
-                    S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j])
-                                        : bplb_fs1_sum(st, lam, t[j], (uint64_t)bplb_fs1_zero(lk, c, st.maxw, lam));
+                if (valid) {
+                    switch (kind) {
+                    case K_MT: S = bplb_mt_sum(lk, c, st.r, lam); break;
+                    case K_RAD2: S = bplb_rad2_sum(lk, c, st.r, lam); break;
+                    case K_CCM1: S = ccm1_sum_g(b.rec, st, c, lam); break;
+                    default: S = bj1_sum_g(b.rec, st, c, lam); break;
+                    }
+                }
                 int64_t bd = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
-                int64_t m = emit_warp(valid, lam, bd, s->lo[kind], &s->key[kind], lam_out, p.out_lo, p.out_hi);
+                int64_t m = emit_warp_cached(valid, lam, bd, lo_k, &s->key[kind], &wa.kc[kind], lam_out, p.out_lo, p.out_hi);
                 wmax = m > wmax ? m : wmax;
             }
+        } else if (sg.type == T_WLOOK) {
+            const int64_t lam = sg.lo + rel;
+            n_eval = 1;
+            if (pruned && lam_skip<true>(thr_from_key(*(volatile u64*)&s->key[kind]), kind, st, c, lo_k, lam)) break;
+            const int L = (int)lam;
+            int64_t S;
+            if (kind == K_CCM1) {
+                const int64_t base = (int64_t)st.n_small + st.r - st.n_big;
+                int64_t part = ccm1_part_g(b.rec, (int)c, L, 1 + lane, 32, (int)(((c - 1) / 2) / lam), base);
+                part = (int64_t)warp_sum_u64((u64)part);
+                S = bplb_ccm1_from_part(st, c, lam, part);
+            } else {
+                const int tmax = st.maxw / L;
+                int64_t fl, rem;
+                bj1_part_g(b.rec, (int)c, L, (int)(c % lam), st.r, lane, 32, tmax, tmax, &fl, &rem);
+                fl = (int64_t)warp_sum_u64((u64)fl);
+                rem = (int64_t)warp_sum_u64((u64)rem);
+                S = bplb_bj1_from_parts(c, lam, fl, rem);
+            }
+            const int64_t bd = bplb_bound(S, bplb_fc(kind, c, lam));
+            wmax = emit_warp_cached(lane == 0, lam, bd, lo_k, &s->key[kind], &wa.kc[kind], lam_out, p.out_lo, p.out_hi);
+        } else if (sg.type == T_HSL) {
+            // one term slice of one lambda: partial sums into hacc (wide_final);
+            // with pruning the decision uses the post-seed snapshot, identical
+            // in every slice and in wide_final
+            const int64_t lam = sg.lo + rel / sg.nslice;
+            const int slice = (int)(rel % sg.nslice);
+            n_eval = slice == 0 ? 1 : 0;
+            if (ro.prune && lam_skip<true>(thr_from_key(ro.thr[kind]), kind, st, c, lo_k, lam)) break;
+            const int L = (int)lam;
+            if (kind == K_CCM1) {
+                const int tmax = (int)(((c - 1) / 2) / lam);
+                const int ta = 1 + slice * HSL_TS, tb = min(tmax, ta + HSL_TS - 1);
+                if (ta > tb) break;
+                const int64_t base = (int64_t)st.n_small + st.r - st.n_big;
+                const u64 part = warp_sum_u64((u64)ccm1_part_g(b.rec, (int)c, L, ta + lane, 32, tb, base));
+                if (lane == 0) atomicAdd(&b.hacc[lam], part);
+            } else {
+                const int tmax = st.maxw / L;
+                const int ta = slice * HSL_TS, tb = min(tmax, ta + HSL_TS - 1);
+                if (ta > tb) break;
+                int64_t fl, rem;
+                bj1_part_g(b.rec, (int)c, L, (int)(c % lam), st.r, ta + lane, 32, tb, tmax, &fl, &rem);
+                const u64 f = warp_sum_u64((u64)fl), m = warp_sum_u64((u64)rem);
+                if (lane == 0) {
+                    atomicAdd(&b.hacc[b.hn + lam], f);
+                    atomicAdd(&b.hacc[2 * b.hn + lam], m);
+                }
+            }
+        } else {  // T_MOD
+            const long long chunk = rel / sg.nslice;
+            const int slice = (int)(rel % sg.nslice);
+            // the pruned VB2 rest: only the chunks the prefilter kept (its evals
+            // were counted there)
+            const bool listed = ro.prune && si == ro.vb2_seg;
+            const int64_t lam_a = listed ? lo_k + (int64_t)b.vlist[chunk] * LMOD : sg.lo + chunk * sg.chunk;
+            const int64_t lam_b = min(sg.hi, lam_a + sg.chunk - 1);
+            const int L = (int)(lam_b - lam_a + 1);
+            const int n_items = kind == K_VB2 ? ro.n_vb2 : st.r;
+            const int* items = kind == K_VB2 ? b.vb2 : p.w;
+            const int i0 = slice * ISLICE, i1 = min(n_items, i0 + ISLICE);
+            const int warp = threadIdx.x >> 5;
+            u64* t = tot + warp * LMOD;
+            for (int j = lane; j < LMOD; j += kWarp) t[j] = 0;
+            __syncwarp();
+            const uint32_t c32 = (uint32_t)c;
+            const u64 cinv = bplb_cinv(c32);
+            mod_walk<WIDE>(items, i0, i1, c32, cinv, lam_a, L, t, p.one, kind == K_VB2);
+            __syncwarp();
+            if (sg.nslice > 1) {
+                for (int j = lane; j < L; j += kWarp) {
+                    if (kind == K_VB2) atomicAdd(&b.acc[lam_a + j], t[j]);
+                    else atomicAdd(&b.pz[lam_a + j], t[j]);
+                }
+                n_eval = (slice == 0 && !listed) ? L : 0;  // count each lambda once
+            } else {
+                n_eval = listed ? 0 : L;
+                for (int j0 = 0; j0 < L; j0 += kWarp) {
+                    const int j = j0 + lane;
+                    const bool valid = j < L;
+                    const int64_t lam = lam_a + j;
+                    int64_t S = 0;
+                    if (valid)
+                        S = (kind == K_VB2) ? bplb_vb2_sum(st, c, lam, t[j])
+                                            : bplb_fs1_sum(st, lam, t[j], (uint64_t)bplb_fs1_zero(lk, c, st.maxw, lam));
+                    int64_t bd = valid ? bplb_bound(S, bplb_fc(kind, c, lam)) : 0;
+                    int64_t m = emit_warp_cached(valid, lam, bd, lo_k, &s->key[kind], &wa.kc[kind], lam_out, p.out_lo, p.out_hi);
+                    wmax = m > wmax ? m : wmax;
+                }
+            }
+        }
+    } while (0);
+    if (lane == 0) {
+        wa.ev[kind] += (unsigned long long)n_eval;
+        wa.evd |= 1 << kind;
+        if (wmax > wa.lb_sent) {  // lb: the Alg. 4 guard reads it live
+            atomicMax(&s->lb, (int)wmax);
+            wa.lb_sent = (int)wmax;
         }
     }
-tail:
-    if (lane == 0) {
-        if (n_eval) atomicAdd(&s->evals[kind], (unsigned long long)n_eval);
-        s->evaluated[kind] = 1;
-        if (wmax >= 0) atomicMax(&s->lb, (int)wmax);
-    }
 }
+
+#ifdef WIDE_TRACE
+// Per-unit trace (development builds only: scripts/wide_trace.py builds
+// libbplb_wtrace.so with -DWIDE_TRACE):
+// {seg | part << 8 | smid << 16 | kind << 32 | type << 40, unit - seg.first, t0, t1}.
+constexpr int WIDE_TRACE_CAP = 1 << 18;
+__device__ longlong4 g_wide_trace[WIDE_TRACE_CAP];
+__device__ int g_wide_trace_n;
+#endif
 
 // Persistent warp-unit kernel.  phase_kind >= 0 restricts to that kind's
 // segments (PHASED mode) and applies the Alg. 4 entry guard lb <= k.
 template <bool WIDE>
 __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phase_kind, int part) {
     __shared__ u64 tot[(WT / 32) * LMOD];
+    __shared__ WSeg segs[WIDE_MAX_SEGS];
+    __shared__ WideRO ro;
+    __shared__ WarpAcc wacc[WT / 32];
     __shared__ long long u_begin, u_end;
-    __shared__ int skip;
+    __shared__ int skip, nseg;
     WideState* s = b.state;
     if (threadIdx.x == 0) {
         skip = 0;
+        nseg = s->nseg;
+        ro.st = s->st;
+        for (int kd = 0; kd < K_COUNT; ++kd) {
+            ro.lo[kd] = s->lo[kd];
+            ro.hi[kd] = s->hi[kd];
+            ro.hsl_hi[kd] = s->hsl_hi[kd];
+            ro.thr[kd] = s->thr[kd];
+        }
+        ro.nA = s->nA;
+        ro.prune = s->prune;
+        ro.vb2_seg = s->vb2_seg;
+        ro.n_vb2 = s->n_vb2;
         if (s->bad) skip = 1;
         if (phase_kind >= 0) {
             if (s->stop) skip = 1;
@@ -546,24 +721,111 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
     }
     __syncthreads();
     if (skip) return;
+    for (int i = threadIdx.x; i < nseg; i += WT) segs[i] = s->segs[i];
+    __syncthreads();
     const LkTableG lk{b.rec, p.c};
     const bool cancel = (p.flags & BPLB_F_CANCEL) && phase_kind < 0;
     const int lane = threadIdx.x & 31;
+    int si = 0;
+    WarpAcc& wa = wacc[threadIdx.x >> 5];
+    if (lane < K_COUNT) {
+        wa.ev[lane] = 0;
+        wa.kc[lane] = 0;
+    }
+    if (lane == 0) {
+        wa.evd = 0;
+        wa.lb_sent = -1;
+    }
+    __syncwarp();
+    // unit claims one ahead: the next claim's atomic is in flight while the
+    // current unit runs (a warp's claims still increase)
+    long long u_nx = 0;
+    if (lane == 0) u_nx = u_begin + atomicAdd((unsigned long long*)&s->unit_next, 1ull);
     for (;;) {
-        long long u = 0;
-        if (lane == 0) u = u_begin + atomicAdd((unsigned long long*)&s->unit_next, 1ull);
-        u = __shfl_sync(0xffffffffu, u, 0);
+        const long long u = __shfl_sync(0xffffffffu, u_nx, 0);
         if (u >= u_end) break;
-        if (cancel && (int64_t)(*(volatile int*)&s->lb) > p.k) continue;
-        wide_unit<WIDE>(p, b, s, lk, u, tot);
+        if (lane == 0) u_nx = u_begin + atomicAdd((unsigned long long*)&s->unit_next, 1ull);
+        const bool cancel_now = cancel && (int64_t)(*(volatile int*)&s->lb) > p.k;  // Alg. 4 guard
+#ifdef WIDE_TRACE
+        long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#endif
+        wide_unit<WIDE>(p, b, s, ro, lk, segs, nseg, si, u, tot, cancel_now, wa);
+        __syncwarp();
+#ifdef WIDE_TRACE
+        if (lane == 0) {
+            long long t1;
+            unsigned sm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            const int i = atomicAdd(&g_wide_trace_n, 1);
+            if (i < WIDE_TRACE_CAP)
+                g_wide_trace[i] = make_longlong4((long long)si | ((long long)part << 8) | ((long long)sm << 16) |
+                                                     ((long long)segs[si].kind << 32) |
+                                                     ((long long)segs[si].type << 40),
+                                                 u - segs[si].first, t0, t1);
+        }
+        __syncwarp();
+#endif
+    }
+    __syncwarp();
+    if (lane < K_COUNT) {
+        if (wa.ev[lane]) atomicAdd(&s->evals[lane], wa.ev[lane]);
+        if (wa.evd >> lane & 1) s->evaluated[lane] = 1;
     }
 }
 
-// Pruning: snapshot the per-kind keys after the seeds, reset the unit counter.
-__global__ void wide_snapshot(WideBufs b) {
+// Pruning, between the seeds and the rest (one CTA): snapshot the per-kind
+// keys, reset the unit counter, test every VB2 walk chunk of the rest once
+// against the snapshot (the same range relaxation the units used to apply
+// per slice) and compact the survivors into vlist; the VB2 segment then
+// enumerates only those chunks and the later segments shift down.
+constexpr int PF_T = 1024;
+__global__ void __launch_bounds__(PF_T) wide_prefilter(KParams p, WideBufs b) {
+    __shared__ int wcnt[PF_T / 32];
+    __shared__ int total;
     WideState* s = b.state;
-    for (int kd = 0; kd < K_COUNT; ++kd) s->thr[kd] = s->key[kd];
-    s->unit_next = 0;
+    if (threadIdx.x < K_COUNT) s->thr[threadIdx.x] = s->key[threadIdx.x];
+    if (threadIdx.x == 0) {
+        s->unit_next = 0;
+        total = 0;
+    }
+    __syncthreads();
+    const int si = s->vb2_seg;
+    if (s->bad || si < 0) return;
+    const WSeg g = s->segs[si];
+    const int64_t c = p.c, lo_k = s->lo[K_VB2];
+    const Thr th = thr_from_key(s->thr[K_VB2]);
+    const NodeStats st = s->st;
+    const int64_t nch = (g.hi - g.lo + LMOD) / LMOD;
+    const int64_t first = (g.lo - lo_k) / LMOD;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t c0 = 0; c0 < nch; c0 += PF_T) {
+        const int64_t ch = c0 + threadIdx.x;
+        const int64_t la = g.lo + ch * LMOD;
+        const bool keep = ch < nch && !range_skip(th, K_VB2, st, c, lo_k, la, min(g.hi, la + LMOD - 1));
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wcnt[warp] = __popc(m);
+        __syncthreads();
+        int before = total;
+        for (int i = 0; i < warp; ++i) before += wcnt[i];
+        if (keep) b.vlist[before + __popc(m & ((1u << lane) - 1u))] = (int)(first + ch);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = total;
+            for (int i = 0; i < PF_T / 32; ++i) t += wcnt[i];
+            total = t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s->nvlist = total;
+        s->segs[si].count = (long long)total * g.nslice;
+        for (int j = si + 1; j < s->nseg; ++j) s->segs[j].first = s->segs[j - 1].first + s->segs[j - 1].count;
+        s->nunits = s->segs[s->nseg - 1].first + s->segs[s->nseg - 1].count;
+        s->evals[K_VB2] += (unsigned long long)(g.hi - g.lo + 1);
+        s->evaluated[K_VB2] = 1;
+    }
 }
 
 // Reset the unit counter between phased launches and record the kind.
@@ -573,37 +835,79 @@ __global__ void wide_phase_begin(WideBufs b, int idx) {
     if (!s->stop) s->n_done = idx + 1;
 }
 
-// Per-lambda bounds of item-sliced modular kinds.
-__global__ void __launch_bounds__(WT) wide_final(KParams p, WideBufs b, int only_kind) {
+// Per-lambda bounds of the sliced accumulators: FS1 / VB2 walks cut into
+// item slices (acc / pz) and CCM1 / BJ1 harmonic sums cut into term slices
+// (hacc).  part 0: no pruning (everything); part 1: after the seeds (FS1,
+// the first VB2 chunk); part 2: after the pruned rest (the listed VB2
+// chunks, the sliced CCM1 / BJ1 lambdas the snapshot did not skip).
+__global__ void __launch_bounds__(WT) wide_final(KParams p, WideBufs b, int only_kind, int part) {
     WideState* s = b.state;
-    if (s->bad || !s->need_final) return;
-    const int mod_kinds[2] = {K_FS1, K_VB2};
-    for (int mi = 0; mi < 2; ++mi) {
-        const int kd = mod_kinds[mi];
-        if (only_kind >= 0 && only_kind != kd) continue;
-        if (only_kind >= 0 && s->stop) return;
-        const int64_t lo = s->lo[kd], hi = s->hi[kd];
-        if (hi < lo) continue;
-        const int64_t items = kd == K_VB2 ? s->n_vb2 : s->st.r;
-        if (items <= ISLICE) continue;  // finished inside the units
-        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        int64_t wmax = -1;
-        for (int64_t l0 = lo + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); l0 <= hi;
-             l0 += stride) {
-            const int64_t lam = l0 + (threadIdx.x & 31);
-            bool valid = lam <= hi;
-            if (valid && s->prune && kd == K_VB2) valid = b.chunk_ok[(lam - lo) / LMOD] != 0;
-            int64_t S = 0;
-            if (valid)
-                S = kd == K_VB2 ? bplb_vb2_sum(s->st, p.c, lam, b.acc[lam])
-                                : bplb_fs1_sum(s->st, lam, b.pz[lam],
-                                               (uint64_t)bplb_fs1_zero(LkTableG{b.rec, p.c}, p.c, s->st.maxw, lam));
-            int64_t bd = valid ? bplb_bound(S, bplb_fc(kd, p.c, lam)) : 0;
-            int64_t m = emit_warp(valid, lam, bd, lo, &s->key[kd], p.lam_out, p.out_lo, p.out_hi);
+    if (s->bad) return;
+    if (only_kind >= 0 && s->stop) return;
+    __shared__ NodeStats sst;
+    if (threadIdx.x == 0) sst = s->st;
+    __syncthreads();
+    const int64_t c = p.c;
+    const NodeStats& st = sst;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t j_first = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    int64_t wmax = -1;
+    // one warp-uniform sweep over n lambdas: lam(j) (-1: not evaluated), sum(lam)
+    auto sweep = [&](int kd, int64_t n, auto lam_of, auto sum_of) {
+        for (int64_t j0 = j_first; j0 < n; j0 += stride) {
+            const int64_t j = j0 + lane;
+            const int64_t lam = j < n ? lam_of(j) : -1;
+            const bool valid = lam >= 0;
+            const int64_t S = valid ? sum_of(lam) : 0;
+            const int64_t bd = valid ? bplb_bound(S, bplb_fc(kd, c, lam)) : 0;
+            const int64_t m = emit_warp(valid, lam, bd, s->lo[kd], &s->key[kd], p.lam_out, p.out_lo, p.out_hi);
             wmax = m > wmax ? m : wmax;
         }
-        if ((threadIdx.x & 31) == 0 && wmax >= 0) atomicMax(&s->lb, (int)wmax);
+    };
+    auto want = [&](int kd) { return (only_kind < 0 || only_kind == kd) && s->hi[kd] >= s->lo[kd]; };
+    if (want(K_FS1) && part != 2 && st.r > ISLICE) {
+        const int64_t lo = s->lo[K_FS1];
+        sweep(K_FS1, s->hi[K_FS1] - lo + 1, [&](int64_t j) { return lo + j; },
+              [&](int64_t lam) {
+                  return bplb_fs1_sum(st, lam, b.pz[lam],
+                                      (uint64_t)bplb_fs1_zero(LkTableG{b.rec, c}, c, st.maxw, lam));
+              });
     }
+    if (want(K_VB2) && s->n_vb2 > ISLICE) {
+        const int64_t lo = s->lo[K_VB2], hi = s->hi[K_VB2];
+        auto vsum = [&](int64_t lam) { return bplb_vb2_sum(st, c, lam, b.acc[lam]); };
+        if (part == 0) sweep(K_VB2, hi - lo + 1, [&](int64_t j) { return lo + j; }, vsum);
+        else if (part == 1) sweep(K_VB2, min(hi, lo + LMOD - 1) - lo + 1, [&](int64_t j) { return lo + j; }, vsum);
+        else
+            sweep(K_VB2, (int64_t)s->nvlist * LMOD,
+                  [&](int64_t j) {
+                      const int64_t lam = lo + (int64_t)b.vlist[j / LMOD] * LMOD + j % LMOD;
+                      return lam <= hi ? lam : (int64_t)-1;
+                  },
+                  vsum);
+    }
+    if (part != 1) {
+        const int hk[2] = {K_CCM1, K_BJ1};
+        for (int i = 0; i < 2; ++i) {
+            const int kd = hk[i];
+            if (!want(kd) || s->hsl_hi[kd] < s->lo[kd]) continue;
+            const int64_t lo = s->lo[kd];
+            const Thr th = thr_from_key(s->thr[kd]);
+            sweep(kd, s->hsl_hi[kd] - lo + 1,
+                  [&](int64_t j) {
+                      const int64_t lam = lo + j;
+                      return (s->prune && lam_skip<true>(th, kd, st, c, lo, lam)) ? (int64_t)-1 : lam;
+                  },
+                  [&](int64_t lam) {
+                      return kd == K_CCM1
+                                 ? bplb_ccm1_from_part(st, c, lam, (int64_t)b.hacc[lam])
+                                 : bplb_bj1_from_parts(c, lam, (int64_t)b.hacc[b.hn + lam],
+                                                       (int64_t)b.hacc[2 * b.hn + lam]);
+                  });
+        }
+    }
+    if (lane == 0 && wmax >= 0) atomicMax(&s->lb, (int)wmax);
 }
 
 // After each phased kind: stop further kinds once lb > k (bounds.py:523-525).
@@ -708,22 +1012,22 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     const int g_fin = num_sms * 2;
     if (prune) {
         units<<<grid, WT, 0, st>>>(p, b, -1, 1);
-        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
-        wide_snapshot<<<1, 1, 0, st>>>(b);
+        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1, 1);
+        wide_prefilter<<<1, PF_T, 0, st>>>(p, b);
         units<<<grid, WT, 0, st>>>(p, b, -1, 2);
-        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
+        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1, 2);
         *launches += 5;
     } else if (phased) {
         for (int i = 0; i < p.nk; ++i) {
             wide_phase_begin<<<1, 1, 0, st>>>(b, i);
             units<<<grid, WT, 0, st>>>(p, b, p.kinds[i], 0);
-            wide_final<<<g_fin, WT, 0, st>>>(p, b, p.kinds[i]);
+            wide_final<<<g_fin, WT, 0, st>>>(p, b, p.kinds[i], 0);
             wide_phase_end<<<1, 1, 0, st>>>(b, p.k);
             *launches += 4;
         }
     } else {
         units<<<grid, WT, 0, st>>>(p, b, -1, 0);
-        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1);
+        wide_final<<<g_fin, WT, 0, st>>>(p, b, -1, 0);
         *launches += 2;
     }
     wide_finish<<<1, 32, 0, st>>>(p, b, phased ? 1 : 0);

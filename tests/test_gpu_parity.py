@@ -674,3 +674,18 @@ def test_wide_scan_tiles_dff_vectors(oracle, c):
         got = G.dff_bound_batch(kind, red, lo, hi)
         want = oracle.dff_bound_batch(kind, w, c, lo, hi)
         np.testing.assert_array_equal(got, want, err_msg=f"{kind} c={c}")
+
+
+@pytest.mark.parametrize("c,r", [(1_000_000, 300), (1_048_577, 20_000), (4_000_037, 5_000)])
+def test_wide_sliced_harmonic_vectors(oracle, c, r):
+    """CCM1 / BJ1 at small lambda on the grid-wide path: every lambda whose
+    harmonic loop is longer than HSL_TS terms is cut into term slices on
+    many warps (partial sums per lambda, finished in wide_final), the rest by
+    one warp per lambda; both against the oracle's per-lambda bounds."""
+    rng = np.random.default_rng(c + r)
+    w = rng.integers(1, c + 1, size=r).astype(np.int32)
+    red = ReducedInstance.from_array(c, w)
+    for kind in ("CCM1", "BJ1"):
+        got = G.dff_bound_batch(kind, red, 1, 1200)
+        want = oracle.dff_bound_batch(kind, w, c, 1, 1200)
+        np.testing.assert_array_equal(got, want, err_msg=f"{kind} c={c} r={r}")
