@@ -46,9 +46,10 @@ struct MultiState {
     unsigned long long evals[K_COUNT];
     int evaluated[K_COUNT];
     int lb;
-    int unit_next;
-    int units_done;
     int ctas_done;
+    // the per-unit counters on their own L2 lines
+    alignas(256) int unit_next;
+    alignas(256) int units_done;
 };
 
 struct KParams {
@@ -272,7 +273,8 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
         ctl.evaluated[kind] = 1;
         if (wmax >= 0) {
             atomicMax(&ctl.lb, (int)wmax);
-            if (p.ms) {
+            // the cross-CTA running maxima only feed the PHASED / CANCEL guards
+            if (p.ms && (p.flags & (BPLB_F_PHASED | BPLB_F_CANCEL))) {
                 atomicMax(&p.ms->lb, (int)wmax);
                 atomicMax(&p.ms->kmax[kind], (int)wmax);
             }
@@ -324,7 +326,7 @@ __device__ void sweep_multi(const KParams& p, NodeCtl& ctl, const LK& lk, const 
         }
         if (!skip) run_unit<TABLE, WIDE>(p, ctl, lk, m, u, single);
         __syncwarp();
-        if (lane == 0) {
+        if (guard && lane == 0) {  // completion count: only the guards wait on it
             __threadfence();
             atomicAdd(&ms->units_done, 1);
         }

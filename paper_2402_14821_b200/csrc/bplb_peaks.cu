@@ -14,6 +14,9 @@
 //   ffma  : FP32 FMA (FMA pipe), reported in flop/s
 //   clock : the SM clock during the runs (clock64 cycles / globaltimer ns)
 // Rates are warp-instructions/s (x32 for thread ops) over 148 SMs.
+//   gather: independent random 16-byte loads from an L2-resident table (the
+//           grid-wide path's {W, N} record lookups): 32-byte sectors / s
+//           delivered L2 -> SM, 16 loads in flight per thread.
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -97,9 +100,62 @@ int run_one(int sms, int per_sm, int iters, double* rate, double* mhz) {
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+constexpr int kG = 16;  // gather: loads in flight per thread
+
+__global__ void __launch_bounds__(kNT) gather_kernel(const ulonglong2* __restrict__ tab, uint32_t mask, int iters,
+                                                     unsigned long long* sink) {
+    uint32_t h = (blockIdx.x * kNT + threadIdx.x) * 2654435761u + 12345u;
+    unsigned long long acc = 0;
+    for (int it = 0; it < iters; ++it) {
+        ulonglong2 v[kG];
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            h = h * 1664525u + 1013904223u;
+            v[j] = __ldg(&tab[(h >> 7) & mask]);
+        }
+#pragma unroll
+        for (int j = 0; j < kG; ++j) acc += v[j].x ^ v[j].y;
+    }
+    if (acc == 0x123456789ull) sink[0] = acc;
+}
+
 }  // namespace
 
 extern "C" {
+
+// out[0]: random 16-byte gathers/s from a 16 MB L2-resident table (one
+// 32-byte sector each), out[1]: the same in GB/s of sectors.  Returns 0 on success.
+__attribute__((visibility("default"))) int bplb_measure_gather_peak(int device, double* out) {
+    if (cudaSetDevice(device) != cudaSuccess) return -1;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const uint32_t n = 1u << 20;  // 16 MB of 16-byte records, as at c = 1e6
+    ulonglong2* tab;
+    unsigned long long* sink;
+    if (cudaMalloc(&tab, (size_t)n * 16) != cudaSuccess) return -1;
+    if (cudaMalloc(&sink, 8) != cudaSuccess) return -1;
+    cudaMemset(tab, 1, (size_t)n * 16);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = sms * 4, iters = 256;
+    gather_kernel<<<grid, kNT>>>(tab, n - 1, 16, sink);  // warm-up (table into L2)
+    cudaEventRecord(e0);
+    gather_kernel<<<grid, kNT>>>(tab, n - 1, iters, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double loads = (double)grid * kNT * iters * kG;
+    out[0] = loads / (ms * 1e-3);
+    out[1] = out[0] * 32 / 1e9;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(tab);
+    cudaFree(sink);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 
 // out[0..3]: warp-instructions/s for alu, imad, mix, ffma; out[4..7]: the SM
 // MHz seen by each run; out[8]: SM count.  Returns 0 on success.

@@ -33,7 +33,9 @@ namespace bplb {
 
 constexpr int WT = 256;              // threads per CTA (wide kernels)
 constexpr int ISLICE = 1024;         // items per modular tile (2 x 16 per lane)
-constexpr int LLW = 128;             // lambdas per lane-lookup unit (4 x 32)
+constexpr int ISLICE_SEED = 256;     // ... for the pruning seeds (short units: they gate the rest)
+constexpr int LLW = 128;             // lambdas per lane-lookup unit, MT / RAD2 (4 x 32)
+constexpr int LLW_H = 32;            // ... CCM1 / BJ1 (harmonic loop per lane)
 constexpr int HSL_TS = 2048;         // harmonic terms per sliced CCM1 / BJ1 unit (64 per lane)
 constexpr int WIDE_MAX_SEGS = 64;
 enum { T_HSL = 4 };                  // CCM1 / BJ1 lambda with more than HSL_TS terms: term slices
@@ -56,14 +58,15 @@ struct WSeg {
     int kind, type;
     int64_t lo, hi;
     int chunk;
-    int nslice;       // T_MOD: item slices per lambda chunk
+    int nslice;       // T_MOD: item slices per lambda chunk; T_HSL: term slices per lambda
+    int islice;       // T_MOD: items per slice
     long long first, count;
 };
 
 struct WideState {
     NodeStats st;
     int bad;
-    int n_vb2;
+    int fin_fs1, fin_vb2[3];  // wide_final work: FS1 item-sliced; VB2 item-sliced per part (0, 1, 2)
     int64_t lo[K_COUNT], hi[K_COUNT];
     WSeg segs[WIDE_MAX_SEGS];
     int nseg;
@@ -78,13 +81,14 @@ struct WideState {
     int stop;              // PHASED: set when a completed kind exceeded k
     int n_done;
     alignas(256) long long unit_next;
+    alignas(256) int n_vb2;
+    alignas(256) int nvlist;  // pruning: surviving VB2 walk chunks
     alignas(256) long long unit_end;
     int scan_blocks_done;
     int prune;             // bound pruning: seeds (units [0, nA)) then the pruned rest
     long long nA;
     u64 thr[K_COUNT];      // per-kind keys after the seeds (VB2 chunk / sliced-lambda decisions)
     int vb2_seg;           // pruning: the VB2 rest segment, enumerated through vlist (-1: none)
-    int nvlist;            // surviving VB2 walk chunks
     int64_t hsl_hi[K_COUNT];  // CCM1 / BJ1: lambdas [lo, hsl_hi] are term-sliced (T_HSL)
 };
 
@@ -187,17 +191,35 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
     l_W = (long long)warp_sum_u64((u64)l_W);
     l_Vs = (long long)warp_sum_u64((u64)l_Vs);
     l_Vm = (long long)warp_sum_u64((u64)l_Vm);
-    if ((threadIdx.x & 31) == 0) {
+    // block-level reduction first: one set of global atomics per block
+    __shared__ int s_i[6];
+    __shared__ unsigned long long s_l[3];
+    if (threadIdx.x < 6) s_i[threadIdx.x] = 0;
+    if (threadIdx.x < 3) s_l[threadIdx.x] = 0;
+    __syncthreads();
+    if (lane == 0) {
+        atomicMax(&s_i[0], l_max);
+        atomicOr(&s_i[1], l_bad);
+        atomicAdd(&s_i[2], l_s);
+        atomicAdd(&s_i[3], l_e);
+        atomicAdd(&s_i[4], l_b);
+        atomicAdd(&s_i[5], l_f);
+        atomicAdd(&s_l[0], (unsigned long long)l_W);
+        atomicAdd(&s_l[1], (unsigned long long)l_Vs);
+        atomicAdd(&s_l[2], (unsigned long long)l_Vm);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         NodeStats* st = &b.state->st;
-        atomicMax(&st->maxw, l_max);
-        if (l_bad) atomicExch(&b.state->bad, 1);
-        if (l_s) atomicAdd(&st->n_small, l_s);
-        if (l_e) atomicAdd(&st->n_eq, l_e);
-        if (l_b) atomicAdd(&st->n_big, l_b);
-        if (l_f) atomicAdd(&st->n_full, l_f);
-        atomicAdd((unsigned long long*)&st->W, (unsigned long long)l_W);
-        atomicAdd((unsigned long long*)&st->Vs, (unsigned long long)l_Vs);
-        atomicAdd((unsigned long long*)&st->Vm, (unsigned long long)l_Vm);
+        atomicMax(&st->maxw, s_i[0]);
+        if (s_i[1]) atomicExch(&b.state->bad, 1);
+        if (s_i[2]) atomicAdd(&st->n_small, s_i[2]);
+        if (s_i[3]) atomicAdd(&st->n_eq, s_i[3]);
+        if (s_i[4]) atomicAdd(&st->n_big, s_i[4]);
+        if (s_i[5]) atomicAdd(&st->n_full, s_i[5]);
+        atomicAdd((unsigned long long*)&st->W, s_l[0]);
+        atomicAdd((unsigned long long*)&st->Vs, s_l[1]);
+        atomicAdd((unsigned long long*)&st->Vm, s_l[2]);
     }
 }
 
@@ -283,12 +305,11 @@ __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
     }
 }
 
-// Lambda ranges and the unit plan (one thread).
-__global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int use_range,
-                          int64_t lo0, int64_t hi0, int kinds0, int kinds1, int kinds2, int kinds3,
-                          int kinds4, int kinds5, int phased, int prune) {
-    WideState* s = b.state;
-    const int kinds[K_COUNT] = {kinds0, kinds1, kinds2, kinds3, kinds4, kinds5};
+// Lambda ranges and the unit plan (one thread, on a shared-memory copy of
+// the state: the plan's read-modify-write chains through global memory were
+// dependent L2 round trips).
+__device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int use_range, int64_t lo0,
+                          int64_t hi0, int phased, int prune) {
     bplb_stats_finish(&s->st, c);
     s->st.r = s->st.n_small + s->st.n_eq + s->st.n_big;
     for (int kd = 0; kd < K_COUNT; ++kd) {
@@ -309,12 +330,14 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
     s->nunits = 0;
     s->vb2_seg = -1;
     s->nvlist = 0;
+    s->fin_fs1 = 0;
+    s->fin_vb2[0] = s->fin_vb2[1] = s->fin_vb2[2] = 0;
     if (s->bad) return;
     const NodeStats& st = s->st;
-    auto push = [&](int kind, int type, int64_t a, int64_t z, int chunk, int nslice) {
+    auto push = [&](int kind, int type, int64_t a, int64_t z, int chunk, int nslice, int islice = 0) {
         if (z < a) return;
         WSeg& g = s->segs[s->nseg++];
-        g.kind = kind; g.type = type; g.lo = a; g.hi = z; g.chunk = chunk; g.nslice = nslice;
+        g.kind = kind; g.type = type; g.lo = a; g.hi = z; g.chunk = chunk; g.nslice = nslice; g.islice = islice;
         g.first = s->nunits;
         g.count = ((z - a + chunk) / chunk) * nslice;
         s->nunits += g.count;
@@ -329,7 +352,8 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
     // is longer than 64, one lane per lambda after.  The sliced lambdas come
     // in doubling groups so every lambda of a group needs about the group's
     // slice count (the surplus slices of its upper lambdas are empty).
-    auto push_div_look = [&](int kd, int64_t a, int64_t z) {
+    // types: bit 0 T_HSL, bit 1 T_WLOOK, bit 2 T_LOOKUP (segment order control).
+    auto push_div_look = [&](int kd, int64_t a, int64_t z, int types) {
         if (z < a) return;
         const int64_t span = kd == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
         int64_t sh = span / HSL_TS + 1;
@@ -338,25 +362,29 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
         int64_t sp = span / 64 + 1;
         if (sp < sh) sp = sh;
         if (sp > z + 1) sp = z + 1;
-        for (int64_t x = a; x < sh;) {
-            const int64_t y = min(sh - 1, 2 * x - 1);
-            push(kd, T_HSL, x, y, 1, (int)(span / x / HSL_TS + 1));
-            x = y + 1;
+        if (types & 1) {
+            for (int64_t x = a; x < sh;) {
+                const int64_t y = min(sh - 1, 2 * x - 1);
+                push(kd, T_HSL, x, y, 1, (int)(span / x / HSL_TS + 1));
+                x = y + 1;
+            }
+            if (sh > a) s->hsl_hi[kd] = sh - 1;
         }
-        if (sh > a) s->hsl_hi[kd] = sh - 1;
-        push(kd, T_WLOOK, sh, sp - 1, 1, 1);
-        push(kd, T_LOOKUP, sp, z, LLW, 1);
+        if (types & 2) push(kd, T_WLOOK, sh, sp - 1, 1, 1);
+        if (types & 4) push(kd, T_LOOKUP, sp, z, LLW_H, 1);
     };
-    auto push_mod = [&](int kd, int64_t a, int64_t z) {
+    auto push_mod = [&](int kd, int64_t a, int64_t z, int islice) {
         const int64_t items = kd == K_VB2 ? s->n_vb2 : st.r;
-        int nsl = (int)((items + ISLICE - 1) / ISLICE);
+        int nsl = (int)((items + islice - 1) / islice);
         if (nsl < 1) nsl = 1;
-        push(kd, T_MOD, a, z, LMOD, nsl);
+        push(kd, T_MOD, a, z, LMOD, nsl, islice);
+        return nsl > 1;
     };
     if (prune) {
         // seeds (units [0, nA)): MT, RAD2 and FS1 complete, VB2's first walk
         // chunk, a CCM1 / BJ1 window at c/4 + 1; then every other lambda,
-        // tested against the seeds' keys (bplb_prune.cuh bounds)
+        // tested against the seeds' keys (bplb_prune.cuh bounds).  The seed
+        // walks are cut finer (they gate the rest).
         int64_t w0[K_COUNT], w1[K_COUNT];
         for (int i = 0; i < nk; ++i) {
             const int kd = kinds[i];
@@ -366,30 +394,37 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
             if (hi < lo) continue;
             switch (kd) {
             case K_MT: case K_RAD2: push(kd, T_LOOKUP, lo, hi, LLW, 1); break;
-            case K_FS1: push_mod(kd, lo, hi); break;
-            case K_VB2: push_mod(kd, lo, min(hi, lo + LMOD - 1)); break;
+            case K_FS1: s->fin_fs1 = push_mod(kd, lo, hi, ISLICE_SEED); break;
+            case K_VB2: s->fin_vb2[1] = push_mod(kd, lo, min(hi, lo + LMOD - 1), ISLICE_SEED); break;
             default: {
                 int64_t a = c / 4 + 1;
                 a = a < lo ? lo : (a > hi ? hi : a);
                 w0[kd] = a; w1[kd] = min(hi, a + 31);
-                push(kd, T_LOOKUP, w0[kd], w1[kd], LLW, 1);
+                push(kd, T_LOOKUP, w0[kd], w1[kd], LLW_H, 1);
             }
             }
         }
         s->nA = s->nunits;
-        for (int i = 0; i < nk; ++i) {
-            const int kd = kinds[i];
-            const int64_t lo = s->lo[kd], hi = s->hi[kd];
-            if (hi < lo) continue;
-            if (kd == K_VB2 && hi >= lo + LMOD) {
-                s->vb2_seg = s->nseg;  // enumerated through the prefilter's chunk list
-                push_mod(kd, lo + LMOD, hi);
+        // the rest, longest units first (claims follow segment order): the
+        // VB2 walk chunks, the long per-lane CCM1 / BJ1 loops below the seed
+        // window, the term slices, the short loops above it, one warp per
+        // lambda last
+        for (int pass = 0; pass < 4; ++pass)
+            for (int i = 0; i < nk; ++i) {
+                const int kd = kinds[i];
+                const int64_t lo = s->lo[kd], hi = s->hi[kd];
+                if (hi < lo) continue;
+                if (kd == K_VB2 && pass == 0 && hi >= lo + LMOD) {
+                    s->vb2_seg = s->nseg;  // enumerated through the prefilter's chunk list
+                    s->fin_vb2[2] = push_mod(kd, lo + LMOD, hi, ISLICE);
+                }
+                if (kd == K_CCM1 || kd == K_BJ1) {
+                    if (pass == 0) push_div_look(kd, lo, w0[kd] - 1, 4);
+                    if (pass == 1) push_div_look(kd, lo, w0[kd] - 1, 1);
+                    if (pass == 2) push_div_look(kd, w1[kd] + 1, hi, 7);
+                    if (pass == 3) push_div_look(kd, lo, w0[kd] - 1, 2);
+                }
             }
-            if (kd == K_CCM1 || kd == K_BJ1) {
-                push_div_look(kd, lo, w0[kd] - 1);
-                push_div_look(kd, w1[kd] + 1, hi);
-            }
-        }
         return;
     }
     // Heavy modular units first in concurrent mode (longest-processing-time
@@ -410,10 +445,30 @@ __global__ void wide_plan(WideBufs b, int64_t c, int nk, const int* kinds_d, int
         if (hi < lo) continue;
         switch (kd) {
         case K_MT: case K_RAD2: push(kd, T_LOOKUP, lo, hi, LLW, 1); break;
-        case K_FS1: case K_VB2: push_mod(kd, lo, hi); break;
-        default: push_div_look(kd, lo, hi);
+        case K_FS1: s->fin_fs1 = push_mod(kd, lo, hi, ISLICE); break;
+        case K_VB2: s->fin_vb2[0] = push_mod(kd, lo, hi, ISLICE); break;
+        default: push_div_look(kd, lo, hi, 7);
         }
     }
+}
+
+constexpr int PLAN_T = 128;
+__global__ void __launch_bounds__(PLAN_T) wide_plan(WideBufs b, int64_t c, int nk, int use_range, int64_t lo0,
+                                                    int64_t hi0, int kinds0, int kinds1, int kinds2, int kinds3,
+                                                    int kinds4, int kinds5, int phased, int prune) {
+    __shared__ WideState ls;
+    static_assert(sizeof(WideState) % 4 == 0, "word copy");
+    const int nw = (int)(sizeof(WideState) / 4);
+    unsigned* g = (unsigned*)b.state;
+    unsigned* l = (unsigned*)&ls;
+    for (int i = threadIdx.x; i < nw; i += PLAN_T) l[i] = g[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int kinds[K_COUNT] = {kinds0, kinds1, kinds2, kinds3, kinds4, kinds5};
+        plan_body(&ls, c, nk, kinds, use_range, lo0, hi0, phased, prune);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nw; i += PLAN_T) g[i] = l[i];
 }
 
 // ---- batched harmonic loops over the global records (LkTableG layout) -------
@@ -626,7 +681,7 @@ __device__ void wide_unit(const KParams& p, WideBufs& b, WideState* s, const Wid
             const int L = (int)(lam_b - lam_a + 1);
             const int n_items = kind == K_VB2 ? ro.n_vb2 : st.r;
             const int* items = kind == K_VB2 ? b.vb2 : p.w;
-            const int i0 = slice * ISLICE, i1 = min(n_items, i0 + ISLICE);
+            const int i0 = slice * sg.islice, i1 = min(n_items, i0 + sg.islice);
             const int warp = threadIdx.x >> 5;
             u64* t = tot + warp * LMOD;
             for (int j = lane; j < LMOD; j += kWarp) t[j] = 0;
@@ -679,8 +734,11 @@ __device__ int g_wide_trace_n;
 
 // Persistent warp-unit kernel.  phase_kind >= 0 restricts to that kind's
 // segments (PHASED mode) and applies the Alg. 4 entry guard lb <= k.
+#ifndef WIDE_MINB
+#define WIDE_MINB 3  // resident wide_units CTAs per SM the register budget is sized for
+#endif
 template <bool WIDE>
-__global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phase_kind, int part) {
+__global__ void __launch_bounds__(WT, WIDE_MINB) wide_units(KParams p, WideBufs b, int phase_kind, int part) {
     __shared__ u64 tot[(WT / 32) * LMOD];
     __shared__ WSeg segs[WIDE_MAX_SEGS];
     __shared__ WideRO ro;
@@ -722,6 +780,13 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
     __syncthreads();
     if (skip) return;
     for (int i = threadIdx.x; i < nseg; i += WT) segs[i] = s->segs[i];
+    __syncthreads();
+    if (part == 2 && threadIdx.x == 0 && ro.vb2_seg >= 0) {  // the pruned VB2 rest: the prefilter's list
+        const int v = ro.vb2_seg;
+        segs[v].count = (long long)s->nvlist * segs[v].nslice;
+        for (int j = v + 1; j < nseg; ++j) segs[j].first = segs[j - 1].first + segs[j - 1].count;
+        u_end = segs[nseg - 1].first + segs[nseg - 1].count;
+    }
     __syncthreads();
     const LkTableG lk{b.rec, p.c};
     const bool cancel = (p.flags & BPLB_F_CANCEL) && phase_kind < 0;
@@ -775,56 +840,40 @@ __global__ void __launch_bounds__(WT) wide_units(KParams p, WideBufs b, int phas
     }
 }
 
-// Pruning, between the seeds and the rest (one CTA): snapshot the per-kind
-// keys, reset the unit counter, test every VB2 walk chunk of the rest once
-// against the snapshot (the same range relaxation the units used to apply
-// per slice) and compact the survivors into vlist; the VB2 segment then
-// enumerates only those chunks and the later segments shift down.
-constexpr int PF_T = 1024;
+// Pruning, between the seeds and the rest: snapshot the per-kind keys, reset
+// the unit counter, test every VB2 walk chunk of the rest once against the
+// keys (the range relaxation the units used to apply per slice) and append
+// the survivors to vlist (any order); each wide_units CTA of the rest then
+// resizes the VB2 segment to the list in its shared copy of the plan.
+constexpr int PF_T = 256;
 __global__ void __launch_bounds__(PF_T) wide_prefilter(KParams p, WideBufs b) {
-    __shared__ int wcnt[PF_T / 32];
-    __shared__ int total;
     WideState* s = b.state;
-    if (threadIdx.x < K_COUNT) s->thr[threadIdx.x] = s->key[threadIdx.x];
-    if (threadIdx.x == 0) {
-        s->unit_next = 0;
-        total = 0;
-    }
-    __syncthreads();
     const int si = s->vb2_seg;
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < K_COUNT) s->thr[threadIdx.x] = s->key[threadIdx.x];
+        if (threadIdx.x == 0) s->unit_next = 0;
+    }
     if (s->bad || si < 0) return;
     const WSeg g = s->segs[si];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // every lambda of the rest is accounted here
+        atomicAdd(&s->evals[K_VB2], (unsigned long long)(g.hi - g.lo + 1));
+        s->evaluated[K_VB2] = 1;
+    }
     const int64_t c = p.c, lo_k = s->lo[K_VB2];
-    const Thr th = thr_from_key(s->thr[K_VB2]);
+    const Thr th = thr_from_key(s->key[K_VB2]);  // no unit runs now: the keys are final for this step
     const NodeStats st = s->st;
     const int64_t nch = (g.hi - g.lo + LMOD) / LMOD;
     const int64_t first = (g.lo - lo_k) / LMOD;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t c0 = 0; c0 < nch; c0 += PF_T) {
-        const int64_t ch = c0 + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    for (int64_t c0 = (int64_t)blockIdx.x * PF_T + (threadIdx.x & ~31); c0 < nch; c0 += (int64_t)gridDim.x * PF_T) {
+        const int64_t ch = c0 + lane;
         const int64_t la = g.lo + ch * LMOD;
         const bool keep = ch < nch && !range_skip(th, K_VB2, st, c, lo_k, la, min(g.hi, la + LMOD - 1));
         const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wcnt[warp] = __popc(m);
-        __syncthreads();
-        int before = total;
-        for (int i = 0; i < warp; ++i) before += wcnt[i];
-        if (keep) b.vlist[before + __popc(m & ((1u << lane) - 1u))] = (int)(first + ch);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int t = total;
-            for (int i = 0; i < PF_T / 32; ++i) t += wcnt[i];
-            total = t;
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        s->nvlist = total;
-        s->segs[si].count = (long long)total * g.nslice;
-        for (int j = si + 1; j < s->nseg; ++j) s->segs[j].first = s->segs[j - 1].first + s->segs[j - 1].count;
-        s->nunits = s->segs[s->nseg - 1].first + s->segs[s->nseg - 1].count;
-        s->evals[K_VB2] += (unsigned long long)(g.hi - g.lo + 1);
-        s->evaluated[K_VB2] = 1;
+        int pos = 0;
+        if (lane == 0 && m) pos = atomicAdd(&s->nvlist, __popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (keep) b.vlist[pos + __popc(m & ((1u << lane) - 1u))] = (int)(first + ch);
     }
 }
 
@@ -866,15 +915,27 @@ __global__ void __launch_bounds__(WT) wide_final(KParams p, WideBufs b, int only
         }
     };
     auto want = [&](int kd) { return (only_kind < 0 || only_kind == kd) && s->hi[kd] >= s->lo[kd]; };
-    if (want(K_FS1) && part != 2 && st.r > ISLICE) {
-        const int64_t lo = s->lo[K_FS1];
-        sweep(K_FS1, s->hi[K_FS1] - lo + 1, [&](int64_t j) { return lo + j; },
-              [&](int64_t lam) {
-                  return bplb_fs1_sum(st, lam, b.pz[lam],
-                                      (uint64_t)bplb_fs1_zero(LkTableG{b.rec, c}, c, st.maxw, lam));
-              });
+    if (want(K_FS1) && part != 2 && s->fin_fs1) {
+        // one warp per lambda: Z = sum over the multiples v of m = c / gcd(c,
+        // lambda + 1) of W(v) - W(v-1), split over the lanes (<= maxw / m terms)
+        const int64_t lo = s->lo[K_FS1], n = s->hi[K_FS1] - lo + 1;
+        const int64_t nwarps = stride / 32;
+        for (int64_t j = j_first / 32; j < n; j += nwarps) {
+            const int64_t lam = lo + j;
+            const int64_t m = c / bplb_gcd(c, lam + 1);
+            long long z = 0;
+            for (int64_t v = m * (1 + lane); v <= st.maxw; v += 32 * m) {
+                const ulonglong2 h = __ldg(&b.rec[v + 1]), l = __ldg(&b.rec[v]);
+                z += (long long)(h.x - l.x);
+            }
+            z = (long long)warp_sum_u64((u64)z);
+            const int64_t S = bplb_fs1_sum(st, lam, b.pz[lam], (uint64_t)z);
+            const int64_t bd = bplb_bound(S, bplb_fc(K_FS1, c, lam));
+            const int64_t mm = emit_warp(lane == 0, lam, bd, lo, &s->key[K_FS1], p.lam_out, p.out_lo, p.out_hi);
+            wmax = mm > wmax ? mm : wmax;
+        }
     }
-    if (want(K_VB2) && s->n_vb2 > ISLICE) {
+    if (want(K_VB2) && s->fin_vb2[part]) {
         const int64_t lo = s->lo[K_VB2], hi = s->hi[K_VB2];
         auto vsum = [&](int64_t lam) { return bplb_vb2_sum(st, c, lam, b.acc[lam]); };
         if (part == 0) sweep(K_VB2, hi - lo + 1, [&](int64_t j) { return lo + j; }, vsum);
@@ -1000,8 +1061,8 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     // integer envelope of the bplb_prune.cuh bounds
     const bool prune = !phased && !(p.flags & (BPLB_F_CANCEL | BPLB_F_NOPRUNE)) && !p.lam_out && !p.use_range &&
                        c <= WIDE_PRUNE_MAX_C && r <= WIDE_PRUNE_MAX_R;
-    wide_plan<<<1, 1, 0, st>>>(b, c, p.nk, nullptr, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3],
-                               ks[4], ks[5], (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0, prune ? 1 : 0);
+    wide_plan<<<1, PLAN_T, 0, st>>>(b, c, p.nk, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3], ks[4], ks[5],
+                                    (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0, prune ? 1 : 0);
     *launches += 5;
     int per_sm = 0;
     const bool wide = c >= (1 << 23);
@@ -1013,7 +1074,8 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     if (prune) {
         units<<<grid, WT, 0, st>>>(p, b, -1, 1);
         wide_final<<<g_fin, WT, 0, st>>>(p, b, -1, 1);
-        wide_prefilter<<<1, PF_T, 0, st>>>(p, b);
+        wide_prefilter<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((c / LMOD + PF_T) / PF_T, num_sms)), PF_T, 0,
+                         st>>>(p, b);
         units<<<grid, WT, 0, st>>>(p, b, -1, 2);
         wide_final<<<g_fin, WT, 0, st>>>(p, b, -1, 2);
         *launches += 5;

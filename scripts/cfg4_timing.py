@@ -11,13 +11,16 @@ import numpy as np  # noqa: E402
 
 from paper_2402_14821_b200 import _native, workloads as W  # noqa: E402
 
+if os.environ.get("BPLB_LIB"):  # a development build (e.g. another launch-bounds variant)
+    _native.load_library(os.environ["BPLB_LIB"])
 c, w = W.cfg4()
 eng = _native.Engine(0)
 g = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "configs.npz"))
-for label, fl in (("pruned", 0), ("dense", _native.F_NOPRUNE)):
+modes = (("pruned", 0),) if os.environ.get("PRUNED_ONLY") else (("pruned", 0), ("dense", _native.F_NOPRUNE))
+for label, fl in modes:
     eng.check(w, c, 2**62, list(range(6)), fl | _native.F_TIMING)
     ts = []
-    for _ in range(5):
+    for _ in range(9):
         r = eng.check(w, c, 2**62, list(range(6)), fl | _native.F_TIMING)
         ts.append(eng.last_device_ms())
     best = [int(r.best[i]) for i in range(6)]

@@ -1,7 +1,12 @@
 """Parse an ncu --csv capture of scripts/cfg4_one.py (two cfg4 checks) into
 profiles/cfg4_wide_ncu.json: per-kernel duration / warp instructions / DRAM
 bytes of the SECOND check's launch sequence (wide_init .. wide_finish) and the
-wide_units totals bench.py's cfg4 roofline uses."""
+wide_units totals bench.py's cfg4 roofline uses.
+
+    ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,\
+l1tex__m_xbar2l1tex_read_sectors_mem_lg_op_ld.sum --clock-control none --csv \
+        python scripts/cfg4_one.py > gpurun_out/ncu_cfg4_metrics.csv
+"""
 import collections
 import csv
 import json
@@ -26,6 +31,7 @@ out = {
     "wide_units_warp_inst": sum(d["smsp__inst_executed.sum"] for d in units),
     "wide_units_us": sum(d["gpu__time_duration.sum"] for d in units) / 1e3,
     "wide_units_dram_bytes": sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in units),
+    "wide_units_l2_sectors": sum(d.get("l1tex__m_xbar2l1tex_read_sectors_mem_lg_op_ld.sum", 0) for d in units),
     "sequence_us_serialised": sum(d.get("gpu__time_duration.sum", 0) for d in second) / 1e3,
     "source": os.path.basename(path) + " (ncu --metrics, --clock-control none, second of two cfg4 checks)",
 }
