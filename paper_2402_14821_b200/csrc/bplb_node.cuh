@@ -19,6 +19,7 @@
 #pragma once
 #include <climits>
 #include "bplb_device.cuh"
+#include "bplb_ubound.cuh"
 #include "../../include/bplb.h"
 
 namespace bplb {
@@ -50,6 +51,7 @@ struct MultiState {
     // the per-unit counters on their own L2 lines
     alignas(256) int unit_next;
     alignas(256) int units_done;
+    alignas(256) u64 live[K_COUNT];  // VB2 pruning: the best key any CTA has published
 };
 
 struct KParams {
@@ -95,6 +97,7 @@ struct NodeCtl {
     int n_done;
     int bad;
     int skip;
+    int vprune_seg;  // multi-CTA full check: the VB2 rest segment, pruned against ms->live (-1: none)
     long long wsum[NW];
     long long wsum2[NW];
 };
@@ -238,6 +241,12 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
         const bool valid = lam <= lam_b;
         int64_t b = valid ? bplb_bound(mine, bplb_fc(kind, c, lam)) : 0;
         wmax = emit_warp(valid, lam, b, ctl.lo[kind], &ctl.key[kind], lam_out, p.out_lo, p.out_hi);
+    } else if (si == ctl.vprune_seg &&
+               range_skip(thr_from_key(*(volatile u64*)&p.ms->live[K_VB2]), K_VB2, st, c, ctl.lo[K_VB2], lam_a,
+                          lam_b)) {
+        // the whole chunk provably cannot beat the best VB2 key published so
+        // far (bplb_prune.cuh relaxation; skipped lambdas count as evaluated)
+        wmax = -1;
     } else {
         const int warp = threadIdx.x >> 5;
         u64* t = m.tot + warp * LMOD;
@@ -273,6 +282,7 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
         ctl.evaluated[kind] = 1;
         if (wmax >= 0) {
             atomicMax(&ctl.lb, (int)wmax);
+            if (ctl.vprune_seg >= 0 && kind == K_VB2) atomicMax(&p.ms->live[K_VB2], ctl.key[K_VB2]);
             // the cross-CTA running maxima only feed the PHASED / CANCEL guards
             if (p.ms && (p.flags & (BPLB_F_PHASED | BPLB_F_CANCEL))) {
                 atomicMax(&p.ms->lb, (int)wmax);
@@ -689,7 +699,32 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                 if (!kind_in(p, kd)) hi = lo - 1;
                 ctl.lo[kd] = lo; ctl.hi[kd] = hi;
             }
-            for (int i = 0; i < p.nk; ++i) add_kind_segs(ctl, p.kinds[i], TABLE, c);
+            // multi-CTA full checks inside the pruning envelope: VB2 as a
+            // 32-lambda seed unit first, the other kinds, then the VB2 rest,
+            // whose chunks are tested against the best published VB2 key
+            const bool vprune = multi && !single && !(p.flags & (BPLB_F_PHASED | BPLB_F_CANCEL | BPLB_F_NOPRUNE)) &&
+                                c <= ((int64_t)1 << 20) && kind_in(p, K_VB2) &&
+                                ctl.hi[K_VB2] >= ctl.lo[K_VB2] + 32 + LMOD;
+            ctl.vprune_seg = -1;
+            if (vprune) {
+                const int64_t vlo = ctl.lo[K_VB2], vhi = ctl.hi[K_VB2];
+                auto pushv = [&](int64_t a, int64_t b, int chunk) {
+                    Seg& g = ctl.segs[ctl.nseg++];
+                    g.kind = K_VB2; g.type = T_MOD; g.lo = a; g.hi = b; g.chunk = chunk;
+                    g.first = ctl.nunits;
+                    g.count = (int)((b - a + chunk) / chunk);
+                    ctl.nunits += g.count;
+                };
+                pushv(vlo, vlo + 31, 32);
+                for (int i = 0; i < p.nk; ++i)
+                    if (p.kinds[i] != K_VB2) add_kind_segs(ctl, p.kinds[i], TABLE, c);
+                ctl.vprune_seg = ctl.nseg;
+                pushv(vlo + 32, vhi, LMOD);
+                ctl.kind_seg_first[K_VB2] = 0;
+                ctl.kind_seg_count[K_VB2] = 2;  // (kind bookkeeping: only the guards use it)
+            } else {
+                for (int i = 0; i < p.nk; ++i) add_kind_segs(ctl, p.kinds[i], TABLE, c);
+            }
             if (ctl.bad) {
                 ctl.nunits = 0; ctl.nseg = 0;
                 for (int kd = 0; kd < K_COUNT; ++kd) ctl.kind_seg_count[kd] = 0;

@@ -237,3 +237,29 @@ def test_wide_path_pruned_equals_dense(eng, shape):
         got = list(a.best)
         assert [x for i, x in enumerate(got) if i != 4] == [x for i, x in enumerate(want) if i != 4]
         assert got[4] == 50011 and a.arg_lambda[4] == 3
+
+
+@pytest.mark.parametrize("shape", [("cfg3", 0, 0), ("cfg3u", 0, 0), ("u", 3_000, 200_003), ("u", 900, 65_537),
+                                   ("tri", 2_000, 99_991)])
+def test_multi_cta_node_vb2_pruned_equals_dense(eng, shape):
+    """Single full-collection checks on the multi-CTA node kernel: the VB2
+    rest is tested chunk by chunk against the best VB2 key any CTA has
+    published (seed chunk first); per-kind best, arg lambda, evals and lb equal
+    the dense sweep's (F_NOPRUNE)."""
+    kind, r, c = shape
+    rng = np.random.default_rng(r + c + 7)
+    if kind == "cfg3":
+        c, w = W.cfg3()
+    elif kind == "cfg3u":
+        c, w = W.cfg3u()
+    elif kind == "u":
+        w = rng.integers(1, c + 1, r)
+    else:
+        w = rng.integers(c // 4 + 1, c // 2, r)
+    w = w.astype(np.int32)
+    a = eng.check(w, c, 2**62, ALL, 0)
+    path = eng.last_path()[0]
+    b = eng.check(w, c, 2**62, ALL, _native.F_NOPRUNE)
+    for f in ("best", "arg_lambda", "evals", "evaluated"):
+        assert list(getattr(a, f)) == list(getattr(b, f)), (f, path)
+    assert a.lb == b.lb
