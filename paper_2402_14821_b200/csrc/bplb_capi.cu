@@ -159,6 +159,11 @@ struct bplb_engine {
     std::vector<int32_t> inst_host;   // what d_inst holds
     DevBuf d_skeys;                   // single-check table path: keys[8] + CTA counter
     MappedBuf m_single;               // single-check table path: weights in, result out
+    MappedBuf m_nres;                 // single-check node path: result + error word out
+    bool multi_dirty = true;          // the MultiState needs zeroing (first use, or a failed check)
+    const void* node_attr_kern = nullptr;  // launch_node: kernel / smem / occupancy of the last launch
+    size_t node_attr_smem = 0;
+    int node_attr_per_sm = 0;
     MappedBuf m_err;                  // batch calls: error flag written by the kernels
     bool skeys_zeroed = false;
     size_t tab_attr_smem = 0;
@@ -738,10 +743,17 @@ int launch_node(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_r
     if (smem > e->smem_optin) return fail(BPLB_ERANGE, "node needs more shared memory than available");
     auto kern = table ? bplb::node_kernel<true, false>
                       : (p.c >= (1 << 23) ? bplb::node_kernel<false, true> : bplb::node_kernel<false, false>);
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::NT, smem));
-    if (per_sm < 1) per_sm = 1;
+    if (e->node_attr_kern == (const void*)kern && e->node_attr_smem == smem) {  // (host API calls cost us)
+        per_sm = e->node_attr_per_sm;
+    } else {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::NT, smem));
+        if (per_sm < 1) per_sm = 1;
+        e->node_attr_kern = (const void*)kern;
+        e->node_attr_smem = smem;
+        e->node_attr_per_sm = per_sm;
+    }
     int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
     if (multi) {  // co-resident grid (CTAs may wait on each other), sized by the work
         // at most one CTA per SM: two per SM measured 7-10 % slower (cfg3
@@ -882,6 +894,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     e->h_stage.release();
     e->h_res.release();
     e->m_single.release();
+    e->m_nres.release();
     e->m_err.release();
     cudaEventDestroy(e->ev0);
     if (e->ev_tail) cudaEventDestroy(e->ev_tail);
@@ -1046,14 +1059,6 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     }
     // weights through the pinned staging buffer (the copy stays asynchronous)
     if (int rc2 = e->h_stage.grow((size_t)r * 4 + 64)) return rc2;
-    if (r > 0) {
-        std::memcpy(e->h_stage.p, w, (size_t)r * 4);
-        CUDA_TRY(cudaMemcpyAsync(e->d_w.p, e->h_stage.p, (size_t)r * 4, cudaMemcpyHostToDevice, e->stream));
-    }
-    p.w = (const int*)e->d_w.p;
-    p.res_out = (bplb_result*)e->d_res.p;
-    p.err_out = (int*)((char*)e->d_res.p + sizeof(bplb_result));  // copied back with the result
-    CUDA_TRY(cudaMemsetAsync(p.err_out, 0, 4, e->stream));
     // the grid-wide path for nodes beyond the node-resident kernels, and for
     // full-collection checks it can prune (seeded keys + bound tests): one
     // launch sequence over all SMs beats the multi-CTA node kernel's phase
@@ -1062,20 +1067,50 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
                              c <= bplb::WIDE_PRUNE_MAX_C && r <= bplb::WIDE_PRUNE_MAX_R &&
                              r * c >= e->wide_prune_min_cells;
     if (!node_fits(r, c) || wide_prunes) {
+        if (r > 0) {
+            std::memcpy(e->h_stage.p, w, (size_t)r * 4);
+            CUDA_TRY(cudaMemcpyAsync(e->d_w.p, e->h_stage.p, (size_t)r * 4, cudaMemcpyHostToDevice, e->stream));
+        }
+        p.w = (const int*)e->d_w.p;
+        p.res_out = (bplb_result*)e->d_res.p;
+        p.err_out = (int*)((char*)e->d_res.p + sizeof(bplb_result));  // copied back with the result
+        CUDA_TRY(cudaMemsetAsync(p.err_out, 0, 4, e->stream));
         e->last_path = BPLB_PATH_WIDE;
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
                               p, r, nullptr);
         if (rc) return fail(rc, bplb::wide_error());
     } else {
-        // single node: offsets and the cross-CTA state
-        int64_t off_h[2] = {0, r};
-        if ((rc = e->d_off.grow(16))) return rc;
+        // single node, multi-CTA: the offsets travel with the weights (one
+        // H2D copy), the cross-CTA state is zeroed by the kernel's last CTA
+        // for the next call (here only on first use or after a failure), and
+        // the result and the error word land in mapped pinned memory
         if ((rc = e->d_multi.grow(sizeof(bplb::MultiState)))) return rc;
-        CUDA_TRY(cudaMemcpyAsync(e->d_off.p, off_h, 16, cudaMemcpyHostToDevice, e->stream));
-        CUDA_TRY(cudaMemsetAsync(e->d_multi.p, 0, sizeof(bplb::MultiState), e->stream));
-        p.off = (const int64_t*)e->d_off.p;
+        if ((rc = e->m_nres.grow(sizeof(bplb_result) + 16))) return rc;
+        if (e->multi_dirty) CUDA_TRY(cudaMemsetAsync(e->d_multi.p, 0, sizeof(bplb::MultiState), e->stream));
+        int64_t* hs = (int64_t*)e->h_stage.p;
+        hs[0] = 0;
+        hs[1] = r;
+        if (r > 0) std::memcpy(hs + 2, w, (size_t)r * 4);  // (h_stage holds r * 4 + 64 bytes)
+        CUDA_TRY(cudaMemcpyAsync(e->d_w.p, hs, 16 + (size_t)r * 4, cudaMemcpyHostToDevice, e->stream));
+        p.off = (const int64_t*)e->d_w.p;
+        p.w = (const int*)((const char*)e->d_w.p + 16);
+        p.res_out = (bplb_result*)e->m_nres.d;
+        p.err_out = (int*)((char*)e->m_nres.d + sizeof(bplb_result));
         p.ms = (bplb::MultiState*)e->d_multi.p;
+        e->multi_dirty = true;
         if ((rc = launch_node(e, p, 1, r, 0, true))) return rc;
+        if (timing) CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+        e->multi_dirty = false;
+        if (timing) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+            e->last_ms = ms;
+        }
+        if (*(volatile int*)((char*)e->m_nres.h + sizeof(bplb_result)))
+            return fail(BPLB_EINVAL, "reduced weight outside [1, c]");
+        std::memcpy(out, e->m_nres.h, sizeof(bplb_result));
+        return 0;
     }
     CUDA_TRY(cudaMemcpyAsync(e->h_res.p, e->d_res.p, sizeof(bplb_result) + 4, cudaMemcpyDeviceToHost,
                              e->stream));
@@ -1672,6 +1707,13 @@ BPLB_API int bplb_wide_trace(long long* out, int cap) {
     int z = 0;
     cudaMemcpyToSymbol(bplb::g_wide_trace_n, &z, sizeof(int));
     return n;
+}
+#endif
+
+#ifdef NODE_TRACE
+BPLB_API int bplb_node_trace(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, bplb::g_node_trace, sizeof(bplb::g_node_trace));
+    return 0;
 }
 #endif
 

@@ -98,6 +98,7 @@ struct NodeCtl {
     int bad;
     int skip;
     int vprune_seg;  // multi-CTA full check: the VB2 rest segment, pruned against ms->live (-1: none)
+    u64 pub[K_COUNT];  // ... the keys this CTA has published to ms->live
     long long wsum[NW];
     long long wsum2[NW];
 };
@@ -140,8 +141,23 @@ __device__ __forceinline__ int64_t div_split(int kind, const NodeStats& st, int6
     return (4 * (int64_t)st.maxw) / n + 1;
 }
 
+#ifdef NODE_TRACE
+// phase stamps of every CTA (development builds: scripts/node_trace.py)
+__device__ unsigned long long g_node_trace[1024][8];
+#define NODE_STAMP(i)                                                               \
+    do {                                                                            \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                \
+            unsigned long long t_;                                                  \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+            g_node_trace[blockIdx.x][i] = t_;                                       \
+        }                                                                           \
+    } while (0)
+#else
+#define NODE_STAMP(i) do {} while (0)
+#endif
+
 // Build the unit segments of one kind (thread 0).
-__device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c) {
+__device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c, int ldiv = LDIV) {
     const int64_t lo = ctl.lo[kind], hi = ctl.hi[kind];
     ctl.kind_seg_first[kind] = ctl.nseg;
     ctl.kind_seg_count[kind] = 0;
@@ -176,7 +192,7 @@ __device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c) {
             sp = div_split(kind, ctl.st, c);
             if (sp < lo) sp = lo;
             if (sp > hi + 1) sp = hi + 1;
-            push(T_DIV, lo, sp - 1, LDIV);
+            push(T_DIV, lo, sp - 1, ldiv);
         }
         int64_t sw = span / 64 + 1;  // one warp per lambda while the loop is long
         if (sw < sp) sw = sp;
@@ -282,7 +298,13 @@ __device__ void run_unit(const KParams& p, NodeCtl& ctl, const LK& lk, const Nod
         ctl.evaluated[kind] = 1;
         if (wmax >= 0) {
             atomicMax(&ctl.lb, (int)wmax);
-            if (ctl.vprune_seg >= 0 && kind == K_VB2) atomicMax(&p.ms->live[K_VB2], ctl.key[K_VB2]);
+            if (ctl.vprune_seg >= 0 && kind == K_VB2) {
+                const u64 kk = *(volatile u64*)&ctl.key[kind];
+                if (kk > ctl.pub[kind]) {  // publish only what improved (one L2 line for every CTA)
+                    ctl.pub[kind] = kk;
+                    atomicMax(&p.ms->live[kind], kk);
+                }
+            }
             // the cross-CTA running maxima only feed the PHASED / CANCEL guards
             if (p.ms && (p.flags & (BPLB_F_PHASED | BPLB_F_CANCEL))) {
                 atomicMax(&p.ms->lb, (int)wmax);
@@ -551,6 +573,7 @@ __host__ __device__ inline size_t node_smem_bytes(bool table, int rcap, int64_t 
 template <bool TABLE, bool WIDE>
 __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
     extern __shared__ __align__(16) unsigned char smem[];
+    NODE_STAMP(0);
     __shared__ NodeCtl ctl;
     const int64_t c = p.c;
     NodeMem m;
@@ -604,6 +627,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
         for (int i = threadIdx.x; i < (TABLE ? r : pw); i += NT)
             m.sw[i] = i < r ? load_w(p, base + i) : INT_MAX;
         __syncthreads();
+        NODE_STAMP(1);
         // ---- statistics ------------------------------------------------------
         {
             int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
@@ -640,6 +664,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
             }
         }
         __syncthreads();
+        NODE_STAMP(2);
         // ---- lookup structure -----------------------------------------------
         if (TABLE) {
             // distinct (value, count) pairs for the modular walks (G11: order free)
@@ -706,6 +731,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                                 c <= ((int64_t)1 << 20) && kind_in(p, K_VB2) &&
                                 ctl.hi[K_VB2] >= ctl.lo[K_VB2] + 32 + LMOD;
             ctl.vprune_seg = -1;
+            for (int kd = 0; kd < K_COUNT; ++kd) ctl.pub[kd] = 0;
             if (vprune) {
                 const int64_t vlo = ctl.lo[K_VB2], vhi = ctl.hi[K_VB2];
                 auto pushv = [&](int64_t a, int64_t b, int chunk) {
@@ -716,14 +742,16 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                     ctl.nunits += g.count;
                 };
                 pushv(vlo, vlo + 31, 32);
+                // (dense-division units of 4 lambdas: 32 of them, a pass over
+                // the items each, made one unit the whole sweep's tail)
                 for (int i = 0; i < p.nk; ++i)
-                    if (p.kinds[i] != K_VB2) add_kind_segs(ctl, p.kinds[i], TABLE, c);
+                    if (p.kinds[i] != K_VB2) add_kind_segs(ctl, p.kinds[i], TABLE, c, 4);
                 ctl.vprune_seg = ctl.nseg;
-                pushv(vlo + 32, vhi, LMOD);
+                pushv(vlo + 32, vhi, 32);  // short chunks: a surviving one must not become the tail
                 ctl.kind_seg_first[K_VB2] = 0;
                 ctl.kind_seg_count[K_VB2] = 2;  // (kind bookkeeping: only the guards use it)
             } else {
-                for (int i = 0; i < p.nk; ++i) add_kind_segs(ctl, p.kinds[i], TABLE, c);
+                for (int i = 0; i < p.nk; ++i) add_kind_segs(ctl, p.kinds[i], TABLE, c, multi ? 4 : LDIV);
             }
             if (ctl.bad) {
                 ctl.nunits = 0; ctl.nseg = 0;
@@ -731,6 +759,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
             }
         }
         __syncthreads();
+        NODE_STAMP(3);
         // ---- sweep -------------------------------------------------------------
         if (TABLE) {
             LkTable lk{m.cnt, m.pre, c};
@@ -742,6 +771,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
             else sweep_node<TABLE, WIDE>(p, ctl, lk, m, single, phased, cancel);
         }
         __syncthreads();
+        NODE_STAMP(4);
         // ---- outputs ----------------------------------------------------------
         if (multi) {
             __shared__ int last;
@@ -774,13 +804,23 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                         }
                     }
                     ctl.n_done = nd;
+                    // every other CTA is past its last access: leave the
+                    // cross-CTA state zeroed for the next check
+                    for (int kd = 0; kd < K_COUNT; ++kd) {
+                        ms->key[kd] = 0; ms->kmax[kd] = 0; ms->evals[kd] = 0; ms->evaluated[kd] = 0;
+                        ms->live[kd] = 0;
+                    }
+                    ms->lb = 0; ms->ctas_done = 0; ms->unit_next = 0; ms->units_done = 0;
                 }
             }
             __syncthreads();
             if (!last) break;
         }
         if (threadIdx.x == 0) {
-            if (ctl.bad && p.err_out) atomicExch(p.err_out, 1);
+            if (p.err_out) {
+                if (multi) *p.err_out = ctl.bad ? 1 : 0;  // (written every check: no host memset)
+                else if (ctl.bad) atomicExch(p.err_out, 1);
+            }
             int64_t lb = 0;
             bplb_result res;
             for (int kd = 0; kd < K_COUNT; ++kd) {

@@ -9,8 +9,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2402_14821_b200 as G  # noqa: E402
 from paper_2402_14821_b200 import _native, workloads as W  # noqa: E402
 
+if os.environ.get("BPLB_LIB"):  # a development build
+    _native.load_library(os.environ["BPLB_LIB"])
 eng = _native.default_engine(0)
-for name, gen in (("cfg1", W.cfg1), ("cfg3", W.cfg3), ("cfg3u", W.cfg3u), ("cfg4", W.cfg4)):
+cfgs = (("cfg1", W.cfg1), ("cfg3", W.cfg3), ("cfg3u", W.cfg3u), ("cfg4", W.cfg4))
+if os.environ.get("ONLY"):
+    cfgs = [x for x in cfgs if x[0] in os.environ["ONLY"].split(",")]
+for name, gen in cfgs:
     c, w = gen()
     red = G.ReducedInstance.from_array(c, w)
     for _ in range(3):
