@@ -1720,6 +1720,7 @@ BPLB_API int bplb_node_trace(unsigned long long* out) {
 #ifdef TC_TRACE
 BPLB_API int bplb_tc_trace(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, bplb::g_tc_trace, 64 * 8);
+    cudaMemcpyFromSymbol(out + 64, bplb::g_tc_cta, 256 * 3 * 8);
     return 0;
 }
 #endif

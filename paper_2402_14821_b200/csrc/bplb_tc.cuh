@@ -128,6 +128,15 @@ __device__ __forceinline__ int tc_load_w(const void* w, int64_t i) {
 
 #ifdef TC_TRACE
 __device__ unsigned long long g_tc_trace[64];  // CTA 0: globaltimer at the phase boundaries
+__device__ unsigned long long g_tc_cta[256][3];  // every CTA: start, histogram done, end
+#define TC_CTA(i)                                                                              \
+    do {                                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x < 256) {                                            \
+            unsigned long long t_;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+            g_tc_cta[blockIdx.x][i] = t_;                                                      \
+        }                                                                                      \
+    } while (0)
 #define TC_STAMP(i)                                                                            \
     do {                                                                                       \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                             \
@@ -138,6 +147,7 @@ __device__ unsigned long long g_tc_trace[64];  // CTA 0: globaltimer at the phas
     } while (0)
 #else
 #define TC_STAMP(i) do {} while (0)
+#define TC_CTA(i) do {} while (0)
 #endif
 
 // Shared memory: A planes | X = counts, then B buffer 0 + meta 0 | (DB) B
@@ -197,6 +207,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     const int nn = (int)(rem < t.rows ? rem : t.rows);
     const int c = (int)p.c;
     TC_STAMP(0);
+    TC_CTA(0);
 
     if (tid == 0) {
         s_bad = 0;
@@ -286,6 +297,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
     if (__any_sync(0xffffffffu, bad) && lane == 0) s_bad = 1;
     __syncthreads();
     TC_STAMP(1);
+    TC_CTA(1);
     // ---- A planes: row tid % 128, a quarter of its 16-byte core rows -----------
     {
         const int arow = tid & (TC_M - 1), part = tid >> 7;
@@ -440,6 +452,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_kernel(KParams p, TcDev t) {
         tab_node_emit(p, kk, n0 + tid);
     }
     TC_STAMP(41);
+    TC_CTA(2);
 }
 
 }  // namespace bplb

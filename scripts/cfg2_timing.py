@@ -42,6 +42,19 @@ for label, fl in (("tc", 0), ("fp32", _native.F_NOTC)):
     res[label] = lb.cpu().numpy().copy()
     print(f"{label:5s} {statistics.median(ts):8.1f} us per 10^4 nodes  path {eng.last_path()}")
 print("tc == fp32:", bool(np.array_equal(res["tc"], res["fp32"])))
+# the contraction kernel alone (events around the launch inside the C ABI;
+# graph replay off), same L2 flush
+eng._lib.bplb_profile_kernel(eng.handle, 1)
+ks = []
+for i in range(20):
+    with torch.cuda.stream(s):
+        flush.fill_(i)
+    eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, max_r, c, 2**62, list(range(6)), 0,
+                           lb.data_ptr(), ex.data_ptr(), stream_ptr=s.cuda_stream, wbytes=1)
+    s.synchronize()
+    ks.append(eng.last_kernel_ms() * 1e3)
+eng._lib.bplb_profile_kernel(eng.handle, 0)
+print(f"tc kernel alone {statistics.median(ks):8.1f} us per 10^4 nodes")
 from oracle import oracle as O  # noqa: E402
 
 O.set_threads(O.max_threads())

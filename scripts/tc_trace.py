@@ -31,11 +31,15 @@ lb = torch.empty(n, dtype=torch.int64, device="cuda")
 ex = torch.empty(n, dtype=torch.uint8, device="cuda")
 eng = _native.Engine(0)
 s = torch.cuda.Stream()
-for _ in range(3):
+flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
+for i in range(3):
+    if os.environ.get("FLUSH"):
+        with torch.cuda.stream(s):
+            flush.fill_(i)
     eng.check_batch_device(d_w.data_ptr(), d_off.data_ptr(), n, int(np.diff(off).max()), c, 2**62, list(range(6)), 0,
                            lb.data_ptr(), ex.data_ptr(), stream_ptr=s.cuda_stream, wbytes=1)
     s.synchronize()
-buf = np.zeros(64, dtype=np.uint64)
+buf = np.zeros(64 + 256 * 3, dtype=np.uint64)
 lib.bplb_tc_trace(buf.ctypes.data)
 t0 = int(buf[0])
 names = {0: "start", 1: "hist done", 2: "A planes done", 40: "epilogues done", 41: "outputs done"}
@@ -48,3 +52,10 @@ for i in sorted(names):
     if buf[i]:
         print(f"{names[i]:28s} {(int(buf[i]) - t0) / 1e3:8.2f} us")
 print("path", eng.last_path())
+cta = buf[64:].reshape(256, 3).astype(np.int64)
+g = int(eng.last_path()[1]) if False else int((cta[:, 0] > 0).sum())
+cta = cta[:g]
+base = cta[:, 0].min()
+st, hd, en = (cta[:, 0] - base) / 1e3, (cta[:, 1] - base) / 1e3, (cta[:, 2] - base) / 1e3
+print(f"CTAs {g}: start min/median/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f} us; "
+      f"hist done {np.median(hd):.2f}/{hd.max():.2f}; end median {np.median(en):.2f} max {en.max():.2f} us")
