@@ -53,7 +53,9 @@ constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
 constexpr int PR_QMAX = 32;            // block bounds for CCM1 where floor(c / lambda) <= PR_QMAX
 constexpr int PR_QMAX_BJ1 = 32;        // ... and for BJ1 (its block bound costs O(q) lookups per q-piece)
-constexpr int PR_BLK_UNIT = 32 * 256;  // lambdas per block unit: 32 blocks of 256, one per lane
+constexpr int PR_BLK_UNIT = 32 * 256;     // lambdas per block unit: 32 blocks of 256, one per lane (lb mode)
+constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds prune less, shorter units balance
+                                          // better (cfg5 1.22 vs 1.34 us/node; lb mode 0.77 vs 0.86)
 #ifndef PR_MINB
 #define PR_MINB 3  // resident CTAs per SM the register budget is sized for
 #endif
@@ -329,7 +331,7 @@ __device__ int64_t ccm1_dense_smem(const int* w, int n, const NodeStats& st, int
 // phase 0: exact seeds (MT / RAD2 candidates, FS1, the first VB2 window, a
 // CCM1 / BJ1 window at c/4+1 where their maxima sit on typical nodes);
 // phase 1: the pruned remainder of VB2, CCM1, BJ1.
-__device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, int r) {
+__device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, int r, int blk_unit) {
     const int64_t lo = ctl.lo[kind], hi = ctl.hi[kind];
     if (hi < lo) return;
     auto push = [&](int type, int64_t a, int64_t b, int chunk, int count) {
@@ -362,7 +364,7 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
         break;
     case K_VB2:
         if (phase == 0) pushr(PU_WALK, lo, min(hi, lo + 31), 32);
-        else pushr(PU_PRUNE, lo + 32, hi, PR_BLK_UNIT);
+        else pushr(PU_PRUNE, lo + 32, hi, blk_unit);
         break;
     default: {  // CCM1, BJ1
         int64_t s0 = c / 4 + 1;
@@ -376,8 +378,8 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
             const int64_t bl = max(lo, c / ((kind == K_BJ1 ? PR_QMAX_BJ1 : PR_QMAX) + 1) + 1);
             auto region = [&](int64_t a, int64_t b) {  // [a, b] outside the seed window
                 if (b < a) return;
-                if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), PR_BLK_UNIT);
-                if (b >= bl) pushr(PU_BLK, max(a, bl), b, PR_BLK_UNIT);
+                if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), blk_unit);
+                if (b >= bl) pushr(PU_BLK, max(a, bl), b, blk_unit);
             };
             region(s1 + 1, hi);
             region(lo, s0 - 1);
@@ -914,13 +916,14 @@ __global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap
                     for (int i = 0; i < p.nk; ++i) {
                         const int kd = p.kinds[i];
                         ctl.kseg_first[kd] = ctl.nunits;
-                        prune_add_kind(ctl, kd, 0, c, r);
-                        prune_add_kind(ctl, kd, 1, c, r);
+                        prune_add_kind(ctl, kd, 0, c, r, PR_BLK_UNIT);
+                        prune_add_kind(ctl, kd, 1, c, r, PR_BLK_UNIT);
                         ctl.kseg_count[kd] = ctl.nunits - ctl.kseg_first[kd];  // units of the kind
                     }
                 } else {
                     for (int ph = 0; ph < 2; ++ph)
-                        for (int i = 0; i < p.nk; ++i) prune_add_kind(ctl, p.kinds[i], ph, c, r);
+                        for (int i = 0; i < p.nk; ++i)
+                            prune_add_kind(ctl, p.kinds[i], ph, c, r, lbm ? PR_BLK_UNIT : PR_BLK_UNIT_KEY);
                 }
             }
         }

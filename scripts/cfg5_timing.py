@@ -7,6 +7,8 @@ from paper_2402_14821_b200 import _native, workloads as W
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 ndense = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+if os.environ.get("BPLB_LIB"):  # a development build
+    _native.load_library(os.environ["BPLB_LIB"])
 c, k, w = W.cfg5_instance()
 t = time.time()
 flat, off = W.gen_nodes_device(w, c, k, W.CFG5_SEED, n, device="cuda:0")
