@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                 __syncthreads();
                 block_sort(m.sw, pw);
             }
+            NODE_STAMP(5);
             block_prefix_i64(m.sw, m.pre, r, ctl.wsum);
             const NodeStats& st = ctl.st;
             const int nm = st.n_big - st.n_full;
@@ -711,6 +712,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                 }
             }
             if (threadIdx.x == 0) ctl.n_vb2 = st.n_small + nm;
+            NODE_STAMP(6);
         }
         if (threadIdx.x == 0) {
             bplb_stats_finish(&ctl.st, c);

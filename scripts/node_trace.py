@@ -34,11 +34,11 @@ for _ in range(3):
     r = eng.check(w, c, 2**62, list(range(6)), 0)
 lib.bplb_node_trace(buf.ctypes.data)
 g = eng.last_path()[1]
-t = buf[:g, :5].astype(np.int64)
+t = buf[:g, :7].astype(np.int64)
 t0 = t[:, 0].min()
 rel = (t - t0) / 1e3
 print("lb", r.lb, "path", eng.last_path())
-names = ["start", "staged", "stats", "tables+plan", "sweep end"]
+names = ["start", "staged", "stats", "tables+plan", "sweep end", "bucket sort", "prefix+vb2"]
 for i, nm in enumerate(names):
     col = rel[:, i]
     print(f"{nm:12s} min {col.min():7.1f}  median {np.median(col):7.1f}  max {col.max():7.1f} us")
