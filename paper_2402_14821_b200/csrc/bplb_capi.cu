@@ -705,17 +705,21 @@ int launch_prune(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_
     const int rcap = bplb::prune_rcap(max_r);
     const size_t smem = bplb::prune_smem_bytes(rcap, p.c);
     if (smem > e->prune_attr_smem) {
-        CUDA_TRY(cudaFuncSetAttribute(bplb::prune_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(bplb::prune_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(bplb::prune_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(bplb::prune_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         e->prune_attr_smem = smem;
     }
+    const int lbmode = !p.best_out && !p.arg_out && !p.res_out;
+    const bool plain = !(p.flags & (BPLB_F_PHASED | BPLB_F_CANCEL));
+    auto kern = !plain ? bplb::prune_kernel<0> : (lbmode ? bplb::prune_kernel<1> : bplb::prune_kernel<2>);
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bplb::prune_kernel, bplb::PNT, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::PNT, smem));
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
     if (grid < 1) return 0;
     p.n_nodes = n_nodes;
-    const int lbmode = !p.best_out && !p.arg_out && !p.res_out;
-    bplb::prune_kernel<<<(unsigned)grid, bplb::PNT, smem, e->stream>>>(p, rcap, lbmode);
+    kern<<<(unsigned)grid, bplb::PNT, smem, e->stream>>>(p, rcap, lbmode);
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     e->last_path = BPLB_PATH_PRUNE;
