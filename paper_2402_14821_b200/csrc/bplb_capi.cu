@@ -140,6 +140,24 @@ struct GraphKey {
     }
 };
 
+// The grid-wide single check's launch sequence, replayed from a CUDA graph
+// while its arguments repeat (eleven launches; their gaps were ~40 us of
+// cfg4's 340).
+struct WideKey {
+    int64_t c = -1, r = -1, k = 0;
+    int flags = 0, nk = 0, kinds[6] = {0, 0, 0, 0, 0, 0};
+    const void *w = nullptr, *res = nullptr, *err = nullptr, *buf = nullptr;
+    size_t cap = 0;
+    bool operator==(const WideKey& o) const {
+        if (c != o.c || r != o.r || k != o.k || flags != o.flags || nk != o.nk || w != o.w || res != o.res ||
+            err != o.err || buf != o.buf || cap != o.cap)
+            return false;
+        for (int i = 0; i < nk; ++i)
+            if (kinds[i] != o.kinds[i]) return false;
+        return true;
+    }
+};
+
 struct bplb_engine {
     int device = 0;
     int num_sms = 0;
@@ -160,6 +178,10 @@ struct bplb_engine {
     DevBuf d_skeys;                   // single-check table path: keys[8] + CTA counter
     MappedBuf m_single;               // single-check table path: weights in, result out
     MappedBuf m_nres;                 // single-check node path: result + error word out
+    int64_t wide_cnt_zero = 0;        // leading histogram counts of d_wide known to be zero
+    cudaGraphExec_t wide_exec = nullptr;   // the captured grid-wide sequence (wide_key), its launch count
+    WideKey wide_key, wide_seen;
+    int64_t wide_exec_launches = 0;
     bool multi_dirty = true;          // the MultiState needs zeroing (first use, or a failed check)
     const void* node_attr_kern = nullptr;  // launch_node: kernel / smem / occupancy of the last launch
     size_t node_attr_smem = 0;
@@ -905,6 +927,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     cudaEventDestroy(e->ev1);
     for (auto& g : e->graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (e->wide_exec) cudaGraphExecDestroy(e->wide_exec);
     if (e->ev_pk0) cudaEventDestroy(e->ev_pk0);
     if (e->ev_pk1) cudaEventDestroy(e->ev_pk1);
     for (int i = 0; i < 4; ++i) {
@@ -950,6 +973,64 @@ double bplb_last_kernel_ms(bplb_engine* e) {
     return ms;
 }
 double bplb_last_device_ms(bplb_engine* e) { return e ? e->last_ms : 0.0; }
+
+// The grid-wide check on e->stream: direct launches the first time an argument
+// set is seen, captured into a graph the second time, replayed after that.
+int wide_check_graph(bplb_engine* e, bplb::KParams& p, int64_t r) {
+    WideKey key;
+    key.c = p.c; key.r = r; key.k = p.k; key.flags = p.flags; key.nk = p.nk;
+    for (int i = 0; i < p.nk; ++i) key.kinds[i] = p.kinds[i];
+    key.w = p.w; key.res = p.res_out; key.err = p.err_out; key.buf = e->d_wide.p; key.cap = e->d_wide.cap;
+    auto direct = [&]() {
+        int rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches, p, r,
+                                  &e->wide_cnt_zero);
+        return rc ? fail(rc, bplb::wide_error()) : 0;
+    };
+    if (!e->graphs_ok || e->prof_kernel) return direct();
+    if (!(e->wide_exec && e->wide_key == key)) {
+        if (!(e->wide_seen == key)) {
+            e->wide_seen = key;
+            return direct();
+        }
+        if (e->wide_exec) cudaGraphExecDestroy(e->wide_exec);
+        e->wide_exec = nullptr;
+        if (int rc = direct()) return rc;  // (this call's result; the capture below only records)
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            e->graphs_ok = false;
+            return 0;
+        }
+        const int64_t l0 = e->launches;
+        const int rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches, p, r,
+                                        &e->wide_cnt_zero);
+        cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+        e->wide_exec_launches = e->launches - l0;
+        e->launches = l0;
+        if (!rc && ce == cudaSuccess) ce = cudaGraphInstantiate(&e->wide_exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (rc || ce != cudaSuccess || e->d_wide.p != key.buf) {
+            cudaGetLastError();
+            if (e->wide_exec) cudaGraphExecDestroy(e->wide_exec);
+            e->wide_exec = nullptr;
+            e->graphs_ok = rc == 0 && ce == cudaSuccess;
+        } else {
+            e->wide_key = key;
+        }
+        return 0;
+    }
+    // replay: the histogram counts must be zero up to c + 2 (another instance
+    // size may have reused those bytes since the capture)
+    if (e->wide_cnt_zero < p.c + 2) {
+        bplb::WideBufs b = bplb::wide_carve(e->d_wide.p, r, p.c);
+        CUDA_TRY(cudaMemsetAsync(b.cnt + e->wide_cnt_zero, 0, (size_t)(p.c + 2 - e->wide_cnt_zero) * 4, e->stream));
+    }
+    e->wide_cnt_zero = p.c + 2;  // (this layout's other arrays reuse the bytes past it)
+    cudaError_t ce = cudaGraphLaunch(e->wide_exec, e->stream);
+    if (ce != cudaSuccess) return fail(BPLB_ECUDA, std::string("graph launch: ") + cudaGetErrorString(ce));
+    e->launches += e->wide_exec_launches;
+    return 0;
+}
 
 int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k,
                const int32_t* kinds, int32_t nkinds, int32_t flags, bplb_result* out) {
@@ -1080,9 +1161,8 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
         p.err_out = (int*)((char*)e->d_res.p + sizeof(bplb_result));  // copied back with the result
         CUDA_TRY(cudaMemsetAsync(p.err_out, 0, 4, e->stream));
         e->last_path = BPLB_PATH_WIDE;
-        rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
-                              p, r, nullptr);
-        if (rc) return fail(rc, bplb::wide_error());
+        rc = wide_check_graph(e, p, r);
+        if (rc) return rc;
     } else {
         // single node, multi-CTA: the offsets travel with the weights (one
         // H2D copy), the cross-CTA state is zeroed by the kernel's last CTA
@@ -1175,7 +1255,7 @@ int bplb_dff_bound_batch(bplb_engine* e, int32_t kind, const int32_t* w, int64_t
     } else if (!node_fits(r, c)) {
         e->last_path = BPLB_PATH_WIDE;
         rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches,
-                              p, r, nullptr);
+                              p, r, &e->wide_cnt_zero);
         if (rc) return fail(rc, bplb::wide_error());
     } else {
         int64_t off_h[2] = {0, r};
@@ -1389,7 +1469,7 @@ int bplb_check_batch_ex(bplb_engine* e, const void* w, int32_t wbytes, const int
             q.arg_out = p.arg_out ? p.arg_out + i * K_COUNT : nullptr;
             e->last_path = BPLB_PATH_WIDE;
             rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap,
-                                  &e->launches, q, off[i + 1] - off[i], nullptr);
+                                  &e->launches, q, off[i + 1] - off[i], &e->wide_cnt_zero);
             if (rc) return fail(rc, bplb::wide_error());
         }
     }

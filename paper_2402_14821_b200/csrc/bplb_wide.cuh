@@ -97,6 +97,8 @@ struct WideBufs {
     ulonglong2* rec;            // [c+2] {W<=(x), N<=(x)} at index x+1 (one 16-byte load)
     unsigned long long* bsum;   // [2 * nblocks] block sums for the scan
     int* vb2;                   // [r]
+    unsigned* cnt;              // [c+2] histogram counts (index x+1): zero between checks -- the
+                                // scan that consumes them clears them (no 16 MB zeroing pass)
     unsigned long long* acc;    // [c+1] VB2 per-lambda D (indexed by lambda)
     unsigned long long* pz;     // [2*101] FS1 P and Z (indexed by lambda)
     int* vlist;                 // [c/LMOD + 2] pruning: surviving VB2 walk chunks (index from lo)
@@ -112,6 +114,7 @@ inline size_t wide_bytes(int64_t r, int64_t c, int64_t* nblocks_out) {
     size_t b = 0;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     b += al(sizeof(WideState));
+    b += al((size_t)n * 4);
     b += al((size_t)n * 16);
     b += al((size_t)nb * 16);
     b += al((size_t)std::max<int64_t>(r, 1) * 4);
@@ -129,6 +132,7 @@ inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
     WideBufs w;
     w.tile = scan_tile(n);
     w.state = (WideState*)p; p += al(sizeof(WideState));
+    w.cnt = (unsigned*)p; p += al((size_t)n * 4);  // right after the state: a fixed offset for every c
     w.rec = (ulonglong2*)p; p += al((size_t)n * 16);
     w.bsum = (unsigned long long*)p; p += al((size_t)nb * 16);
     w.vb2 = (int*)p; p += al((size_t)std::max<int64_t>(r, 1) * 4);
@@ -141,12 +145,12 @@ inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
 }
 
 // -------------------------------------------------------------------------
-__global__ void wide_init(WideBufs b, int64_t c) {
-    const int64_t n = c + 2;
+// acc_n: VB2 accumulators to clear (all of them without pruning; with it the
+// seed chunk only -- the prefilter clears the surviving chunks)
+__global__ void wide_init(WideBufs b, int64_t c, int64_t acc_n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = i0; i < n; i += stride) b.rec[i] = make_ulonglong2(0ull, 0ull);
-    for (int64_t i = i0; i < c + 1; i += stride) b.acc[i] = 0;
+    for (int64_t i = i0; i < acc_n; i += stride) b.acc[i] = 0;
     for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
     for (int64_t i = i0; i < 3 * b.hn; i += stride) b.hacc[i] = 0;
     unsigned int* st = (unsigned int*)b.state;  // zero the state word by word
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
             if (2 * (int64_t)x < c) { l_s++; l_Vs += x; }
             else if (2 * (int64_t)x == c) l_e++;
             else { l_b++; l_Vm += c - x; if (x == c) l_f++; }
-            atomicAdd(&b.rec[x + 1].y, 1ull);
+            atomicAdd(&b.cnt[x + 1], 1u);
             isv = 2 * (int64_t)x != c && x < c;
         }
         const unsigned m = __ballot_sync(0xffffffffu, isv);
@@ -224,11 +228,11 @@ __global__ void __launch_bounds__(WT) wide_stats(WideBufs b, const int* __restri
 }
 
 // Block-level sums of (count, count*(i-1)) over one scan tile.
-__device__ __forceinline__ void tile_sums(const ulonglong2* rec, int64_t n, int64_t t0, int64_t tile,
+__device__ __forceinline__ void tile_sums(const unsigned* cnt, int64_t n, int64_t t0, int64_t tile,
                                           unsigned long long* sc, unsigned long long* sw) {
     unsigned long long a = 0, bw = 0;
     for (int64_t i = t0 + threadIdx.x; i < min(n, t0 + tile); i += WT) {
-        unsigned long long x = rec[i].y;
+        unsigned long long x = cnt[i];
         a += x;
         bw += x * (unsigned long long)(i - 1);
     }
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(WT) wide_scan_reduce(WideBufs b, int64_t c) {
     __shared__ unsigned long long red[WT / 32];
     const int64_t n = c + 2;
     unsigned long long sc, sw;
-    tile_sums(b.rec, n, (int64_t)blockIdx.x * b.tile, b.tile, &sc, &sw);
+    tile_sums(b.cnt, n, (int64_t)blockIdx.x * b.tile, b.tile, &sc, &sw);
     unsigned long long tc = block_sum_u64(sc, red);
     unsigned long long tw = block_sum_u64(sw, red);
     if (threadIdx.x == 0) {
@@ -282,7 +286,11 @@ __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
     const int64_t t1 = min(n, t0 + b.tile);
     for (int64_t s = t0; s < t1; s += WT) {
         const int64_t i = s + threadIdx.x;
-        unsigned long long x = i < t1 ? b.rec[i].y : 0;
+        unsigned long long x = 0;
+        if (i < t1) {
+            x = b.cnt[i];
+            b.cnt[i] = 0u;  // consumed: zero for the next check
+        }
         unsigned long long y = x * (unsigned long long)(i - 1);
         // inclusive warp scan
 #pragma unroll
@@ -339,7 +347,9 @@ __device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int
         WSeg& g = s->segs[s->nseg++];
         g.kind = kind; g.type = type; g.lo = a; g.hi = z; g.chunk = chunk; g.nslice = nslice; g.islice = islice;
         g.first = s->nunits;
-        g.count = ((z - a + chunk) / chunk) * nslice;
+        // 32-bit divisions throughout the plan (lambda ranges <= c <= 2^27,
+        // item counts < 2^31): the 64-bit ones were most of its 17 us
+        g.count = (long long)((uint32_t)(z - a + chunk) / (uint32_t)chunk) * nslice;
         s->nunits += g.count;
         s->kind_seg_count[kind]++;
     };
@@ -365,7 +375,7 @@ __device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int
         if (types & 1) {
             for (int64_t x = a; x < sh;) {
                 const int64_t y = min(sh - 1, 2 * x - 1);
-                push(kd, T_HSL, x, y, 1, (int)(span / x / HSL_TS + 1));
+                push(kd, T_HSL, x, y, 1, (int)((uint32_t)span / (uint32_t)x / HSL_TS + 1));
                 x = y + 1;
             }
             if (sh > a) s->hsl_hi[kd] = sh - 1;
@@ -375,7 +385,7 @@ __device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int
     };
     auto push_mod = [&](int kd, int64_t a, int64_t z, int islice) {
         const int64_t items = kd == K_VB2 ? s->n_vb2 : st.r;
-        int nsl = (int)((items + islice - 1) / islice);
+        int nsl = (int)((uint32_t)(items + islice - 1) / (uint32_t)islice);
         if (nsl < 1) nsl = 1;
         push(kd, T_MOD, a, z, LMOD, nsl, islice);
         return nsl > 1;
@@ -873,7 +883,10 @@ __global__ void __launch_bounds__(PF_T) wide_prefilter(KParams p, WideBufs b) {
         int pos = 0;
         if (lane == 0 && m) pos = atomicAdd(&s->nvlist, __popc(m));
         pos = __shfl_sync(0xffffffffu, pos, 0);
-        if (keep) b.vlist[pos + __popc(m & ((1u << lane) - 1u))] = (int)(first + ch);
+        if (keep) {
+            b.vlist[pos + __popc(m & ((1u << lane) - 1u))] = (int)(first + ch);
+            for (int j = 0; j < LMOD && la + j <= g.hi; ++j) b.acc[la + j] = 0;  // (wide_init: the seed chunk only)
+        }
     }
 }
 
@@ -1025,8 +1038,10 @@ inline bool wide_preferred(int64_t r, int64_t c) {
     return cells > 2000000 && c <= WIDE_MAX_C;
 }
 
+// cnt_zero: how many leading histogram counts of *buf are known to be zero
+// (the engine's; the scan keeps [0, c + 2) zero after every check).
 inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int64_t* launches,
-                      const KParams& p0, int64_t r, void*) {
+                      const KParams& p0, int64_t r, int64_t* cnt_zero) {
     KParams p = p0;
     const int64_t c = p.c;
     if (c > WIDE_MAX_C) {
@@ -1044,23 +1059,31 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
             return BPLB_ENOMEM;
         }
         *cap = need;
+        *cnt_zero = 0;
     }
     WideBufs b = wide_carve(*buf, r, c);
+    if (*cnt_zero < c + 2 &&
+        cudaMemsetAsync(b.cnt + *cnt_zero, 0, (size_t)(c + 2 - *cnt_zero) * 4, st) != cudaSuccess) {
+        wide_err_ref() = "cudaMemsetAsync failed (wide path)";
+        return BPLB_ECUDA;
+    }
+    *cnt_zero = c + 2;  // (the bytes past it may hold other arrays of this layout)
     const bool phased = p.flags & BPLB_F_PHASED;
     int ks[K_COUNT] = {0, 0, 0, 0, 0, 0};
     for (int i = 0; i < p.nk; ++i) ks[i] = p.kinds[i];
     int64_t lo0 = p.use_range ? p.rng_lo[p.kinds[0]] : 0;
     int64_t hi0 = p.use_range ? p.rng_hi[p.kinds[0]] : 0;
-    const int g_init = (int)std::min<int64_t>((c + 2 + WT - 1) / WT, (int64_t)num_sms * 8);
-    wide_init<<<std::max(g_init, 1), WT, 0, st>>>(b, c);
-    const int g_stats = (int)std::max<int64_t>(1, std::min<int64_t>((r + WT - 1) / WT, (int64_t)num_sms * 4));
-    wide_stats<<<g_stats, WT, 0, st>>>(b, p.w, r, c);
-    wide_scan_reduce<<<(unsigned)nb, WT, 0, st>>>(b, c);
-    wide_scan_apply<<<(unsigned)nb, WT, 0, st>>>(b, c);
     // bound pruning: full-collection checks (no per-lambda output) inside the
     // integer envelope of the bplb_prune.cuh bounds
     const bool prune = !phased && !(p.flags & (BPLB_F_CANCEL | BPLB_F_NOPRUNE)) && !p.lam_out && !p.use_range &&
                        c <= WIDE_PRUNE_MAX_C && r <= WIDE_PRUNE_MAX_R;
+    const int64_t acc_n = prune ? std::min<int64_t>(c + 1, LMOD + 4) : c + 1;
+    const int g_init = (int)std::min<int64_t>((acc_n + WT - 1) / WT, (int64_t)num_sms * 8);
+    wide_init<<<std::max(g_init, 1), WT, 0, st>>>(b, c, acc_n);
+    const int g_stats = (int)std::max<int64_t>(1, std::min<int64_t>((r + WT - 1) / WT, (int64_t)num_sms * 4));
+    wide_stats<<<g_stats, WT, 0, st>>>(b, p.w, r, c);
+    wide_scan_reduce<<<(unsigned)nb, WT, 0, st>>>(b, c);
+    wide_scan_apply<<<(unsigned)nb, WT, 0, st>>>(b, c);
     wide_plan<<<1, PLAN_T, 0, st>>>(b, c, p.nk, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3], ks[4], ks[5],
                                     (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0, prune ? 1 : 0);
     *launches += 5;

@@ -263,3 +263,25 @@ def test_multi_cta_node_vb2_pruned_equals_dense(eng, shape):
     for f in ("best", "arg_lambda", "evals", "evaluated"):
         assert list(getattr(a, f)) == list(getattr(b, f)), (f, path)
     assert a.lb == b.lb
+
+
+def test_wide_graph_replay_and_table_reuse(eng):
+    """The grid-wide single check is captured into a CUDA graph on the second
+    call with an argument set and replayed after; instances of another size in
+    between reuse the table buffer (the histogram counts are re-zeroed before a
+    replay).  Every repeat returns the first call's result."""
+    rng = np.random.default_rng(11)
+    a = (1_000_000, rng.integers(1, 1_000_001, 30_000).astype(np.int32))
+    b = (200_003, rng.integers(1, 200_004, 20_000).astype(np.int32))
+    want = {}
+    for c, w in (a, b, a, a, b, b, a, b, a):
+        res = eng.check(w, c, 2**62, ALL, 0)
+        assert eng.last_path()[0] == "wide"
+        got = (res.lb, list(res.best), list(res.arg_lambda), list(res.evals))
+        want.setdefault(c, got)
+        assert got == want[c], c
+    # a different weight vector of the same size (same argument set: replayed)
+    w2 = rng.integers(1, 1_000_001, 30_000).astype(np.int32)
+    r1 = eng.check(w2, a[0], 2**62, ALL, 0)
+    r2 = eng.check(w2, a[0], 2**62, ALL, _native.F_NOPRUNE)
+    assert r1.lb == r2.lb and list(r1.best) == list(r2.best)
