@@ -462,7 +462,7 @@ __device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int
     }
 }
 
-constexpr int PLAN_T = 128;
+constexpr int PLAN_T = 512;  // (the copy in is ~1500 words: a few loads in flight per thread)
 __global__ void __launch_bounds__(PLAN_T) wide_plan(WideBufs b, int64_t c, int nk, int use_range, int64_t lo0,
                                                     int64_t hi0, int kinds0, int kinds1, int kinds2, int kinds3,
                                                     int kinds4, int kinds5, int phased, int prune) {
@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(PLAN_T) wide_plan(WideBufs b, int64_t c, int n
     const int nw = (int)(sizeof(WideState) / 4);
     unsigned* g = (unsigned*)b.state;
     unsigned* l = (unsigned*)&ls;
+#pragma unroll 4
     for (int i = threadIdx.x; i < nw; i += PLAN_T) l[i] = g[i];
     __syncthreads();
     if (threadIdx.x == 0) {
