@@ -170,6 +170,23 @@ def test_random_vs_oracle(oracle, max_c, max_r, n):
         assert {k.name: v for k, v in got.arg.items()} == want.arg, (c, len(w))
 
 
+@pytest.mark.parametrize("max_c,max_r,n", [(200_000, 800, 12), (60_000, 2000, 8), (4096, 3000, 10),
+                                           (1_000_000, 600, 6)])
+def test_random_full_collection_vs_oracle(oracle, max_c, max_r, n):
+    """Full-collection single checks (lower_bound_par without cancellation):
+    the bound-pruned multi-CTA node kernel / grid-wide path, per-kind best and
+    arg lambda against the oracle's full sweep."""
+    rng = random.Random(max_c * 11 + max_r)
+    for _ in range(n):
+        c, w = random_reduced_pair(rng, max_r, max_c)
+        red = ReducedInstance(c, w)
+        got = G.lower_bound_par(red, 2**62, cancellation=False)
+        want = oracle.lower_bound_seq(w, c, 2**62)
+        assert {k.name: v for k, v in got.per_dff.items()} == want.per_dff, (c, len(w))
+        assert {k.name: v for k, v in got.arg.items()} == want.arg, (c, len(w))
+        assert got.lb == want.lb
+
+
 def test_random_batch_vs_oracle(oracle):
     rng = np.random.default_rng(7)
     for c in (1, 2, 3, 7, 8, 150, 1000, 4094, 4095, 65536, 100_000, 999_983):
