@@ -119,9 +119,34 @@ __global__ void __launch_bounds__(kNT) gather_kernel(const ulonglong2* __restric
     if (acc == 0x123456789ull) sink[0] = acc;
 }
 
+// L2 flush for timing harnesses: writes `bytes` with a CTA that holds
+// `smem` bytes of dynamic shared memory, so the SMs keep the shared-memory
+// carveout of the kernel being measured (a flush kernel without shared memory
+// leaves the SMs configured for L1, and the next launch pays the switch).
+__global__ void flush_kernel(uint4* p, size_t n) {
+    extern __shared__ unsigned char fl_smem[];
+    if (threadIdx.x == 0 && n == 0) fl_smem[0] = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4((unsigned)i, 0u, 0u, 0u);
+}
+
 }  // namespace
 
 extern "C" {
+
+__attribute__((visibility("default"))) int bplb_flush_l2(void* p, size_t bytes, void* stream, int smem) {
+    static int attr = -1;
+    if (smem > 48 * 1024 && smem != attr) {
+        if (cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+            return -1;
+        attr = smem;
+    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    flush_kernel<<<sms, 512, (size_t)smem, (cudaStream_t)stream>>>((uint4*)p, bytes / 16);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
 
 // out[0]: random 16-byte gathers/s from a 16 MB L2-resident table (one
 // 32-byte sector each), out[1]: the same in GB/s of sectors.  Returns 0 on success.

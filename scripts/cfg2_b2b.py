@@ -34,7 +34,26 @@ def call(i):
 for i in range(NC):
     call(i)
 torch.cuda.synchronize()
-for label in ("flush", "cycle", "warm"):
+import ctypes  # noqa: E402
+
+peaks = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2402_14821_b200",
+                                 "libbplb_peaks.so"))
+peaks.bplb_flush_l2.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int]
+for label in ("flush", "flush_smem", "flush_smem_only", "cycle", "warm"):
+    if label.startswith("flush_smem"):
+        sm = int(os.environ.get("FLUSH_SMEM", str(200 * 1024)))
+        tot = 0.0
+        for i in range(20):
+            peaks.bplb_flush_l2(flush.data_ptr(), flush.numel() * 4, s.cuda_stream, sm)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            if label == "flush_smem":
+                call(0)
+            e1.record(s)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        print(f"{label:6s} {tot / 20 * 1e3:8.1f} us per 10^4-node batch")
+        continue
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if label == "flush":
         tot = 0.0
