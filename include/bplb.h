@@ -179,6 +179,28 @@ BPLB_API int bplb_check_batch_multi(bplb_multi *m, const void *w_concat, int32_t
                            const int32_t *kinds, int32_t nkinds, int32_t flags, int64_t *lb_out,
                            uint8_t *exceeded_out, int64_t *best_out, int64_t *arg_out);
 
+/* One reduced instance over every engine of m (the
+ * cfg4-size single check sharded over GPUs): each kind's lambda range is cut
+ * into contiguous slices, one per engine, each slice checked with bound
+ * pruning on its own device from its own host thread, and the per-kind
+ * (best, lowest arg lambda) merged as an allreduce(MAX) of packed keys would.
+ * flags: 0 / NOPRUNE (full collection), PHASED (replayed on the merged
+ * per-kind results: n_done, per-kind fields of unreached kinds zeroed), CANCEL
+ * (runs the full collection).  Result as bplb_check's.  Replaces the
+ * reference's lambda-chunk dispatch of one check over worker processes
+ * (parallel.py:84-119) with one call over devices. */
+BPLB_API int bplb_check_multi(bplb_multi *m, const int32_t *w, int64_t r, int64_t c, int64_t k,
+                     const int32_t *kinds, int32_t nkinds, int32_t flags, bplb_result *out);
+
+/* bplb_check restricted to per-kind lambda ranges [rng_lo[kd], rng_hi[kd]]
+ * (empty when hi < lo; inside the kind's domain): one slice of a
+ * lambda-split check (the per-rank primitive of the torch.distributed form).
+ * Full collection only (PHASED / CANCEL -> BPLB_EINVAL); per-kind best / arg /
+ * evals refer to the slice. */
+BPLB_API int bplb_check_ranges(bplb_engine *eng, const int32_t *w, int64_t r, int64_t c, int64_t k,
+                      const int32_t *kinds, int32_t nkinds, int32_t flags, const int64_t *rng_lo,
+                      const int64_t *rng_hi, bplb_result *out);
+
 /* Number of kernel launches issued by the engine since creation (for the
  * bench's gpu_launches claim), and device time of the last TIMING call. */
 BPLB_API int64_t bplb_launch_count(bplb_engine *eng);

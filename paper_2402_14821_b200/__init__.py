@@ -21,7 +21,8 @@ from .bounds import (
     lower_bound_seq,
 )
 from .instances import ArrayReducedInstance, ReducedInstance, reduce_packing_arrays
-from .parallel import GpuBoundEngine, ParallelBoundEngine, SharedMax, default_workers, lower_bound_par
+from .parallel import (GpuBoundEngine, ParallelBoundEngine, SharedMax, default_workers, lower_bound_multi,
+                       lower_bound_par)
 from .batch import (csr_from_lists, lower_bound_batch, lower_bound_batch_assign, lower_bound_batch_multi, open_marker,
                     reduce_packing_batch)
 
@@ -55,6 +56,7 @@ __all__ = [
     "open_marker",
     "reduce_packing_batch",
     "lower_bound_par",
+    "lower_bound_multi",
     "lower_bound_seq",
     "reduce_packing_arrays",
     "__version__",

@@ -62,6 +62,10 @@ SIGNATURES = {
     # ctypes' data_as/byref conversions cost microseconds each
     "bplb_check": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                   _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
+    "bplb_check_ranges": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                         _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, _vp]),
+    "bplb_check_multi": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                        _vp, ctypes.c_int32, ctypes.c_int32, _vp]),
     "bplb_dff_bound_batch": (ctypes.c_int, [_vp, ctypes.c_int32, _i32p, ctypes.c_int64, ctypes.c_int64,
                                             ctypes.c_int64, ctypes.c_int64, _i64p]),
     "bplb_check_batch": (ctypes.c_int, [_vp, _i32p, _i64p, ctypes.c_int64, ctypes.c_int64,
@@ -228,6 +232,21 @@ class Engine:
             _raise(rc, "bplb_check")
         return res
 
+    def check_ranges(self, w: np.ndarray, c: int, k: int, kinds, flags: int, rng_lo, rng_hi) -> BplbResult:
+        """One slice of a lambda-split check: every kind restricted to
+        [rng_lo[kd], rng_hi[kd]] (empty when hi < lo), full collection."""
+        w = as_i32(w)
+        ks = (ctypes.c_int32 * len(kinds))(*kinds)
+        lo = np.ascontiguousarray(rng_lo, dtype=np.int64)
+        hi = np.ascontiguousarray(rng_hi, dtype=np.int64)
+        res = BplbResult()
+        rc = self._lib.bplb_check_ranges(self.handle, w.ctypes.data if len(w) else None, len(w), int(c),
+                                         _clamp_k(k), ctypes.addressof(ks), len(kinds), int(flags),
+                                         lo.ctypes.data, hi.ctypes.data, ctypes.addressof(res))
+        if rc != 0:
+            _raise(rc, "bplb_check_ranges")
+        return res
+
     def dff_bound_batch(self, kind: int, w: np.ndarray, c: int, lo: int, hi: int) -> np.ndarray:
         w = as_i32(w)
         n = max(0, int(hi) - int(lo) + 1)
@@ -377,6 +396,22 @@ class MultiEngine:
             if self._lib.bplb_multi_engine(self._h, i, ctypes.byref(e)) == 0:
                 total += int(self._lib.bplb_launch_count(e))
         return total
+
+    def check(self, w: np.ndarray, c: int, k: int, kinds, flags: int) -> BplbResult:
+        """One reduced instance over every device: each kind's lambda range
+        split into one contiguous slice per engine, results merged
+        (``bplb_check_multi``)."""
+        w = as_i32(w)
+        key = tuple(kinds)
+        ks = self._kinds_cache.get(key)
+        if ks is None:
+            ks = self._kinds_cache[key] = (ctypes.c_int32 * len(key))(*key)
+        res = BplbResult()
+        rc = self._lib.bplb_check_multi(self._h, w.ctypes.data if len(w) else None, len(w), int(c), _clamp_k(k),
+                                        ctypes.addressof(ks), len(key), int(flags), ctypes.addressof(res))
+        if rc != 0:
+            _raise(rc, "bplb_check_multi")
+        return res
 
     def check_batch(self, w: np.ndarray, offsets: np.ndarray, c: int, k: int, kinds, flags: int,
                     want_best: bool = False):

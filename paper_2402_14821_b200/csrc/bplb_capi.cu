@@ -145,15 +145,19 @@ struct GraphKey {
 // cfg4's 340).
 struct WideKey {
     int64_t c = -1, r = -1, k = 0;
-    int flags = 0, nk = 0, kinds[6] = {0, 0, 0, 0, 0, 0};
+    int flags = 0, nk = 0, kinds[6] = {0, 0, 0, 0, 0, 0}, use_range = 0;
+    int64_t rlo[6] = {0, 0, 0, 0, 0, 0}, rhi[6] = {0, 0, 0, 0, 0, 0};
     const void *w = nullptr, *res = nullptr, *err = nullptr, *buf = nullptr;
     size_t cap = 0;
     bool operator==(const WideKey& o) const {
         if (c != o.c || r != o.r || k != o.k || flags != o.flags || nk != o.nk || w != o.w || res != o.res ||
-            err != o.err || buf != o.buf || cap != o.cap)
+            err != o.err || buf != o.buf || cap != o.cap || use_range != o.use_range)
             return false;
         for (int i = 0; i < nk; ++i)
             if (kinds[i] != o.kinds[i]) return false;
+        if (use_range)
+            for (int i = 0; i < 6; ++i)
+                if (rlo[i] != o.rlo[i] || rhi[i] != o.rhi[i]) return false;
         return true;
     }
 };
@@ -981,6 +985,11 @@ int wide_check_graph(bplb_engine* e, bplb::KParams& p, int64_t r) {
     key.c = p.c; key.r = r; key.k = p.k; key.flags = p.flags; key.nk = p.nk;
     for (int i = 0; i < p.nk; ++i) key.kinds[i] = p.kinds[i];
     key.w = p.w; key.res = p.res_out; key.err = p.err_out; key.buf = e->d_wide.p; key.cap = e->d_wide.cap;
+    key.use_range = p.use_range;
+    for (int i = 0; i < 6; ++i) {
+        key.rlo[i] = p.rng_lo[i];
+        key.rhi[i] = p.rng_hi[i];
+    }
     auto direct = [&]() {
         int rc = bplb::wide_check(e->stream, e->num_sms, &e->d_wide.p, &e->d_wide.cap, &e->launches, p, r,
                                   &e->wide_cnt_zero);
@@ -1032,8 +1041,32 @@ int wide_check_graph(bplb_engine* e, bplb::KParams& p, int64_t r) {
     return 0;
 }
 
+static int check_impl(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k, const int32_t* kinds,
+                      int32_t nkinds, int32_t flags, const int64_t* rng_lo, const int64_t* rng_hi,
+                      bplb_result* out);
+
 int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k,
                const int32_t* kinds, int32_t nkinds, int32_t flags, bplb_result* out) {
+    return check_impl(e, w, r, c, k, kinds, nkinds, flags, nullptr, nullptr, out);
+}
+
+int bplb_check_ranges(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k, const int32_t* kinds,
+                      int32_t nkinds, int32_t flags, const int64_t* rng_lo, const int64_t* rng_hi,
+                      bplb_result* out) {
+    if (!rng_lo || !rng_hi) return fail(BPLB_EINVAL, "null lambda ranges");
+    if (flags & (BPLB_F_PHASED | BPLB_F_CANCEL)) return fail(BPLB_EINVAL, "lambda ranges: full collection only");
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        int64_t lo, hi;
+        bplb_domain(kd, c, &lo, &hi);
+        if (rng_hi[kd] >= rng_lo[kd] && (rng_lo[kd] < lo || rng_hi[kd] > hi))
+            return fail(BPLB_ERANGE, "lambda range outside the kind's domain");
+    }
+    return check_impl(e, w, r, c, k, kinds, nkinds, flags, rng_lo, rng_hi, out);
+}
+
+static int check_impl(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k, const int32_t* kinds,
+                      int32_t nkinds, int32_t flags, const int64_t* rng_lo, const int64_t* rng_hi,
+                      bplb_result* out) {
     if (!e || !out) return fail(BPLB_EINVAL, "null engine or output");
     if (r < 0 || (r > 0 && !w)) return fail(BPLB_EINVAL, "bad weight array");
     if (r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items for the GPU envelope");
@@ -1054,9 +1087,16 @@ int bplb_check(bplb_engine* e, const int32_t* w, int64_t r, int64_t c, int64_t k
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
     bplb::KParams p;
     fill_params(p, c, k, ks, nkinds, flags);
+    if (rng_lo) {  // per-kind lambda ranges (a slice of a lambda-split check): node or grid-wide path
+        p.use_range = 1;
+        for (int kd = 0; kd < K_COUNT; ++kd) {
+            p.rng_lo[kd] = rng_lo[kd];
+            p.rng_hi[kd] = rng_hi[kd];
+        }
+    }
     int rc;
     const int64_t maxf = (tab_kmask(p) >> K_FS1 & 1) ? 101 * c : 2 * c;
-    const bool small_tab = c <= bplb::TAB_MAX_C && r <= 65535 && r * maxf < (1ll << 23) &&
+    const bool small_tab = !rng_lo && c <= bplb::TAB_MAX_C && r <= 65535 && r * maxf < (1ll << 23) &&
                            !(flags & BPLB_F_NOTAB) && tab_warps(e, ((int)c + 3) / 4 * 4) >= 2;
     if (small_tab) {
         // small capacity: the cached table, one CTA per 64-column sub-chunk;
@@ -1765,6 +1805,96 @@ int bplb_check_batch_multi(bplb_multi* m, const void* w, int32_t wbytes, const i
     for (auto& t : th) t.join();
     for (int g = 0; g < G; ++g)
         if (rcs[(size_t)g]) return fail(rcs[(size_t)g], "shard " + std::to_string(g) + ": " + errs[(size_t)g]);
+    return 0;
+}
+
+// One reduced instance on every engine of m: each kind's lambda range cut into
+// contiguous slices, one per engine, every slice a full bound-pruned check of
+// its lambdas, the per-kind results merged on the host as an allreduce(MAX) of
+// packed (best << 32 | ~arg) keys would.  PHASED is replayed
+// on the merged per-kind results (kinds in order until the running max exceeds
+// k); CANCEL runs the full collection (the guard only skips work).
+int bplb_check_multi(bplb_multi* m, const int32_t* w, int64_t r, int64_t c, int64_t k, const int32_t* kinds,
+                     int32_t nkinds, int32_t flags, bplb_result* out) {
+    if (!m || !out) return fail(BPLB_EINVAL, "null multi-engine or output");
+    if (r < 0 || (r > 0 && !w)) return fail(BPLB_EINVAL, "bad weight array");
+    if (r > BPLB_MAX_R) return fail(BPLB_ERANGE, "too many items for the GPU envelope");
+    if (int rc = check_c(c)) return rc;
+    int ks[K_COUNT];
+    if (int rc = check_kinds(kinds, nkinds, ks)) return rc;
+    std::lock_guard<std::mutex> lock(m->mu);
+    const int G = (int)m->engines.size();
+    int64_t maxw = 0;
+    for (int64_t i = 0; i < r; ++i) maxw = std::max<int64_t>(maxw, w[i]);
+    int64_t dlo[K_COUNT], dhi[K_COUNT];
+    bool in[K_COUNT] = {false, false, false, false, false, false};
+    for (int i = 0; i < nkinds; ++i) in[ks[i]] = true;
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        bplb_domain(kd, c, &dlo[kd], &dhi[kd]);
+        if (kd == K_VB2) dhi[kd] = bplb_vb2_hi(c, r, maxw);
+        if (!in[kd]) dhi[kd] = dlo[kd] - 1;
+    }
+    const int32_t sflags = flags & ~(BPLB_F_PHASED | BPLB_F_CANCEL | BPLB_F_TIMING);
+    std::vector<bplb_result> res((size_t)G);
+    std::vector<int> rcs((size_t)G, 0);
+    std::vector<std::string> errs((size_t)G);
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g) {
+        th.emplace_back([&, g]() {
+            int64_t lo[K_COUNT], hi[K_COUNT];
+            for (int kd = 0; kd < K_COUNT; ++kd) {  // slice g of [dlo, dhi]: contiguous, near-equal
+                const int64_t n = std::max<int64_t>(0, dhi[kd] - dlo[kd] + 1);
+                lo[kd] = dlo[kd] + n * g / G;
+                hi[kd] = dlo[kd] + n * (g + 1) / G - 1;
+            }
+            rcs[(size_t)g] = check_impl(m->engines[(size_t)g], w, r, c, k, kinds, nkinds, sflags, lo, hi,
+                                        &res[(size_t)g]);
+            if (rcs[(size_t)g]) errs[(size_t)g] = g_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G; ++g)
+        if (rcs[(size_t)g]) return fail(rcs[(size_t)g], "slice " + std::to_string(g) + ": " + errs[(size_t)g]);
+    bplb_result o;
+    std::memset(&o, 0, sizeof(o));
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        unsigned long long key = 0;  // (best << 32 | 0xFFFFFFFF - (arg - lo)): the allreduce(MAX) operand
+        for (int g = 0; g < G; ++g) {
+            const bplb_result& x = res[(size_t)g];
+            o.evals[kd] += x.evals[kd];
+            if (!x.evaluated[kd]) continue;
+            o.evaluated[kd] = 1;
+            const unsigned long long kk = ((unsigned long long)x.best[kd] << 32) |
+                                          (0xFFFFFFFFull - (unsigned long long)(x.arg_lambda[kd] - dlo[kd]));
+            key = std::max(key, kk);
+        }
+        o.best[kd] = o.evaluated[kd] ? (int64_t)(key >> 32) : 0;
+        o.arg_lambda[kd] = o.evaluated[kd] ? dlo[kd] + (int64_t)(0xFFFFFFFFull - (key & 0xFFFFFFFFull)) : dlo[kd];
+        o.n_lambda[kd] = std::max<int64_t>(0, dhi[kd] - dlo[kd] + 1);
+    }
+    int nd = nkinds;
+    int64_t lb = 0;
+    for (int i = 0; i < nkinds; ++i) {
+        const int kd = ks[i];
+        if (o.evaluated[kd]) lb = std::max(lb, o.best[kd]);
+        if ((flags & BPLB_F_PHASED) && lb > k) {
+            nd = i + 1;
+            break;
+        }
+    }
+    if (flags & BPLB_F_PHASED)
+        for (int i = nd; i < nkinds; ++i) {  // kinds the sequential sweep never reached
+            const int kd = ks[i];
+            o.evaluated[kd] = 0;
+            o.evals[kd] = 0;
+            o.best[kd] = 0;
+            o.arg_lambda[kd] = dlo[kd];
+        }
+    o.lb = lb;
+    o.exceeded = lb > k;
+    o.n_done = nd;
+    for (int kd = 0; kd < K_COUNT; ++kd) o.evals_total += o.evals[kd];
+    *out = o;
     return 0;
 }
 

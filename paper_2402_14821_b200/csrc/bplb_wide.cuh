@@ -145,12 +145,12 @@ inline WideBufs wide_carve(void* base, int64_t r, int64_t c) {
 }
 
 // -------------------------------------------------------------------------
-// acc_n: VB2 accumulators to clear (all of them without pruning; with it the
-// seed chunk only -- the prefilter clears the surviving chunks)
-__global__ void wide_init(WideBufs b, int64_t c, int64_t acc_n) {
+// acc[acc_lo, acc_lo + acc_n): VB2 accumulators to clear (all of them without
+// pruning; with it the seed chunk only -- the prefilter clears the surviving chunks)
+__global__ void wide_init(WideBufs b, int64_t c, int64_t acc_lo, int64_t acc_n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t i = i0; i < acc_n; i += stride) b.acc[i] = 0;
+    for (int64_t i = i0; i < acc_n; i += stride) b.acc[acc_lo + i] = 0;
     for (int64_t i = i0; i < 2 * 101; i += stride) b.pz[i] = 0;
     for (int64_t i = i0; i < 3 * b.hn; i += stride) b.hacc[i] = 0;
     unsigned int* st = (unsigned int*)b.state;  // zero the state word by word
@@ -316,8 +316,12 @@ __global__ void __launch_bounds__(WT) wide_scan_apply(WideBufs b, int64_t c) {
 // Lambda ranges and the unit plan (one thread, on a shared-memory copy of
 // the state: the plan's read-modify-write chains through global memory were
 // dependent L2 round trips).
-__device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int use_range, int64_t lo0,
-                          int64_t hi0, int phased, int prune) {
+struct KRange {  // per-kind lambda ranges when use_range (dff_bound_batch; lambda-split checks)
+    int64_t lo[K_COUNT], hi[K_COUNT];
+};
+
+__device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int use_range, const KRange& rg,
+                          int phased, int prune) {
     bplb_stats_finish(&s->st, c);
     s->st.r = s->st.n_small + s->st.n_eq + s->st.n_big;
     for (int kd = 0; kd < K_COUNT; ++kd) {
@@ -326,7 +330,7 @@ __device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int
         if (kd == K_VB2) hi = bplb_vb2_hi(c, s->st.r, s->st.maxw);
         bool in = false;
         for (int i = 0; i < nk; ++i) in |= kinds[i] == kd;
-        if (use_range) { lo = lo0; hi = hi0; }
+        if (use_range) { lo = rg.lo[kd]; hi = rg.hi[kd]; }
         if (!in) hi = lo - 1;
         s->lo[kd] = lo;
         s->hi[kd] = hi;
@@ -463,8 +467,8 @@ __device__ void plan_body(WideState* s, int64_t c, int nk, const int* kinds, int
 }
 
 constexpr int PLAN_T = 512;  // (the copy in is ~1500 words: a few loads in flight per thread)
-__global__ void __launch_bounds__(PLAN_T) wide_plan(WideBufs b, int64_t c, int nk, int use_range, int64_t lo0,
-                                                    int64_t hi0, int kinds0, int kinds1, int kinds2, int kinds3,
+__global__ void __launch_bounds__(PLAN_T) wide_plan(WideBufs b, int64_t c, int nk, int use_range, KRange rg,
+                                                    int kinds0, int kinds1, int kinds2, int kinds3,
                                                     int kinds4, int kinds5, int phased, int prune) {
     __shared__ WideState ls;
     static_assert(sizeof(WideState) % 4 == 0, "word copy");
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(PLAN_T) wide_plan(WideBufs b, int64_t c, int n
     __syncthreads();
     if (threadIdx.x == 0) {
         const int kinds[K_COUNT] = {kinds0, kinds1, kinds2, kinds3, kinds4, kinds5};
-        plan_body(&ls, c, nk, kinds, use_range, lo0, hi0, phased, prune);
+        plan_body(&ls, c, nk, kinds, use_range, rg, phased, prune);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nw; i += PLAN_T) g[i] = l[i];
@@ -1072,20 +1076,25 @@ inline int wide_check(cudaStream_t st, int num_sms, void** buf, size_t* cap, int
     const bool phased = p.flags & BPLB_F_PHASED;
     int ks[K_COUNT] = {0, 0, 0, 0, 0, 0};
     for (int i = 0; i < p.nk; ++i) ks[i] = p.kinds[i];
-    int64_t lo0 = p.use_range ? p.rng_lo[p.kinds[0]] : 0;
-    int64_t hi0 = p.use_range ? p.rng_hi[p.kinds[0]] : 0;
+    KRange rg;
+    for (int kd = 0; kd < K_COUNT; ++kd) {
+        rg.lo[kd] = p.use_range ? p.rng_lo[kd] : 0;
+        rg.hi[kd] = p.use_range ? p.rng_hi[kd] : -1;
+    }
     // bound pruning: full-collection checks (no per-lambda output) inside the
     // integer envelope of the bplb_prune.cuh bounds
-    const bool prune = !phased && !(p.flags & (BPLB_F_CANCEL | BPLB_F_NOPRUNE)) && !p.lam_out && !p.use_range &&
+    // (per-kind ranges without per-lambda output -- a lambda-split slice -- prune too)
+    const bool prune = !phased && !(p.flags & (BPLB_F_CANCEL | BPLB_F_NOPRUNE)) && !p.lam_out &&
                        c <= WIDE_PRUNE_MAX_C && r <= WIDE_PRUNE_MAX_R;
-    const int64_t acc_n = prune ? std::min<int64_t>(c + 1, LMOD + 4) : c + 1;
+    const int64_t acc_lo = prune ? std::min<int64_t>(std::max<int64_t>(rg.lo[K_VB2], 0), c) : 0;
+    const int64_t acc_n = prune ? std::min<int64_t>(c + 1 - acc_lo, LMOD + 2) : c + 1;
     const int g_init = (int)std::min<int64_t>((acc_n + WT - 1) / WT, (int64_t)num_sms * 8);
-    wide_init<<<std::max(g_init, 1), WT, 0, st>>>(b, c, acc_n);
+    wide_init<<<std::max(g_init, 1), WT, 0, st>>>(b, c, acc_lo, acc_n);
     const int g_stats = (int)std::max<int64_t>(1, std::min<int64_t>((r + WT - 1) / WT, (int64_t)num_sms * 4));
     wide_stats<<<g_stats, WT, 0, st>>>(b, p.w, r, c);
     wide_scan_reduce<<<(unsigned)nb, WT, 0, st>>>(b, c);
     wide_scan_apply<<<(unsigned)nb, WT, 0, st>>>(b, c);
-    wide_plan<<<1, PLAN_T, 0, st>>>(b, c, p.nk, p.use_range, lo0, hi0, ks[0], ks[1], ks[2], ks[3], ks[4], ks[5],
+    wide_plan<<<1, PLAN_T, 0, st>>>(b, c, p.nk, p.use_range, rg, ks[0], ks[1], ks[2], ks[3], ks[4], ks[5],
                                     (phased || (p.flags & BPLB_F_CANCEL)) ? 1 : 0, prune ? 1 : 0);
     *launches += 5;
     int per_sm = 0;

@@ -26,7 +26,7 @@ import numpy as np
 from .bounds import DEFAULT_DFF_ORDER
 
 __all__ = ["shard_range", "pack_verdicts", "unpack_verdicts", "lower_bound_batch_sharded",
-           "check_shard_device", "rank_engine"]
+           "check_shard_device", "rank_engine", "lambda_slices", "lower_bound_lambda_split"]
 
 EXCEEDED_BIT = 62
 
@@ -157,3 +157,80 @@ def lower_bound_batch_sharded(c: int, weights: np.ndarray, offsets: np.ndarray, 
         a, b = shard_range(n_total, world, r_)
         out[a:b] = host[r_, :b - a]
     return unpack_verdicts(out)
+
+
+# ---------------------------------------------------------------------------
+# One large check split over ranks by lambda (optional row)
+# ---------------------------------------------------------------------------
+def lambda_slices(c: int, red, kinds, world: int, rank: int):
+    """Per-kind lambda slice ``(lo[6], hi[6])`` of ``rank``: each kind's range
+    (``lambda_range``, VB2 cap included) cut into ``world`` contiguous
+    near-equal parts; kinds outside ``kinds`` are empty (hi < lo).  Also
+    returns the full ranges ``(dlo[6], dhi[6])``."""
+    from .bounds import DEFAULT_DFF_ORDER as ORDER, lambda_range, resolve_kinds
+
+    kinds_t, ids = resolve_kinds(kinds)
+    dlo = np.zeros(6, dtype=np.int64)
+    dhi = np.full(6, -1, dtype=np.int64)
+    for kd, kind in enumerate(ORDER):
+        lr = lambda_range(kind, c, red)
+        dlo[kd] = lr.lo
+        dhi[kd] = lr.hi if kd in ids else lr.lo - 1
+    n = np.maximum(0, dhi - dlo + 1)
+    lo = dlo + n * rank // world
+    hi = dlo + n * (rank + 1) // world - 1
+    return lo, hi, dlo, dhi
+
+
+def _slice_compute_gpu(c, w, k, ids, lo, hi, engine=None):
+    r = (engine or rank_engine()).check_ranges(w, c, k, ids, 0, lo, hi)
+    return (np.array(r.best[:], dtype=np.int64), np.array(r.arg_lambda[:], dtype=np.int64),
+            np.array(r.evals[:], dtype=np.int64), np.array(r.evaluated[:], dtype=np.int64))
+
+
+def lower_bound_lambda_split(red, k: int, kinds: Sequence = DEFAULT_DFF_ORDER, *, group=None,
+                             compute: Callable | None = None, engine=None):
+    """Every rank checks its lambda slice of the SAME instance (bound pruning
+    inside the slice) and the ranks meet in ONE exchange step: an
+    all-reduce(MAX) of six packed keys ``best << 32 | ~(arg - lo)`` (plus the
+    per-kind evals / evaluated, summed / max-ed in the same collective).
+    Returns a lower_bound_par(cancellation=False) ``BoundResult`` on every
+    rank.  ``compute(c, w, k, ids, lo, hi) -> (best, arg, evals, evaluated)``
+    is injectable (the gloo tests); the default is this rank's GPU
+    (``bplb_check_ranges``)."""
+    import torch
+    import torch.distributed as dist
+
+    from .bounds import resolve_kinds
+    from .instances import as_reduced
+    from .parallel import _result_par
+    from ._native import BplbResult
+
+    kinds_t, ids = resolve_kinds(kinds)
+    c, w = as_reduced(red)
+    init = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if init else 1
+    rank = dist.get_rank(group) if init else 0
+    lo, hi, dlo, dhi = lambda_slices(c, red, kinds_t, world, rank)
+    fn = compute or (lambda *a: _slice_compute_gpu(*a, engine=engine))
+    best, arg, evals, ev = fn(c, w, k, list(ids), lo, hi)
+    keys = np.where(ev > 0, (best << 32) | (0xFFFFFFFF - (arg - dlo)), 0).astype(np.int64)
+    if init:
+        dev = torch.device("cpu")
+        if dist.get_backend(group) == "nccl":
+            dev = torch.device("cuda", (engine or rank_engine()).device)
+        t = torch.from_numpy(np.concatenate([keys, ev])).to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        e = torch.from_numpy(evals.copy()).to(dev)
+        dist.all_reduce(e, group=group)
+        t, e = t.cpu().numpy(), e.cpu().numpy()
+        keys, ev, evals = t[:6], t[6:], e
+    res = BplbResult()
+    for kd in range(6):
+        res.evaluated[kd] = int(ev[kd] > 0)
+        res.best[kd] = int(keys[kd] >> 32) if ev[kd] else 0
+        res.arg_lambda[kd] = int(dlo[kd] + (0xFFFFFFFF - (int(keys[kd]) & 0xFFFFFFFF))) if ev[kd] else int(dlo[kd])
+        res.evals[kd] = int(evals[kd])
+        res.n_lambda[kd] = int(max(0, dhi[kd] - dlo[kd] + 1))
+    res.evals_total = int(evals.sum())
+    return _result_par(res, kinds_t, ids, k)

@@ -23,7 +23,7 @@ from . import _native
 from .bounds import DEFAULT_DFF_ORDER, BoundResult, DffKind, _kind, _result_seq, resolve_kinds
 from .instances import as_reduced
 
-__all__ = ["SharedMax", "lower_bound_par", "GpuBoundEngine", "ParallelBoundEngine",
+__all__ = ["SharedMax", "lower_bound_par", "lower_bound_multi", "GpuBoundEngine", "ParallelBoundEngine",
            "default_workers", "CHUNK"]
 
 #: Reference cancellation granularity (parallel.py:33); the GPU checks its
@@ -87,6 +87,36 @@ def lower_bound_par(red, k: int, kinds: Sequence = DEFAULT_DFF_ORDER, workers: i
     if workers < 1:
         raise ValueError("workers must be >= 1")
     return _run_par(_native.default_engine(), red, k, kinds, cancellation)
+
+
+_multi_engines: dict = {}
+_multi_lock = threading.Lock()
+
+
+def lower_bound_multi(red, k: int, devices: Sequence[int], kinds: Sequence = DEFAULT_DFF_ORDER,
+                      mode: str = "par") -> BoundResult:
+    """One check of one (large) reduced instance over several GPUs in one call
+    (SURVEY.md 8(e)): every kind's lambda range is cut into one contiguous
+    slice per device, each slice a bound-pruned check on its own device, the
+    per-kind (best, lowest arg lambda) merged like an allreduce(MAX) of packed
+    keys (``bplb_check_multi``).  The multi-device counterpart of the
+    reference's lambda-chunk dispatch of one check (parallel.py:84-119).
+    ``mode="par"``: lower_bound_par(cancellation=False) semantics (the full
+    collection); ``mode="seq"``: lower_bound_seq semantics (kinds in order,
+    early exit replayed on the merged per-kind results)."""
+    if mode not in ("par", "seq"):
+        raise ValueError("mode must be 'par' or 'seq'")
+    kinds, ids = resolve_kinds(kinds)
+    c, w = as_reduced(red)
+    if not kinds:
+        return BoundResult(lb=0, exceeded_k=0 > k)
+    key = tuple(int(d) for d in devices)
+    with _multi_lock:
+        eng = _multi_engines.get(key)
+        if eng is None:
+            eng = _multi_engines[key] = _native.MultiEngine(key)
+    res = eng.check(w, c, k, ids, _native.F_PHASED if mode == "seq" else 0)
+    return _result_seq(res, kinds, ids, k) if mode == "seq" else _result_par(res, kinds, ids, k)
 
 
 class GpuBoundEngine:

@@ -152,3 +152,98 @@ def _bad_worker(rank, world, port, q):
             q.put((rank, "ValueError"))
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# One check split over ranks by lambda: slice results from the
+# oracle's per-lambda vectors, one all-reduce(MAX) of packed keys
+# ---------------------------------------------------------------------------
+_KN = ["MT", "RAD2", "FS1", "CCM1", "VB2", "BJ1"]
+
+
+def _oracle_slice(c, w, k, ids, lo, hi):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    best = np.zeros(6, dtype=np.int64)
+    arg = lo.copy()
+    evals = np.zeros(6, dtype=np.int64)
+    ev = np.zeros(6, dtype=np.int64)
+    for kd in ids:
+        if hi[kd] < lo[kd]:
+            continue
+        v = O.dff_bound_batch(_KN[kd], w, c, int(lo[kd]), int(hi[kd]))
+        j = int(np.argmax(v))  # first maximum: the lowest lambda
+        best[kd], arg[kd], evals[kd], ev[kd] = v[j], lo[kd] + j, len(v), 1
+    return best, arg, evals, ev
+
+
+def _split_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2402_14821_b200 import ReducedInstance
+    from paper_2402_14821_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        rng = np.random.default_rng(5)
+        for c, n in ((150, 120), (997, 300), (5000, 200)):
+            w = rng.integers(1, c + 1, n).astype(np.int32)
+            res = D.lower_bound_lambda_split(ReducedInstance.from_array(c, w), 2**62, compute=_oracle_slice)
+            out.append(({kk.name: v for kk, v in res.per_dff.items()}, {kk.name: v for kk, v in res.arg.items()},
+                        res.lb, res.evals))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_lambda_split_gloo_matches_oracle(world):
+    import multiprocessing as mp
+
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(5)
+    want = []
+    for c, n in ((150, 120), (997, 300), (5000, 200)):
+        w = rng.integers(1, c + 1, n).astype(np.int32)
+        o = O.lower_bound_seq(w, c, 2**62)
+        want.append((o.per_dff, o.arg, o.lb, o.evals))
+    for rank, out in res:
+        for got, exp in zip(out, want):
+            assert got == exp, rank
+
+
+def test_lambda_slices_cover_every_range():
+    from paper_2402_14821_b200 import DEFAULT_DFF_ORDER, ReducedInstance
+    from paper_2402_14821_b200.distributed import lambda_slices
+
+    red = ReducedInstance.from_array(1000, np.arange(1, 400, dtype=np.int32))
+    for world in (1, 2, 3, 8):
+        parts = [lambda_slices(1000, red, DEFAULT_DFF_ORDER, world, r) for r in range(world)]
+        dlo, dhi = parts[0][2], parts[0][3]
+        for kd in range(6):
+            assert parts[0][0][kd] == dlo[kd] and parts[-1][1][kd] == dhi[kd]
+            for a, b in zip(parts, parts[1:]):
+                assert a[1][kd] + 1 == b[0][kd]

@@ -285,3 +285,32 @@ def test_wide_graph_replay_and_table_reuse(eng):
     r1 = eng.check(w2, a[0], 2**62, ALL, 0)
     r2 = eng.check(w2, a[0], 2**62, ALL, _native.F_NOPRUNE)
     assert r1.lb == r2.lb and list(r1.best) == list(r2.best)
+
+
+@pytest.mark.parametrize("devices", [(0, 0), (0, 0, 0)])
+def test_lambda_split_multi_device(devices):
+    """bplb_check_multi: one instance, each kind's lambda range split over the
+    engines (a repeated device id stands in for several GPUs), per-kind keys
+    merged -- identical to the single-engine full check (grid-wide cfg4 and a
+    node-path instance), and lower_bound_seq semantics replayed."""
+    import paper_2402_14821_b200 as G
+    from paper_2402_14821_b200 import _native as N
+
+    m = N.MultiEngine(devices)
+    try:
+        eng = N.Engine(0)
+        rng = np.random.default_rng(3)
+        for c, w in (W.cfg4(), (100_000, rng.integers(1, 100_001, 900).astype(np.int32)), W.cfg3()):
+            a = m.check(w, c, 2**62, ALL, 0)
+            b = eng.check(w, c, 2**62, ALL, 0)
+            for f in ("best", "arg_lambda", "evals", "evaluated", "n_lambda"):
+                assert list(getattr(a, f)) == list(getattr(b, f)), (c, f)
+            assert a.lb == b.lb and a.exceeded == b.exceeded
+            red = G.ReducedInstance.from_array(c, w)
+            for k in (2**62, int(b.lb) - 1):
+                s1 = G.lower_bound_multi(red, k, devices, mode="seq")
+                s2 = G.lower_bound_seq(red, k)
+                assert s1.per_dff == s2.per_dff and s1.lb == s2.lb and s1.evals == s2.evals, (c, k)
+        eng.close()
+    finally:
+        m.close()
