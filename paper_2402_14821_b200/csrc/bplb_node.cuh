@@ -171,8 +171,8 @@ __device__ void add_kind_segs(NodeCtl& ctl, int kind, bool table, int64_t c, int
         s.hi = b;
         s.chunk = chunk;
         s.first = ctl.nunits;
-        s.count = (int)((b - a + chunk) / chunk);
-        ctl.nunits += s.count;
+        s.count = (int)((uint32_t)(b - a + chunk) / (uint32_t)chunk);  // (32-bit: c <= 2^30; thread 0 plans
+        ctl.nunits += s.count;                                           // while the CTA waits)
         ctl.kind_seg_count[kind]++;
     };
     switch (kind) {
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
                     Seg& g = ctl.segs[ctl.nseg++];
                     g.kind = K_VB2; g.type = T_MOD; g.lo = a; g.hi = b; g.chunk = chunk;
                     g.first = ctl.nunits;
-                    g.count = (int)((b - a + chunk) / chunk);
+                    g.count = (int)((uint32_t)(b - a + chunk) / (uint32_t)chunk);
                     ctl.nunits += g.count;
                 };
                 pushv(vlo, vlo + 31, 32);
