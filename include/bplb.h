@@ -201,6 +201,46 @@ BPLB_API int bplb_check_ranges(bplb_engine *eng, const int32_t *w, int64_t r, in
                       const int32_t *kinds, int32_t nkinds, int32_t flags, const int64_t *rng_lo,
                       const int64_t *rng_hi, bplb_result *out);
 
+/* Batched exact knapsack reasoning per bin, the bitset
+ * subset-sum DP of propagator.py:98-224 for n_bins independent bins in one
+ * launch.  Bin b: committed load committed[b] (>= 0), load interval
+ * [lo[b], hi[b]] (0 <= lo <= hi <= c), open candidate items with weights
+ * w_concat[offsets[b] .. offsets[b+1]) in [1, c], in the reference's
+ * open_items_of_bin order.  Outputs:
+ *   status_out[b]  0 ok; 1 Wipeout "no reachable load in its interval"
+ *                  (_knapsack_bin :206-207 / knapsack_load_tightening :136-137)
+ *   lo_out/hi_out  lowest / highest reachable load inside [lo, hi] (the
+ *                  tightened interval, set_lo / set_hi :208-209); the input
+ *                  interval when status is 1
+ *   action_out[t]  per open item: 0 keep, 1 remove bin b from the item (no
+ *                  load in the interval uses it), 2 commit it to b (none avoids
+ *                  it), 3 Wipeout "unpackable with or without item" -- on the
+ *                  tightened interval, all 0 when the tightened lo <= committed
+ *                  (_knapsack_bin :212-224).  The reference stops at the first
+ *                  3 in item order; the caller applies actions in that order.
+ *   reach_out      optional (NULL to skip): n_bins * ((c + 32) / 32) u32 words,
+ *                  bit v of bin b = load v reachable (reachable_sums :105-110)
+ * BPLB_KN_REACH_ONLY: reach + tightening only (action_out may be NULL).
+ * BPLB_KN_NO_TIGHTEN: filter on the INPUT interval with no committed-load
+ *   skip (knapsack_item_filter :152-167 semantics).
+ * Capacity <= 1023: one warp per bin (register bitsets); larger c: one CTA
+ * per bin with shared-memory bitsets, BPLB_ERANGE when
+ * (depth(max items) + 2) * words * 4 bytes exceed shared memory. */
+#define BPLB_KN_REACH_ONLY 0x100
+#define BPLB_KN_NO_TIGHTEN 0x200
+BPLB_API int bplb_knapsack_bins(bplb_engine *eng, int64_t c, int64_t n_bins, const int32_t *committed,
+                       const int32_t *lo, const int32_t *hi, const int32_t *w_concat,
+                       const int64_t *offsets, int32_t flags, int32_t *status_out, int32_t *lo_out,
+                       int32_t *hi_out, uint8_t *action_out, uint32_t *reach_out);
+/* Device-resident form (device pointers; max_items bounds every bin's item
+ * count; stream NULL = the engine's stream).  Returns after the launch
+ * completed (error word checked). */
+BPLB_API int bplb_knapsack_bins_device(bplb_engine *eng, int64_t c, int64_t n_bins,
+                       const int32_t *d_committed, const int32_t *d_lo, const int32_t *d_hi,
+                       const int32_t *d_w_concat, const int64_t *d_offsets, int64_t max_items,
+                       int32_t flags, int32_t *d_status, int32_t *d_lo_out, int32_t *d_hi_out,
+                       uint8_t *d_action, uint32_t *d_reach, void *stream);
+
 /* Number of kernel launches issued by the engine since creation (for the
  * bench's gpu_launches claim), and device time of the last TIMING call. */
 BPLB_API int64_t bplb_launch_count(bplb_engine *eng);
@@ -225,6 +265,7 @@ BPLB_API double bplb_last_kernel_ms(bplb_engine *eng);
 #define BPLB_PATH_NODE_SORT 5    /* CTA-per-node kernel, sorted weights                */
 #define BPLB_PATH_WIDE 6         /* grid-wide kernels (one large instance)             */
 #define BPLB_PATH_PRUNE 7        /* CTA-per-node bound-pruned sweep (bplb_prune.cuh)   */
+#define BPLB_PATH_KNAP 9         /* knapsack bins (bplb_knap.cuh); detail = threads per bin */
 #define BPLB_PATH_TC 8           /* histogram x table contraction on tcgen05 (bplb_tc.cuh) */
 BPLB_API int bplb_last_path(bplb_engine *eng, int32_t *detail);
 

@@ -453,3 +453,116 @@ void or_check_batch(const int64_t *w, const int64_t *offsets, int64_t n_nodes, i
     par_for(saved, n_nodes, 1, batch_range, &x);
     g_threads = saved;
 }
+
+/* ---- knapsack reasoning per bin ---------------------------
+ * Restates /root/reference/pkg/src/binpack/propagator.py:98-224 with the
+ * reference's own structure: a bitset over loads 0..c (Python int there,
+ * uint64 words here), _add_weights (:98-102: bits |= bits << w, cut at c),
+ * reachable_sums (:105-110), _window (:123-126), _use_avoid (:144-149),
+ * _exclusion_sums (:170-187, the same divide and conquer) and _knapsack_bin
+ * (:190-224).  Output conventions as bplb_knapsack_bins (include/bplb.h):
+ * returns 0 ok / 1 Wipeout "no reachable load"; action per open item 0 keep,
+ * 1 remove, 2 commit, 3 Wipeout; flags 0x100 reach only, 0x200 filter on the
+ * input interval without the committed-load skip (knapsack_item_filter). */
+typedef struct { int64_t nw; int64_t c; } kb_t;
+
+static void kb_add(const kb_t *k, uint64_t *bits, int64_t w) { /* :98-102, one weight */
+    const int64_t ws = w >> 6, bs = w & 63;
+    for (int64_t i = k->nw - 1; i >= ws; --i) {
+        uint64_t v = bits[i - ws] << bs;
+        if (bs && i - ws - 1 >= 0) v |= bits[i - ws - 1] >> (64 - bs);
+        bits[i] |= v;
+    }
+    const int64_t top = (k->c + 1) & 63;
+    if (top) bits[k->nw - 1] &= ((uint64_t)1 << top) - 1;
+}
+
+static int kb_any(const kb_t *k, const uint64_t *bits, int64_t lo, int64_t hi) { /* bits & _window(lo, hi) */
+    if (hi < lo) return 0;
+    if (lo < 0) lo = 0;
+    if (hi > k->c) hi = k->c;
+    for (int64_t v = lo; v <= hi; ) {
+        const int64_t i = v >> 6, b = v & 63;
+        uint64_t word = bits[i] >> b;
+        const int64_t span = hi - v + 1;
+        if (span < 64 - b) word &= ((uint64_t)1 << span) - 1;
+        if (word) return 1;
+        v += 64 - b;
+    }
+    return 0;
+}
+
+static void kb_excl(const kb_t *k, const int32_t *w, int64_t lo, int64_t hi, const uint64_t *excl,
+                    uint64_t **out, int depth, uint64_t *scratch_base) { /* rec, :177-183 */
+    if (hi - lo == 1) { memcpy(out[lo], excl, (size_t)k->nw * 8); return; }
+    const int64_t mid = (lo + hi) / 2;
+    uint64_t *t = scratch_base + (size_t)depth * k->nw;
+    memcpy(t, excl, (size_t)k->nw * 8);
+    for (int64_t i = mid; i < hi; ++i) kb_add(k, t, w[i]);
+    kb_excl(k, w, lo, mid, t, out, depth + 1, scratch_base);
+    memcpy(t, excl, (size_t)k->nw * 8);
+    for (int64_t i = lo; i < mid; ++i) kb_add(k, t, w[i]);
+    kb_excl(k, w, mid, hi, t, out, depth + 1, scratch_base);
+}
+
+int or_knapsack_bin(int64_t c, int64_t committed, int64_t lo, int64_t hi, const int32_t *w, int64_t m,
+                    int32_t flags, int32_t *lo_out, int32_t *hi_out, uint8_t *action, uint64_t *reach_out) {
+    kb_t k = {(c + 64) / 64, c};
+    uint64_t *reach = (uint64_t *)calloc((size_t)k.nw, 8);
+    if (committed <= c) reach[committed >> 6] = (uint64_t)1 << (committed & 63); /* base, :109 */
+    uint64_t *base = (uint64_t *)malloc((size_t)k.nw * 8);
+    memcpy(base, reach, (size_t)k.nw * 8);
+    for (int64_t i = 0; i < m; ++i) kb_add(&k, reach, w[i]);               /* :110 / :202 */
+    if (reach_out) memcpy(reach_out, reach, (size_t)k.nw * 8);
+    int64_t first = -1, last = -1;                                           /* :203-209 */
+    for (int64_t v = lo; v <= hi; ++v)
+        if (reach[v >> 6] >> (v & 63) & 1) { if (first < 0) first = v; last = v; }
+    free(reach);
+    if (first < 0) {
+        *lo_out = (int32_t)lo; *hi_out = (int32_t)hi;
+        if (action && !(flags & 0x100)) for (int64_t i = 0; i < m; ++i) action[i] = 0;
+        free(base);
+        return 1;
+    }
+    *lo_out = (int32_t)first; *hi_out = (int32_t)last;
+    if (!(flags & 0x200)) { lo = first; hi = last; }
+    if ((flags & 0x100)) { free(base); return 0; }
+    if ((!(flags & 0x200) && lo <= committed) || m == 0) {                  /* :213-218 */
+        for (int64_t i = 0; i < m; ++i) action[i] = 0;
+        free(base);
+        return 0;
+    }
+    int depth = 1;
+    for (int64_t t = m; t > 1; t = (t + 1) / 2) ++depth;
+    uint64_t *excl_mem = (uint64_t *)malloc((size_t)m * k.nw * 8);
+    uint64_t **excl = (uint64_t **)malloc((size_t)m * sizeof(uint64_t *));
+    uint64_t *scratch = (uint64_t *)malloc((size_t)(depth + 1) * k.nw * 8);
+    for (int64_t i = 0; i < m; ++i) excl[i] = excl_mem + (size_t)i * k.nw;
+    kb_excl(&k, w, 0, m, base, excl, 0, scratch);                           /* :219 */
+    for (int64_t i = 0; i < m; ++i) {                                        /* :220-224 / :144-149 */
+        const int64_t wt = w[i];
+        const int use = hi >= wt ? kb_any(&k, excl[i], lo - wt < 0 ? 0 : lo - wt, hi - wt) : 0;
+        const int avoid = kb_any(&k, excl[i], lo, hi);
+        action[i] = (uint8_t)(use ? (avoid ? 0 : 2) : (avoid ? 1 : 3));
+    }
+    free(scratch); free(excl); free(excl_mem); free(base);
+    return 0;
+}
+
+typedef struct {
+    int64_t c; const int64_t *cl, *lo, *hi, *off; const int32_t *w; int32_t flags;
+    int32_t *st, *lo_out, *hi_out; uint8_t *act;
+} kbb_t;
+static void kbb_range(void *p, int64_t b, int64_t e) {
+    kbb_t *q = (kbb_t *)p;
+    for (int64_t i = b; i < e; ++i)
+        q->st[i] = or_knapsack_bin(q->c, q->cl[i], q->lo[i], q->hi[i], q->w + q->off[i], q->off[i + 1] - q->off[i],
+                                   q->flags, q->lo_out + i, q->hi_out + i, q->act ? q->act + q->off[i] : NULL, NULL);
+}
+/* many independent bins (the batched form the GPU runs), g_threads threads */
+void or_knapsack_bins(int64_t c, int64_t n, const int64_t *cl, const int64_t *lo, const int64_t *hi,
+                      const int32_t *w, const int64_t *off, int32_t flags, int32_t *st, int32_t *lo_out,
+                      int32_t *hi_out, uint8_t *act) {
+    kbb_t q = {c, cl, lo, hi, off, w, flags, st, lo_out, hi_out, act};
+    par_for(g_threads, n, 16, kbb_range, &q);
+}

@@ -26,10 +26,15 @@ from .parallel import (GpuBoundEngine, ParallelBoundEngine, SharedMax, default_w
 from .batch import (csr_from_lists, lower_bound_batch, lower_bound_batch_assign, lower_bound_batch_multi, open_marker,
                     reduce_packing_batch)
 
+from .knapsack import KnapsackBatch, install_knapsack_gpu, knapsack_bins
+
 __version__ = "0.1.0"
 
 __all__ = [
     "ArrayReducedInstance",
+    "KnapsackBatch",
+    "install_knapsack_gpu",
+    "knapsack_bins",
     "BoundResult",
     "DEFAULT_DFF_ORDER",
     "DffKind",

@@ -27,7 +27,9 @@ F_NOTC = 0x20  # batched table path on the FP32 pipe instead of the tensor cores
 
 # bplb_last_path ids (include/bplb.h)
 PATHS = {0: "none", 1: "tab", 2: "tab_single", 3: "warp", 4: "node_table", 5: "node_sort", 6: "wide", 7: "prune",
-         8: "tc"}
+         8: "tc", 9: "knap"}
+KN_REACH_ONLY = 0x100  # knapsack bins: reach + tightening only
+KN_NO_TIGHTEN = 0x200  # knapsack bins: filter on the input interval (knapsack_item_filter)
 
 E_INVAL, E_RANGE, E_CUDA, E_NOMEM, E_NODEV = -1, -2, -3, -4, -5
 
@@ -92,6 +94,10 @@ SIGNATURES = {
     "bplb_check_batch_multi": (ctypes.c_int, [_vp, _vp, ctypes.c_int32, _vp, ctypes.c_int64,
                                               ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_int32,
                                               ctypes.c_int32, _vp, _vp, _vp, _vp]),
+    "bplb_knapsack_bins": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp,
+                                          ctypes.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "bplb_knapsack_bins_device": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp,
+                                                 ctypes.c_int64, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "bplb_launch_count": (ctypes.c_int64, [_vp]),
     "bplb_last_device_ms": (ctypes.c_double, [_vp]),
     "bplb_profile_kernel": (ctypes.c_int, [_vp, ctypes.c_int]),
@@ -353,6 +359,43 @@ class Engine:
             flags, lb_ptr, ex_ptr, best_ptr or None, arg_ptr or None, stream_ptr or None)
         if rc != 0:
             _raise(rc, "bplb_check_batch_device")
+
+    def knapsack_bins(self, c: int, committed, lo, hi, w, offsets, flags: int = 0, want_reach: bool = False):
+        """bplb_knapsack_bins: (status, lo, hi, action, reach or None) per bin."""
+        cl = np.ascontiguousarray(committed, dtype=np.int32)
+        l = np.ascontiguousarray(lo, dtype=np.int32)
+        h = np.ascontiguousarray(hi, dtype=np.int32)
+        ww = as_i32(w)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        n = len(cl)
+        if len(l) != n or len(h) != n or len(off) != n + 1:
+            raise ValueError("committed / lo / hi / offsets sizes disagree")
+        if n and int(off[-1]) > len(ww):
+            raise ValueError("offsets run past the weights")
+        st = np.empty(n, dtype=np.int32)
+        lo_o = np.empty(n, dtype=np.int32)
+        hi_o = np.empty(n, dtype=np.int32)
+        act = np.zeros(max(1, int(off[-1]) if n else 0), dtype=np.uint8)
+        words = (int(c) + 32) // 32
+        reach = np.zeros(max(1, n * words), dtype=np.uint32) if want_reach else None
+        rc = self._lib.bplb_knapsack_bins(self.handle, int(c), n, _vp(cl.ctypes.data), _vp(l.ctypes.data),
+                                          _vp(h.ctypes.data), _vp(ww.ctypes.data), _vp(off.ctypes.data), int(flags),
+                                          _vp(st.ctypes.data), _vp(lo_o.ctypes.data), _vp(hi_o.ctypes.data),
+                                          _vp(act.ctypes.data), _vp(reach.ctypes.data) if want_reach else None)
+        if rc != 0:
+            _raise(rc, "bplb_knapsack_bins")
+        return st, lo_o, hi_o, act[:int(off[-1]) if n else 0], (reach[:n * words].reshape(n, words)
+                                                                  if want_reach else None)
+
+    def knapsack_bins_device(self, c: int, n_bins: int, cl_ptr: int, lo_ptr: int, hi_ptr: int, w_ptr: int,
+                             off_ptr: int, max_items: int, flags: int, st_ptr: int, lo_out_ptr: int,
+                             hi_out_ptr: int, act_ptr: int, reach_ptr: int = 0, stream_ptr: int = 0) -> None:
+        rc = self._lib.bplb_knapsack_bins_device(self.handle, int(c), int(n_bins), cl_ptr, lo_ptr, hi_ptr,
+                                                 w_ptr or None, off_ptr, int(max_items), int(flags), st_ptr,
+                                                 lo_out_ptr, hi_out_ptr, act_ptr or None, reach_ptr or None,
+                                                 stream_ptr or None)
+        if rc != 0:
+            _raise(rc, "bplb_knapsack_bins_device")
 
 
 class MultiEngine:

@@ -13,7 +13,7 @@ OUT = os.path.join(HERE, "libbplb.so")
 GEN_OUT = os.path.join(HERE, "libbplb_gen.so")  # synthetic node generator (workload data, not the path)
 PEAKS_OUT = os.path.join(HERE, "libbplb_peaks.so")  # measured issue-rate denominators (bench.py only)
 SOURCES = ["bplb_capi.cu"]
-HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_prune.cuh", "bplb_ubound.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh", "bplb_reduce.cuh"]
+HEADERS = ["bplb_core.h", "bplb_device.cuh", "bplb_node.cuh", "bplb_prune.cuh", "bplb_ubound.cuh", "bplb_warp.cuh", "bplb_wide.cuh", "bplb_tab.cuh", "bplb_reduce.cuh", "bplb_knap.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

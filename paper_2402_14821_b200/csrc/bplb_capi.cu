@@ -19,6 +19,7 @@
 #include "bplb_tab.cuh"
 #include "bplb_tc.cuh"
 #include "bplb_reduce.cuh"
+#include "bplb_knap.cuh"
 #include <thread>
 #include <vector>
 
@@ -206,6 +207,7 @@ struct bplb_engine {
     int64_t wide_prune_min_cells = (int64_t)1 << 62;
     bool tc_on = true;          // BPLB_TC=0: the table path on the FP32 pipe instead of tcgen05
     DevBuf d_tcB, d_tcmeta;     // tensor-core table planes / column constants
+    DevBuf d_knin, d_knout;     // knapsack bins: packed inputs / outputs (host-array entry)
     int64_t tc_c = -1;
     int tc_kmask = -1, tc_KT = 0, tc_nnt = 0;
     size_t tc_attr_smem = 0;
@@ -919,7 +921,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
                       &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
                       &e->d_tabkeys, &e->d_tabhist, &e->d_tabready, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys,
-                      &e->d_tcB, &e->d_tcmeta})
+                      &e->d_tcB, &e->d_tcmeta, &e->d_knin, &e->d_knout})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -1940,3 +1942,166 @@ BPLB_API int bplb_tc_trace(unsigned long long* out) {
 #endif
 
 }  // extern "C"
+
+
+// ---- batched exact knapsack reasoning per bin -----------
+// propagator.py:98-224 (reachable_sums, knapsack_load_tightening,
+// knapsack_item_filter, _knapsack_bin) for many bins in one launch;
+// kernels in bplb_knap.cuh.
+namespace {
+
+int knap_launch(bplb_engine* e, cudaStream_t s, int64_t c, int64_t n_bins, int64_t max_items, int32_t flags,
+                bplb::knap::KnParams& p) {
+    using namespace bplb::knap;
+    p.c = (int32_t)c;
+    p.words = (int32_t)((c + 32) / 32);
+    p.n_bins = n_bins;
+    p.flags = flags & (KN_F_REACH_ONLY | KN_F_NO_TIGHTEN);
+    const bool timing = flags & BPLB_F_TIMING;
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev0, s));
+    if (p.words <= 32) {
+        p.nbuf = 0;
+        const size_t smem = (size_t)KN_WARP_BINS * KN_MAXD * 32 * 4;
+        CUDA_TRY(cudaFuncSetAttribute(kn_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int64_t grid = std::min<int64_t>((n_bins + KN_WARP_BINS - 1) / KN_WARP_BINS, (int64_t)e->num_sms * 64);
+        kn_warp_kernel<<<(unsigned)grid, 32 * KN_WARP_BINS, smem, s>>>(p);
+        e->last_detail = 32;
+    } else {
+        p.nbuf = std::max(3, kn_depth(max_items) + 2);
+        const size_t smem = (size_t)p.nbuf * p.words * 4;
+        if (smem + 64 > e->smem_optin)
+            return fail(BPLB_ERANGE, "knapsack bitsets of this capacity / item count exceed shared memory");
+        CUDA_TRY(cudaFuncSetAttribute(kn_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 1;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn_cta_kernel, KN_NT, smem));
+        const int64_t grid = std::min<int64_t>(n_bins, (int64_t)e->num_sms * std::max(per_sm, 1));
+        kn_cta_kernel<<<(unsigned)grid, KN_NT, smem, s>>>(p);
+        e->last_detail = KN_NT;
+    }
+    CUDA_TRY(cudaGetLastError());
+    e->launches++;
+    e->last_path = BPLB_PATH_KNAP;
+    if (timing) CUDA_TRY(cudaEventRecord(e->ev1, s));
+    return 0;
+}
+
+int knap_check_args(int64_t c, int64_t n_bins) {
+    if (c < 1 || c > BPLB_MAX_C) return fail(BPLB_ERANGE, "capacity outside [1, 2^30]");
+    if (n_bins < 0) return fail(BPLB_EINVAL, "negative bin count");
+    return 0;
+}
+
+}  // namespace
+
+int bplb_knapsack_bins_device(bplb_engine* e, int64_t c, int64_t n_bins, const int32_t* d_committed,
+                              const int32_t* d_lo, const int32_t* d_hi, const int32_t* d_w, const int64_t* d_off,
+                              int64_t max_items, int32_t flags, int32_t* d_status, int32_t* d_lo_out,
+                              int32_t* d_hi_out, uint8_t* d_action, uint32_t* d_reach, void* stream) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (int rc = knap_check_args(c, n_bins)) return rc;
+    if (max_items < 0) return fail(BPLB_EINVAL, "negative max_items");
+    if (n_bins == 0) return 0;
+    if (!d_committed || !d_lo || !d_hi || !d_off || !d_status || !d_lo_out || !d_hi_out ||
+        (!d_action && !(flags & BPLB_KN_REACH_ONLY)) || (max_items > 0 && !d_w))
+        return fail(BPLB_EINVAL, "null array");
+    cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, s)) return rc;
+    if (int rc = e->d_err.grow(16)) return rc;
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, s));
+    bplb::knap::KnParams p{};
+    p.off = d_off; p.committed = d_committed; p.lo = d_lo; p.hi = d_hi; p.w = d_w;
+    p.status = d_status; p.lo_out = d_lo_out; p.hi_out = d_hi_out; p.action = d_action; p.reach = d_reach;
+    p.err = (int*)e->d_err.p;
+    if (int rc = knap_launch(e, s, c, n_bins, max_items, flags, p)) return rc;
+    int err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&err, e->d_err.p, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (int rc = mark_tail(e, s)) return rc;
+    if (flags & BPLB_F_TIMING) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+        e->last_ms = ms;
+    }
+    if (err) return fail(BPLB_EINVAL, "knapsack bin with a weight outside [1, c], an interval outside [0, c], "
+                                      "lo > hi, a negative committed load or more items than max_items");
+    return 0;
+}
+
+int bplb_knapsack_bins(bplb_engine* e, int64_t c, int64_t n_bins, const int32_t* committed, const int32_t* lo,
+                       const int32_t* hi, const int32_t* w, const int64_t* off, int32_t flags, int32_t* status_out,
+                       int32_t* lo_out, int32_t* hi_out, uint8_t* action_out, uint32_t* reach_out) {
+    if (!e) return fail(BPLB_EINVAL, "null engine");
+    if (int rc = knap_check_args(c, n_bins)) return rc;
+    if (n_bins == 0) return 0;
+    if (!committed || !lo || !hi || !off || !status_out || !lo_out || !hi_out)
+        return fail(BPLB_EINVAL, "null array");
+    if (off[0] != 0) return fail(BPLB_EINVAL, "offsets[0] must be 0");
+    int64_t max_items = 0;
+    for (int64_t b = 0; b < n_bins; ++b) {
+        const int64_t m = off[b + 1] - off[b];
+        if (m < 0) return fail(BPLB_EINVAL, "offsets must be non-decreasing");
+        max_items = std::max(max_items, m);
+    }
+    const int64_t total = off[n_bins];
+    if (total > 0 && !w) return fail(BPLB_EINVAL, "null weights");
+    if (total > 0 && !action_out && !(flags & BPLB_KN_REACH_ONLY)) return fail(BPLB_EINVAL, "null action array");
+    const int64_t words = (c + 32) / 32;
+    // packed inputs: off | committed | lo | hi | w ; outputs: status | lo | hi | reach | action
+    const size_t in_off = 0, in_cl = in_off + (size_t)(n_bins + 1) * 8, in_lo = in_cl + (size_t)n_bins * 4,
+                 in_hi = in_lo + (size_t)n_bins * 4, in_w = in_hi + (size_t)n_bins * 4,
+                 in_bytes = in_w + (size_t)total * 4;
+    const size_t o_st = 0, o_lo = (size_t)n_bins * 4, o_hi = o_lo + (size_t)n_bins * 4,
+                 o_reach = o_hi + (size_t)n_bins * 4, o_act = o_reach + (reach_out ? (size_t)n_bins * words * 4 : 0),
+                 out_bytes = o_act + (size_t)total;
+    std::lock_guard<std::mutex> lock(e->mu);
+    CUDA_TRY(cudaSetDevice(e->device));
+    if (int rc = join_stream(e, e->stream)) return rc;
+    if (int rc = e->d_knin.grow(in_bytes + 64)) return rc;
+    if (int rc = e->d_knout.grow(out_bytes + 64)) return rc;
+    if (int rc = e->h_stage.grow(std::max(in_bytes, out_bytes) + 64)) return rc;
+    if (int rc = e->d_err.grow(16)) return rc;
+    char* hs = (char*)e->h_stage.p;
+    std::memcpy(hs + in_off, off, (size_t)(n_bins + 1) * 8);
+    std::memcpy(hs + in_cl, committed, (size_t)n_bins * 4);
+    std::memcpy(hs + in_lo, lo, (size_t)n_bins * 4);
+    std::memcpy(hs + in_hi, hi, (size_t)n_bins * 4);
+    if (total) std::memcpy(hs + in_w, w, (size_t)total * 4);
+    char* di = (char*)e->d_knin.p;
+    char* dout = (char*)e->d_knout.p;
+    CUDA_TRY(cudaMemcpyAsync(di, hs, in_bytes, cudaMemcpyHostToDevice, e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    bplb::knap::KnParams p{};
+    p.off = (const int64_t*)(di + in_off);
+    p.committed = (const int32_t*)(di + in_cl);
+    p.lo = (const int32_t*)(di + in_lo);
+    p.hi = (const int32_t*)(di + in_hi);
+    p.w = (const int32_t*)(di + in_w);
+    p.status = (int32_t*)(dout + o_st);
+    p.lo_out = (int32_t*)(dout + o_lo);
+    p.hi_out = (int32_t*)(dout + o_hi);
+    p.reach = reach_out ? (uint32_t*)(dout + o_reach) : nullptr;
+    p.action = (uint8_t*)(dout + o_act);
+    p.err = (int*)e->d_err.p;
+    if (int rc = knap_launch(e, e->stream, c, n_bins, max_items, flags, p)) return rc;
+    // the stage is reused for the outputs: the H2D copy above completed in stream order
+    CUDA_TRY(cudaMemcpyAsync(hs, dout, out_bytes, cudaMemcpyDeviceToHost, e->stream));
+    int* herr = (int*)(hs + out_bytes + ((8 - out_bytes % 8) % 8));
+    CUDA_TRY(cudaMemcpyAsync(herr, e->d_err.p, 4, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (int rc = mark_tail(e, e->stream)) return rc;
+    if (flags & BPLB_F_TIMING) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+        e->last_ms = ms;
+    }
+    if (*herr) return fail(BPLB_EINVAL, "knapsack bin with a weight outside [1, c], an interval outside [0, c], "
+                                        "lo > hi or a negative committed load");
+    std::memcpy(status_out, hs + o_st, (size_t)n_bins * 4);
+    std::memcpy(lo_out, hs + o_lo, (size_t)n_bins * 4);
+    std::memcpy(hi_out, hs + o_hi, (size_t)n_bins * 4);
+    if (reach_out) std::memcpy(reach_out, hs + o_reach, (size_t)n_bins * words * 4);
+    if (total && action_out && !(flags & BPLB_KN_REACH_ONLY)) std::memcpy(action_out, hs + o_act, (size_t)total);
+    return 0;
+}
