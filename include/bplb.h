@@ -208,21 +208,21 @@ BPLB_API int bplb_check_ranges(bplb_engine *eng, const int32_t *w, int64_t r, in
  * w_concat[offsets[b] .. offsets[b+1]) in [1, c], in the reference's
  * open_items_of_bin order.  Outputs:
  *   status_out[b]  0 ok; 1 Wipeout "no reachable load in its interval"
- *                  (_knapsack_bin :206-207 / knapsack_load_tightening :136-137)
+ *                  (_knapsack_bin :203-204 / knapsack_load_tightening :139-140)
  *   lo_out/hi_out  lowest / highest reachable load inside [lo, hi] (the
- *                  tightened interval, set_lo / set_hi :208-209); the input
+ *                  tightened interval, set_lo / set_hi :205-206); the input
  *                  interval when status is 1
  *   action_out[t]  per open item: 0 keep, 1 remove bin b from the item (no
  *                  load in the interval uses it), 2 commit it to b (none avoids
  *                  it), 3 Wipeout "unpackable with or without item" -- on the
  *                  tightened interval, all 0 when the tightened lo <= committed
- *                  (_knapsack_bin :212-224).  The reference stops at the first
+ *                  (_knapsack_bin :208-227).  The reference stops at the first
  *                  3 in item order; the caller applies actions in that order.
  *   reach_out      optional (NULL to skip): n_bins * ((c + 32) / 32) u32 words,
  *                  bit v of bin b = load v reachable (reachable_sums :105-110)
  * BPLB_KN_REACH_ONLY: reach + tightening only (action_out may be NULL).
  * BPLB_KN_NO_TIGHTEN: filter on the INPUT interval with no committed-load
- *   skip (knapsack_item_filter :152-167 semantics).
+ *   skip (knapsack_item_filter :153-168 semantics).
  * Capacity <= 1023: one warp per bin (register bitsets); larger c: one CTA
  * per bin with shared-memory bitsets, BPLB_ERANGE when
  * (depth(max items) + 2) * words * 4 bytes exceed shared memory. */

@@ -3,12 +3,12 @@
 // Restates, on the GPU and for many bins in one launch, the reference's
 // bitset subset-sum DP (/root/reference/pkg/src/binpack/propagator.py):
 //   reachable_sums      :105-110   reach = base | subset sums of the open items, cut at c
-//   knapsack_load_tightening :133-141   [lo, hi] <- [lowest, highest] reachable load inside it
-//   _exclusion_sums     :170-187   per item, the subset sums of all OTHER open items
+//   knapsack_load_tightening :136-143   [lo, hi] <- [lowest, highest] reachable load inside it
+//   _exclusion_sums     :171-187   per item, the subset sums of all OTHER open items
 //                                   (divide and conquer: m log m shifts)
-//   _use_avoid / knapsack_item_filter :144-167   per item: a load in [lo, hi] that uses it /
+//   _use_avoid / knapsack_item_filter :146-168   per item: a load in [lo, hi] that uses it /
 //                                   avoids it -> keep, remove bin, commit, or wipeout
-//   _knapsack_bin       :190-224   all of the above for one bin, sharing one reach pass
+//   _knapsack_bin       :190-227   all of the above for one bin, sharing one reach pass
 //
 // A bin is a bitset over loads 0..c in u32 words (bit v of word v >> 5).
 // Adding an item of weight w is bits |= bits << w (a funnel shift per word),
@@ -30,7 +30,7 @@
 // (0 keep, 1 remove the bin: no load uses it, 2 commit: no load avoids it,
 // 3 wipeout: neither).  As in _knapsack_bin, the item filter runs on the
 // TIGHTENED interval and is skipped (all actions 0) when the tightened lo is
-// <= the committed load (propagator.py:213-218).  KN_NO_TIGHTEN filters on
+// <= the committed load (propagator.py:208-212).  KN_NO_TIGHTEN filters on
 // the input interval with no skip (knapsack_item_filter's semantics).
 #pragma once
 #include <cstdint>
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(32 * KN_WARP_BINS) kn_warp_kernel(KnParams p) 
         const uint32_t base = (cl <= c && lane == (cl >> 5)) ? (1u << (cl & 31)) : 0u;
         const uint32_t reach = kn_warp_add_range(base, p.w, s, e, lane, lmask);
         if (p.reach && lane < words) p.reach[(size_t)b * words + lane] = reach;
-        // tightening (propagator.py:205-211)
+        // tightening (propagator.py:201-207)
         const uint32_t inter = lane < words ? reach & kn_win(lane, lo, hi) : 0u;
         const int first = __reduce_min_sync(0xffffffffu, inter ? lane * 32 + __ffs(inter) - 1 : 0x7fffffff);
         const int last = __reduce_max_sync(0xffffffffu, inter ? lane * 32 + 31 - __clz(inter) : -1);
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(32 * KN_WARP_BINS) kn_warp_kernel(KnParams p) 
                 for (int64_t t = s + lane; t < e; t += 32) p.action[t] = 0;
             continue;
         }
-        // exclusion sums by divide and conquer (propagator.py:170-187); the
+        // exclusion sums by divide and conquer (propagator.py:171-187); the
         // stack bounds are uniform across the warp
         int slo[KN_MAXD], shi[KN_MAXD], st[KN_MAXD];
         int d = 0;

@@ -268,3 +268,45 @@ def cfg5_instance():
     """cfg5: the cfg3 instance (1000 items, c = 1e5) and k = 334 bins."""
     c, w = cfg3()
     return c, 334, w
+
+
+def knapsack_bins_workload(which: str, n_bins: int, seed: int = 21):
+    """Synthetic per-bin knapsack states (SURVEY.md 8(f)4 measurement): the
+    dirty bins a propagate() pass hands to _knapsack_bin
+    (propagator.py:259-260), drawn from a BASELINE instance's items.
+
+    which = "cfg2": the Scholl-1-shaped instance (c = 150, warp-per-bin path);
+            "cfg5": the AI/ANI-shaped 1000-item instance (c = 10^5, CTA path).
+    Per bin: 8..64 open candidate items, a committed load of a few items
+    (<= c), and an interval above the committed load (so the item filter
+    runs, propagator.py:208-212): lo in (committed, c], hi = lo + up to c/8.
+    Returns (c, committed, lo, hi, weights_concat int32, offsets int64)."""
+    if which == "cfg2":
+        c, inst = cfg2_instance()
+    elif which == "cfg5":
+        c, _, inst = cfg5_instance()
+    else:
+        raise ValueError(which)
+    inst = np.asarray(inst, dtype=np.int64)
+    rng = np.random.default_rng(seed)
+    m = rng.integers(8, 65, n_bins)
+    off = np.concatenate([[0], np.cumsum(m)]).astype(np.int64)
+    w = inst[rng.integers(0, len(inst), int(off[-1]))].astype(np.int32)
+    k_c = rng.integers(0, 4, n_bins)
+    cl = np.zeros(n_bins, np.int64)
+    for t in range(4):
+        add = inst[rng.integers(0, len(inst), n_bins)]
+        sel = (k_c > t) & (cl + add <= c)
+        cl[sel] += add[sel]
+    lo = np.minimum(c, cl + 1 + (rng.random(n_bins) * (c - cl)).astype(np.int64))
+    hi = np.minimum(c, lo + (rng.random(n_bins) * (c // 8 + 1)).astype(np.int64))
+    return c, cl, lo, hi, w, off
+
+
+def knapsack_shift_count(m: int) -> int:
+    """Bitset shifts _knapsack_bin performs for m open items when the item
+    filter runs: m for the reach pass plus m per level of the exclusion-sum
+    recursion (propagator.py:171-187, 201-202)."""
+    def rec(n: int) -> int:
+        return 0 if n <= 1 else n + rec(n // 2) + rec(n - n // 2)
+    return m + rec(m)
