@@ -208,6 +208,7 @@ struct bplb_engine {
     bool tc_on = true;          // BPLB_TC=0: the table path on the FP32 pipe instead of tcgen05
     DevBuf d_tcB, d_tcmeta;     // tensor-core table planes / column constants
     DevBuf d_knin, d_knout;     // knapsack bins: packed inputs / outputs (host-array entry)
+    DevBuf d_knord;             // knapsack bins grouped by item count (warp path)
     int64_t tc_c = -1;
     int tc_kmask = -1, tc_KT = 0, tc_nnt = 0;
     size_t tc_attr_smem = 0;
@@ -921,7 +922,7 @@ int bplb_engine_destroy(bplb_engine* e) {
     for (DevBuf* b : {&e->d_w, &e->d_off, &e->d_res, &e->d_lb, &e->d_ex, &e->d_best, &e->d_arg,
                       &e->d_err, &e->d_lam, &e->d_wide, &e->d_multi, &e->d_tab, &e->d_tabmeta,
                       &e->d_tabkeys, &e->d_tabhist, &e->d_tabready, &e->d_inst, &e->d_assign, &e->d_redr, &e->d_skeys,
-                      &e->d_tcB, &e->d_tcmeta, &e->d_knin, &e->d_knout})
+                      &e->d_tcB, &e->d_tcmeta, &e->d_knin, &e->d_knout, &e->d_knord})
         b->release();
     e->h_stage.release();
     e->h_res.release();
@@ -1961,11 +1962,25 @@ int knap_launch(bplb_engine* e, cudaStream_t s, int64_t c, int64_t n_bins, int64
     if (timing) CUDA_TRY(cudaEventRecord(e->ev0, s));
     if (p.words <= 32) {
         p.nbuf = 0;
+        const int seg = p.words <= 8 ? 8 : p.words <= 16 ? 16 : 32;  // lanes per bin
         const size_t smem = (size_t)KN_WARP_BINS * KN_MAXD * 32 * 4;
-        CUDA_TRY(cudaFuncSetAttribute(kn_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int64_t grid = std::min<int64_t>((n_bins + KN_WARP_BINS - 1) / KN_WARP_BINS, (int64_t)e->num_sms * 64);
-        kn_warp_kernel<<<(unsigned)grid, 32 * KN_WARP_BINS, smem, s>>>(p);
-        e->last_detail = 32;
+        const int64_t per_cta = (int64_t)KN_WARP_BINS * (32 / seg);
+        const int64_t grid = std::min<int64_t>((n_bins + per_cta - 1) / per_cta, (int64_t)e->num_sms * 64);
+        const void* kern = seg == 8 ? (const void*)kn_warp_kernel<8>
+                         : seg == 16 ? (const void*)kn_warp_kernel<16> : (const void*)kn_warp_kernel<32>;
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        p.order = nullptr;
+        if (seg < 32 && n_bins >= 2 * per_cta && n_bins < ((int64_t)1 << 31)) {  // group bins by item count
+            if (int rc = e->d_knord.grow((size_t)n_bins * 4)) return rc;
+            kn_order_kernel<<<1, KN_ORDER_NT, 0, s>>>(p.off, n_bins, (int32_t*)e->d_knord.p);
+            CUDA_TRY(cudaGetLastError());
+            e->launches++;
+            p.order = (const int32_t*)e->d_knord.p;
+        }
+        if (seg == 8) kn_warp_kernel<8><<<(unsigned)grid, 32 * KN_WARP_BINS, smem, s>>>(p);
+        else if (seg == 16) kn_warp_kernel<16><<<(unsigned)grid, 32 * KN_WARP_BINS, smem, s>>>(p);
+        else kn_warp_kernel<32><<<(unsigned)grid, 32 * KN_WARP_BINS, smem, s>>>(p);
+        e->last_detail = seg;
     } else {
         p.nbuf = std::max(3, kn_depth(max_items) + 2);
         const size_t smem = (size_t)p.nbuf * p.words * 4;

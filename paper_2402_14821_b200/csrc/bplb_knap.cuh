@@ -13,7 +13,8 @@
 // A bin is a bitset over loads 0..c in u32 words (bit v of word v >> 5).
 // Adding an item of weight w is bits |= bits << w (a funnel shift per word),
 // masked at c.  Two code paths, chosen per launch by the word count:
-//   * words <= 32 (c <= 1023): one WARP per bin, lane i holds word i in a
+//   * words <= 32 (c <= 1023): one lane segment of 8 / 16 / 32 lanes per bin
+//     (4 / 2 / 1 bins per warp), lane i of the segment holds word i in a
 //     register; a shift is two __shfl_up_sync + a funnel shift, no shared
 //     memory traffic except the divide-and-conquer stack (one word per lane
 //     per level).
@@ -34,6 +35,7 @@
 // the input interval with no skip (knapsack_item_filter's semantics).
 #pragma once
 #include <cstdint>
+#include <cub/block/block_scan.cuh>
 
 namespace bplb {
 namespace knap {
@@ -58,6 +60,7 @@ struct KnParams {
     uint8_t* action;             // per open item (same CSR positions)
     uint32_t* reach;             // optional: n_bins * words
     int* err;                    // set to 1 on invalid input
+    const int32_t* order;        // warp path: bins grouped by item count (kn_order_kernel), or null
 };
 
 __device__ __forceinline__ uint32_t kn_last_mask(int c) {
@@ -87,66 +90,79 @@ __host__ __device__ __forceinline__ int kn_depth(int64_t m) {
 }
 
 // ---- warp path: words <= 32 -------------------------------------------------
+// SEG lanes per bin (SEG = 8 / 16 / 32 for c <= 255 / 511 / 1023): a warp
+// runs 32 / SEG bins side by side, each on its own lane segment (segment
+// masks on every shuffle / vote, so segments may diverge).
 
-// bits |= bits << w on the warp's register bitset (lane = word)
-__device__ __forceinline__ uint32_t kn_warp_add(uint32_t v, int w, int lane, uint32_t lmask) {
+// bits |= bits << w on the segment's register bitset (lane sl = word sl)
+template <int SEG>
+__device__ __forceinline__ uint32_t kn_warp_add(uint32_t v, int w, int sl, uint32_t lmask, uint32_t smask) {
     const int ws = w >> 5, bs = w & 31;
-    uint32_t h = __shfl_up_sync(0xffffffffu, v, ws);
-    uint32_t l = __shfl_up_sync(0xffffffffu, v, (ws + 1) & 31);
-    h = lane >= ws ? h : 0u;
-    l = lane >= ws + 1 ? l : 0u;
+    uint32_t h = __shfl_up_sync(smask, v, ws, SEG);
+    uint32_t l = __shfl_up_sync(smask, v, (ws + 1) & (SEG - 1), SEG);
+    h = sl >= ws ? h : 0u;
+    l = sl >= ws + 1 ? l : 0u;
     v |= bs ? __funnelshift_l(l, h, bs) : h;
     return v & lmask;
 }
 
 // v + the subset sums of w[a .. b)
-__device__ __forceinline__ uint32_t kn_warp_add_range(uint32_t v, const int32_t* w, int64_t a, int64_t b,
-                                                      int lane, uint32_t lmask) {
-    for (int64_t t0 = a; t0 < b; t0 += 32) {
-        const int n = (int)(b - t0 < 32 ? b - t0 : 32);
-        const int mine = lane < n ? w[t0 + lane] : 0;
-        for (int j = 0; j < n; ++j) v = kn_warp_add(v, __shfl_sync(0xffffffffu, mine, j), lane, lmask);
+template <int SEG>
+__device__ __forceinline__ uint32_t kn_warp_add_range(uint32_t v, const int32_t* w, int64_t a, int64_t b, int sl,
+                                                      uint32_t lmask, uint32_t smask) {
+    for (int64_t t0 = a; t0 < b; t0 += SEG) {
+        const int n = (int)(b - t0 < SEG ? b - t0 : SEG);
+        const int mine = sl < n ? w[t0 + sl] : 0;
+        for (int j = 0; j < n; ++j)
+            v = kn_warp_add<SEG>(v, __shfl_sync(smask, mine, j, SEG), sl, lmask, smask);
     }
     return v;
 }
 
+template <int SEG>
 __global__ void __launch_bounds__(32 * KN_WARP_BINS) kn_warp_kernel(KnParams p) {
+    constexpr int NSEG = 32 / SEG;
     extern __shared__ uint32_t kn_smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* stack = kn_smem + (size_t)warp * KN_MAXD * 32;  // level d word of this lane: stack[d * 32 + lane]
+    const int seg = lane / SEG, sl = lane % SEG;
+    const uint32_t smask = SEG == 32 ? 0xffffffffu : ((1u << SEG) - 1u) << (seg * SEG);
+    // recursion level d word of this lane: stack[d * SEG + sl]
+    uint32_t* stack = kn_smem + ((size_t)warp * NSEG + seg) * KN_MAXD * SEG;
     const int c = p.c, words = p.words;
-    const uint32_t lmask = lane < words - 1 ? 0xffffffffu : lane == words - 1 ? kn_last_mask(c) : 0u;
-    for (int64_t b = (int64_t)blockIdx.x * KN_WARP_BINS + warp; b < p.n_bins; b += (int64_t)gridDim.x * KN_WARP_BINS) {
+    const uint32_t lmask = sl < words - 1 ? 0xffffffffu : sl == words - 1 ? kn_last_mask(c) : 0u;
+    const int64_t stride = (int64_t)gridDim.x * KN_WARP_BINS * NSEG;
+    for (int64_t i = ((int64_t)blockIdx.x * KN_WARP_BINS + warp) * NSEG + seg; i < p.n_bins; i += stride) {
+        const int64_t b = p.order ? p.order[i] : i;
         const int64_t s = p.off[b], e = p.off[b + 1];
         const int m = (int)(e - s);
         const int cl = p.committed[b];
         int lo = p.lo[b], hi = p.hi[b];
         bool bad = cl < 0 || lo < 0 || lo > hi || hi > c || m < 0 || kn_depth(m) >= KN_MAXD;
-        for (int64_t t = s + lane; t < e && !bad; t += 32) {
+        for (int64_t t = s + sl; t < e && !bad; t += SEG) {
             const int x = p.w[t];
             if (x < 1 || x > c) bad = true;
         }
-        bad = __any_sync(0xffffffffu, bad);
+        bad = __any_sync(smask, bad);
         if (bad) {
-            if (lane == 0) { p.status[b] = -1; atomicExch(p.err, 1); }
+            if (sl == 0) { p.status[b] = -1; atomicExch(p.err, 1); }
             continue;
         }
         // base: the committed load (absent when above c: such a bit can never
         // reach a window inside [0, c], propagator.py:109-110)
-        const uint32_t base = (cl <= c && lane == (cl >> 5)) ? (1u << (cl & 31)) : 0u;
-        const uint32_t reach = kn_warp_add_range(base, p.w, s, e, lane, lmask);
-        if (p.reach && lane < words) p.reach[(size_t)b * words + lane] = reach;
+        const uint32_t base = (cl <= c && sl == (cl >> 5)) ? (1u << (cl & 31)) : 0u;
+        const uint32_t reach = kn_warp_add_range<SEG>(base, p.w, s, e, sl, lmask, smask);
+        if (p.reach && sl < words) p.reach[(size_t)b * words + sl] = reach;
         // tightening (propagator.py:201-207)
-        const uint32_t inter = lane < words ? reach & kn_win(lane, lo, hi) : 0u;
-        const int first = __reduce_min_sync(0xffffffffu, inter ? lane * 32 + __ffs(inter) - 1 : 0x7fffffff);
-        const int last = __reduce_max_sync(0xffffffffu, inter ? lane * 32 + 31 - __clz(inter) : -1);
+        const uint32_t inter = sl < words ? reach & kn_win(sl, lo, hi) : 0u;
+        const int first = __reduce_min_sync(smask, inter ? sl * 32 + __ffs(inter) - 1 : 0x7fffffff);
+        const int last = __reduce_max_sync(smask, inter ? sl * 32 + 31 - __clz(inter) : -1);
         if (last < 0) {  // Wipeout: no reachable load in the interval (actions written as 0)
-            if (lane == 0) { p.status[b] = 1; p.lo_out[b] = lo; p.hi_out[b] = hi; }
+            if (sl == 0) { p.status[b] = 1; p.lo_out[b] = lo; p.hi_out[b] = hi; }
             if (!(p.flags & KN_F_REACH_ONLY))
-                for (int64_t t = s + lane; t < e; t += 32) p.action[t] = 0;
+                for (int64_t t = s + sl; t < e; t += SEG) p.action[t] = 0;
             continue;
         }
-        if (lane == 0) { p.status[b] = 0; p.lo_out[b] = first; p.hi_out[b] = last; }
+        if (sl == 0) { p.status[b] = 0; p.lo_out[b] = first; p.hi_out[b] = last; }
         if (!(p.flags & KN_F_NO_TIGHTEN)) {
             lo = first;
             hi = last;
@@ -154,44 +170,72 @@ __global__ void __launch_bounds__(32 * KN_WARP_BINS) kn_warp_kernel(KnParams p) 
         const bool skip = (p.flags & KN_F_REACH_ONLY) || (!(p.flags & KN_F_NO_TIGHTEN) && lo <= cl);
         if (skip || m == 0) {
             if (!(p.flags & KN_F_REACH_ONLY))
-                for (int64_t t = s + lane; t < e; t += 32) p.action[t] = 0;
+                for (int64_t t = s + sl; t < e; t += SEG) p.action[t] = 0;
             continue;
         }
         // exclusion sums by divide and conquer (propagator.py:171-187); the
-        // stack bounds are uniform across the warp
+        // stack bounds are uniform across the segment
         int slo[KN_MAXD], shi[KN_MAXD], st[KN_MAXD];
         int d = 0;
         slo[0] = 0; shi[0] = m; st[0] = 0;
-        stack[lane] = base & lmask;
+        stack[sl] = base & lmask;
         while (d >= 0) {
             const int a = slo[d], z = shi[d];
             if (z - a == 1) {  // leaf: the sums without item a
-                const uint32_t x = stack[d * 32 + lane];
+                const uint32_t x = stack[d * SEG + sl];
                 const int wt = p.w[s + a];
-                const bool use = hi >= wt && __any_sync(0xffffffffu, lane < words && (x & kn_win(lane, max(0, lo - wt), hi - wt)));
-                const bool avoid = __any_sync(0xffffffffu, lane < words && (x & kn_win(lane, lo, hi)));
-                if (lane == 0) p.action[s + a] = (uint8_t)kn_action(use, avoid);
+                const bool use = hi >= wt && __any_sync(smask, sl < words && (x & kn_win(sl, max(0, lo - wt), hi - wt)));
+                const bool avoid = __any_sync(smask, sl < words && (x & kn_win(sl, lo, hi)));
+                if (sl == 0) p.action[s + a] = (uint8_t)kn_action(use, avoid);
                 --d;
                 continue;
             }
             const int mid = (a + z) >> 1;
             if (st[d] == 2) { --d; continue; }
-            const uint32_t v = stack[d * 32 + lane];
+            const uint32_t v = stack[d * SEG + sl];
             uint32_t nv;
             if (st[d] == 0) {  // left half keeps the right half's weights
-                nv = kn_warp_add_range(v, p.w, s + mid, s + z, lane, lmask);
+                nv = kn_warp_add_range<SEG>(v, p.w, s + mid, s + z, sl, lmask, smask);
                 st[d] = 1;
                 slo[d + 1] = a; shi[d + 1] = mid;
             } else {
-                nv = kn_warp_add_range(v, p.w, s + a, s + mid, lane, lmask);
+                nv = kn_warp_add_range<SEG>(v, p.w, s + a, s + mid, sl, lmask, smask);
                 st[d] = 2;
                 slo[d + 1] = mid; shi[d + 1] = z;
             }
             ++d;
             st[d] = 0;
-            stack[d * 32 + lane] = nv;
+            stack[d * SEG + sl] = nv;
         }
     }
+}
+
+// Bins of equal item count run the same divide-and-conquer schedule, so the
+// segments of a warp stay converged when they get such bins: one CTA
+// counting-sorts the bin ids by item count (capped at KN_ORDER_MAXM).
+constexpr int KN_ORDER_MAXM = 4095;
+constexpr int KN_ORDER_NT = 1024;
+__device__ __forceinline__ int kn_order_key(const int64_t* off, int64_t b) {
+    const int64_t m = off[b + 1] - off[b];
+    return m < KN_ORDER_MAXM ? (int)m : KN_ORDER_MAXM;
+}
+__global__ void __launch_bounds__(KN_ORDER_NT) kn_order_kernel(const int64_t* off, int64_t n, int32_t* order) {
+    __shared__ int cnt[KN_ORDER_MAXM + 1];
+    using Scan = cub::BlockScan<int, KN_ORDER_NT>;
+    __shared__ typename Scan::TempStorage tmp;
+    for (int i = threadIdx.x; i <= KN_ORDER_MAXM; i += KN_ORDER_NT) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < n; b += KN_ORDER_NT)
+        atomicAdd(&cnt[kn_order_key(off, b)], 1);
+    __syncthreads();
+    int v[4];
+    for (int j = 0; j < 4; ++j) v[j] = cnt[threadIdx.x * 4 + j];
+    Scan(tmp).ExclusiveSum(v, v);
+    __syncthreads();
+    for (int j = 0; j < 4; ++j) cnt[threadIdx.x * 4 + j] = v[j];
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < n; b += KN_ORDER_NT)
+        order[atomicAdd(&cnt[kn_order_key(off, b)], 1)] = (int32_t)b;
 }
 
 // ---- CTA path: one bin per CTA, shared-memory bitsets ------------------------

@@ -120,7 +120,8 @@ def _random_bins(rng: np.random.Generator, c: int, n: int, max_m: int):
 
 
 @pytest.mark.parametrize("c,n,max_m,detail", [
-    (1, 200, 6, 32), (31, 500, 12, 32), (150, 3000, 40, 32), (150, 300, 400, 32), (1023, 1000, 30, 32),
+    (1, 200, 6, 8), (31, 500, 12, 8), (150, 3000, 40, 8), (150, 300, 400, 8), (255, 1001, 30, 8),
+    (256, 999, 30, 16), (511, 700, 30, 16), (512, 700, 30, 32), (1023, 1000, 30, 32),
     (1024, 500, 30, 256), (5000, 400, 60, 256), (100000, 96, 40, 256)])
 @pytest.mark.parametrize("flags", [0, 0x200])
 def test_knapsack_bins_vs_oracle(eng, c, n, max_m, detail, flags):
