@@ -1990,6 +1990,15 @@ int knap_launch(bplb_engine* e, cudaStream_t s, int64_t c, int64_t n_bins, int64
         int per_sm = 1;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn_cta_kernel, KN_NT, smem));
         const int64_t grid = std::min<int64_t>(n_bins, (int64_t)e->num_sms * std::max(per_sm, 1));
+        p.order = nullptr;
+        if (n_bins > grid && n_bins < ((int64_t)1 << 31)) {  // longest bins first from a dynamic counter
+            if (int rc = e->d_knord.grow((size_t)n_bins * 4)) return rc;
+            kn_order_kernel<<<1, KN_ORDER_NT, 0, s>>>(p.off, n_bins, (int32_t*)e->d_knord.p);
+            CUDA_TRY(cudaGetLastError());
+            e->launches++;
+            p.order = (const int32_t*)e->d_knord.p;
+        }
+        p.next = (unsigned long long*)((char*)e->d_err.p + 8);
         kn_cta_kernel<<<(unsigned)grid, KN_NT, smem, s>>>(p);
         e->last_detail = KN_NT;
     }
@@ -2024,7 +2033,7 @@ int bplb_knapsack_bins_device(bplb_engine* e, int64_t c, int64_t n_bins, const i
     CUDA_TRY(cudaSetDevice(e->device));
     if (int rc = join_stream(e, s)) return rc;
     if (int rc = e->d_err.grow(16)) return rc;
-    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, s));
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 16, s));  // error word + bin counter
     bplb::knap::KnParams p{};
     p.off = d_off; p.committed = d_committed; p.lo = d_lo; p.hi = d_hi; p.w = d_w;
     p.status = d_status; p.lo_out = d_lo_out; p.hi_out = d_hi_out; p.action = d_action; p.reach = d_reach;
@@ -2086,7 +2095,7 @@ int bplb_knapsack_bins(bplb_engine* e, int64_t c, int64_t n_bins, const int32_t*
     char* di = (char*)e->d_knin.p;
     char* dout = (char*)e->d_knout.p;
     CUDA_TRY(cudaMemcpyAsync(di, hs, in_bytes, cudaMemcpyHostToDevice, e->stream));
-    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 4, e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->d_err.p, 0, 16, e->stream));  // error word + bin counter
     bplb::knap::KnParams p{};
     p.off = (const int64_t*)(di + in_off);
     p.committed = (const int32_t*)(di + in_cl);

@@ -60,7 +60,8 @@ struct KnParams {
     uint8_t* action;             // per open item (same CSR positions)
     uint32_t* reach;             // optional: n_bins * words
     int* err;                    // set to 1 on invalid input
-    const int32_t* order;        // warp path: bins grouped by item count (kn_order_kernel), or null
+    const int32_t* order;        // bins grouped by item count (kn_order_kernel), or null
+    unsigned long long* next;    // CTA path: dynamic bin counter (zeroed per launch)
 };
 
 __device__ __forceinline__ uint32_t kn_last_mask(int c) {
@@ -309,7 +310,15 @@ __global__ void __launch_bounds__(KN_NT) kn_cta_kernel(KnParams p) {
     __shared__ int s_bad, s_first, s_last;
     const int c = p.c, words = p.words;
     const uint32_t lm = kn_last_mask(c);
-    for (int64_t b = blockIdx.x; b < p.n_bins; b += gridDim.x) {
+    __shared__ int64_t s_bin;
+    for (;;) {
+        // dynamic bins, most items first (the order is ascending by item count)
+        if (threadIdx.x == 0) s_bin = (int64_t)atomicAdd(p.next, 1ull);
+        __syncthreads();
+        const int64_t i = s_bin;
+        __syncthreads();
+        if (i >= p.n_bins) break;
+        const int64_t b = p.order ? p.order[p.n_bins - 1 - i] : i;
         const int64_t s = p.off[b], e = p.off[b + 1];
         const int m = (int)(e - s);
         const int cl = p.committed[b];
