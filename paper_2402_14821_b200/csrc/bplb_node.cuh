@@ -430,6 +430,7 @@ __device__ __forceinline__ void block_sort(int* a, int n) {  // bitonic, n power
 
 // Exclusive block-wide scan of one value per thread (warp shuffles + one
 // shared word per warp).  Returns the sum of v over threads < threadIdx.x.
+template <int NWARPS = NW>
 __device__ __forceinline__ long long block_excl_scan(long long v, long long* wsum) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     long long x = v;
@@ -441,13 +442,13 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long* wsu
     if (lane == 31) wsum[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        long long t = lane < NW ? wsum[lane] : 0;
+        long long t = lane < NWARPS ? wsum[lane] : 0;
 #pragma unroll
-        for (int o = 1; o < NW; o <<= 1) {
+        for (int o = 1; o < NWARPS; o <<= 1) {
             long long y = __shfl_up_sync(0xffffffffu, t, o);
             if (lane >= o) t += y;
         }
-        if (lane < NW) wsum[lane] = t;
+        if (lane < NWARPS) wsum[lane] = t;
     }
     __syncthreads();
     long long res = (warp ? wsum[warp - 1] : 0) + x - v;

@@ -57,7 +57,8 @@ constexpr int PR_BLK_UNIT = 32 * 256;     // lambdas per block unit: 32 blocks o
 constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds prune less, shorter units balance
                                           // better (cfg5 1.22 vs 1.34 us/node; lb mode 0.77 vs 0.86)
 #ifndef PR_MINB
-#define PR_MINB 3  // resident CTAs per SM the register budget is sized for
+#define PR_MINB 2  // resident CTAs per SM the register budget is sized for (2 x 256 threads measured
+                   // 0.639 vs 0.724 us/node at 3 x 256 on cfg5 lb mode, key mode 0.948 vs 1.145)
 #endif
 #ifndef PR_QCAP_N
 #define PR_QCAP_N 2048
@@ -877,7 +878,7 @@ __global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap
             const int b0 = threadIdx.x * per, b1 = min(nwords, b0 + per);
             long long s = 0;
             for (int i = b0; i < b1; ++i) s += __popc(m.rk[i].x);
-            long long run = block_excl_scan(s, ctl.wsum);
+            long long run = block_excl_scan<PNW>(s, ctl.wsum);
             for (int i = b0; i < b1; ++i) {
                 m.rk[i].y = (unsigned)run;
                 run += __popc(m.rk[i].x);
@@ -899,8 +900,8 @@ __global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap
             const int e0 = threadIdx.x * pe, e1 = min(nd, e0 + pe);
             long long sc = 0, sw = 0;
             for (int i = e0; i < e1; ++i) { sc += m.cn[i]; sw += m.cw[i]; }
-            long long rc = block_excl_scan(sc, ctl.wsum);
-            long long rw = block_excl_scan(sw, ctl.wsum2);
+            long long rc = block_excl_scan<PNW>(sc, ctl.wsum);
+            long long rw = block_excl_scan<PNW>(sw, ctl.wsum2);
             for (int i = e0; i < e1; ++i) {
                 rc += m.cn[i];
                 rw += m.cw[i];
