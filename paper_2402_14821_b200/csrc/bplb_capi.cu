@@ -743,12 +743,13 @@ int launch_prune(bplb_engine* e, bplb::KParams& p, int64_t n_nodes, int64_t max_
     const bool plain = !(p.flags & (BPLB_F_PHASED | BPLB_F_CANCEL));
     auto kern = !plain ? bplb::prune_kernel<0> : (lbmode ? bplb::prune_kernel<1> : bplb::prune_kernel<2>);
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bplb::PNT, smem));
+    const int nt = bplb::prune_threads(!plain ? 0 : (lbmode ? 1 : 2));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
     if (per_sm < 1) per_sm = 1;
     const int64_t grid = std::min<int64_t>(n_nodes, (int64_t)per_sm * e->num_sms);
     if (grid < 1) return 0;
     p.n_nodes = n_nodes;
-    kern<<<(unsigned)grid, bplb::PNT, smem, e->stream>>>(p, rcap, lbmode);
+    kern<<<(unsigned)grid, nt, smem, e->stream>>>(p, rcap, lbmode);
     e->launches++;
     CUDA_TRY(cudaGetLastError());
     e->last_path = BPLB_PATH_PRUNE;

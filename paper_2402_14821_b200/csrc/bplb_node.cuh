@@ -572,7 +572,10 @@ __host__ __device__ inline size_t node_smem_bytes(bool table, int rcap, int64_t 
 
 // WIDE: 64-bit lane partials in the modular walk, needed when c >= 2^23.
 template <bool TABLE, bool WIDE>
-__global__ void __launch_bounds__(NT, 2) node_kernel(KParams p, int rcap) {
+#ifndef NODE_MINB
+#define NODE_MINB 2  // resident node_kernel CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(NT, NODE_MINB) node_kernel(KParams p, int rcap) {
     extern __shared__ __align__(16) unsigned char smem[];
     NODE_STAMP(0);
     __shared__ NodeCtl ctl;

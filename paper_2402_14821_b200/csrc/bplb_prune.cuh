@@ -47,8 +47,13 @@ namespace bplb {
 #ifndef PR_PNT
 #define PR_PNT 256  // threads per CTA (one node per CTA at a time)
 #endif
+#ifndef PR_PNT_LB
+#define PR_PNT_LB 384  // threads per CTA of the lb-mode full-collection instantiation (FAST = 1)
+#endif
 constexpr int PNT = PR_PNT;
-constexpr int PNW = PNT / 32;
+constexpr int PNT_LB = PR_PNT_LB;
+constexpr int PNW = (PNT > PNT_LB ? PNT : PNT_LB) / 32;  // per-warp arrays sized for the larger CTA
+__host__ __device__ constexpr int prune_threads(int fast) { return fast == 1 ? PNT_LB : PNT; }
 constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in smem
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
 constexpr int PR_QMAX = 32;            // block bounds for CCM1 where floor(c / lambda) <= PR_QMAX
@@ -799,7 +804,8 @@ __device__ void prune_run(const KParams& p, PruneCtl& ctl, const LK& lk, const P
 // compile-time constant there -- half the code for a kernel whose warps stall
 // on instruction fetch (lb mode 0.751 -> 0.712 us/node); FAST = 0: any mode.
 template <int FAST>
-__global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap, int lbmode) {
+__global__ void __launch_bounds__(prune_threads(FAST), PR_MINB) prune_kernel(KParams p, int rcap, int lbmode) {
+    constexpr int KNT = prune_threads(FAST);
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ PruneCtl ctl;
     const int64_t c = p.c;
@@ -830,15 +836,15 @@ __global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap
             }
             ctl.lb = 0; ctl.n_vb2 = 0; ctl.nseg = 0; ctl.nunits = 0; ctl.n_done = 0; ctl.bad = 0;
         }
-        for (int i = threadIdx.x; i <= nwords; i += PNT) m.rk[i] = make_uint2(0u, 0u);
-        for (int i = threadIdx.x; i < r + 2; i += PNT) { m.cn[i] = 0; m.cw[i] = 0; }
-        for (int i = threadIdx.x; i < r; i += PNT) m.sw[i] = load_w(p, base + i);
+        for (int i = threadIdx.x; i <= nwords; i += KNT) m.rk[i] = make_uint2(0u, 0u);
+        for (int i = threadIdx.x; i < r + 2; i += KNT) { m.cn[i] = 0; m.cw[i] = 0; }
+        for (int i = threadIdx.x; i < r; i += KNT) m.sw[i] = load_w(p, base + i);
         __syncthreads();
         // ---- statistics, presence bits, VB2 item list --------------------------
         {
             int l_max = 0, l_bad = 0, l_s = 0, l_e = 0, l_b = 0, l_f = 0;
             long long l_W = 0, l_Vs = 0, l_Vm = 0;
-            for (int i = threadIdx.x; i < r; i += PNT) {
+            for (int i = threadIdx.x; i < r; i += KNT) {
                 const int x = m.sw[i];
                 if (x < 1 || (int64_t)x > c) { l_bad = 1; continue; }
                 l_max = max(l_max, x);
@@ -874,19 +880,19 @@ __global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap
         const bool bad = ctl.bad;
         if (!bad) {
             // rank prefixes over the presence words (contiguous range per thread)
-            const int per = (nwords + PNT - 1) / PNT;
+            const int per = (nwords + KNT - 1) / KNT;
             const int b0 = threadIdx.x * per, b1 = min(nwords, b0 + per);
             long long s = 0;
             for (int i = b0; i < b1; ++i) s += __popc(m.rk[i].x);
-            long long run = block_excl_scan<PNW>(s, ctl.wsum);
+            long long run = block_excl_scan<KNT / 32>(s, ctl.wsum);
             for (int i = b0; i < b1; ++i) {
                 m.rk[i].y = (unsigned)run;
                 run += __popc(m.rk[i].x);
             }
-            if (threadIdx.x == PNT - 1) ctl.d = (int)run;
+            if (threadIdx.x == KNT - 1) ctl.d = (int)run;
             __syncthreads();
             // counts / weights per distinct value (index = its 1-based rank)
-            for (int i = threadIdx.x; i < r; i += PNT) {
+            for (int i = threadIdx.x; i < r; i += KNT) {
                 const int x = m.sw[i];
                 const uint2 e = m.rk[x >> 5];
                 const int j = (int)e.y + __popc(e.x & (0xFFFFFFFFu >> (31 - (x & 31))));
@@ -896,12 +902,12 @@ __global__ void __launch_bounds__(PNT, PR_MINB) prune_kernel(KParams p, int rcap
             __syncthreads();
             // inclusive scan of cn / cw over [0, d]
             const int nd = ctl.d + 1;
-            const int pe = (nd + PNT - 1) / PNT;
+            const int pe = (nd + KNT - 1) / KNT;
             const int e0 = threadIdx.x * pe, e1 = min(nd, e0 + pe);
             long long sc = 0, sw = 0;
             for (int i = e0; i < e1; ++i) { sc += m.cn[i]; sw += m.cw[i]; }
-            long long rc = block_excl_scan<PNW>(sc, ctl.wsum);
-            long long rw = block_excl_scan<PNW>(sw, ctl.wsum2);
+            long long rc = block_excl_scan<KNT / 32>(sc, ctl.wsum);
+            long long rw = block_excl_scan<KNT / 32>(sw, ctl.wsum2);
             for (int i = e0; i < e1; ++i) {
                 rc += m.cn[i];
                 rw += m.cw[i];
