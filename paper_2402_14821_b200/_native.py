@@ -360,11 +360,12 @@ class Engine:
         if rc != 0:
             _raise(rc, "bplb_check_batch_device")
 
-    def knapsack_bins(self, c: int, committed, lo, hi, w, offsets, flags: int = 0, want_reach: bool = False):
-        """bplb_knapsack_bins: (status, lo, hi, action, reach or None) per bin."""
-        cl = np.ascontiguousarray(committed, dtype=np.int32)
-        l = np.ascontiguousarray(lo, dtype=np.int32)
-        h = np.ascontiguousarray(hi, dtype=np.int32)
+    def knapsack_bins(self, c: int, committed, lo, hi, w, offsets, flags: int = 0, want_reach: bool = False,
+                      action_out: np.ndarray | None = None):
+        """bplb_knapsack_bins: (status, lo, hi, action, reach or None) per bin.
+        ``action_out`` (uint8, >= total items; pinned for a direct D2H copy)
+        receives the per-item actions instead of a fresh array."""
+        cl, l, h = (as_i32(x) for x in (committed, lo, hi))  # values outside int32 raise
         ww = as_i32(w)
         off = np.ascontiguousarray(offsets, dtype=np.int64)
         n = len(cl)
@@ -375,7 +376,13 @@ class Engine:
         st = np.empty(n, dtype=np.int32)
         lo_o = np.empty(n, dtype=np.int32)
         hi_o = np.empty(n, dtype=np.int32)
-        act = np.zeros(max(1, int(off[-1]) if n else 0), dtype=np.uint8)
+        total = int(off[-1]) if n else 0
+        if action_out is not None:
+            if action_out.dtype != np.uint8 or not action_out.flags.c_contiguous or len(action_out) < total:
+                raise ValueError("action_out must be a contiguous uint8 array of at least the item count")
+            act = action_out
+        else:
+            act = np.zeros(max(1, total), dtype=np.uint8)
         words = (int(c) + 32) // 32
         reach = np.zeros(max(1, n * words), dtype=np.uint32) if want_reach else None
         rc = self._lib.bplb_knapsack_bins(self.handle, int(c), n, _vp(cl.ctypes.data), _vp(l.ctypes.data),
@@ -384,8 +391,7 @@ class Engine:
                                           _vp(act.ctypes.data), _vp(reach.ctypes.data) if want_reach else None)
         if rc != 0:
             _raise(rc, "bplb_knapsack_bins")
-        return st, lo_o, hi_o, act[:int(off[-1]) if n else 0], (reach[:n * words].reshape(n, words)
-                                                                  if want_reach else None)
+        return st, lo_o, hi_o, act[:total], (reach[:n * words].reshape(n, words) if want_reach else None)
 
     def knapsack_bins_device(self, c: int, n_bins: int, cl_ptr: int, lo_ptr: int, hi_ptr: int, w_ptr: int,
                              off_ptr: int, max_items: int, flags: int, st_ptr: int, lo_out_ptr: int,
