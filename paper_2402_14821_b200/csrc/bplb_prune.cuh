@@ -65,6 +65,9 @@ constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds p
 #define PR_MINB 2  // resident CTAs per SM the register budget is sized for (2 x 256 threads measured
                    // 0.639 vs 0.724 us/node at 3 x 256 on cfg5 lb mode, key mode 0.948 vs 1.145)
 #endif
+#ifndef PR_P1_ORDER
+#define PR_P1_ORDER 0  // unit order of the pruned remainder (phase 1)
+#endif
 #ifndef PR_QCAP_N
 #define PR_QCAP_N 2048
 #endif
@@ -388,8 +391,13 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
                 if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), blk_unit);
                 if (b >= bl) pushr(PU_BLK, max(a, bl), b, blk_unit);
             };
+#if PR_P1_ORDER
+            region(lo, s0 - 1);  // the costly block tests near bl first (shorter tail before the drain)
+            region(s1 + 1, hi);
+#else
             region(s1 + 1, hi);
             region(lo, s0 - 1);
+#endif
         }
     }
     }
@@ -935,7 +943,12 @@ __global__ void __launch_bounds__(prune_threads(FAST), PR_MINB) prune_kernel(KPa
                     }
                 } else {
                     for (int ph = 0; ph < 2; ++ph)
-                        for (int i = 0; i < p.nk; ++i) {
+                        for (int ii = 0; ii < p.nk; ++ii) {
+#if PR_P1_ORDER
+                            const int i = ph ? p.nk - 1 - ii : ii;  // phase 1: BJ1 / VB2 / CCM1 units first
+#else
+                            const int i = ii;
+#endif
                             // (compile-time unit sizes: a runtime one cost lb mode 1.3 %)
                             if (lbm) prune_add_kind<PR_BLK_UNIT>(ctl, p.kinds[i], ph, c, r);
                             else prune_add_kind<PR_BLK_UNIT_KEY>(ctl, p.kinds[i], ph, c, r);
