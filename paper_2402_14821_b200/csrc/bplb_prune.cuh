@@ -56,8 +56,20 @@ constexpr int PNW = (PNT > PNT_LB ? PNT : PNT_LB) / 32;  // per-warp arrays size
 __host__ __device__ constexpr int prune_threads(int fast) { return fast == 1 ? PNT_LB : PNT; }
 constexpr int64_t PR_MAX_C = 1 << 18;  // presence bitmask: c/32 8-byte words in smem
 constexpr int PR_SUPER = 256;          // lambdas per prune unit (8 sub-blocks of 32)
-constexpr int PR_QMAX = 32;            // block bounds for CCM1 where floor(c / lambda) <= PR_QMAX
-constexpr int PR_QMAX_BJ1 = 32;        // ... and for BJ1 (its block bound costs O(q) lookups per q-piece)
+#ifndef PR_QMAX_N
+#define PR_QMAX_N 32
+#endif
+#ifndef PR_QMAX_BJ1_N
+#define PR_QMAX_BJ1_N 32
+#endif
+#ifndef PR_QMAX_CCM1_N
+#define PR_QMAX_CCM1_N 96  // cfg5: 96 / 64 / 48 / 32 -> lb 0.606 / 0.607 / 0.605 / 0.616 us/node, key 0.892 /
+                           // 0.900 / 0.910 / 0.947 (160: 0.613 / 0.899)
+#endif
+constexpr int PR_QMAX = PR_QMAX_N;          // block bounds where floor(c / lambda) <= PR_QMAX (grid-wide path)
+constexpr int PR_QMAX_CCM1 = PR_QMAX_CCM1_N;  // prune_kernel: CCM1 block units where floor(c / lambda) <= this
+                                              // (its block bound costs O(c / lambda) lookups, no q-envelope)
+constexpr int PR_QMAX_BJ1 = PR_QMAX_BJ1_N;  // ... and for BJ1 (its block bound costs O(q) lookups per q-piece)
 constexpr int PR_BLK_UNIT = 32 * 256;     // lambdas per block unit: 32 blocks of 256, one per lane (lb mode)
 constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds prune less, shorter units balance
                                           // better (cfg5 1.22 vs 1.34 us/node; lb mode 0.77 vs 0.86)
@@ -385,7 +397,7 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
             // block bounds where floor(c / l) <= PR_QMAX (l >= bl), per-lambda
             // relaxations below (tight there: the dropped floors are small
             // against c / l)
-            const int64_t bl = max(lo, c / ((kind == K_BJ1 ? PR_QMAX_BJ1 : PR_QMAX) + 1) + 1);
+            const int64_t bl = max(lo, c / ((kind == K_BJ1 ? PR_QMAX_BJ1 : PR_QMAX_CCM1) + 1) + 1);
             auto region = [&](int64_t a, int64_t b) {  // [a, b] outside the seed window
                 if (b < a) return;
                 if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), blk_unit);
