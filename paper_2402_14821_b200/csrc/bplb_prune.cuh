@@ -80,6 +80,23 @@ constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds p
 #ifndef PR_P1_ORDER
 #define PR_P1_ORDER 0  // unit order of the pruned remainder (phase 1)
 #endif
+// Cost model of the exact per-lambda sums in the drain: weight of one
+// harmonic lookup term against the per-lambda overhead (24) of the
+// warp-split loop and the dense division pass.  26 / 40 (CCM1 / BJ1) until
+// session 4; at 2 CTAs/SM lane-per-lambda lookups win almost everywhere:
+// cfg5 lb / key 0.605 / 0.893 -> 0.546 / 0.790 us/node with 1 / 1 (0 / 0 picks
+// lane lookups even at the smallest lambdas: key mode 2.3 us/node); uniform
+// c = 1e5 batches 2.57 -> 2.06 (lb), 6.87 -> 5.96 (key); cfg2-shaped nodes
+// unchanged (scripts/prune_shapes.py).
+#ifndef PR_T_CCM1
+#define PR_T_CCM1 1
+#endif
+#ifndef PR_T_BJ1
+#define PR_T_BJ1 1
+#endif
+#ifndef PR_T_DENSE
+#define PR_T_DENSE 10  // ... per item of a dense division pass
+#endif
 #ifndef PR_QCAP_N
 #define PR_QCAP_N 2048
 #endif
@@ -551,10 +568,10 @@ __device__ int64_t prune_sub(const KParams& p, PruneCtl& ctl, const LK& lk, cons
                 } else {  // CCM1 / BJ1: harmonic lookups or a dense item pass
                     const int64_t span = kind == K_CCM1 ? (c - 1) / 2 : (int64_t)st.maxw;
                     const int64_t tmax = (int64_t)((uint32_t)span / (uint32_t)sub);
-                    const int64_t T = kind == K_CCM1 ? 26 : 40;
+                    const int64_t T = kind == K_CCM1 ? PR_T_CCM1 : PR_T_BJ1;
                     const int64_t cost_lane = T * (tmax + 1);
                     const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + 24);
-                    const int64_t cost_dense = n * (10 * (((int64_t)st.r + 31) / 32) + 24);
+                    const int64_t cost_dense = n * (PR_T_DENSE * (((int64_t)st.r + 31) / 32) + 24);
                     if (cost_lane <= cost_coop && cost_lane <= cost_dense) {
                         if (in) {
                             have = true;
