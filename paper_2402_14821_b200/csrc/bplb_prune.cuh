@@ -70,6 +70,11 @@ constexpr int PR_QMAX = PR_QMAX_N;          // block bounds where floor(c / lamb
 constexpr int PR_QMAX_CCM1 = PR_QMAX_CCM1_N;  // prune_kernel: CCM1 block units where floor(c / lambda) <= this
                                               // (its block bound costs O(c / lambda) lookups, no q-envelope)
 constexpr int PR_QMAX_BJ1 = PR_QMAX_BJ1_N;  // ... and for BJ1 (its block bound costs O(q) lookups per q-piece)
+#ifndef PR_QMAX_BJ1_LB_N
+#define PR_QMAX_BJ1_LB_N 20  // lb-mode units (cross-kind threshold): cfg5 lb 32 / 24 / 20 / 16 / 12 ->
+                             // 0.546 / 0.512 / 0.496 / 0.497 / 0.513 us/node (key mode keeps 32: 0.790 vs 0.803)
+#endif
+constexpr int PR_QMAX_BJ1_LB = PR_QMAX_BJ1_LB_N;
 constexpr int PR_BLK_UNIT = 32 * 256;     // lambdas per block unit: 32 blocks of 256, one per lane (lb mode)
 constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds prune less, shorter units balance
                                           // better (cfg5 1.22 vs 1.34 us/node; lb mode 0.77 vs 0.86)
@@ -414,7 +419,8 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
             // block bounds where floor(c / l) <= PR_QMAX (l >= bl), per-lambda
             // relaxations below (tight there: the dropped floors are small
             // against c / l)
-            const int64_t bl = max(lo, c / ((kind == K_BJ1 ? PR_QMAX_BJ1 : PR_QMAX_CCM1) + 1) + 1);
+            const int qbj = blk_unit == PR_BLK_UNIT_KEY ? PR_QMAX_BJ1 : PR_QMAX_BJ1_LB;
+            const int64_t bl = max(lo, c / ((kind == K_BJ1 ? qbj : PR_QMAX_CCM1) + 1) + 1);
             auto region = [&](int64_t a, int64_t b) {  // [a, b] outside the seed window
                 if (b < a) return;
                 if (a < bl) pushr(PU_PRUNE, a, min(b, bl - 1), blk_unit);
