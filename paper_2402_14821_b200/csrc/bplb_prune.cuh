@@ -102,6 +102,12 @@ constexpr int PR_BLK_UNIT_KEY = 8 * 256;  // ... key mode: per-kind thresholds p
 #ifndef PR_T_DENSE
 #define PR_T_DENSE 10  // ... per item of a dense division pass
 #endif
+#ifndef PR_OVH
+#define PR_OVH 24  // ... per-lambda overhead of the warp-split loop / dense pass
+#endif
+#ifndef PR_SEED_DIV
+#define PR_SEED_DIV 4  // CCM1 / BJ1 seed window at c / PR_SEED_DIV + 1
+#endif
 #ifndef PR_QCAP_N
 #define PR_QCAP_N 2048
 #endif
@@ -411,7 +417,7 @@ __device__ void prune_add_kind(PruneCtl& ctl, int kind, int phase, int64_t c, in
         else pushr(PU_PRUNE, lo + 32, hi, blk_unit);
         break;
     default: {  // CCM1, BJ1
-        int64_t s0 = c / 4 + 1;
+        int64_t s0 = c / PR_SEED_DIV + 1;
         s0 = s0 < lo ? lo : (s0 > hi ? hi : s0);
         const int64_t s1 = min(hi, s0 + 31);
         if (phase == 0) pushr(PU_LOOK, s0, s1, 32);
@@ -576,8 +582,8 @@ __device__ int64_t prune_sub(const KParams& p, PruneCtl& ctl, const LK& lk, cons
                     const int64_t tmax = (int64_t)((uint32_t)span / (uint32_t)sub);
                     const int64_t T = kind == K_CCM1 ? PR_T_CCM1 : PR_T_BJ1;
                     const int64_t cost_lane = T * (tmax + 1);
-                    const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + 24);
-                    const int64_t cost_dense = n * (PR_T_DENSE * (((int64_t)st.r + 31) / 32) + 24);
+                    const int64_t cost_coop = n * (T * ((tmax + 32) / 32) + PR_OVH);
+                    const int64_t cost_dense = n * (PR_T_DENSE * (((int64_t)st.r + 31) / 32) + PR_OVH);
                     if (cost_lane <= cost_coop && cost_lane <= cost_dense) {
                         if (in) {
                             have = true;
