@@ -40,7 +40,10 @@
 namespace bplb {
 namespace knap {
 
-constexpr int KN_NT = 256;          // threads per CTA (CTA-per-bin path)
+#ifndef KN_NT_N
+#define KN_NT_N 256
+#endif
+constexpr int KN_NT = KN_NT_N;      // threads per CTA (CTA-per-bin path)
 constexpr int KN_WARP_BINS = 8;     // bins per CTA on the warp path (one per warp)
 constexpr int KN_MAXD = 26;         // deepest divide-and-conquer stack (m < 2^25 items per bin)
 constexpr int KN_F_REACH_ONLY = 0x100;
