@@ -132,13 +132,19 @@ __device__ __forceinline__ bool kind_in(const KParams& p, int kind) {
 // Threshold below which CCM1/BJ1 lambdas are summed densely (SORT mode) --
 // harmonic lookups cost ~2 * 8 instructions per term, a dense pass ~3 (CCM1)
 // or ~5 (BJ1) per item.
+#ifndef NODE_DS_CCM1
+#define NODE_DS_CCM1 16
+#endif
+#ifndef NODE_DS_BJ1
+#define NODE_DS_BJ1 4
+#endif
 __device__ __forceinline__ int64_t div_split(int kind, const NodeStats& st, int64_t c) {
     const int64_t n = st.r > 0 ? st.r : 1;
     if (kind == K_CCM1) {
         const int64_t hs = (c - 1) / 2;
-        return (16 * hs) / (3 * n + 30) + 1;
+        return (NODE_DS_CCM1 * hs) / (3 * n + 30) + 1;
     }
-    return (4 * (int64_t)st.maxw) / n + 1;
+    return (NODE_DS_BJ1 * (int64_t)st.maxw) / n + 1;
 }
 
 #ifdef NODE_TRACE
